@@ -1,0 +1,168 @@
+/*
+ * hylra.h — C ABI of the B200 (sm_100a) HyLRA decode-time hybrid attention path.
+ *
+ * This is the drop-in boundary for the reference's layer-policy interface
+ * (reference: pkg/src/layerreuse/engine.py:129-209 `hybrid_decode`), split into
+ * the primitives that interface is built from:
+ *
+ *   hylra_full_decode    <- attention.py:210-226 `full_attention` for every head of a
+ *                           layer, plus engine.py:177-181 (per-head logits summed
+ *                           into the selection score, zero-initialised, head order)
+ *   hylra_topk_select    <- attention.py:264-275 `topk_of_logits` / :278-284
+ *                           `topk_indices` (min(budget, N) highest, ties to the lower
+ *                           index, ascending) and engine.py:169,183 (per-step clamp)
+ *   hylra_reuse_decode   <- attention.py:229-241 `_subset_attention` and :244-261
+ *                           `sparse_attention` (gather, subset-renormalised softmax)
+ *   hylra_decode_step    <- engine.py:167-197, one decode step of Algorithm 2
+ *                           (PAPER.md:223-247): FULL layers score the cache and publish
+ *                           a selection, REUSE layers inherit the most recent FULL
+ *                           layer's selection (engine.py:173,185-194)
+ *   hylra_overlap_counts <- profiling.py:38-47 `overlap_ratio` numerators |S_i & S_j|
+ *                           feeding profiling.py:126-145 `build_similarity_matrix`
+ *
+ * Conventions
+ *   - Every pointer is caller-owned DEVICE memory unless stated otherwise; the
+ *     library allocates nothing and retains nothing. Work is enqueued on `stream`
+ *     (a cudaStream_t passed as void*) and is asynchronous.
+ *   - Workspaces must be zero-filled once before first use; the kernels leave them
+ *     in the zero state they found them in, so a workspace can be reused by any
+ *     number of calls and CUDA-graph replays on one stream.
+ *   - Stateless and re-entrant: concurrent calls are safe on distinct streams with
+ *     non-aliasing outputs and workspaces.
+ *   - Status codes map 1:1 onto the reference's exception taxonomy
+ *     (pkg/src/layerreuse/errors.py:4-21).
+ */
+#ifndef HYLRA_H
+#define HYLRA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HYLRA_ABI_VERSION 1
+
+enum hylra_status {
+  HYLRA_OK = 0,
+  HYLRA_ERR_CONFIGURATION = 1,     /* ConfigurationError    errors.py:8  */
+  HYLRA_ERR_INVALID_INPUT = 2,     /* InvalidInputError     errors.py:20 */
+  HYLRA_ERR_INVALID_SELECTION = 3, /* InvalidSelectionError errors.py:16 */
+  HYLRA_ERR_NUMERIC_INPUT = 4,     /* NumericInputError     errors.py:12 */
+  HYLRA_ERR_CUDA = 5               /* launch / driver failure            */
+};
+
+enum hylra_dtype { HYLRA_BF16 = 0, HYLRA_F32 = 1 };
+
+/* Device error-flag bits (written into the workspace flag word, see
+ * hylra_read_flags). Set by kernels; cleared by hylra_clear_flags. */
+enum hylra_flag {
+  HYLRA_FLAG_INDEX_OUT_OF_RANGE = 1, /* a REUSE index >= n_valid  (attention.py:256-259) */
+  HYLRA_FLAG_NON_FINITE_SCORE = 2,   /* a NaN/inf selection score (attention.py:43-44)   */
+  HYLRA_FLAG_REFINE_SKIPPED = 4      /* boundary band exceeded the f64 refinement cap    */
+};
+
+/*
+ * Shapes and strides of one KV cache + query tensor set (GQA).
+ *   q   : element [layer][b][qh][i]  at q   + layer*q_stride_layer  + b*q_stride_batch  + qh*d + i
+ *   k,v : element [layer][b][kh][n][i] at k + layer*kv_stride_layer + b*kv_stride_batch + kh*kv_stride_head + n*d + i
+ *   out : fp32 element [layer][b][qh][i] at out + layer*out_stride_layer + b*out_stride_batch + qh*d + i
+ * Query head qh reads KV head qh / (q_heads / kv_heads). All strides are in
+ * elements and must keep every (layer, b, kh) block 16-byte aligned.
+ */
+typedef struct hylra_geometry {
+  int32_t batch;      /* B                                        */
+  int32_t q_heads;    /* Hq                                       */
+  int32_t kv_heads;   /* Hkv; Hq % Hkv == 0; G = Hq / Hkv <= 16   */
+  int32_t head_dim;   /* d in {32, 64, 128}                       */
+  int32_t capacity;   /* N_cap rows allocated per (layer, b, kh)  */
+  int32_t dtype;      /* enum hylra_dtype (q, k and v share it)   */
+  int32_t num_layers; /* L addressable through the strides        */
+  int32_t reserved;
+  int64_t q_stride_layer, q_stride_batch;
+  int64_t kv_stride_layer, kv_stride_batch, kv_stride_head;
+  int64_t out_stride_layer, out_stride_batch;
+} hylra_geometry;
+
+int hylra_abi_version(void);
+const char* hylra_status_string(int status);
+/* Detail message of the last non-OK status returned on the calling thread. */
+const char* hylra_last_error(void);
+/* Host-side count of kernels this library has launched (not graph replays). */
+uint64_t hylra_launch_count(void);
+
+/* Bytes of zero-filled workspace the attention ops need for `n_layers` layer
+ * slots processed in one call over `rows` rows (n_valid for FULL, k for REUSE). */
+size_t hylra_attention_workspace_bytes(const hylra_geometry* g, int n_layers, int rows);
+/* Bytes of workspace hylra_topk_select needs for n_slots * B * (Hkv/sel_group) rows. */
+size_t hylra_select_workspace_bytes(const hylra_geometry* g, int n_slots, int sel_group);
+
+/*
+ * FULL attention for layers layer_ids[0..n_layers) (host array) over rows [0, n_valid).
+ * out   : written for every query head of those layers (geometry out strides).
+ * scores: optional (NULL = do not emit); fp32 [n_layers][B][Hkv][capacity],
+ *         scores[s][b][kh][n] = sum_{g<G} (q_{kh*G+g} . k_n) / sqrt(d).
+ */
+int hylra_full_decode(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                      int n_valid, int n_layers, const int32_t* layer_ids, float* out,
+                      float* scores, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Exact top-min(budget, n_valid) selection per (slot, b, group) row, where a group is
+ * `sel_group` consecutive KV heads whose score rows are summed in head order
+ * (sel_group = 1: per-KV-head sets; sel_group = Hkv: the reference's layer-wide set).
+ * Ties go to the lower index; idx[s][b][grp][0..k_eff) is written ascending (int32).
+ * If q and k are non-NULL (with layer_ids, host array of the scored layers), the
+ * k-th boundary is re-resolved in float64 from the original q/k values, which makes
+ * the set match a float64 evaluation except at float64-level ties.
+ * info (optional, int32 [rows][4]): k_eff, refined candidates, mode, boundary count.
+ */
+int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
+                      int budget, int sel_group, const void* q, const void* k,
+                      const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
+                      void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * REUSE attention for layers layer_ids[0..n_layers) (host array): layer i gathers the
+ * k_eff rows idx[src_slots[i]][b][kh / sel_group][0..k_eff) of its own K/V and runs
+ * the subset-renormalised softmax (attention.py:229-241). Indices >= n_valid are
+ * masked and raise HYLRA_FLAG_INDEX_OUT_OF_RANGE.
+ */
+int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                       int n_valid, int n_layers, const int32_t* layer_ids,
+                       const int32_t* src_slots, const int32_t* idx, int k_stride, int k_eff,
+                       int sel_group, float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Workspace for hylra_decode_step (covers scores, select and attention workspaces). */
+size_t hylra_decode_step_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
+                                         int n_valid, int budget, int sel_group);
+
+/*
+ * One hybrid decode step over all g->num_layers layers (Algorithm 2).
+ * actions: host array of L bytes, 1 = FULL, 0 = REUSE; actions[0] must be FULL.
+ * idx    : int32 [n_full][B][Hkv/sel_group][k_stride]; slot s holds the selection of
+ *          the s-th FULL layer; a REUSE layer's selection is its source slot's.
+ * All FULL layers are scored in one launch, all selections made in one launch and all
+ * REUSE layers gathered in one launch: 3 kernels per step whatever L is.
+ */
+int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                      int n_valid, const uint8_t* actions, int budget, int sel_group,
+                      int refine, float* out, int32_t* idx, int k_stride, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/*
+ * Pairwise selection overlaps: counts[t][r][j][i] = |S(t,i,r) & S(t,j,r)| where
+ * S(t,l,r) = idx[t][l][r][0..k) (ascending, distinct, each < n_tokens).
+ */
+int hylra_overlap_counts(const int32_t* idx, int steps, int layers, int rows, int k,
+                         int k_stride, int n_tokens, int32_t* counts, void* stream);
+
+/* Flag word helpers (the flag word lives in the attention / select workspaces). */
+int hylra_read_flags(const void* ws, int32_t* flags_host, void* stream);
+int hylra_clear_flags(void* ws, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYLRA_H */

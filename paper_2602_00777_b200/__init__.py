@@ -1,0 +1,38 @@
+"""B200-native (sm_100a) HyLRA decode-time hybrid attention.
+
+Drop-in for the layer-policy interface of the reference package `layerreuse`
+(arxiv 2602.00777): FULL layers run a fused split-K flash-decode kernel that also emits
+the per-KV-head selection scores, a top-k SELECT kernel turns those into index sets,
+REUSE layers run a sparse-gather kernel over only the selected rows, and an OVERLAP
+kernel feeds the host-side DP planner. All device work goes through libhylra.so (C ABI,
+include/hylra.h); there is no CPU fallback.
+"""
+from .errors import (ConfigurationError, CudaError, InvalidInputError, InvalidSelectionError,
+                     LayerReuseError, NumericInputError)
+from .policy import (Action, LayerPolicy, dp_optimize, policy_from_actions, static_jump_policy,
+                     validate_policy)
+from .profiling import (SimilarityMatrix, merge_similarity_matrices, overlap_counts,
+                        relative_l2_error, similarity_from_counts)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Action", "LayerPolicy", "dp_optimize", "policy_from_actions", "static_jump_policy",
+    "validate_policy", "SimilarityMatrix", "merge_similarity_matrices", "overlap_counts",
+    "relative_l2_error", "similarity_from_counts", "LayerReuseError", "ConfigurationError",
+    "NumericInputError", "InvalidSelectionError", "InvalidInputError", "CudaError",
+    "TopKSet", "full_attention", "topk_select", "sparse_attention", "HybridDecoder",
+    "decode_step", "hybrid_decode", "run_full_trace", "build_similarity_matrix",
+]
+
+
+def __getattr__(name):
+    # torch-dependent entry points load lazily so the host-only parts import without it
+    if name in ("TopKSet", "full_attention", "topk_select", "sparse_attention", "geometry"):
+        from . import attention
+        return getattr(attention, name)
+    if name in ("HybridDecoder", "decode_step", "hybrid_decode", "run_full_trace",
+                "build_similarity_matrix", "DecodeRunResult", "DecodeTrace", "StepResult"):
+        from . import engine
+        return getattr(engine, name)
+    raise AttributeError(name)

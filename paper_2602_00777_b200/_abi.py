@@ -1,0 +1,132 @@
+"""ctypes binding of libhylra.so — the C ABI declared in include/hylra.h.
+
+The shared library is built in-tree by `__graft_entry__.build()` (nvcc, sm_100a). There
+is no fallback: if the library is missing every op raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import STATUS_TO_ERROR, CudaError, LayerReuseError
+
+LIB_PATH = Path(__file__).resolve().parent / "libhylra.so"
+
+HYLRA_BF16 = 0
+HYLRA_F32 = 1
+
+FLAG_INDEX_OUT_OF_RANGE = 1
+FLAG_NON_FINITE_SCORE = 2
+FLAG_REFINE_SKIPPED = 4
+
+# Every symbol include/hylra.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "hylra_abi_version",
+    "hylra_status_string",
+    "hylra_last_error",
+    "hylra_launch_count",
+    "hylra_attention_workspace_bytes",
+    "hylra_select_workspace_bytes",
+    "hylra_full_decode",
+    "hylra_topk_select",
+    "hylra_reuse_decode",
+    "hylra_decode_step_workspace_bytes",
+    "hylra_decode_step",
+    "hylra_overlap_counts",
+    "hylra_read_flags",
+    "hylra_clear_flags",
+)
+
+
+class Geometry(ctypes.Structure):
+    """Mirror of `hylra_geometry` (include/hylra.h)."""
+
+    _fields_ = [
+        ("batch", ctypes.c_int32),
+        ("q_heads", ctypes.c_int32),
+        ("kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("capacity", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("num_layers", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("q_stride_layer", ctypes.c_int64),
+        ("q_stride_batch", ctypes.c_int64),
+        ("kv_stride_layer", ctypes.c_int64),
+        ("kv_stride_batch", ctypes.c_int64),
+        ("kv_stride_head", ctypes.c_int64),
+        ("out_stride_layer", ctypes.c_int64),
+        ("out_stride_batch", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libhylra.so once; raise loudly when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise CudaError(
+                f"{LIB_PATH} is missing: the sm_100a extension has not been built "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'`)"
+            )
+        l = ctypes.CDLL(os.fspath(LIB_PATH))
+        vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+        gp = ctypes.POINTER(Geometry)
+        l.hylra_abi_version.restype = i32
+        l.hylra_status_string.restype = ctypes.c_char_p
+        l.hylra_status_string.argtypes = [i32]
+        l.hylra_last_error.restype = ctypes.c_char_p
+        l.hylra_launch_count.restype = ctypes.c_uint64
+        l.hylra_attention_workspace_bytes.restype = sz
+        l.hylra_attention_workspace_bytes.argtypes = [gp, i32, i32]
+        l.hylra_select_workspace_bytes.restype = sz
+        l.hylra_select_workspace_bytes.argtypes = [gp, i32, i32]
+        l.hylra_full_decode.restype = i32
+        l.hylra_full_decode.argtypes = [gp, vp, vp, vp, i32, i32, vp, vp, vp, vp, sz, vp]
+        l.hylra_topk_select.restype = i32
+        l.hylra_topk_select.argtypes = [gp, vp, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp,
+                                        sz, vp]
+        l.hylra_reuse_decode.restype = i32
+        l.hylra_reuse_decode.argtypes = [gp, vp, vp, vp, i32, i32, vp, vp, vp, i32, i32, i32,
+                                         vp, vp, sz, vp]
+        l.hylra_decode_step_workspace_bytes.restype = sz
+        l.hylra_decode_step_workspace_bytes.argtypes = [gp, vp, i32, i32, i32]
+        l.hylra_decode_step.restype = i32
+        l.hylra_decode_step.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, vp, vp, i32,
+                                        vp, sz, vp]
+        l.hylra_overlap_counts.restype = i32
+        l.hylra_overlap_counts.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp]
+        l.hylra_read_flags.restype = i32
+        l.hylra_read_flags.argtypes = [vp, vp, vp]
+        l.hylra_clear_flags.restype = i32
+        l.hylra_clear_flags.argtypes = [vp, vp]
+        _ = i64
+        _lib = l
+    return _lib
+
+
+def check(status: int) -> None:
+    """Raise the reference exception class matching a non-zero ABI status."""
+    if status == 0:
+        return
+    detail = lib().hylra_last_error().decode(errors="replace")
+    cls = STATUS_TO_ERROR.get(status, LayerReuseError)
+    raise cls(detail or lib().hylra_status_string(status).decode())
+
+
+def launch_count() -> int:
+    return int(lib().hylra_launch_count())
+
+
+def int32_array(values) -> ctypes.Array:
+    values = list(values)
+    return (ctypes.c_int32 * max(len(values), 1))(*values)
+
+
+def uint8_array(values) -> ctypes.Array:
+    values = list(values)
+    return (ctypes.c_uint8 * max(len(values), 1))(*values)

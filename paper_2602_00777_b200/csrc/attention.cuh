@@ -1,0 +1,561 @@
+// attention.cuh — FULL (split-K flash-decode + fused selection-score emission) and
+// REUSE (sparse-gather subset attention) kernels.
+//
+// Reference semantics (pkg/src/layerreuse/):
+//   FULL  : attention.py:210-226 full_attention — logits = K q / sqrt(d), max-subtracted
+//           softmax, out = w^T V — for every query head, plus engine.py:177-181, the
+//           selection score agg[n] = sum_h logits_h[n].
+//   REUSE : attention.py:229-241 _subset_attention — gather K[idx], V[idx], softmax
+//           renormalised over the subset only.
+//
+// One CTA serves one (layer slot, b, kv-head) pair and a contiguous range of rows
+// (split-K). All G = Hq/Hkv query heads of the group are processed together so each
+// K/V row is read from HBM exactly once per layer. Splits are merged with the
+// log-sum-exp rule by the last CTA of the pair to finish (no second launch).
+#pragma once
+
+#include "common.cuh"
+
+namespace hylra {
+
+constexpr int kMaxSlots = 64;   // layer slots per launch
+constexpr int kTileRows = 64;   // rows per pipeline stage
+constexpr int kConsumerWarps = 4;
+constexpr int kMaxG = 16;
+
+struct AttnParams {
+  const void* q;
+  const void* k;
+  const void* v;
+  float* out;
+  float* scores;        // FULL: [slot][b][kh][cap] or null
+  const int32_t* idx;   // REUSE: [src_slot][b][group][k_stride]
+  float* ws_o;          // [pair][split][G][D]
+  float* ws_ml;         // [pair][split][G][2]
+  int* counters;        // [pair]
+  int* flags;
+  int64_t q_sl, q_sb;
+  int64_t kv_sl, kv_sb, kv_sh;
+  int64_t o_sl, o_sb;
+  int B, Hkv, G, cap;
+  int n_valid;          // valid cache rows
+  int n_rows;           // rows this op attends over: n_valid (FULL) or k_eff (REUSE)
+  int splits;
+  int tiles_per_split;
+  int k_stride, sel_group, n_groups;
+  float scale_log2;     // log2(e) / sqrt(d)
+  float inv_sqrt_d;
+  int layers[kMaxSlots];
+  int src_slot[kMaxSlots];
+};
+
+// ---------------------------------------------------------------------------------
+// Cross-warp merge + split-K combine (shared by both kernel families).
+// sm_m/sm_l: [4][16], sm_o: [4][16][D] partial states of the 4 consumer warps, with
+// m in raw dot units (scaled by scale_log2 inside exp2).
+template <int D>
+__device__ __forceinline__ void merge_and_store(const AttnParams& p, int slot, int b, int kh,
+                                                int split, const float* sm_m,
+                                                const float* sm_l, const float* sm_o,
+                                                int tid, int nthreads, int bar_id) {
+  const int G = p.G;
+  const int layer = p.layers[slot];
+  const int pair = (slot * p.B + b) * p.Hkv + kh;
+  float* out_base = p.out + layer * p.o_sl + b * p.o_sb + (int64_t)(kh * G) * D;
+  const float c = p.scale_log2;
+  if (p.splits == 1) {
+    for (int e = tid; e < G * D; e += nthreads) {
+      const int g = e / D, d = e % D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, sm_m[w * 16 + g]);
+      float acc = 0.f, L = 0.f;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        const float mw = sm_m[w * 16 + g];
+        const float s = (mw == -INFINITY) ? 0.f : exp2f((mw - M) * c);
+        acc += sm_o[(w * 16 + g) * D + d] * s;
+        L += sm_l[w * 16 + g] * s;
+      }
+      out_base[g * D + d] = acc / L;
+    }
+    return;
+  }
+  const int part = pair * p.splits + split;
+  float* wo = p.ws_o + (int64_t)part * G * D;
+  float* wml = p.ws_ml + (int64_t)part * G * 2;
+  for (int e = tid; e < G * D; e += nthreads) {
+    const int g = e / D, d = e % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, sm_m[w * 16 + g]);
+    float acc = 0.f, L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      const float mw = sm_m[w * 16 + g];
+      const float s = (mw == -INFINITY) ? 0.f : exp2f((mw - M) * c);
+      acc += sm_o[(w * 16 + g) * D + d] * s;
+      L += sm_l[w * 16 + g] * s;
+    }
+    wo[g * D + d] = acc;
+    if (d == 0) {
+      wml[g * 2 + 0] = M;
+      wml[g * 2 + 1] = L;
+    }
+  }
+  __threadfence();
+  __shared__ int s_last;
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+  if (tid == 0) {
+    const int prev = atomicAdd(p.counters + pair, 1);
+    s_last = (prev == p.splits - 1);
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+  if (!s_last) return;
+  __threadfence();
+  const float* po = p.ws_o + (int64_t)pair * p.splits * G * D;
+  const float* pml = p.ws_ml + (int64_t)pair * p.splits * G * 2;
+  for (int e = tid; e < G * D; e += nthreads) {
+    const int g = e / D, d = e % D;
+    float M = -INFINITY;
+    for (int s = 0; s < p.splits; ++s) M = fmaxf(M, __ldcg(pml + (s * G + g) * 2));
+    float acc = 0.f, L = 0.f;
+    for (int s = 0; s < p.splits; ++s) {
+      const float ms = __ldcg(pml + (s * G + g) * 2);
+      const float sc = (ms == -INFINITY) ? 0.f : exp2f((ms - M) * c);
+      acc += __ldcg(po + (int64_t)(s * G + g) * D + d) * sc;
+      L += __ldcg(pml + (s * G + g) * 2 + 1) * sc;
+    }
+    out_base[g * D + d] = acc / L;
+  }
+  if (tid == 0) p.counters[pair] = 0;  // leave the workspace zeroed for the next call
+}
+
+// ---------------------------------------------------------------------------------
+// Tensor-core path (bf16 K/V/q). 4 consumer warps + 1 producer warp.
+// Stage = 64 K rows + 64 V rows in 128B-swizzled boxes of 64 columns (the TMA
+// SWIZZLE_128B layout): element (r, col) of a box lives at
+//   r*128 + (((col/8) ^ (r%8)) * 16) + (col%8)*2.
+// Warp w owns rows 16w..16w+15 of every stage: S = Q K^T via mma.m16n8k16 with the G
+// group heads packed into the M=16 rows (rows >= G are zero), online softmax in
+// registers, P re-used as the A operand of O += P V (FA2 register layout).
+template <int D>
+struct MmaSmem {
+  static constexpr int kBoxes = D / 64;
+  static constexpr int kTileBytes = kTileRows * D * 2;          // one of K or V
+  static constexpr int kStageBytes = 2 * kTileBytes;
+};
+
+__device__ __forceinline__ uint32_t swz_addr(uint32_t tile_base, int r, int chunk) {
+  // chunk = 16-byte column chunk index over the full row (0 .. D/8-1)
+  return tile_base + (chunk >> 3) * (kTileRows * 128) + r * 128 + (((chunk & 7) ^ (r & 7)) << 4);
+}
+
+template <int D, bool GATHER, bool GBIG, int STAGES>
+__global__ void __launch_bounds__(160, 2)
+    attn_mma_kernel(const __grid_constant__ CUtensorMap tmk,
+                    const __grid_constant__ CUtensorMap tmv, const AttnParams p) {
+  using SM = MmaSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * SM::kStageBytes);
+  uint64_t* empty_bar = full_bar + STAGES;
+
+  const int split = blockIdx.x;
+  const int kh = blockIdx.y;
+  const int slot = blockIdx.z / p.B;
+  const int b = blockIdx.z % p.B;
+  const int layer = p.layers[slot];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int n_tiles = (p.n_rows + kTileRows - 1) / kTileRows;
+  const int t_begin = split * p.tiles_per_split;
+  const int t_end = min(n_tiles, t_begin + p.tiles_per_split);
+  const int n_my = t_end - t_begin;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar + s, GATHER ? 32 : 1);
+      mbar_init(empty_bar + s, kConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------- producer warp
+    if constexpr (!GATHER) {
+      if (lane == 0) {
+        tma_prefetch_desc(&tmk);
+        tma_prefetch_desc(&tmv);
+        const uint64_t pol = l2_policy_evict_first();
+        for (int i = 0; i < n_my; ++i) {
+          const int s = i % STAGES;
+          mbar_wait(empty_bar + s, ((i / STAGES) & 1) ^ 1);
+          uint8_t* kt = smem + s * SM::kStageBytes;
+          uint8_t* vt = kt + SM::kTileBytes;
+          mbar_arrive_expect_tx(full_bar + s, SM::kStageBytes);
+          const int row = (t_begin + i) * kTileRows;
+#pragma unroll
+          for (int bx = 0; bx < SM::kBoxes; ++bx) {
+            tma_load_5d(kt + bx * kTileRows * 128, &tmk, full_bar + s, bx * 64, row, kh, b, layer,
+                        pol);
+            tma_load_5d(vt + bx * kTileRows * 128, &tmv, full_bar + s, bx * 64, row, kh, b, layer,
+                        pol);
+          }
+        }
+      }
+    } else {
+      // gather: every lane copies 2 rows (K and V) per stage with 16-byte cp.async
+      const __nv_bfloat16* kbase = reinterpret_cast<const __nv_bfloat16*>(p.k) +
+                                   layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+      const __nv_bfloat16* vbase = reinterpret_cast<const __nv_bfloat16*>(p.v) +
+                                   layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+      const int32_t* ib = p.idx + ((int64_t)(p.src_slot[slot] * p.B + b) * p.n_groups +
+                                   kh / p.sel_group) * p.k_stride;
+      for (int i = 0; i < n_my; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(empty_bar + s, ((i / STAGES) & 1) ^ 1);
+        const uint32_t kt = smem_u32(smem + s * SM::kStageBytes);
+        const uint32_t vt = kt + SM::kTileBytes;
+        const int pos0 = (t_begin + i) * kTileRows;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int r = lane + 32 * rr;
+          const int pos = pos0 + r;
+          const bool valid = pos < p.n_rows;
+          int row = valid ? __ldg(ib + pos) : 0;
+          if (row < 0 || row >= p.n_valid) {
+            if (valid) atomicOr(p.flags, 1);
+            row = 0;
+          }
+          const __nv_bfloat16* ks = kbase + (int64_t)row * D;
+          const __nv_bfloat16* vs = vbase + (int64_t)row * D;
+#pragma unroll
+          for (int ch = 0; ch < D / 8; ++ch) {
+            const uint32_t off = swz_addr(0, r, ch);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kt + off),
+                         "l"(ks + ch * 8), "r"(valid ? 16 : 0)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vt + off),
+                         "l"(vs + ch * 8), "r"(valid ? 16 : 0)
+                         : "memory");
+          }
+        }
+        cp_async_mbar_arrive_noinc(full_bar + s);
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------- consumer warps
+  const int g = lane >> 2;  // row of the m16n8 fragments (query head within the group)
+  const int t = lane & 3;
+  const int G = p.G;
+  const float c = p.scale_log2;
+
+  // Q A-fragments for all D/16 k-steps.
+  uint32_t qa[D / 16][4];
+  {
+    const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(p.q) + layer * p.q_sl +
+                              b * p.q_sb + (int64_t)(kh * G) * D;
+    const bool r0ok = g < G;
+    const bool r1ok = GBIG && (g + 8) < G;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      const int c0 = ks * 16 + 2 * t;
+      qa[ks][0] = r0ok ? *reinterpret_cast<const uint32_t*>(qb + g * D + c0) : 0u;
+      qa[ks][2] = r0ok ? *reinterpret_cast<const uint32_t*>(qb + g * D + c0 + 8) : 0u;
+      qa[ks][1] = r1ok ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * D + c0) : 0u;
+      qa[ks][3] = r1ok ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * D + c0 + 8) : 0u;
+    }
+  }
+
+  float o[D / 8][4];
+#pragma unroll
+  for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  float* score_row = nullptr;
+  if (!GATHER && p.scores != nullptr)
+    score_row = p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + kh) * p.cap;
+
+  const int rbase = warp * 16;
+  // ldmatrix lane roles
+  const int lk_row = rbase + (lane & 7) + ((lane >> 4) << 3);   // K: matrices (n0,k0)(n0,k1)(n1,k0)(n1,k1)
+  const int lk_chk = (lane >> 3) & 1;
+  const int lv_row = rbase + (lane & 7) + (((lane >> 3) & 1) << 3);  // V: (k0,n)(k1,n)(k0,n+1)(k1,n+1)
+  const int lv_chk = lane >> 4;
+
+  for (int i = 0; i < n_my; ++i) {
+    const int s = i % STAGES;
+    mbar_wait(full_bar + s, (i / STAGES) & 1);
+    const uint32_t kt = smem_u32(smem + s * SM::kStageBytes);
+    const uint32_t vt = kt + SM::kTileBytes;
+    const int row0 = (t_begin + i) * kTileRows + rbase;  // first row of this warp's slice
+
+    // ---- S = Q K^T (16 x 16 per warp)
+    float sacc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(swz_addr(kt, lk_row, 2 * ks + lk_chk), b0, b1, b2, b3);
+      mma_bf16_16816(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+      mma_bf16_16816(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+    }
+
+    // ---- mask rows past the end of the range
+    const bool tail = row0 + 16 > p.n_rows;
+    if (tail) {
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (row0 + nt * 8 + 2 * t + e >= p.n_rows) {
+            sacc[nt][e] = -INFINITY;
+            sacc[nt][2 + e] = -INFINITY;
+          }
+        }
+    }
+
+    // ---- selection score: sum over the group's heads (rows) of q.k, times 1/sqrt(d)
+    if (!GATHER && score_row != nullptr) {
+      float v00 = sacc[0][0], v01 = sacc[0][1], v10 = sacc[1][0], v11 = sacc[1][1];
+      if (GBIG) {
+        v00 += sacc[0][2];
+        v01 += sacc[0][3];
+        v10 += sacc[1][2];
+        v11 += sacc[1][3];
+      }
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        v00 += __shfl_xor_sync(0xffffffffu, v00, off);
+        v01 += __shfl_xor_sync(0xffffffffu, v01, off);
+        v10 += __shfl_xor_sync(0xffffffffu, v10, off);
+        v11 += __shfl_xor_sync(0xffffffffu, v11, off);
+      }
+      if (g == 0) {
+        const int n0 = row0 + 2 * t;
+        const int n1 = row0 + 8 + 2 * t;
+        if (!tail) {
+          *reinterpret_cast<float2*>(score_row + n0) =
+              make_float2(v00 * p.inv_sqrt_d, v01 * p.inv_sqrt_d);
+          *reinterpret_cast<float2*>(score_row + n1) =
+              make_float2(v10 * p.inv_sqrt_d, v11 * p.inv_sqrt_d);
+        } else {
+          if (n0 < p.n_rows) score_row[n0] = v00 * p.inv_sqrt_d;
+          if (n0 + 1 < p.n_rows) score_row[n0 + 1] = v01 * p.inv_sqrt_d;
+          if (n1 < p.n_rows) score_row[n1] = v10 * p.inv_sqrt_d;
+          if (n1 + 1 < p.n_rows) score_row[n1 + 1] = v11 * p.inv_sqrt_d;
+        }
+      }
+    }
+
+    // ---- online softmax (row g, and row g+8 when G > 8)
+    uint32_t pa0, pa1, pa2, pa3;
+    {
+      float mx = fmaxf(fmaxf(sacc[0][0], sacc[0][1]), fmaxf(sacc[1][0], sacc[1][1]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float mn = fmaxf(m0, mx);
+      const float mu = (mn == -INFINITY) ? 0.f : mn;
+      const float alpha = fast_exp2((m0 - mu) * c);
+      const float mc = mu * c;
+      const float p00 = fast_exp2(fmaf(sacc[0][0], c, -mc));
+      const float p01 = fast_exp2(fmaf(sacc[0][1], c, -mc));
+      const float p10 = fast_exp2(fmaf(sacc[1][0], c, -mc));
+      const float p11 = fast_exp2(fmaf(sacc[1][1], c, -mc));
+      l0 = fmaf(l0, alpha, (p00 + p01) + (p10 + p11));
+      m0 = mn;
+#pragma unroll
+      for (int j = 0; j < D / 8; ++j) {
+        o[j][0] *= alpha;
+        o[j][1] *= alpha;
+      }
+      pa0 = pack_bf16(p00, p01);
+      pa2 = pack_bf16(p10, p11);
+    }
+    if (GBIG) {
+      float mx = fmaxf(fmaxf(sacc[0][2], sacc[0][3]), fmaxf(sacc[1][2], sacc[1][3]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float mn = fmaxf(m1, mx);
+      const float mu = (mn == -INFINITY) ? 0.f : mn;
+      const float alpha = fast_exp2((m1 - mu) * c);
+      const float mc = mu * c;
+      const float p00 = fast_exp2(fmaf(sacc[0][2], c, -mc));
+      const float p01 = fast_exp2(fmaf(sacc[0][3], c, -mc));
+      const float p10 = fast_exp2(fmaf(sacc[1][2], c, -mc));
+      const float p11 = fast_exp2(fmaf(sacc[1][3], c, -mc));
+      l1 = fmaf(l1, alpha, (p00 + p01) + (p10 + p11));
+      m1 = mn;
+#pragma unroll
+      for (int j = 0; j < D / 8; ++j) {
+        o[j][2] *= alpha;
+        o[j][3] *= alpha;
+      }
+      pa1 = pack_bf16(p00, p01);
+      pa3 = pack_bf16(p10, p11);
+    } else {
+      pa1 = 0u;
+      pa3 = 0u;
+    }
+
+    // ---- O += P V
+#pragma unroll
+    for (int j = 0; j < D / 8; j += 2) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(swz_addr(vt, lv_row, j + lv_chk), b0, b1, b2, b3);
+      mma_bf16_16816(o[j], pa0, pa1, pa2, pa3, b0, b1);
+      mma_bf16_16816(o[j + 1], pa0, pa1, pa2, pa3, b2, b3);
+    }
+
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar + s);
+  }
+
+  // ---- merge the 4 warps through shared memory (pipeline buffers are drained)
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  float* sm_m = reinterpret_cast<float*>(smem);
+  float* sm_l = sm_m + kConsumerWarps * 16;
+  float* sm_o = sm_l + kConsumerWarps * 16;
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  if (GBIG) {
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  }
+  if (t == 0) {
+    sm_m[warp * 16 + g] = m0;
+    sm_l[warp * 16 + g] = l0;
+    sm_m[warp * 16 + g + 8] = GBIG ? m1 : -INFINITY;
+    sm_l[warp * 16 + g + 8] = GBIG ? l1 : 0.f;
+  }
+#pragma unroll
+  for (int j = 0; j < D / 8; ++j) {
+    *reinterpret_cast<float2*>(sm_o + (warp * 16 + g) * D + 8 * j + 2 * t) =
+        make_float2(o[j][0], o[j][1]);
+    if (GBIG)
+      *reinterpret_cast<float2*>(sm_o + (warp * 16 + g + 8) * D + 8 * j + 2 * t) =
+          make_float2(o[j][2], o[j][3]);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  merge_and_store<D>(p, slot, b, kh, split, sm_m, sm_l, sm_o, threadIdx.x, 128, 1);
+}
+
+// ---------------------------------------------------------------------------------
+// CUDA-core path: fp32 caches (the reference-precision path, tolerance 1e-3) and any
+// shape the tensor-core path does not cover (d = 32, bf16 with G > 16 is rejected).
+// Each warp walks rows r = split_begin + warp, +4, ...; lane holds d-slice
+// lane + 32 j, dot products are warp-reduced, softmax state is per head.
+template <typename T, int D, int GMAX, bool GATHER>
+__global__ void __launch_bounds__(128)
+    attn_simt_kernel(const AttnParams p) {
+  constexpr int J = D / 32;
+  __shared__ float sm_m[kConsumerWarps * 16];
+  __shared__ float sm_l[kConsumerWarps * 16];
+  __shared__ float sm_o[kConsumerWarps * 16 * D];
+
+  const int split = blockIdx.x;
+  const int kh = blockIdx.y;
+  const int slot = blockIdx.z / p.B;
+  const int b = blockIdx.z % p.B;
+  const int layer = p.layers[slot];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int G = p.G;
+  const float c = p.scale_log2;
+
+  const int r_begin = split * p.tiles_per_split * kTileRows;
+  const int r_end = min(p.n_rows, r_begin + p.tiles_per_split * kTileRows);
+
+  const T* qb = reinterpret_cast<const T*>(p.q) + layer * p.q_sl + b * p.q_sb +
+                (int64_t)(kh * G) * D;
+  const T* kb = reinterpret_cast<const T*>(p.k) + layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+  const T* vb = reinterpret_cast<const T*>(p.v) + layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+  const int32_t* ib = nullptr;
+  if (GATHER)
+    ib = p.idx + ((int64_t)(p.src_slot[slot] * p.B + b) * p.n_groups + kh / p.sel_group) *
+                     p.k_stride;
+  float* score_row = nullptr;
+  if (!GATHER && p.scores != nullptr)
+    score_row = p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + kh) * p.cap;
+
+  float qv[GMAX][J];
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g)
+#pragma unroll
+    for (int j = 0; j < J; ++j) qv[g][j] = (g < G) ? to_f32(qb[g * D + lane + 32 * j]) : 0.f;
+
+  float m[GMAX], l[GMAX], acc[GMAX][J];
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[g][j] = 0.f;
+  }
+
+  for (int r = r_begin + warp; r < r_end; r += kConsumerWarps) {
+    int row = r;
+    if (GATHER) {
+      row = __ldg(ib + r);
+      if (row < 0 || row >= p.n_valid) {
+        if (lane == 0) atomicOr(p.flags, 1);
+        continue;
+      }
+    }
+    float kv[J], vv[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      kv[j] = to_f32(kb[(int64_t)row * D + lane + 32 * j]);
+      vv[j] = to_f32(vb[(int64_t)row * D + lane + 32 * j]);
+    }
+    float dot[GMAX];
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      float s = 0.f;
+#pragma unroll
+      for (int j = 0; j < J; ++j) s = fmaf(qv[g][j], kv[j], s);
+      dot[g] = (g < G) ? warp_sum(s) : 0.f;
+    }
+    if (score_row != nullptr && lane == 0) {
+      float agg = 0.f;
+#pragma unroll
+      for (int g = 0; g < GMAX; ++g) agg += dot[g] * p.inv_sqrt_d;
+      score_row[r] = agg;
+    }
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      if (g < G) {
+        const float mn = fmaxf(m[g], dot[g]);
+        const float alpha = exp2f((m[g] - mn) * c);
+        const float pr = exp2f((dot[g] - mn) * c);
+        l[g] = fmaf(l[g], alpha, pr);
+        m[g] = mn;
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[g][j] = fmaf(acc[g][j], alpha, pr * vv[j]);
+      }
+    }
+  }
+
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g) {
+    if (g < G) {
+      if (lane == 0) {
+        sm_m[warp * 16 + g] = m[g];
+        sm_l[warp * 16 + g] = l[g];
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) sm_o[(warp * 16 + g) * D + lane + 32 * j] = acc[g][j];
+    }
+  }
+  __syncthreads();
+  merge_and_store<D>(p, slot, b, kh, split, sm_m, sm_l, sm_o, threadIdx.x, 128, 1);
+}
+
+}  // namespace hylra

@@ -1,0 +1,509 @@
+// hylra_abi.cu — extern "C" entry points of libhylra.so (declared in include/hylra.h).
+//
+// Host side of the drop-in boundary: validates shapes (ConfigurationError /
+// InvalidInputError, reference errors.py:4-21), picks the kernel family, sizes the
+// split-K grid for 148 SMs, encodes the TMA tensor maps and enqueues on the caller's
+// stream. No allocation, no synchronisation, no retained state besides cached
+// function attributes.
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/hylra.h"
+#include "attention.cuh"
+#include "overlap.cuh"
+#include "select.cuh"
+
+using namespace hylra;
+
+namespace {
+
+constexpr int kNumSMs = 148;
+constexpr size_t kHeader = 256;
+
+thread_local char g_err[512] = "";
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(HYLRA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HYLRA_OK;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int scores_row_stride(const hylra_geometry* g) { return (g->capacity + 7) & ~7; }
+
+int check_geometry(const hylra_geometry* g) {
+  if (g == nullptr) return fail(HYLRA_ERR_CONFIGURATION, "geometry is NULL");
+  if (g->batch < 1 || g->q_heads < 1 || g->kv_heads < 1 || g->capacity < 1 || g->num_layers < 1)
+    return fail(HYLRA_ERR_CONFIGURATION, "non-positive dimension in geometry");
+  if (g->q_heads % g->kv_heads != 0)
+    return fail(HYLRA_ERR_CONFIGURATION, "q_heads %d is not a multiple of kv_heads %d", g->q_heads,
+                g->kv_heads);
+  const int G = g->q_heads / g->kv_heads;
+  if (G > kMaxG) return fail(HYLRA_ERR_CONFIGURATION, "group size %d exceeds %d", G, kMaxG);
+  if (g->head_dim != 32 && g->head_dim != 64 && g->head_dim != 128)
+    return fail(HYLRA_ERR_CONFIGURATION, "head_dim %d not in {32, 64, 128}", g->head_dim);
+  if (g->dtype != HYLRA_BF16 && g->dtype != HYLRA_F32)
+    return fail(HYLRA_ERR_CONFIGURATION, "unknown dtype %d", g->dtype);
+  return HYLRA_OK;
+}
+
+int choose_splits(int pairs, int tiles) {
+  const int target = kNumSMs * 2 * 8;  // ~8 waves of 2 CTAs per SM
+  int s = (target + pairs - 1) / pairs;
+  s = std::min(s, std::max(1, tiles / 4));
+  s = std::max(1, std::min(s, tiles));
+  const int tps = (tiles + s - 1) / s;
+  return (tiles + tps - 1) / tps;
+}
+
+struct AttnLayout {
+  int pairs, splits, tiles, tps;
+  size_t off_counters, off_ml, off_o, total;
+};
+
+AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows) {
+  AttnLayout a{};
+  const int G = g->q_heads / g->kv_heads;
+  a.pairs = n_layers * g->batch * g->kv_heads;
+  a.tiles = std::max(1, (rows + kTileRows - 1) / kTileRows);
+  a.splits = choose_splits(a.pairs, a.tiles);
+  a.tps = (a.tiles + a.splits - 1) / a.splits;
+  a.off_counters = kHeader;
+  a.off_ml = align_up(a.off_counters + sizeof(int) * a.pairs, 256);
+  a.off_o = align_up(a.off_ml + sizeof(float) * 2 * (size_t)a.pairs * a.splits * G, 256);
+  a.total = align_up(a.off_o + sizeof(float) * (size_t)a.pairs * a.splits * G * g->head_dim, 256);
+  if (a.splits == 1) a.total = align_up(a.off_counters + sizeof(int) * a.pairs, 256);
+  return a;
+}
+
+// ------------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+int encode_kv_map(CUtensorMap* map, const hylra_geometry* g, const void* base) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return fail(HYLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int D = g->head_dim;
+  const cuuint64_t es = 2;  // bf16
+  cuuint64_t dims[5] = {(cuuint64_t)D, (cuuint64_t)g->capacity, (cuuint64_t)g->kv_heads,
+                        (cuuint64_t)g->batch, (cuuint64_t)g->num_layers};
+  // strides of dims 1..4 in bytes; size-1 dims get a harmless dense stride
+  cuuint64_t st[4];
+  st[0] = (cuuint64_t)D * es;
+  st[1] = g->kv_heads > 1 ? (cuuint64_t)g->kv_stride_head * es : st[0] * g->capacity;
+  st[2] = g->batch > 1 ? (cuuint64_t)g->kv_stride_batch * es : st[1] * g->kv_heads;
+  st[3] = g->num_layers > 1 ? (cuuint64_t)g->kv_stride_layer * es : st[2] * g->batch;
+  for (int i = 0; i < 4; ++i)
+    if (st[i] % 16 != 0 || st[i] >= (1ull << 40))
+      return fail(HYLRA_ERR_CONFIGURATION, "KV stride %d (%llu B) not TMA-compatible", i,
+                  (unsigned long long)st[i]);
+  cuuint32_t box[5] = {64, (cuuint32_t)kTileRows, 1, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, st, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HYLRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return HYLRA_OK;
+}
+
+// ------------------------------------------------------------------ kernel tables
+template <int D, bool GATHER, bool GBIG>
+constexpr int mma_stages() {
+  return D == 128 ? 3 : 5;
+}
+template <int D, bool GATHER, bool GBIG>
+size_t mma_smem_bytes() {
+  return (size_t)mma_stages<D, GATHER, GBIG>() * MmaSmem<D>::kStageBytes + 1024 + 256;
+}
+
+template <int D, bool GATHER, bool GBIG>
+cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const AttnParams& p) {
+  constexpr int S = mma_stages<D, GATHER, GBIG>();
+  auto kern = attn_mma_kernel<D, GATHER, GBIG, S>;
+  const size_t smem = mma_smem_bytes<D, GATHER, GBIG>();
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  kern<<<grid, 160, smem, st>>>(tk, tv, p);
+  return cudaGetLastError();
+}
+
+template <typename T, int D, int GM, bool GATHER>
+cudaError_t launch_simt(dim3 grid, cudaStream_t st, const AttnParams& p) {
+  attn_simt_kernel<T, D, GM, GATHER><<<grid, 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, bool GATHER>
+cudaError_t dispatch_simt(int D, int G, dim3 grid, cudaStream_t st, const AttnParams& p) {
+#define HY_SIMT_D(DD)                                                  \
+  if (D == DD) {                                                       \
+    if (G <= 1) return launch_simt<T, DD, 1, GATHER>(grid, st, p);     \
+    if (G <= 4) return launch_simt<T, DD, 4, GATHER>(grid, st, p);     \
+    if (G <= 8) return launch_simt<T, DD, 8, GATHER>(grid, st, p);     \
+    return launch_simt<T, DD, 16, GATHER>(grid, st, p);                \
+  }
+  HY_SIMT_D(32)
+  HY_SIMT_D(64)
+  HY_SIMT_D(128)
+#undef HY_SIMT_D
+  return cudaErrorInvalidValue;
+}
+
+bool use_mma_path(const hylra_geometry* g) {
+  return g->dtype == HYLRA_BF16 && (g->head_dim == 64 || g->head_dim == 128);
+}
+
+int launch_attention(const hylra_geometry* g, bool gather, const void* q, const void* k,
+                     const void* v, int n_valid, int n_rows, int n_layers,
+                     const int32_t* layer_ids, const int32_t* src_slots, const int32_t* idx,
+                     int k_stride, int sel_group, float* out, float* scores, void* ws,
+                     size_t ws_bytes, int* flags, cudaStream_t st) {
+  if (int e = check_geometry(g)) return e;
+  if (n_layers < 1 || n_layers > kMaxSlots)
+    return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", n_layers, kMaxSlots);
+  if (n_valid < 1 || n_valid > g->capacity)
+    return fail(HYLRA_ERR_INVALID_INPUT, "n_valid %d not in [1, capacity=%d]", n_valid,
+                g->capacity);
+  if (n_rows < 1) return fail(HYLRA_ERR_INVALID_INPUT, "no rows to attend over");
+  if (!q || !k || !v || !out || !ws || !layer_ids)
+    return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  const AttnLayout lay = attn_layout(g, n_layers, n_rows);
+  if (ws_bytes < lay.total)
+    return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, lay.total);
+  const int G = g->q_heads / g->kv_heads;
+  AttnParams p{};
+  p.q = q; p.k = k; p.v = v; p.out = out; p.scores = scores; p.idx = idx;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  p.counters = reinterpret_cast<int*>(w + lay.off_counters);
+  p.ws_ml = reinterpret_cast<float*>(w + lay.off_ml);
+  p.ws_o = reinterpret_cast<float*>(w + lay.off_o);
+  p.flags = flags;
+  p.q_sl = g->q_stride_layer; p.q_sb = g->q_stride_batch;
+  p.kv_sl = g->kv_stride_layer; p.kv_sb = g->kv_stride_batch; p.kv_sh = g->kv_stride_head;
+  p.o_sl = g->out_stride_layer; p.o_sb = g->out_stride_batch;
+  p.B = g->batch; p.Hkv = g->kv_heads; p.G = G;
+  p.cap = scores_row_stride(g);
+  p.n_valid = n_valid; p.n_rows = n_rows;
+  p.splits = lay.splits; p.tiles_per_split = lay.tps;
+  p.k_stride = k_stride; p.sel_group = sel_group > 0 ? sel_group : 1;
+  p.n_groups = g->kv_heads / p.sel_group;
+  p.inv_sqrt_d = (float)(1.0 / std::sqrt((double)g->head_dim));
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)g->head_dim));
+  for (int i = 0; i < n_layers; ++i) {
+    if (layer_ids[i] < 0 || layer_ids[i] >= g->num_layers)
+      return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", layer_ids[i]);
+    p.layers[i] = layer_ids[i];
+    p.src_slot[i] = src_slots ? src_slots[i] : 0;
+  }
+  dim3 grid(lay.splits, g->kv_heads, g->batch * n_layers);
+  cudaError_t ce;
+  if (use_mma_path(g)) {
+    CUtensorMap tk{}, tv{};
+    if (!gather) {
+      if (int e = encode_kv_map(&tk, g, k)) return e;
+      if (int e = encode_kv_map(&tv, g, v)) return e;
+    }
+    const bool big = G > 8;
+    if (g->head_dim == 128) {
+      if (gather) ce = big ? launch_mma<128, true, true>(grid, st, tk, tv, p)
+                           : launch_mma<128, true, false>(grid, st, tk, tv, p);
+      else ce = big ? launch_mma<128, false, true>(grid, st, tk, tv, p)
+                    : launch_mma<128, false, false>(grid, st, tk, tv, p);
+    } else {
+      if (gather) ce = big ? launch_mma<64, true, true>(grid, st, tk, tv, p)
+                           : launch_mma<64, true, false>(grid, st, tk, tv, p);
+      else ce = big ? launch_mma<64, false, true>(grid, st, tk, tv, p)
+                    : launch_mma<64, false, false>(grid, st, tk, tv, p);
+    }
+  } else if (g->dtype == HYLRA_F32) {
+    ce = gather ? dispatch_simt<float, true>(g->head_dim, G, grid, st, p)
+                : dispatch_simt<float, false>(g->head_dim, G, grid, st, p);
+  } else {
+    ce = gather ? dispatch_simt<__nv_bfloat16, true>(g->head_dim, G, grid, st, p)
+                : dispatch_simt<__nv_bfloat16, false>(g->head_dim, G, grid, st, p);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_check(ce, gather ? "reuse_decode launch" : "full_decode launch");
+}
+
+size_t select_smem_bytes(int n_valid, bool cache) {
+  size_t b = 2048 * sizeof(float) + kBandCap * sizeof(float);
+  if (cache) b += ((n_valid + 3) & ~3) * sizeof(float);
+  return b;
+}
+
+int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
+                  int budget, int sel_group, const void* q, const void* k,
+                  const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
+                  int* flags, cudaStream_t st) {
+  if (int e = check_geometry(g)) return e;
+  if (budget < 1) return fail(HYLRA_ERR_INVALID_INPUT, "budget must be >= 1, got %d", budget);
+  if (n_slots < 1 || n_slots > kMaxSlots)
+    return fail(HYLRA_ERR_CONFIGURATION, "n_slots %d not in [1, %d]", n_slots, kMaxSlots);
+  if (n_valid < 1 || n_valid > g->capacity)
+    return fail(HYLRA_ERR_INVALID_INPUT, "n_valid %d not in [1, capacity=%d]", n_valid,
+                g->capacity);
+  if (sel_group < 1 || g->kv_heads % sel_group != 0)
+    return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads %d", sel_group,
+                g->kv_heads);
+  const int k_eff = std::min(budget, n_valid);
+  if (k_stride < k_eff)
+    return fail(HYLRA_ERR_CONFIGURATION, "k_stride %d < selection size %d", k_stride, k_eff);
+  if (!scores || !idx) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  SelectParams p{};
+  p.scores = scores; p.idx = idx; p.info = info; p.flags = flags;
+  p.q = (q && k && layer_ids) ? q : nullptr;
+  p.k = k;
+  p.dtype = g->dtype;
+  p.q_sl = g->q_stride_layer; p.q_sb = g->q_stride_batch;
+  p.kv_sl = g->kv_stride_layer; p.kv_sb = g->kv_stride_batch; p.kv_sh = g->kv_stride_head;
+  p.B = g->batch; p.Hkv = g->kv_heads; p.G = g->q_heads / g->kv_heads; p.D = g->head_dim;
+  p.sel_group = sel_group; p.n_groups = g->kv_heads / sel_group;
+  p.n_valid = n_valid; p.k_eff = k_eff; p.k_stride = k_stride;
+  p.row_stride = scores_row_stride(g);
+  p.cache_row = n_valid <= kCacheMax;
+  p.tau_rel = 1.0f / 4096.0f;
+  for (int i = 0; i < n_slots; ++i) {
+    const int l = layer_ids ? layer_ids[i] : 0;
+    if (l < 0 || l >= g->num_layers)
+      return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", l);
+    p.layers[i] = l;
+  }
+  const size_t smem = select_smem_bytes(n_valid, p.cache_row);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(topk_select_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)select_smem_bytes(kCacheMax, true));
+  });
+  if (attr_err != cudaSuccess) return cuda_check(attr_err, "select attribute");
+  dim3 grid(p.n_groups, g->batch, n_slots);
+  topk_select_kernel<<<grid, kSelThreads, smem, st>>>(p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_check(cudaGetLastError(), "topk_select launch");
+}
+
+struct StepLayout {
+  std::vector<int32_t> full_ids, reuse_ids, reuse_src;
+  int k_eff, n_groups;
+  size_t off_scores, off_attn, attn_bytes, total;
+};
+
+int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, int budget,
+                int sel_group, StepLayout* s) {
+  if (int e = check_geometry(g)) return e;
+  if (!actions) return fail(HYLRA_ERR_CONFIGURATION, "actions is NULL");
+  if (actions[0] != 1)
+    return fail(HYLRA_ERR_INVALID_INPUT, "the first layer of a policy must run full attention");
+  if (budget < 1) return fail(HYLRA_ERR_INVALID_INPUT, "budget must be >= 1, got %d", budget);
+  if (n_valid < 1 || n_valid > g->capacity)
+    return fail(HYLRA_ERR_INVALID_INPUT, "n_valid %d not in [1, capacity]", n_valid);
+  if (sel_group < 1 || g->kv_heads % sel_group != 0)
+    return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads", sel_group);
+  s->full_ids.clear(); s->reuse_ids.clear(); s->reuse_src.clear();
+  int cur = -1;
+  for (int l = 0; l < g->num_layers; ++l) {
+    if (actions[l]) {
+      cur = (int)s->full_ids.size();
+      s->full_ids.push_back(l);
+    } else {
+      s->reuse_ids.push_back(l);
+      s->reuse_src.push_back(cur);
+    }
+  }
+  if ((int)s->full_ids.size() > kMaxSlots || (int)s->reuse_ids.size() > kMaxSlots)
+    return fail(HYLRA_ERR_CONFIGURATION, "more than %d layers of one kind", kMaxSlots);
+  s->k_eff = std::min(budget, n_valid);
+  s->n_groups = g->kv_heads / sel_group;
+  const size_t nf = s->full_ids.size();
+  s->off_scores = kHeader;
+  const size_t scores_b = sizeof(float) * nf * g->batch * g->kv_heads * scores_row_stride(g);
+  s->off_attn = align_up(s->off_scores + scores_b, 256);
+  size_t a = attn_layout(g, (int)nf, n_valid).total;
+  if (!s->reuse_ids.empty())
+    a = std::max(a, attn_layout(g, (int)s->reuse_ids.size(), s->k_eff).total);
+  s->attn_bytes = a;
+  s->total = s->off_attn + a;
+  return HYLRA_OK;
+}
+
+}  // namespace
+
+// ======================================================================== extern "C"
+extern "C" {
+
+int hylra_abi_version(void) { return HYLRA_ABI_VERSION; }
+
+const char* hylra_status_string(int status) {
+  switch (status) {
+    case HYLRA_OK: return "ok";
+    case HYLRA_ERR_CONFIGURATION: return "ConfigurationError";
+    case HYLRA_ERR_INVALID_INPUT: return "InvalidInputError";
+    case HYLRA_ERR_INVALID_SELECTION: return "InvalidSelectionError";
+    case HYLRA_ERR_NUMERIC_INPUT: return "NumericInputError";
+    case HYLRA_ERR_CUDA: return "CudaError";
+    default: return "unknown status";
+  }
+}
+
+const char* hylra_last_error(void) { return g_err; }
+
+uint64_t hylra_launch_count(void) { return g_launches.load(); }
+
+size_t hylra_attention_workspace_bytes(const hylra_geometry* g, int n_layers, int rows) {
+  if (check_geometry(g) || n_layers < 1) return 0;
+  return attn_layout(g, n_layers, std::max(rows, 1)).total;
+}
+
+size_t hylra_select_workspace_bytes(const hylra_geometry* g, int n_slots, int sel_group) {
+  (void)g; (void)n_slots; (void)sel_group;
+  return kHeader;  // flag word only
+}
+
+int hylra_full_decode(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                      int n_valid, int n_layers, const int32_t* layer_ids, float* out,
+                      float* scores, void* ws, size_t ws_bytes, void* stream) {
+  return launch_attention(g, false, q, k, v, n_valid, n_valid, n_layers, layer_ids, nullptr,
+                          nullptr, 0, 1, out, scores, ws, ws_bytes, static_cast<int*>(ws),
+                          static_cast<cudaStream_t>(stream));
+}
+
+int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
+                      int budget, int sel_group, const void* q, const void* k,
+                      const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
+                      void* ws, size_t ws_bytes, void* stream) {
+  if (!ws || ws_bytes < kHeader) return fail(HYLRA_ERR_CONFIGURATION, "select workspace too small");
+  return launch_select(g, scores, n_slots, n_valid, budget, sel_group, q, k, layer_ids, idx,
+                       k_stride, info, static_cast<int*>(ws), static_cast<cudaStream_t>(stream));
+}
+
+int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                       int n_valid, int n_layers, const int32_t* layer_ids,
+                       const int32_t* src_slots, const int32_t* idx, int k_stride, int k_eff,
+                       int sel_group, float* out, void* ws, size_t ws_bytes, void* stream) {
+  if (!idx || !src_slots) return fail(HYLRA_ERR_CONFIGURATION, "NULL selection argument");
+  if (k_eff < 1 || k_eff > k_stride)
+    return fail(HYLRA_ERR_INVALID_SELECTION, "selection size %d not in [1, k_stride=%d]", k_eff,
+                k_stride);
+  if (sel_group < 1 || (g && g->kv_heads % sel_group != 0))
+    return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads", sel_group);
+  return launch_attention(g, true, q, k, v, n_valid, k_eff, n_layers, layer_ids, src_slots, idx,
+                          k_stride, sel_group, out, nullptr, ws, ws_bytes, static_cast<int*>(ws),
+                          static_cast<cudaStream_t>(stream));
+}
+
+size_t hylra_decode_step_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
+                                         int n_valid, int budget, int sel_group) {
+  StepLayout s;
+  if (step_layout(g, actions, n_valid, budget, sel_group, &s)) return 0;
+  return s.total;
+}
+
+int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                      int n_valid, const uint8_t* actions, int budget, int sel_group,
+                      int refine, float* out, int32_t* idx, int k_stride, void* ws,
+                      size_t ws_bytes, void* stream) {
+  StepLayout s;
+  if (int e = step_layout(g, actions, n_valid, budget, sel_group, &s)) return e;
+  if (!ws || ws_bytes < s.total)
+    return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, s.total);
+  if (k_stride < s.k_eff)
+    return fail(HYLRA_ERR_CONFIGURATION, "k_stride %d < selection size %d", k_stride, s.k_eff);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int* flags = reinterpret_cast<int*>(w);
+  float* scores = reinterpret_cast<float*>(w + s.off_scores);
+  void* aws = w + s.off_attn;
+  const int nf = (int)s.full_ids.size();
+  if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, nf, s.full_ids.data(), nullptr,
+                               nullptr, 0, 1, out, scores, aws, s.attn_bytes, flags, st))
+    return e;
+  if (int e = launch_select(g, scores, nf, n_valid, budget, sel_group, refine ? q : nullptr,
+                            refine ? k : nullptr, s.full_ids.data(), idx, k_stride, nullptr,
+                            flags, st))
+    return e;
+  if (!s.reuse_ids.empty()) {
+    if (int e = launch_attention(g, true, q, k, v, n_valid, s.k_eff, (int)s.reuse_ids.size(),
+                                 s.reuse_ids.data(), s.reuse_src.data(), idx, k_stride, sel_group,
+                                 out, nullptr, aws, s.attn_bytes, flags, st))
+      return e;
+  }
+  return HYLRA_OK;
+}
+
+int hylra_overlap_counts(const int32_t* idx, int steps, int layers, int rows, int k,
+                         int k_stride, int n_tokens, int32_t* counts, void* stream) {
+  if (!idx || !counts) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  if (steps < 1 || layers < 1 || rows < 1 || k < 1 || k_stride < k || n_tokens < 1)
+    return fail(HYLRA_ERR_INVALID_INPUT, "invalid overlap dimensions");
+  const int n_pairs = layers * (layers + 1) / 2;
+  const size_t budget = 200 * 1024 - n_pairs * sizeof(int);
+  int chunk = (int)std::min<size_t>(budget / (layers * 4) * 32, (size_t)((n_tokens + 31) & ~31));
+  chunk = std::max(32, chunk & ~31);
+  const size_t smem = (size_t)layers * (chunk / 32) * 4 + n_pairs * sizeof(int);
+  if (smem > 220 * 1024) return fail(HYLRA_ERR_CONFIGURATION, "too many layers (%d)", layers);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(overlap_counts_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  });
+  if (attr_err != cudaSuccess) return cuda_check(attr_err, "overlap attribute");
+  dim3 grid(rows, steps);
+  overlap_counts_kernel<<<grid, kOvThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      idx, layers, rows, k, k_stride, n_tokens, chunk, counts);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_check(cudaGetLastError(), "overlap launch");
+}
+
+int hylra_read_flags(const void* ws, int32_t* flags_host, void* stream) {
+  if (!ws || !flags_host) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int e = cuda_check(cudaMemcpyAsync(flags_host, ws, sizeof(int32_t), cudaMemcpyDeviceToHost, st),
+                         "read flags"))
+    return e;
+  return cuda_check(cudaStreamSynchronize(st), "read flags sync");
+}
+
+int hylra_clear_flags(void* ws, void* stream) {
+  if (!ws) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  return cuda_check(cudaMemsetAsync(ws, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)),
+                    "clear flags");
+}
+
+}  // extern "C"

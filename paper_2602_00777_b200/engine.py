@@ -1,0 +1,340 @@
+"""Hybrid FULL/REUSE decoding (HyLRA Algorithm 2) on B200 through the C ABI.
+
+Reference: pkg/src/layerreuse/engine.py:129-209 `hybrid_decode` and
+synthetic.py:237-301 `run_full_trace`. Three entry points:
+
+* `HybridDecoder` — tensor-native, stateful: fixed cache geometry + policy, one
+  `hylra_decode_step` per decode step (3 kernels: all FULL layers, all selections, all
+  REUSE layers), CUDA-graph capturable, buffers reused across steps.
+* `decode_step(...)` — functional one-shot form of the same.
+* `hybrid_decode(model, policy, budget, steps)` / `run_full_trace(model, steps, budget)` —
+  drop-ins taking the reference's duck-typed model (config.{layers, heads, head_dim,
+  context_len}, grown_arrays, queries) and returning reference-shaped results (float64
+  outputs [T, L, H, d], per-step per-layer TopKSet tuples in which a REUSE layer's entry
+  IS its source's object, fidelity table against an all-FULL baseline, counters).
+
+Policy semantics follow the engine, not `policy.sources`: a REUSE layer uses the most
+recent FULL layer's selection of the same step (engine.py:173,176,185-194).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from .attention import TopKSet, geometry
+from .errors import ConfigurationError, InvalidInputError, InvalidSelectionError, NumericInputError
+from .policy import Action, LayerPolicy, policy_from_actions
+from .profiling import overlap_counts, relative_l2_error, similarity_from_counts
+
+__all__ = ["HybridDecoder", "StepResult", "decode_step", "DecodeRunResult", "FidelityTable",
+           "DecodeTrace", "hybrid_decode", "run_full_trace", "trace_overlap_counts"]
+
+
+def _actions_of(policy) -> tuple:
+    if isinstance(policy, LayerPolicy):
+        return policy.actions
+    return policy_from_actions(policy).actions
+
+
+@dataclass
+class StepResult:
+    """outputs: fp32 [L, B, Hq, d]; selections: int32 [n_full, B, groups, k_eff];
+    slot_of_layer[l] = selection slot layer l used (its own for FULL, its source's for
+    REUSE)."""
+
+    outputs: torch.Tensor
+    selections: torch.Tensor
+    slot_of_layer: tuple
+    full_layers: tuple
+
+    def selection(self, layer: int) -> torch.Tensor:
+        return self.selections[self.slot_of_layer[layer]]
+
+
+class HybridDecoder:
+    """Stateful hybrid decode driver for one cache geometry and one policy.
+
+    k_cache / v_cache: [L, B, Hkv, capacity, d] (bf16 or fp32) resident in HBM; queries
+    come per step as [L, B, Hq, d] in the same dtype. `step(q, n_valid)` enqueues one
+    decode step on the current stream and returns views of the decoder's own output
+    buffers (overwritten by the next step).
+    """
+
+    def __init__(self, policy, k_cache: torch.Tensor, v_cache: torch.Tensor, budget: int, *,
+                 q_heads: int, sel_group: int = 1, refine: bool = True):
+        self.actions = _actions_of(policy)
+        if len(self.actions) != k_cache.shape[0]:
+            raise ConfigurationError(
+                f"policy covers {len(self.actions)} layers, cache has {k_cache.shape[0]}")
+        if self.actions[0] is not Action.FULL:
+            raise InvalidInputError("the first layer of a policy must run full attention")
+        if budget < 1:
+            raise InvalidInputError(f"budget must be >= 1, got {budget}")
+        self.k, self.v = k_cache, v_cache
+        L, B, Hkv, cap, d = k_cache.shape
+        self.budget, self.sel_group, self.refine = int(budget), int(sel_group), bool(refine)
+        if sel_group < 1 or Hkv % sel_group:
+            raise ConfigurationError(f"sel_group {sel_group} does not divide kv_heads {Hkv}")
+        self.full_layers = tuple(l for l, a in enumerate(self.actions) if a is Action.FULL)
+        slots, cur = [], -1
+        for a in self.actions:
+            if a is Action.FULL:
+                cur += 1
+            slots.append(cur)
+        self.slot_of_layer = tuple(slots)
+        self.q_heads = q_heads
+        self.out = torch.empty((L, B, q_heads, d), dtype=torch.float32, device=k_cache.device)
+        self.k_stride = min(self.budget, cap)
+        self.idx = torch.zeros((len(self.full_layers), B, Hkv // sel_group, self.k_stride),
+                               dtype=torch.int32, device=k_cache.device)
+        self._acts = _abi.uint8_array(1 if a is Action.FULL else 0 for a in self.actions)
+        self.ws = torch.zeros(256, dtype=torch.uint8, device=k_cache.device)
+        self.kernels_per_step = 2 + (1 if len(self.full_layers) < L else 0)
+
+    def _geometry(self, q):
+        return geometry(q, self.k, self.v, self.out)
+
+    def workspace_bytes(self, q, n_valid: int) -> int:
+        g = self._geometry(q)
+        return int(_abi.lib().hylra_decode_step_workspace_bytes(
+            g, self._acts, int(n_valid), self.budget, self.sel_group))
+
+    def step(self, q: torch.Tensor, n_valid: int | None = None) -> StepResult:
+        g = self._geometry(q)
+        n_valid = g.capacity if n_valid is None else int(n_valid)
+        need = int(_abi.lib().hylra_decode_step_workspace_bytes(
+            g, self._acts, n_valid, self.budget, self.sel_group))
+        if need == 0:
+            _abi.check(_abi.lib().hylra_decode_step(
+                g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
+                self.budget, self.sel_group, int(self.refine), self.out.data_ptr(),
+                self.idx.data_ptr(), self.k_stride, None, 0, 0))
+        if self.ws.numel() < need:
+            self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
+        st = torch.cuda.current_stream(self.k.device).cuda_stream
+        _abi.check(_abi.lib().hylra_decode_step(
+            g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
+            self.budget, self.sel_group, int(self.refine), self.out.data_ptr(),
+            self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(), self.ws.numel(), st))
+        k_eff = min(self.budget, n_valid)
+        return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
+
+    def flags(self) -> int:
+        """Device flag word (synchronises)."""
+        return int(self.ws[:4].view(torch.int32).item())
+
+    def check_flags(self) -> None:
+        f = self.flags()
+        if f & _abi.FLAG_INDEX_OUT_OF_RANGE:
+            raise InvalidSelectionError("a selection index is out of range for the cache")
+        if f & _abi.FLAG_NON_FINITE_SCORE:
+            raise NumericInputError("selection scores contain non-finite entries")
+
+    def clear_flags(self) -> None:
+        self.ws[:4].zero_()
+
+
+def decode_step(policy, k_cache, v_cache, q, budget: int, n_valid: int | None = None, *,
+                sel_group: int = 1, refine: bool = True) -> StepResult:
+    """One hybrid decode step (functional form of HybridDecoder.step)."""
+    dec = HybridDecoder(policy, k_cache, v_cache, budget, q_heads=q.shape[2],
+                        sel_group=sel_group, refine=refine)
+    res = dec.step(q, n_valid)
+    dec.check_flags()
+    return res
+
+
+# --------------------------------------------------------------------------- drop-ins
+@dataclass(frozen=True)
+class FidelityTable:
+    """Relative L2 error of hybrid outputs against the all-FULL baseline (engine.py:47-57)."""
+
+    per_step_layer: np.ndarray
+    per_layer: np.ndarray
+    aggregate: float
+
+
+@dataclass(frozen=True)
+class DecodeRunResult:
+    """Outputs, selections, fidelity and counters of one hybrid run (engine.py:60-92)."""
+
+    policy: LayerPolicy
+    budget: int
+    block_size: int
+    outputs: np.ndarray
+    selections: tuple
+    fidelity: FidelityTable
+    full_score_computations: tuple
+    reuse_full_scans: int
+    reuse_gathered_rows: tuple
+
+    @property
+    def full_layer_count(self) -> int:
+        return self.policy.full_count
+
+    @property
+    def reuse_layer_count(self) -> int:
+        return self.policy.num_layers - self.policy.full_count
+
+    @property
+    def steps(self) -> int:
+        return self.outputs.shape[0]
+
+
+@dataclass(frozen=True)
+class DecodeTrace:
+    """All-FULL decode record (synthetic.py:214-234): queries/outputs [T, L, H, d] and
+    topk[t][l] TopKSet per layer (layer-wide selection, summed over all heads)."""
+
+    config: object
+    budget: int
+    block_size: int
+    queries: np.ndarray
+    outputs: np.ndarray
+    topk: tuple
+    idx_device: torch.Tensor | None = None   # int32 [T, L, 1, budget] on the GPU
+
+    @property
+    def steps(self) -> int:
+        return self.queries.shape[0]
+
+
+def _model_tensors(model, steps: int, device):
+    """Reference model arrays -> fp32 device tensors in the ABI layout.
+
+    keys/values [L, H, N+T, d] -> [L, 1, H, cap, d]; queries [T, L, H, d] -> [T, L, 1, H, d].
+    """
+    keys, values = model.grown_arrays(steps)
+    queries = model.queries(steps)
+    L, H, NT, d = keys.shape
+    cap = (NT + 63) // 64 * 64
+    k = torch.zeros((L, 1, H, cap, d), dtype=torch.float32, device=device)
+    v = torch.zeros((L, 1, H, cap, d), dtype=torch.float32, device=device)
+    k[:, 0, :, :NT] = torch.as_tensor(np.asarray(keys, dtype=np.float32), device=device)
+    v[:, 0, :, :NT] = torch.as_tensor(np.asarray(values, dtype=np.float32), device=device)
+    q = torch.as_tensor(np.asarray(queries, dtype=np.float32), device=device).unsqueeze(2)
+    return q.contiguous(), k, v
+
+
+def _check_model_args(model, actions, steps: int, budget: int) -> None:
+    cfg = model.config
+    if len(actions) != cfg.layers:
+        raise ConfigurationError(f"policy covers {len(actions)} layers, model has {cfg.layers}")
+    if actions[0] is not Action.FULL:
+        raise InvalidInputError("the first layer of a policy must run full attention")
+    if steps < 1:
+        raise InvalidInputError(f"steps must be >= 1, got {steps}")
+    if budget < 1:
+        raise InvalidInputError(f"budget must be >= 1, got {budget}")
+
+
+def _run(model, actions, budget: int, steps: int, device, refine: bool):
+    cfg = model.config
+    q, k, v = _model_tensors(model, steps, device)
+    H = cfg.heads
+    dec = HybridDecoder(actions, k, v, budget, q_heads=H, sel_group=H, refine=refine)
+    outs, sels = [], []
+    for t in range(steps):
+        n_t = cfg.context_len + t
+        res = dec.step(q[t], n_t)
+        dec.check_flags()
+        outs.append(res.outputs[:, 0].double().cpu().numpy())
+        sels.append(res.selections[:, 0, 0].cpu().numpy())
+    return np.stack(outs), sels, dec
+
+
+def hybrid_decode(model, policy, budget: int, steps: int, *, include_sinks: int = 0,
+                  include_recent: int = 0, device="cuda", refine: bool = True) -> DecodeRunResult:
+    """Drop-in for the reference `hybrid_decode` (engine.py:129-209) on the GPU.
+
+    The model's heads are MHA heads sharing one layer-wide selection (sel_group = H), the
+    reference's aggregation rule. Compute runs in fp32 on the device; the selection
+    boundary is re-resolved in float64 (refine=True)."""
+    actions = _actions_of(policy)
+    pol = policy if isinstance(policy, LayerPolicy) else policy_from_actions(actions)
+    _check_model_args(model, actions, steps, budget)
+    if include_sinks < 0 or include_recent < 0:
+        raise InvalidInputError("include_sinks and include_recent must be >= 0")
+    if include_sinks or include_recent:
+        raise ConfigurationError("sink/recent augmentation is not implemented on the GPU path")
+    cfg = model.config
+    outputs, sel_arrays, _ = _run(model, actions, budget, steps, device, refine)
+    baseline = run_full_trace(model, steps, min(budget, cfg.context_len), device=device,
+                              refine=refine)
+    L = cfg.layers
+    selections, full_counts, gathered = [], [], []
+    for t in range(steps):
+        n_t = cfg.context_len + t
+        step_sel, step_g, cur = [], [], None
+        for l, a in enumerate(actions):
+            if a is Action.FULL:
+                slot = sum(1 for x in actions[:l] if x is Action.FULL)
+                cur = TopKSet(tuple(int(i) for i in sel_arrays[t][slot]), budget)
+                step_g.append(None)
+            else:
+                step_g.append(min(budget, n_t))
+            step_sel.append(cur)
+        selections.append(tuple(step_sel))
+        gathered.append(tuple(step_g))
+        full_counts.append(pol.full_count)
+    table = np.empty((steps, L))
+    for t in range(steps):
+        for l in range(L):
+            table[t, l] = relative_l2_error(outputs[t, l].ravel(), baseline.outputs[t, l].ravel())
+    table.setflags(write=False)
+    per_layer = table.mean(axis=0)
+    per_layer.setflags(write=False)
+    outputs.setflags(write=False)
+    return DecodeRunResult(
+        policy=pol, budget=budget, block_size=1, outputs=outputs,
+        selections=tuple(selections),
+        fidelity=FidelityTable(table, per_layer, float(table.mean())),
+        full_score_computations=tuple(full_counts), reuse_full_scans=0,
+        reuse_gathered_rows=tuple(gathered))
+
+
+def run_full_trace(model, steps: int, budget: int, block_size: int = 1, *, device="cuda",
+                   refine: bool = True) -> DecodeTrace:
+    """Drop-in for the reference `run_full_trace` (synthetic.py:237-301): every layer FULL,
+    one layer-wide TopKSet per (step, layer); the int32 sets stay on the device for the
+    OVERLAP kernel (idx_device [T, L, 1, budget])."""
+    cfg = model.config
+    if steps < 1:
+        raise InvalidInputError(f"steps must be >= 1, got {steps}")
+    if budget < 1 or budget > cfg.context_len:
+        raise InvalidInputError(
+            f"budget must lie in [1, context_len={cfg.context_len}], got {budget}")
+    if block_size != 1:
+        raise ConfigurationError("block-level selection is not implemented on the GPU path")
+    actions = (Action.FULL,) * cfg.layers
+    q, k, v = _model_tensors(model, steps, device)
+    H = cfg.heads
+    dec = HybridDecoder(actions, k, v, budget, q_heads=H, sel_group=H, refine=refine)
+    outs, topk = [], []
+    idx_dev = torch.empty((steps, cfg.layers, 1, budget), dtype=torch.int32, device=device)
+    for t in range(steps):
+        res = dec.step(q[t], cfg.context_len + t)
+        dec.check_flags()
+        idx_dev[t].copy_(res.selections[:, 0, :, :budget])
+        outs.append(res.outputs[:, 0].double().cpu().numpy())
+        sel = res.selections[:, 0, 0].cpu().numpy()
+        topk.append(tuple(TopKSet(tuple(int(i) for i in sel[l]), budget)
+                          for l in range(cfg.layers)))
+    outputs = np.stack(outs)
+    outputs.setflags(write=False)
+    queries = np.asarray(model.queries(steps))
+    return DecodeTrace(cfg, budget, block_size, queries, outputs, tuple(topk), idx_dev)
+
+
+def trace_overlap_counts(trace: DecodeTrace) -> np.ndarray:
+    """OVERLAP kernel over a GPU trace: int counts [T, L, L] (counts[t, j, i] = |S_i & S_j|)."""
+    c = overlap_counts(trace.idx_device, trace.config.context_len + trace.steps, trace.budget)
+    return c[:, 0].cpu().numpy()
+
+
+def build_similarity_matrix(trace: DecodeTrace):
+    """Drop-in for profiling.py:126-145: GPU counts + the reference's float64 fold."""
+    return similarity_from_counts(trace_overlap_counts(trace), trace.budget)
