@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""Benchmark of one HyLRA hybrid decode step (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" = one hybrid FULL/REUSE decode step over the whole 32-layer attention stack of
+BASELINE config 2 (Llama-3-8B shape: Hq 32, Hkv 8, d 128, bf16 KV, 32K context, top-k 2048,
+FULL layers 0,1,2,8,15,16,24,31), batch 8 per GPU: 3 kernels (all FULL layers + score
+emission, all top-k selections, all REUSE gathers) replayed from a CUDA graph. Inputs are
+resident in HBM (34 GB of KV, far larger than the 126 MB L2, so no flush is needed).
+
+value   : whole-job tok/s = sequences decoded per step (all ranks) / max-over-ranks step time
+e2e     : same metric through the public API (HybridDecoder.step) with the step's inputs
+          (queries + the new token's K/V row per layer) copied from pinned host memory and
+          the outputs copied back every step
+roofline: the FULL kernel (dominant), algorithmic K/V bytes / CUDA-event launch time vs
+          MEASURED_PEAKS.json hbm_gbs
+cpu_baseline: the float64 oracle port of the reference (oracle/cpu_baseline.py) on the
+          host cores, in a torch-free subprocess
+N > 1   : launched by torchrun; KV-head sharding (Hkv/N heads per rank, global batch 8*N:
+          weak scaling), no collective inside the attention path, one NCCL all-gather of
+          the outputs per step.
+--impl reference: the reference algorithm's CPU implementation (the oracle port; the
+          reference is pure Python and cannot be installed as a GPU arm) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASELINE_METRIC = ("decode attention tok/s + HBM GB/s (% peak) at 32K/128K ctx, "
+                   "1/2/4/8 B200 vs CPU ref")
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--batch", type=int, default=None, help="sequences per GPU")
+    ap.add_argument("--no-extra", action="store_true", help="skip the 128K (config 3) line")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(a):
+    """CPU arm: the reference algorithm (float64 oracle port) on this host's cores.
+    Each step = one (sequence, KV-head) group through all layers; tok/s extrapolated."""
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle.cpu_baseline import full_layer, group_data, reuse_layer
+    from paper_2602_00777_b200.synthetic import CONFIGS
+
+    cfg = CONFIGS[a.config]
+    B = (a.batch or cfg.batch) * a.gpus
+    layers = group_data(cfg, 4)
+    acts = cfg.actions
+
+    def one_step():
+        idx = None
+        for l, act in enumerate(acts):
+            q, k, v = layers[l % len(layers)]
+            if act == "full":
+                idx = full_layer(q, k, v, cfg.budget)
+            else:
+                reuse_layer(q, k, v, idx)
+
+    for _ in range(a.warmup):
+        one_step()
+    times = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        one_step()
+        times.append(time.perf_counter() - t0)
+    t_group = float(np.mean(times))
+    step = t_group * cfg.kv_heads * B
+    value = B / step
+    cores = _env_int("OPENBLAS_NUM_THREADS", os.cpu_count() or 1)
+    line = {
+        "impl": "reference",
+        "metric": BASELINE_METRIC, "value": value, "unit": "tok/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) + planted critical tokens)",
+        "config": _config_dict(cfg, B, a.gpus),
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port",
+                         "sample": (f"per step: one (sequence, KV-head) group through all "
+                                    f"{cfg.layers} layers (reference algorithm, float64 numpy "
+                                    f"port), x{cfg.kv_heads * B} groups extrapolated")},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(cfg, batch, world):
+    return {
+        "workload": (f"{cfg.name}: {cfg.layers}-layer hybrid attention stack, "
+                     f"{len(cfg.full_layers)} FULL / {cfg.layers - len(cfg.full_layers)} REUSE, "
+                     f"Hq {cfg.q_heads} / Hkv {cfg.kv_heads}, d {cfg.head_dim}, "
+                     f"{cfg.dtype} KV, context {cfg.context}, top-k {cfg.budget}"),
+        "global_batch": batch, "context": cfg.context, "top_k": cfg.budget,
+        "layers": cfg.layers, "full_layers": list(cfg.full_layers),
+        "parallelism": f"kvhead-shard{world}", "l2": "inputs larger than L2 (no flush)",
+    }
+
+
+# ----------------------------------------------------------------------------- GPU arm
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.4)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        return {}
+
+
+def _ncu_traffic():
+    try:
+        return json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+    except (OSError, ValueError):
+        return {}
+
+
+def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
+    from paper_2602_00777_b200 import _abi
+    from paper_2602_00777_b200.attention import geometry, scores_row_stride
+    from paper_2602_00777_b200.engine import HybridDecoder
+    from paper_2602_00777_b200.sharding import gather_outputs, plan_shards
+    from paper_2602_00777_b200.synthetic import generate_torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    global_batch = batch * world
+    plan = plan_shards(cfg.kv_heads, cfg.q_heads, global_batch, world, mode="kvhead")[rank]
+    local = cfg.with_(batch=global_batch, kv_heads=cfg.kv_heads // world,
+                      q_heads=cfg.q_heads // world, seed=cfg.seed + rank)
+    cap = cfg.context  # the e2e step writes the new token at row context-1
+    q, k, v = generate_torch(local, dev, capacity=cap)
+    L, B, Hq, d = q.shape
+    Hkv = k.shape[2]
+    dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1, refine=True)
+    n_valid = cfg.context
+
+    def step():
+        dec.step(q, n_valid)
+        if world > 1:
+            gather_outputs(dec.out, plan)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    dec.check_flags()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        dec.step(q, n_valid)
+    for _ in range(max(a.warmup, 3)):
+        graph.replay()
+        if world > 1:
+            gather_outputs(dec.out, plan)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(_env_int("LOCAL_RANK", 0))
+    clocks.start()
+    # ---- value: K graph replays, device-timed, max over ranks
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        graph.replay()
+        if world > 1:
+            gather_outputs(dec.out, plan)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = global_batch / (ms * 1e-3)
+
+    # ---- per-kernel times (same launches as the step, timed one op at a time)
+    g = geometry(q, k, v, dec.out)
+    full_ids = [l for l in range(L) if cfg.actions[l] == "full"]
+    reuse_ids = [l for l in range(L) if cfg.actions[l] == "reuse"]
+    slot_of = dec.slot_of_layer
+    nf = len(full_ids)
+    scores = torch.empty((nf, B, Hkv, scores_row_stride(cap)), dtype=torch.float32, device=dev)
+    ws_f = torch.zeros(_abi.lib().hylra_attention_workspace_bytes(g, nf, n_valid),
+                       dtype=torch.uint8, device=dev)
+    k_eff = min(cfg.budget, n_valid)
+    ws_r = torch.zeros(max(256, _abi.lib().hylra_attention_workspace_bytes(
+        g, max(len(reuse_ids), 1), k_eff)), dtype=torch.uint8, device=dev)
+    ws_s = torch.zeros(256, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    lib = _abi.lib()
+    fids = _abi.int32_array(full_ids)
+    rids = _abi.int32_array(reuse_ids)
+    rsrc = _abi.int32_array(slot_of[l] for l in reuse_ids)
+
+    def op_full():
+        _abi.check(lib.hylra_full_decode(g, q.data_ptr(), k.data_ptr(), v.data_ptr(), n_valid, nf,
+                                         fids, dec.out.data_ptr(), scores.data_ptr(),
+                                         ws_f.data_ptr(), ws_f.numel(), st))
+
+    def op_select():
+        _abi.check(lib.hylra_topk_select(g, scores.data_ptr(), nf, n_valid, cfg.budget, 1,
+                                         q.data_ptr(), k.data_ptr(), fids, dec.idx.data_ptr(),
+                                         dec.k_stride, None, ws_s.data_ptr(), ws_s.numel(), st))
+
+    def op_reuse():
+        _abi.check(lib.hylra_reuse_decode(g, q.data_ptr(), k.data_ptr(), v.data_ptr(), n_valid,
+                                          len(reuse_ids), rids, rsrc, dec.idx.data_ptr(),
+                                          dec.k_stride, k_eff, 1, dec.out.data_ptr(),
+                                          ws_r.data_ptr(), ws_r.numel(), st))
+
+    def time_op(fn, reps):
+        for _ in range(3):
+            fn()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
+        for s0, s1 in ev:
+            s0.record()
+            fn()
+            s1.record()
+        torch.cuda.synchronize()
+        return statistics.mean(s0.elapsed_time(s1) for s0, s1 in ev)
+
+    reps = max(10, a.steps // 2)
+    t_full = time_op(op_full, reps)
+    t_sel = time_op(op_select, reps)
+    t_reuse = time_op(op_reuse, reps) if reuse_ids else 0.0
+    es = 2 if cfg.dtype == "bf16" else 4
+    full_bytes = nf * B * Hkv * 2 * n_valid * d * es
+    reuse_bytes = len(reuse_ids) * B * Hkv * 2 * k_eff * d * es
+    step_bytes = full_bytes + reuse_bytes
+
+    # ---- e2e through the public API with host buffers
+    e2e_line = None
+    if e2e:
+        pos = cfg.context - 1
+        q_h = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+        q_h.copy_(q.cpu())
+        kn_h = torch.empty((L, B, Hkv, d), dtype=k.dtype).pin_memory()
+        vn_h = torch.empty((L, B, Hkv, d), dtype=v.dtype).pin_memory()
+        kn_h.copy_(k[:, :, :, pos].cpu())
+        vn_h.copy_(v[:, :, :, pos].cpu())
+        out_h = torch.empty(dec.out.shape, dtype=torch.float32).pin_memory()
+        q_dev = torch.empty_like(q)
+
+        def e2e_step():
+            q_dev.copy_(q_h, non_blocking=True)
+            k[:, :, :, pos].copy_(kn_h, non_blocking=True)
+            v[:, :, :, pos].copy_(vn_h, non_blocking=True)
+            res = dec.step(q_dev, pos + 1)
+            out = gather_outputs(res.outputs, plan) if world > 1 else res.outputs
+            if world > 1:
+                out_h_full = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
+                out_h_full.copy_(out, non_blocking=True)
+            else:
+                out_h.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(3):
+            e2e_step()
+        if world > 1:
+            dist.barrier()
+        n_e2e = max(10, a.steps)
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        t_e2e = (time.perf_counter() - t0) / n_e2e
+        if world > 1:
+            tt = torch.tensor([t_e2e], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        h2d = q.numel() * q.element_size() + 2 * kn_h.numel() * kn_h.element_size()
+        d2h = dec.out.numel() * 4 * (world if world > 1 else 1)
+        e2e_line = {"value": global_batch / t_e2e, "unit": "tok/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": t_e2e * 1e3,
+                    "path": "HybridDecoder.step (eager C-ABI call) + pinned H2D/D2H, wall clock"}
+    clk = clocks.stop()
+
+    peaks = _peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_kind = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback 6650 GB/s"
+    peak = peak or 6650.0
+    full_gbs = full_bytes / (t_full * 1e-3) / 1e9
+    reuse_gbs = reuse_bytes / (t_reuse * 1e-3) / 1e9 if t_reuse else None
+    ncu = _ncu_traffic().get(cfg.name, {})
+    res = {
+        "ms_per_step": ms, "value": value, "global_batch": global_batch,
+        "step_gbs": step_bytes / (ms * 1e-3) / 1e9,
+        "kernels": {
+            "full_ms": t_full, "select_ms": t_sel, "reuse_ms": t_reuse,
+            "select_frac_of_full_plus_select": t_sel / (t_full + t_sel),
+            "full_gbs": full_gbs, "full_frac": full_gbs / peak,
+            "reuse_gbs": reuse_gbs, "reuse_frac": (reuse_gbs / peak) if reuse_gbs else None,
+            "full_bytes_per_launch": full_bytes, "reuse_bytes_per_launch": reuse_bytes,
+        },
+        "roofline": {"bound": "hbm", "achieved": full_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": full_gbs / peak, "peak_kind": peak_kind,
+                     "kernel": "attn_mma_kernel<128,false,false,3> (FULL, all 8 FULL layers "
+                               "per launch)",
+                     "traffic": ncu.get("full_traffic_bytes_per_launch")},
+        "gpu_launches": dec.kernels_per_step * a.steps,
+        "e2e": e2e_line, "clocks": clk,
+    }
+    del graph, dec, q, k, v, scores
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_00777_b200.synthetic import CONFIGS
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[a.config]
+    batch = a.batch or cfg.batch
+    main = measure_config(a, cfg, batch, rank, world, torch, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        env = dict(os.environ)
+        n = os.cpu_count() or 1
+        env.update(OPENBLAS_NUM_THREADS=str(n), OMP_NUM_THREADS=str(n), MKL_NUM_THREADS=str(n))
+        try:
+            r = subprocess.run([sys.executable, "-m", "oracle.cpu_baseline", "--config", cfg.name,
+                                "--batch", str(batch), "--seconds", str(a.cpu_seconds)],
+                               cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+            cpu = json.loads(r.stdout.strip().splitlines()[-1])
+            cpu.pop("step_seconds", None)
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "tok/s", "cores": n, "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    extra = {}
+    if not a.no_extra and world == 1:
+        c3 = CONFIGS["cfg3"]
+        try:
+            r3 = measure_config(a, c3, c3.batch, rank, world, torch, dist, e2e=False)
+            extra["cfg3_128k_b4"] = {k: r3[k] for k in ("value", "ms_per_step", "step_gbs",
+                                                        "kernels", "roofline")}
+        except Exception as exc:  # noqa: BLE001
+            extra["cfg3_128k_b4"] = {"error": str(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC, "value": main["value"], "unit": "tok/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": main["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) Q/K/V, 512 planted critical tokens per layer, "
+                    "10% drift; stands in for model traces)",
+            "config": _config_dict(cfg, main["global_batch"], world),
+            "step_hbm_gbs": main["step_gbs"],
+            "roofline": main["roofline"], "kernels": main["kernels"],
+            "cpu_baseline": cpu, "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
+            "clocks": main["clocks"], "extra": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -215,34 +215,51 @@ __global__ void __launch_bounds__(160, 2)
                                    layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
       const int32_t* ib = p.idx + ((int64_t)(p.src_slot[slot] * p.B + b) * p.n_groups +
                                    kh / p.sel_group) * p.k_stride;
+      // Lane roles: a row of D bf16 is D/8 16-byte chunks; CH = D/8 consecutive lanes copy
+      // one row, so each cp.async instruction touches 32/CH whole rows (few L1 wavefronts).
+      constexpr int CH = D / 8;
+      constexpr int RPI = 32 / CH;  // rows per instruction
+      const int my_ch = lane % CH;
+      const int my_sub = lane / CH;
+      // indices of the next tile are loaded one stage ahead (2 per lane: rows lane, lane+32)
+      auto load_idx = [&](int tile, int rr) -> int {
+        const int pos = tile * kTileRows + lane + 32 * rr;
+        int row = (pos < p.n_rows) ? __ldg(ib + pos) : 0;
+        if (row < 0 || row >= p.n_valid) {
+          if (pos < p.n_rows) atomicOr(p.flags, 1);
+          row = 0;
+        }
+        return row;
+      };
+      int nx0 = 0, nx1 = 0;
+      if (n_my > 0) {
+        nx0 = load_idx(t_begin, 0);
+        nx1 = load_idx(t_begin, 1);
+      }
       for (int i = 0; i < n_my; ++i) {
         const int s = i % STAGES;
+        const int cur0 = nx0, cur1 = nx1;
+        if (i + 1 < n_my) {
+          nx0 = load_idx(t_begin + i + 1, 0);
+          nx1 = load_idx(t_begin + i + 1, 1);
+        }
         mbar_wait(empty_bar + s, ((i / STAGES) & 1) ^ 1);
         const uint32_t kt = smem_u32(smem + s * SM::kStageBytes);
         const uint32_t vt = kt + SM::kTileBytes;
         const int pos0 = (t_begin + i) * kTileRows;
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int r = lane + 32 * rr;
-          const int pos = pos0 + r;
-          const bool valid = pos < p.n_rows;
-          int row = valid ? __ldg(ib + pos) : 0;
-          if (row < 0 || row >= p.n_valid) {
-            if (valid) atomicOr(p.flags, 1);
-            row = 0;
-          }
-          const __nv_bfloat16* ks = kbase + (int64_t)row * D;
-          const __nv_bfloat16* vs = vbase + (int64_t)row * D;
-#pragma unroll
-          for (int ch = 0; ch < D / 8; ++ch) {
-            const uint32_t off = swz_addr(0, r, ch);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kt + off),
-                         "l"(ks + ch * 8), "r"(valid ? 16 : 0)
-                         : "memory");
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vt + off),
-                         "l"(vs + ch * 8), "r"(valid ? 16 : 0)
-                         : "memory");
-          }
+        for (int it = 0; it < kTileRows / RPI; ++it) {
+          const int r = it * RPI + my_sub;  // row of the tile this lane copies now
+          // it*RPI < 32 is warp-uniform (RPI divides 32), so every lane offers the same half
+          const int src = __shfl_sync(0xffffffffu, (it * RPI < 32) ? cur0 : cur1, r & 31);
+          const bool valid = pos0 + r < p.n_rows;
+          const uint32_t off = swz_addr(0, r, my_ch);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kt + off),
+                       "l"(kbase + (int64_t)src * D + my_ch * 8), "r"(valid ? 16 : 0)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vt + off),
+                       "l"(vbase + (int64_t)src * D + my_ch * 8), "r"(valid ? 16 : 0)
+                       : "memory");
         }
         cp_async_mbar_arrive_noinc(full_bar + s);
       }

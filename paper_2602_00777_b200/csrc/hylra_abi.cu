@@ -261,8 +261,8 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
 }
 
 size_t select_smem_bytes(int n_valid, bool cache) {
-  size_t b = 2048 * sizeof(float) + kBandCap * sizeof(float);
-  if (cache) b += ((n_valid + 3) & ~3) * sizeof(float);
+  size_t b = kBandCap * sizeof(float);
+  if (cache) b += (size_t)((n_valid + 3) / 4) * 16;
   return b;
 }
 

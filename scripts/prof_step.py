@@ -1,0 +1,35 @@
+"""Profiling driver: a few eager hybrid decode steps of a BASELINE config (for ncu).
+
+    python scripts/prof_step.py [--config cfg2] [--batch 8] [--steps 3]
+
+Kernel order per step: attn_mma_kernel (FULL, all FULL layers) -> topk_select_kernel ->
+attn_mma_kernel (REUSE gather, all REUSE layers).
+"""
+import argparse
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from paper_2602_00777_b200.engine import HybridDecoder  # noqa: E402
+from paper_2602_00777_b200.synthetic import CONFIGS, generate_torch  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--batch", type=int, default=None)
+ap.add_argument("--steps", type=int, default=3)
+a = ap.parse_args()
+cfg = CONFIGS[a.config]
+if a.batch:
+    cfg = cfg.with_(batch=a.batch)
+q, k, v = generate_torch(cfg, "cuda")
+torch.cuda.synchronize()
+dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
+for _ in range(a.steps):
+    dec.step(q, cfg.context)
+torch.cuda.synchronize()
+dec.check_flags()
+print("ok", cfg.name, cfg.batch)
