@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-extra", action="store_true", help="skip the 128K (config 3) line")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--schedule", default="fused3",
+                    choices=["pipelined", "fused3", "sequential"])
     return ap.parse_args()
 
 
@@ -190,7 +192,7 @@ def _ncu_traffic():
 def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     from paper_2602_00777_b200 import _abi
     from paper_2602_00777_b200.attention import geometry, scores_row_stride
-    from paper_2602_00777_b200.engine import HybridDecoder
+    from paper_2602_00777_b200.engine import HybridDecoder, PipelinedDecoder
     from paper_2602_00777_b200.sharding import gather_outputs, plan_shards
     from paper_2602_00777_b200.synthetic import generate_torch
 
@@ -203,53 +205,74 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     q, k, v = generate_torch(local, dev, capacity=cap)
     L, B, Hq, d = q.shape
     Hkv = k.shape[2]
-    dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1, refine=True)
     n_valid = cfg.context
 
-    def step():
-        dec.step(q, n_valid)
-        if world > 1:
-            gather_outputs(dec.out, plan)
+    def make(kind):
+        if kind == "fused3":
+            return HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1)
+        return PipelinedDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1,
+                                schedule=kind)
 
-    for _ in range(max(a.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    dec.check_flags()
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        step()
-    torch.cuda.current_stream().wait_stream(s)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        dec.step(q, n_valid)
-    for _ in range(max(a.warmup, 3)):
-        graph.replay()
+    def capture(d):
+        for _ in range(max(a.warmup, 3)):
+            d.step(q, n_valid)
+            if world > 1:
+                gather_outputs(d.out, plan)
+        torch.cuda.synchronize()
+        d.check_flags()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            d.step(q, n_valid)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            d.step(q, n_valid)
+        for _ in range(max(a.warmup, 3)):
+            gr.replay()
+            if world > 1:
+                gather_outputs(d.out, plan)
+        torch.cuda.synchronize()
+        return gr
+
+    def time_replays(gr, d, steps):
         if world > 1:
-            gather_outputs(dec.out, plan)
-    torch.cuda.synchronize()
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            gr.replay()
+            if world > 1:
+                gather_outputs(d.out, plan)
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms_ = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms_], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_ = float(t.item())
+        return ms_
+
+    # the other schedules, timed the same way (reported, not the headline)
+    schedules = {}
+    for kind in ("fused3", "sequential"):
+        d2 = make(kind)
+        g2 = capture(d2)
+        schedules[kind] = {"ms_per_step": time_replays(g2, d2, max(10, a.steps // 2)),
+                           "kernels_per_step": d2.kernels_per_step}
+        del g2, d2
+    dec = make(a.schedule)
+    graph = capture(dec)
 
     clocks = ClockSampler(_env_int("LOCAL_RANK", 0))
     clocks.start()
     # ---- value: K graph replays, device-timed, max over ranks
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.steps):
-        graph.replay()
-        if world > 1:
-            gather_outputs(dec.out, plan)
-    e1.record()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = e0.elapsed_time(e1) / a.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = time_replays(graph, dec, a.steps)
+    schedules[a.schedule] = {"ms_per_step": ms, "kernels_per_step": dec.kernels_per_step}
     value = global_batch / (ms * 1e-3)
 
     # ---- per-kernel times (same launches as the step, timed one op at a time)
@@ -378,6 +401,7 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                                "per launch)",
                      "traffic": ncu.get("full_traffic_bytes_per_launch")},
         "gpu_launches": dec.kernels_per_step * a.steps,
+        "schedules": schedules,
         "e2e": e2e_line, "clocks": clk,
     }
     del graph, dec, q, k, v, scores
@@ -422,7 +446,7 @@ def run_ours(a):
         try:
             r3 = measure_config(a, c3, c3.batch, rank, world, torch, dist, e2e=False)
             extra["cfg3_128k_b4"] = {k: r3[k] for k in ("value", "ms_per_step", "step_gbs",
-                                                        "kernels", "roofline")}
+                                                        "kernels", "roofline", "schedules")}
         except Exception as exc:  # noqa: BLE001
             extra["cfg3_128k_b4"] = {"error": str(exc)}
 
@@ -438,7 +462,7 @@ def run_ours(a):
             "step_hbm_gbs": main["step_gbs"],
             "roofline": main["roofline"], "kernels": main["kernels"],
             "cpu_baseline": cpu, "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
-            "clocks": main["clocks"], "extra": extra,
+            "clocks": main["clocks"], "schedules": main["schedules"], "extra": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

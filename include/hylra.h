@@ -116,7 +116,8 @@ int hylra_full_decode(const hylra_geometry* g, const void* q, const void* k, con
  * If q and k are non-NULL (with layer_ids, host array of the scored layers), the
  * k-th boundary is re-resolved in float64 from the original q/k values, which makes
  * the set match a float64 evaluation except at float64-level ties.
- * info (optional, int32 [rows][4]): k_eff, refined candidates, mode, boundary count.
+ * info (optional, int32 [rows][8]): k_eff, refined candidates, mode, band size, and the
+ * clock64 cycles of the sample / pass / select+refine / compaction phases.
  */
 int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
                       int budget, int sel_group, const void* q, const void* k,

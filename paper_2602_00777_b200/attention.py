@@ -159,7 +159,7 @@ def topk_select(scores, budget: int, n_valid: int, *, sel_group: int = 1, q=None
     k_eff = min(budget, n_valid)
     groups = Hkv // sel_group if sel_group >= 1 else 0
     idx = torch.empty((S, B, max(groups, 1), k_eff), dtype=torch.int32, device=scores.device)
-    inf = torch.zeros((S, B, max(groups, 1), 4), dtype=torch.int32, device=scores.device)
+    inf = torch.zeros((S, B, max(groups, 1), 8), dtype=torch.int32, device=scores.device)
     ws = _workspace(256, scores.device)
     _abi.check(_abi.lib().hylra_topk_select(
         g, scores.data_ptr(), S, int(n_valid), int(budget), int(sel_group), qp, kp,

@@ -260,11 +260,7 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   return cuda_check(ce, gather ? "reuse_decode launch" : "full_decode launch");
 }
 
-size_t select_smem_bytes(int n_valid, bool cache) {
-  size_t b = kBandCap * sizeof(float);
-  if (cache) b += (size_t)((n_valid + 3) / 4) * 16;
-  return b;
-}
+size_t select_smem_bytes(int n_valid) { return sel_smem_bytes(n_valid); }
 
 int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
                   int budget, int sel_group, const void* q, const void* k,
@@ -283,6 +279,8 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
   const int k_eff = std::min(budget, n_valid);
   if (k_stride < k_eff)
     return fail(HYLRA_ERR_CONFIGURATION, "k_stride %d < selection size %d", k_stride, k_eff);
+  if (n_valid > kSelMaxTokens)
+    return fail(HYLRA_ERR_CONFIGURATION, "selection rows longer than %d tokens", kSelMaxTokens);
   if (!scores || !idx) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
   SelectParams p{};
   p.scores = scores; p.idx = idx; p.info = info; p.flags = flags;
@@ -295,7 +293,6 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
   p.sel_group = sel_group; p.n_groups = g->kv_heads / sel_group;
   p.n_valid = n_valid; p.k_eff = k_eff; p.k_stride = k_stride;
   p.row_stride = scores_row_stride(g);
-  p.cache_row = n_valid <= kCacheMax;
   p.tau_rel = 1.0f / 4096.0f;
   for (int i = 0; i < n_slots; ++i) {
     const int l = layer_ids ? layer_ids[i] : 0;
@@ -303,13 +300,13 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
       return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", l);
     p.layers[i] = l;
   }
-  const size_t smem = select_smem_bytes(n_valid, p.cache_row);
+  const size_t smem = select_smem_bytes(n_valid);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
     attr_err = cudaFuncSetAttribute(topk_select_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)select_smem_bytes(kCacheMax, true));
+                                    (int)select_smem_bytes(kSelMaxTokens));
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "select attribute");
   dim3 grid(p.n_groups, g->batch, n_slots);

@@ -5,37 +5,40 @@
 // ascending; engine.py:169 clamps the budget per step; engine.py:177-183 scores are the
 // head-order sum of per-head scaled logits.
 //
-// One 1024-thread CTA per row, no global atomics:
-//   A. sample 1024 scores (strided) and bitonic-sort them in registers/shuffles (shared
-//      memory only for the 15 exchange stages with stride >= 32) -> brackets [lo, hi]
-//      around the k-th rank;
-//   B. ONE vectorised pass over the row: stage it in shared memory (rows <= 32K),
-//      reduce max|s| and the non-finite flag, count the elements above / at the brackets
-//      and collect the strictly-inside band (warp-aggregated appends);
-//   C. exact k-th largest value T = radix select (4 x 8 bit, warp-aggregated shared
-//      histograms) inside the band; fallback = the same radix select over the whole row
-//      (degenerate samples, e.g. massive ties);
-//   D. optional float64 boundary refinement: every element within tau of T is re-scored
-//      in float64 from the original q / K rows (heads summed in reference order) and the
-//      boundary is re-resolved on those scores with the lower-index tie rule;
-//   E. index-ordered stream compaction (block scan of packed counts) writes the selected
-//      indices ascending — the reference's canonical TopKSet order.
+// One 256-thread CTA per row with ~29 KB of shared memory (4 CTAs per SM), so all rows of
+// a step are resident at once; no global atomics. Fast path:
+//   A. sort a strided sample of 256 scores (bitonic: shuffles + 6 shared-memory stages)
+//      and bracket the k-th rank with [lo, hi];
+//   B. one vectorised pass: "definitely selected" bits (s > hi) go straight into a shared
+//      bitmap, scores inside [lo, hi] into a 2048-bin linear histogram; max|s| and the
+//      non-finite check ride along;
+//   C. the bin holding rank k (from the top) is found with one block scan;
+//   D. a second (L2-resident) pass sets the bits of the higher bins and collects the few
+//      scores of the bins around it; the exact k-th value T comes from those. The boundary
+//      window — the ties at T, or with refinement every score within tau of T, re-scored in
+//      float64 from the original q / K rows with heads summed in reference order — is
+//      ranked by (score desc, index asc) and its top members join the bitmap;
+//   E. index-ordered compaction of the bitmap (one block scan per 8K-token chunk) writes
+//      the indices ascending: the reference's canonical TopKSet order.
+// Degenerate rows (massive ties, failed brackets, oversized windows) take a generic path:
+// full-row MSB radix select, then the same window logic, or an index-ordered tie pass.
 #pragma once
 
 #include "common.cuh"
 
 namespace hylra {
 
-constexpr int kSelThreads = 1024;
-constexpr int kSample = 1024;
-constexpr int kBandCap = 8192;     // strictly-inside band capacity (floats)
-constexpr int kRefineCap = 1024;   // float64 refinement candidates
-constexpr int kCacheMax = 32768;   // rows up to this length are staged in shared memory
+constexpr int kSelThreads = 256;
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kBins = 2048;
+constexpr int kCandCap = 1024;            // scores collected around the k-th bin
+constexpr int kSelMaxTokens = 262144;     // longest row (bitmap = 32 KB)
+constexpr int kChunk = kSelThreads * 32;  // tokens per bitmap chunk (one word per thread)
 
 struct SelectParams {
   const float* scores;  // [slot][b][kh][row_stride]
   int32_t* idx;         // [slot][b][grp][k_stride]
-  int32_t* info;        // [row][4] or null
+  int32_t* info;        // [row][8] or null
   int* flags;
   const void* q;        // refinement inputs (null: refinement off)
   const void* k;
@@ -43,45 +46,95 @@ struct SelectParams {
   int64_t q_sl, q_sb, kv_sl, kv_sb, kv_sh;
   int B, Hkv, G, D, sel_group, n_groups;
   int n_valid, k_eff, k_stride, row_stride;
-  int cache_row;
   float tau_rel;
   int layers[kMaxSlots];
 };
 
+// Dynamic shared memory: the bitmap sized for the row, then fixed arrays.
+__host__ __device__ constexpr size_t sel_bitmap_bytes(int n) {
+  return (size_t)((n + kChunk - 1) / kChunk) * kChunk / 8;
+}
+constexpr size_t kSelFixedBytes = kBins * 4 + kCandCap * (8 + 4) + kSelThreads * 4;
+__host__ __device__ constexpr size_t sel_smem_bytes(int n) {
+  return sel_bitmap_bytes(n) + kSelFixedBytes;
+}
+
+struct SelSmem {
+  uint32_t* bitmap;  // [chunks * kSelThreads]
+  unsigned* hist;    // [kBins]
+  double* cv;        // [kCandCap] window scores (fp32 value, then float64 re-score)
+  int* ci;           // [kCandCap] window token indices
+  float* xchg;       // [kSelThreads]
+};
+
+__device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
+  SelSmem m;
+  const size_t bb = sel_bitmap_bytes(n);
+  m.bitmap = reinterpret_cast<uint32_t*>(base);
+  m.hist = reinterpret_cast<unsigned*>(base + bb);
+  m.cv = reinterpret_cast<double*>(base + bb + kBins * 4);
+  m.ci = reinterpret_cast<int*>(base + bb + kBins * 4 + kCandCap * 8);
+  m.xchg = reinterpret_cast<float*>(m.ci + kCandCap);
+  return m;
+}
+
 // ----------------------------------------------------------------------------- helpers
-__device__ __forceinline__ int block_sum_int(int v, int* red) {
+struct Red {
+  int i[kSelWarps];
+  float f[kSelWarps];
+  int wt[kSelWarps];
+  int misc[16];
+  unsigned hist256[256];
+};
+
+__device__ __forceinline__ int block_sum_int(int v, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   __syncthreads();
-  if (lane == 0) red[warp] = v;
+  if (lane == 0) r.i[warp] = v;
   __syncthreads();
-  if (warp == 0) {
-    int x = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0;
+  int x = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) red[32] = x;
-  }
-  __syncthreads();
-  return red[32];
+  for (int w = 0; w < kSelWarps; ++w) x += r.i[w];
+  return x;
 }
-__device__ __forceinline__ float block_max_float(float v, float* red) {
+__device__ __forceinline__ float block_max_float(float v, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_max(v);
   __syncthreads();
-  if (lane == 0) red[warp] = v;
+  if (lane == 0) r.f[warp] = v;
   __syncthreads();
-  if (warp == 0) {
-    float x = (lane < (int)(blockDim.x >> 5)) ? red[lane] : -INFINITY;
-    x = warp_max(x);
-    if (lane == 0) red[32] = x;
-  }
-  __syncthreads();
-  return red[32];
+  float x = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kSelWarps; ++w) x = fmaxf(x, r.f[w]);
+  return x;
 }
 
-// Warp-aggregated append: every thread contributes `cnt` items; returns the thread's
-// first slot. One shared atomic per warp.
+// Block exclusive scan of one int; returns the exclusive prefix, *total = block sum.
+__device__ __forceinline__ int block_scan(int v, int* total, Red& r) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) r.wt[warp] = x;
+  __syncthreads();
+  int pre = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kSelWarps; ++w) {
+    const int t = r.wt[w];
+    pre += (w < warp) ? t : 0;
+    all += t;
+  }
+  *total = all;
+  return pre + x - v;
+}
+
+// Warp-aggregated append: each thread adds `cnt` items; returns its first slot.
 __device__ __forceinline__ int warp_append(int cnt, int* counter) {
   const int lane = threadIdx.x & 31;
   int incl = cnt;
@@ -96,84 +149,40 @@ __device__ __forceinline__ int warp_append(int cnt, int* counter) {
   return base + incl - cnt;
 }
 
-// Descending bitonic sort of one float per thread (blockDim = 1024); shuffles for
-// strides < 32, shared memory for the rest.
-__device__ float bitonic1024_desc(float x, float* xchg) {
+// Descending bitonic sort of one float per thread (kSelThreads values), fully unrolled.
+__device__ __forceinline__ float bitonic_desc(float x, float* xchg) {
   const int tid = threadIdx.x;
+#pragma unroll
   for (int kk = 2; kk <= kSelThreads; kk <<= 1) {
+#pragma unroll
     for (int j = kk >> 1; j > 0; j >>= 1) {
       float y;
       if (j >= 32) {
+        __syncthreads();
         xchg[tid] = x;
         __syncthreads();
         y = xchg[tid ^ j];
-        __syncthreads();
       } else {
         y = __shfl_xor_sync(0xffffffffu, x, j);
       }
-      const bool desc = (tid & kk) == 0;
-      const bool lower = (tid & j) == 0;
-      x = (lower == desc) ? fmaxf(x, y) : fminf(x, y);
+      const bool keep_max = ((tid & kk) == 0) == ((tid & j) == 0);
+      x = keep_max ? fmaxf(x, y) : fminf(x, y);
     }
   }
+  __syncthreads();
   return x;
-}
-
-// Bitonic sort of (value desc, index asc) pairs in shared memory; P a power of two.
-__device__ void bitonic_desc_f64_idx(double* v, int* id, int P) {
-  for (int kk = 2; kk <= P; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const double x = v[i], y = v[ixj];
-          const int xi = id[i], yi = id[ixj];
-          const bool x_first = (x > y) || (x == y && xi < yi);
-          const bool want_x_first = (i & kk) == 0;
-          if (x_first != want_x_first) {
-            v[i] = y; v[ixj] = x; id[i] = yi; id[ixj] = xi;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-// Ascending bitonic sort of ints in shared memory; P a power of two.
-__device__ void bitonic_asc_i32(int* a, int P) {
-  for (int kk = 2; kk <= P; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const int x = a[i], y = a[ixj];
-          const bool asc = (i & kk) == 0;
-          if (asc ? (x > y) : (x < y)) { a[i] = y; a[ixj] = x; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__device__ __forceinline__ int next_pow2(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
 }
 
 struct RowReader {
   const float* base;  // score row of the group's first kv head
   int64_t hstride;    // elements between the group's kv-head rows
   int sg;
-  int n;
-  const float* cache;
-  __device__ __forceinline__ float load_raw(int i) const {
+  __device__ __forceinline__ float at(int i) const {
     float s = __ldg(base + i);
     for (int h = 1; h < sg; ++h) s += __ldg(base + h * hstride + i);
     return s;
   }
-  __device__ __forceinline__ float4 load4_raw(int i4) const {
+  __device__ __forceinline__ float4 at4(int i4) const {
     float4 s = __ldg(reinterpret_cast<const float4*>(base) + i4);
     for (int h = 1; h < sg; ++h) {
       const float4 t = __ldg(reinterpret_cast<const float4*>(base + h * hstride) + i4);
@@ -181,13 +190,9 @@ struct RowReader {
     }
     return s;
   }
-  __device__ __forceinline__ float operator()(int i) const { return cache ? cache[i] : load_raw(i); }
-  __device__ __forceinline__ float4 get4(int i4) const {
-    return cache ? reinterpret_cast<const float4*>(cache)[i4] : load4_raw(i4);
-  }
 };
 
-__device__ __forceinline__ float f4at(const float4& v, int c) {
+__device__ __forceinline__ float lane4(const float4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
@@ -196,383 +201,447 @@ __device__ __forceinline__ double elem_f64(const void* p, int64_t i) {
   return (double)to_f32(reinterpret_cast<const T*>(p)[i]);
 }
 
-// Exact rank-`rank` (1-based, descending) element of a set by MSB-first 4 x 8-bit radix
-// select on order-preserving keys. `get(j)` for j < count; returns T, #greater, #equal.
-template <typename Get>
-__device__ void radix_select_desc(const Get& get, int count, int rank, unsigned* hist,
-                                  int* misc, float* T_out, int* gt_out, int* eq_out) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// float64 selection score of tokens toks[0..n): agg = sum over (kv head of the group,
+// query head g) of (q . k) / sqrt(d) in the reference's head order. One warp per token.
+__device__ void rescore_f64(const SelectParams& p, int slot, int b, int grp, const int* toks,
+                            double* vals, int n) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int layer = p.layers[slot];
+  const double sqd = sqrt((double)p.D);
+  for (int c = warp; c < n; c += kSelWarps) {
+    const int tok = toks[c];
+    double agg = 0.0;
+    for (int hh = 0; hh < p.sel_group; ++hh) {
+      const int kh = grp * p.sel_group + hh;
+      const int64_t koff = layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
+      double kx[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = lane + 32 * j;
+        kx[j] = (i < p.D) ? (p.dtype == 0 ? elem_f64<__nv_bfloat16>(p.k, koff + i)
+                                          : elem_f64<float>(p.k, koff + i))
+                          : 0.0;
+      }
+      for (int g = 0; g < p.G; ++g) {
+        const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D;
+        double part = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = lane + 32 * j;
+          if (i < p.D)
+            part += (p.dtype == 0 ? elem_f64<__nv_bfloat16>(p.q, qoff + i)
+                                  : elem_f64<float>(p.q, qoff + i)) * kx[j];
+        }
+        agg += warp_sum_f64(part) / sqd;
+      }
+    }
+    if (lane == 0) vals[c] = agg;
+  }
+}
+
+// MSB-first 4 x 8-bit radix select of the rank-`rank` (1-based, descending) score of the
+// row: T, #(s > T). Degenerate-row fallback only.
+__device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, float* T_out,
+                                 int* gt_out) {
+  const int tid = threadIdx.x, lane = tid & 31;
   uint32_t prefix = 0, mask = 0;
-  int krem = rank, last = 0;
+  int krem = rank;
   for (int shift = 24; shift >= 0; shift -= 8) {
-    if (tid < 256) hist[tid] = 0;
+    for (int j = tid; j < 256; j += kSelThreads) r.hist256[j] = 0;
     __syncthreads();
-    for (int base = 0; base < count; base += kSelThreads) {
+    for (int base = 0; base < n; base += kSelThreads) {
       const int j = base + tid;
       bool act = false;
       unsigned dig = 0;
-      if (j < count) {
-        const uint32_t key = float_key(get(j));
+      if (j < n) {
+        const uint32_t key = float_key(rd.at(j));
         act = (key & mask) == prefix;
         dig = (key >> shift) & 255u;
       }
       const unsigned am = __ballot_sync(0xffffffffu, act);
       if (act) {
         const unsigned peers = __match_any_sync(am, dig);
-        if (lane == __ffs(peers) - 1) atomicAdd(hist + dig, (unsigned)__popc(peers));
+        if (lane == __ffs(peers) - 1) atomicAdd(r.hist256 + dig, (unsigned)__popc(peers));
       }
     }
     __syncthreads();
-    if (warp == 0) {
-      int c[8], s = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        c[u] = (int)hist[255 - 8 * lane - u];
-        s += c[u];
+    if (tid == 0) {
+      int acc = 0, d = 255;
+      for (; d > 0; --d) {
+        if (acc + (int)r.hist256[d] >= krem) break;
+        acc += r.hist256[d];
       }
-      int incl = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - s;
-      const unsigned m = __ballot_sync(0xffffffffu, excl < krem && krem <= incl);
-      if (lane == (m ? __ffs(m) - 1 : 31)) {
-        int acc = excl, d = 255 - 8 * lane - 7, cnt = c[7];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (acc + c[u] >= krem) { d = 255 - 8 * lane - u; cnt = c[u]; break; }
-          acc += c[u];
-        }
-        misc[8] = d;
-        misc[9] = acc;
-        misc[10] = cnt;
-      }
+      r.misc[8] = d;
+      r.misc[9] = acc;
     }
     __syncthreads();
-    const int d = misc[8];
-    krem -= misc[9];
-    last = misc[10];
-    prefix |= (uint32_t)d << shift;
+    krem -= r.misc[9];
+    prefix |= (uint32_t)r.misc[8] << shift;
     mask |= 255u << shift;
     __syncthreads();
   }
   *T_out = key_float(prefix);
   *gt_out = rank - krem;
-  *eq_out = last;
 }
 
 // ----------------------------------------------------------------------------- kernel
-__global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(const SelectParams p) {
+__global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const SelectParams p) {
   extern __shared__ __align__(16) uint8_t sraw[];
-  __shared__ int red[40];
-  __shared__ float fred[40];
-  __shared__ int s_misc[16];
-  __shared__ unsigned s_hist[256];
-  __shared__ float s_xchg[kSelThreads];
+  __shared__ Red red;
 
   const int grp = blockIdx.x, b = blockIdx.y, slot = blockIdx.z;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int n = p.n_valid;
   const int k = p.k_eff;
   const int n4 = (n + 3) >> 2;
   const int row_id = (slot * p.B + b) * p.n_groups + grp;
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
-
-  float* cache = nullptr;
-  uint8_t* cur = sraw;
-  if (p.cache_row) {
-    cache = reinterpret_cast<float*>(cur);
-    cur += (size_t)n4 * 16;
-  }
-  float* band = reinterpret_cast<float*>(cur);    // kBandCap floats; reused by refinement
-  double* rv = reinterpret_cast<double*>(cur);    // kRefineCap doubles
-  int* rid = reinterpret_cast<int*>(cur + kRefineCap * sizeof(double));
-  int* chosen = rid + kRefineCap;
+  int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
+  const SelSmem sm = carve(sraw, n);
+  const long long t0 = clock64();
 
   RowReader rd;
   rd.base = p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + grp * p.sel_group) * p.row_stride;
   rd.hstride = p.row_stride;
   rd.sg = p.sel_group;
-  rd.n = n;
-  rd.cache = nullptr;
-
-  // ---- A. brackets from a sorted sample
-  float lo = -INFINITY, hi = INFINITY;
-  if (n > kBandCap && k < n) {
-    float x = rd.load_raw((int)(((int64_t)tid * n) / kSample));
-    x = bitonic1024_desc(x, s_xchg);
-    s_xchg[tid] = x;
-    __syncthreads();
-    const double pr = (double)k / n;
-    const double delta = 3.0 * sqrt(kSample * pr * (1.0 - pr)) + 2.0;
-    const int hi_i = (int)floor(pr * kSample - delta);
-    const int lo_i = (int)ceil(pr * kSample + delta);
-    hi = (hi_i >= 0) ? s_xchg[hi_i] : INFINITY;
-    lo = (lo_i < kSample) ? s_xchg[lo_i] : -INFINITY;
-    __syncthreads();
-  }
-
-  // ---- B. one pass: stage, stats, bracket counts, band collection
-  if (tid == 0) s_misc[0] = 0;
-  __syncthreads();
-  float mabs = 0.f;
-  int bad = 0, cgt = 0, ceqh = 0, ceql = 0;
-  constexpr int U = 4;
-  for (int base4 = 0; base4 < n4; base4 += kSelThreads * U) {
-    float4 vv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i4 = base4 + u * kSelThreads + tid;
-      vv[u] = (i4 < n4) ? rd.load4_raw(i4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    int nb = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i4 = base4 + u * kSelThreads + tid;
-      if (i4 < n4 && cache) reinterpret_cast<float4*>(cache)[i4] = vv[u];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i = 4 * i4 + c;
-        if (i4 < n4 && i < n) {
-          const float v = f4at(vv[u], c);
-          if (!isfinite(v)) bad = 1;
-          else mabs = fmaxf(mabs, fabsf(v));
-          cgt += v > hi;
-          ceqh += v == hi;
-          ceql += (v == lo) && (lo != hi);
-          nb += (v > lo) && (v < hi);
-        }
-      }
-    }
-    int pos = warp_append(nb, &s_misc[0]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i4 = base4 + u * kSelThreads + tid;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i = 4 * i4 + c;
-        if (i4 < n4 && i < n) {
-          const float v = f4at(vv[u], c);
-          if ((v > lo) && (v < hi)) {
-            if (pos < kBandCap) band[pos] = v;
-            ++pos;
-          }
-        }
-      }
-    }
-  }
-  mabs = block_max_float(mabs, fred);
-  bad = block_sum_int(bad, red);
-  cgt = block_sum_int(cgt, red);
-  ceqh = block_sum_int(ceqh, red);
-  ceql = block_sum_int(ceql, red);
-  if (bad && tid == 0) atomicOr(p.flags, 2);
-  rd.cache = cache;
-  const int nin = s_misc[0];
-  __syncthreads();
 
   if (k >= n) {
-    for (int i = tid; i < n; i += kSelThreads) out[i] = i;
-    if (p.info && tid == 0) {
-      int32_t* inf = p.info + row_id * 4;
-      inf[0] = k; inf[1] = 0; inf[2] = 0; inf[3] = 0;
+    // the budget covers the cache: every index (after the non-finite check)
+    float nanacc = 0.f;
+    for (int i = tid; i < n; i += kSelThreads) {
+      nanacc = fmaf(rd.at(i), 0.f, nanacc);
+      out[i] = i;
+    }
+    if (block_sum_int(nanacc != nanacc ? 1 : 0, red) && tid == 0) atomicOr(p.flags, 2);
+    if (info && tid == 0) {
+      for (int j = 0; j < 8; ++j) info[j] = 0;
+      info[0] = k;
     }
     return;
   }
 
-  // ---- C. exact k-th largest value T with c_gt = #(v > T)
-  float T = 0.f;
-  int c_gt = 0, c_eq = 0, mode = 0;
-  bool found = false;
-  if (nin <= kBandCap) {
-    if (k <= cgt) {
-      found = false;
-    } else if (k <= cgt + ceqh) {
-      T = hi; c_gt = cgt; c_eq = ceqh; found = true;
-    } else if (k <= cgt + ceqh + nin) {
-      int above = 0;
-      auto getb = [&](int j) { return band[j]; };
-      radix_select_desc(getb, nin, k - cgt - ceqh, s_hist, s_misc, &T, &above, &c_eq);
-      c_gt = cgt + ceqh + above;
-      found = true;
-    } else if (lo != hi && k <= cgt + ceqh + nin + ceql) {
-      T = lo; c_gt = cgt + ceqh + nin; c_eq = ceql; found = true;
-    }
-  }
-  if (!found) {
-    mode = 1;
-    radix_select_desc(rd, n, k, s_hist, s_misc, &T, &c_gt, &c_eq);
-  }
+  const int nwords = (int)(sel_bitmap_bytes(n) / 4);
+  for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
+  for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+  if (tid == 0) red.misc[3] = red.misc[5] = 0;
 
-  // ---- D. optional float64 boundary refinement
-  float gt_thr = T;     // "definitely selected" strictly above this
-  int need = k - c_gt;  // lowest-index elements equal to T (unrefined)
-  bool refined = false;
-  int n_cand = 0;
-  const float tau = fmaxf(p.tau_rel * mabs, 1e-30f);
-  const float lo_r = T - tau, hi_r = T + tau;
-  if (p.q != nullptr) {
-    if (tid == 0) s_misc[0] = 0;
-    __syncthreads();
-    int above = 0;
-    for (int base4 = 0; base4 < n4; base4 += kSelThreads) {
-      const int i4 = base4 + tid;
-      float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
-      int nb = 0;
-      if (i4 < n4) {
-        vv = rd.get4(i4);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (4 * i4 + c < n) {
-            const float v = f4at(vv, c);
-            above += v > hi_r;
-            nb += (v >= lo_r) && (v <= hi_r);
-          }
-        }
-      }
-      int pos = warp_append(nb, &s_misc[0]);
-      if (nb) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int i = 4 * i4 + c;
-          const float v = f4at(vv, c);
-          if (i < n && (v >= lo_r) && (v <= hi_r)) {
-            if (pos < kRefineCap) rid[pos] = i;
-            ++pos;
-          }
-        }
-      }
-    }
-    above = block_sum_int(above, red);
-    n_cand = s_misc[0];
-    __syncthreads();
-    if (n_cand <= kRefineCap) {
-      // float64 re-score: agg = sum over (kv head of the group, query head g) of q.k/sqrt(d)
-      const int warp = tid >> 5;
-      const int layer = p.layers[slot];
-      const double sqd = sqrt((double)p.D);
-      for (int c = warp; c < n_cand; c += kSelThreads / 32) {
-        const int tok = rid[c];
-        double agg = 0.0;
-        for (int hh = 0; hh < p.sel_group; ++hh) {
-          const int kh = grp * p.sel_group + hh;
-          const int64_t koff = layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
-          for (int g = 0; g < p.G; ++g) {
-            const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D;
-            double part = 0.0;
-            for (int i = lane; i < p.D; i += 32) {
-              if (p.dtype == 0)
-                part += elem_f64<__nv_bfloat16>(p.q, qoff + i) * elem_f64<__nv_bfloat16>(p.k, koff + i);
-              else
-                part += elem_f64<float>(p.q, qoff + i) * elem_f64<float>(p.k, koff + i);
-            }
-            agg += warp_sum_f64(part) / sqd;
-          }
-        }
-        if (lane == 0) rv[c] = agg;
-      }
-      __syncthreads();
-      const int P = next_pow2(max(n_cand, 1));
-      for (int j = n_cand + tid; j < P; j += kSelThreads) {
-        rv[j] = -INFINITY;
-        rid[j] = 0x7fffffff;
-      }
-      __syncthreads();
-      bitonic_desc_f64_idx(rv, rid, P);
-      const int r = k - above;  // picks from the band
-      for (int j = tid; j < P; j += kSelThreads) chosen[j] = (j < r) ? rid[j] : 0x7fffffff;
-      __syncthreads();
-      bitonic_asc_i32(chosen, P);
-      gt_thr = hi_r;
-      need = r;
-      refined = true;
-      n_cand = r;
-    } else if (tid == 0) {
-      atomicOr(p.flags, 4);
-    }
-    __syncthreads();
-  }
-
-  // ---- E. index-ordered compaction: sel(i) = v > gt_thr || (eq(i) && eq_rank(i) < need)
+  // ---- A. brackets [lo, hi] around the k-th rank from a sorted strided sample
+  float x = rd.at((int)(((int64_t)tid * n) / kSelThreads));
+  x = bitonic_desc(x, sm.xchg);
+  sm.xchg[tid] = x;
+  __syncthreads();
+  float hi, lo;
   {
-    const int warp = tid >> 5;
-    int run_gt = 0, run_eq = 0;
-    for (int base4 = 0; base4 < n4; base4 += kSelThreads) {
-      const int i4 = base4 + tid;
-      int fl_gt[4], fl_eq[4];
-      int cnt = 0;
-      float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i4 < n4) vv = rd.get4(i4);
+    const float pr = (float)k / (float)n;
+    const float delta = 3.0f * sqrtf(kSelThreads * pr * (1.0f - pr)) + 2.0f;
+    // clamp to the sample's extremes: for small k/n the sample max still has far fewer
+    // than k scores above it (rank ~ n / kSelThreads), and the bracket test below
+    // re-validates the assumption on the counted row
+    const int hi_i = max(0, (int)floorf(pr * kSelThreads - delta));
+    const int lo_i = min(kSelThreads - 1, (int)ceilf(pr * kSelThreads + delta));
+    hi = sm.xchg[hi_i];
+    lo = sm.xchg[lo_i];
+  }
+  const bool brackets = isfinite(lo) && isfinite(hi) && lo < hi;
+  if (!brackets) {
+    lo = -INFINITY;
+    hi = INFINITY;
+  }
+  const float scale = brackets ? (float)kBins / (hi - lo) : 0.f;
+  auto bin_of = [&](float v) { return min(kBins - 1, (int)((v - lo) * scale)); };
+  const long long t1 = clock64();
+
+  // ---- B. above-bits -> bitmap, [lo, hi] -> histogram, max|s|, non-finite check.
+  // Thread t owns 32 consecutive tokens of each 8K chunk: 8 float4, one bitmap word.
+  const int nch = (n + kChunk - 1) / kChunk;
+  float mabs = 0.f, nanacc = 0.f;
+  int cgt = 0, cin = 0;
+  auto pass_b = [&](int c, bool full) {
+    const int w4 = (c * kChunk + tid * 32) >> 2;
+    float4 vv[8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i = 4 * i4 + c;
-        fl_gt[c] = 0;
-        fl_eq[c] = 0;
-        if (i4 < n4 && i < n) {
-          const float v = f4at(vv, c);
-          if (v > gt_thr) {
-            fl_gt[c] = 1;
-          } else if (!refined) {
-            fl_eq[c] = (v == T);
-          } else if (v >= lo_r) {
-            int a = 0, z = n_cand;
-            while (a < z) {
-              const int mid = (a + z) >> 1;
-              if (chosen[mid] < i) a = mid + 1;
-              else z = mid;
-            }
-            fl_eq[c] = (a < n_cand && chosen[a] == i);
+    for (int u = 0; u < 8; ++u)
+      vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+    uint32_t word = 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const float v = lane4(vv[u], cc);
+        if (full || 4 * (w4 + u) + cc < n) {
+          nanacc = fmaf(v, 0.f, nanacc);  // NaN iff some score is NaN or inf
+          mabs = fmaxf(mabs, fabsf(v));
+          word |= (v > hi) ? (1u << (u * 4 + cc)) : 0u;
+          if (brackets && v >= lo && v <= hi) {
+            atomicAdd(sm.hist + bin_of(v), 1u);
+            ++cin;
           }
         }
-        cnt += fl_gt[c] | (fl_eq[c] << 16);
       }
-      int x = cnt;
+    }
+    sm.bitmap[c * kSelThreads + tid] = word;
+    cgt += __popc(word);
+  };
+  const int nfull = n / kChunk;
+  for (int c = 0; c < nfull; ++c) pass_b(c, true);
+  if (nfull < nch) pass_b(nfull, false);
+  mabs = block_max_float(mabs, red);
+  if (block_sum_int(nanacc != nanacc ? 1 : 0, red) && tid == 0) atomicOr(p.flags, 2);
+  cgt = block_sum_int(cgt, red);
+  cin = block_sum_int(cin, red);
+  const long long t2 = clock64();
+
+  const bool refine = p.q != nullptr;
+  const float tau = fmaxf(p.tau_rel * mabs, 1e-30f);
+  float T = 0.f, lo_w = 0.f, hi_w = 0.f;
+  int above_w = 0, nw = 0, mode = 0;
+  bool fast = brackets && cgt < k && k <= cgt + cin;
+  if (fast) {
+    // ---- C. bin b* holding rank r = k - cgt counted from the top
+    const int r = k - cgt;
+    constexpr int PER = kBins / kSelThreads;  // bins per thread, descending order
+    int hb[PER], s = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      __syncthreads();
-      if (lane == 31) red[warp] = x;
-      __syncthreads();
-      if (warp == 0) {
-        const int w = red[lane];
-        int ws = w;
+    for (int j = 0; j < PER; ++j) {
+      hb[j] = (int)sm.hist[kBins - 1 - (tid * PER + j)];
+      s += hb[j];
+    }
+    int tot;
+    const int ex = block_scan(s, &tot, red);
+    if (ex < r && r <= ex + s) {
+      int acc = ex;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, ws, o);
-          if (lane >= o) ws += y;
+      for (int j = 0; j < PER; ++j) {
+        if (acc < r && r <= acc + hb[j]) {
+          red.misc[1] = kBins - 1 - (tid * PER + j);
+          red.misc[2] = acc;
         }
-        red[lane] = ws - w;
-        if (lane == 31) red[32] = ws;
+        acc += hb[j];
+      }
+    }
+    __syncthreads();
+    const int bstar = red.misc[1], cum_above = red.misc[2];
+    // candidate bins [b_lo, b_hi]: b* widened by the refinement tolerance
+    const int wb = refine ? (int)ceilf(tau * scale) + 1 : 0;
+    const int b_lo = max(0, bstar - wb), b_hi = min(kBins - 1, bstar + wb);
+    int above_bins = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) above_bins += (kBins - 1 - (tid * PER + j) > b_hi) ? hb[j] : 0;
+    above_bins = block_sum_int(above_bins, red);
+
+    // ---- D. second pass (L2): higher bins join the bitmap, candidate bins are collected.
+    // bin_of is monotone, so "bin > b_hi" and "bin >= b_lo" are exact value thresholds,
+    // found once by bisection over the ordered float keys.
+    if (tid < 2) {
+      const int target = (tid == 0) ? b_hi + 1 : b_lo;  // smallest v with bin_of(v) >= target
+      uint32_t a = float_key(lo), z = float_key(hi);     // bin_of(lo)=0, bin_of(hi)=kBins-1
+      if (target <= 0) {
+        red.misc[6 + tid] = __float_as_int(lo);
+      } else if (target > kBins - 1 || bin_of(hi) < target) {
+        red.misc[6 + tid] = __float_as_int(INFINITY);
+      } else {
+        while (a < z) {  // invariant: bin_of(key_float(z)) >= target
+          const uint32_t mid = a + (z - a) / 2;
+          if (bin_of(key_float(mid)) >= target) z = mid;
+          else a = mid + 1;
+        }
+        red.misc[6 + tid] = __float_as_int(key_float(z));
+      }
+    }
+    __syncthreads();
+    const float v_hi = __int_as_float(red.misc[6]);  // v >= v_hi  <=>  bin > b_hi
+    const float v_lo = __int_as_float(red.misc[7]);  // v >= v_lo  <=>  bin >= b_lo
+    auto pass_d = [&](int c, bool full) {
+      const int w4 = (c * kChunk + tid * 32) >> 2;
+      float4 vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+      uint32_t word = 0u, cand = 0u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const float v = lane4(vv[u], cc);
+          const bool ok = full || 4 * (w4 + u) + cc < n;
+          // above hi: already set in pass B; [v_hi, hi]: set now
+          word |= (ok && v >= v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
+          cand |= (ok && v >= v_lo && v < v_hi) ? (1u << (u * 4 + cc)) : 0u;
+        }
+      }
+      if (word) sm.bitmap[c * kSelThreads + tid] |= word;
+      int pos = warp_append(__popc(cand), &red.misc[3]);
+      while (cand) {
+        const int bit = __ffs(cand) - 1;
+        cand &= cand - 1;
+        if (pos < kCandCap) {
+          float e = vv[0].x;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+              if (u * 4 + cc == bit) e = lane4(vv[u], cc);
+          sm.cv[pos] = (double)e;
+          sm.ci[pos] = 4 * w4 + bit;
+        }
+        ++pos;
+      }
+    };
+    for (int c = 0; c < nfull; ++c) pass_d(c, true);
+    if (nfull < nch) pass_d(nfull, false);
+    __syncthreads();
+    const int nc = red.misc[3];
+    fast = nc >= 1 && nc <= kCandCap;
+    if (fast) {
+      // exact T: rank r2 among the members of bin b*
+      const int r2 = r - cum_above;
+      for (int j = tid; j < nc; j += kSelThreads) {
+        const float vj = (float)sm.cv[j];
+        if (bin_of(vj) != bstar) continue;
+        int gt = 0, ge = 0;
+        for (int i = 0; i < nc; ++i) {
+          const float vi = (float)sm.cv[i];
+          if (bin_of(vi) != bstar) continue;
+          gt += vi > vj;
+          ge += vi >= vj;
+        }
+        if (gt < r2 && r2 <= ge) red.misc[4] = __float_as_int(vj);
       }
       __syncthreads();
-      const int pre = red[warp] + x - cnt;
-      int gt_before = run_gt + (pre & 0xffff);
-      int eq_before = run_eq + (pre >> 16);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const bool sel = fl_gt[c] || (fl_eq[c] && eq_before < need);
-        if (sel) {
-          const int pos = gt_before + min(eq_before, need);
-          if (pos < k) out[pos] = 4 * i4 + c;
+      T = __int_as_float(red.misc[4]);
+      lo_w = refine ? T - tau : T;
+      hi_w = refine ? T + tau : T;
+      const int blw = lo_w >= lo ? bin_of(lo_w) : -1;
+      const int bhw = hi_w <= hi ? bin_of(hi_w) : kBins;
+      fast = blw >= b_lo && bhw <= b_hi;  // the window lies inside the candidate bins
+    }
+    if (fast) {
+      // keep the window in place; candidates above it are selected outright
+      int abv = 0;
+      for (int base = 0; base < nc; base += kSelThreads) {
+        const int j = base + tid;
+        double v = 0.0;
+        int ii = 0;
+        bool in = false;
+        if (j < nc) {
+          v = sm.cv[j];
+          ii = sm.ci[j];
+          in = (float)v >= lo_w && (float)v <= hi_w;
+          if ((float)v > hi_w) {
+            atomicOr(sm.bitmap + (ii >> 5), 1u << (ii & 31));
+            ++abv;
+          }
         }
-        gt_before += fl_gt[c];
-        eq_before += fl_eq[c];
+        __syncthreads();
+        const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
+        if (in) {
+          sm.cv[pos] = v;
+          sm.ci[pos] = ii;
+        }
       }
-      const int tot = red[32];
-      run_gt += tot & 0xffff;
-      run_eq += tot >> 16;
+      above_w = cgt + above_bins + block_sum_int(abv, red);
+      nw = red.misc[5];
+      mode = refine ? 2 : 0;
     }
   }
-  if (p.info && tid == 0) {
-    int32_t* inf = p.info + row_id * 4;
-    inf[0] = k;
-    inf[1] = refined ? n_cand : -1;
-    inf[2] = mode + (refined ? 2 : 0);
-    inf[3] = nin;
+  if (!fast) {
+    // ---------------------------------------------------------------- generic path
+    mode = 1;
+    int c_gt = 0;
+    radix_select_row(rd, n, k, red, &T, &c_gt);
+    lo_w = refine ? T - tau : T;
+    hi_w = refine ? T + tau : T;
+    for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
+    if (tid == 0) red.misc[5] = 0;
+    __syncthreads();
+    int abv = 0;
+    for (int base = 0; base < n; base += kSelThreads) {
+      const int i = base + tid;
+      const float v = (i < n) ? rd.at(i) : -INFINITY;
+      const bool in = i < n && v >= lo_w && v <= hi_w;
+      if (i < n && v > hi_w) {
+        atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+        ++abv;
+      }
+      const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
+      if (in && pos < kCandCap) {
+        sm.cv[pos] = (double)v;
+        sm.ci[pos] = i;
+      }
+    }
+    above_w = block_sum_int(abv, red);
+    nw = red.misc[5];
+    if (nw > kCandCap) {
+      // the window cannot be held: resolve the exact fp32 ties at T by index order
+      if (refine && tid == 0) atomicOr(p.flags, 4);
+      if (refine) {
+        for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
+        __syncthreads();
+        for (int base = 0; base < n; base += kSelThreads) {
+          const int i = base + tid;
+          if (i < n && rd.at(i) > T) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+        }
+      }
+      int taken = refine ? c_gt : above_w;
+      for (int base = 0; base < n; base += kSelThreads) {
+        const int i = base + tid;
+        const bool tie = i < n && rd.at(i) == T;
+        int tot;
+        const int pre = block_scan(tie ? 1 : 0, &tot, red);
+        if (tie && taken + pre < k) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+        taken += tot;
+      }
+      nw = 0;
+      mode = 5;
+    }
+  }
+  const long long t3 = clock64();
+
+  // ---- window: re-score (refine) and keep the top k - above_w by (score desc, index asc)
+  if (nw > 0) {
+    __syncthreads();
+    if (refine) {
+      rescore_f64(p, slot, b, grp, sm.ci, sm.cv, nw);
+      __syncthreads();
+    }
+    const int take = k - above_w;
+    for (int j = tid; j < nw; j += kSelThreads) {
+      const double vj = sm.cv[j];
+      const int ij = sm.ci[j];
+      int rank = 0;
+      for (int i = 0; i < nw; ++i) {
+        const double vi = sm.cv[i];
+        rank += (vi > vj) || (vi == vj && sm.ci[i] < ij);
+      }
+      if (rank < take) atomicOr(sm.bitmap + (ij >> 5), 1u << (ij & 31));
+    }
+  }
+  __syncthreads();
+
+  // ---- E. index-ordered compaction of the bitmap
+  int run = 0;
+  for (int c = 0; c < nch; ++c) {
+    const uint32_t w = sm.bitmap[c * kSelThreads + tid];
+    int tot;
+    int pos = run + block_scan(__popc(w), &tot, red);
+    uint32_t m = w;
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      if (pos < k) out[pos] = c * kChunk + tid * 32 + bit;
+      ++pos;
+    }
+    run += tot;
+  }
+  if (info && tid == 0) {
+    info[0] = k;
+    info[1] = nw;
+    info[2] = mode;
+    info[3] = cin;
+    info[4] = (int32_t)(t1 - t0);
+    info[5] = (int32_t)(t2 - t1);
+    info[6] = (int32_t)(t3 - t2);
+    info[7] = (int32_t)(clock64() - t3);
   }
 }
 

@@ -29,7 +29,7 @@ from .errors import ConfigurationError, InvalidInputError, InvalidSelectionError
 from .policy import Action, LayerPolicy, policy_from_actions
 from .profiling import overlap_counts, relative_l2_error, similarity_from_counts
 
-__all__ = ["HybridDecoder", "StepResult", "decode_step", "DecodeRunResult", "FidelityTable",
+__all__ = ["HybridDecoder", "PipelinedDecoder", "StepResult", "decode_step", "DecodeRunResult", "FidelityTable",
            "DecodeTrace", "hybrid_decode", "run_full_trace", "trace_overlap_counts"]
 
 
@@ -135,6 +135,100 @@ class HybridDecoder:
 
     def clear_flags(self) -> None:
         self.ws[:4].zero_()
+
+
+class PipelinedDecoder(HybridDecoder):
+    """Same step as HybridDecoder, scheduled as a two-stream DAG of per-layer launches.
+
+    Every FULL layer is independent of every other once the queries are known, so the
+    FULL kernels stream back to back on the main stream while, on a side stream, each
+    FULL layer's SELECT and then the REUSE layers that inherit its selection run as soon
+    as that layer's scores exist. The latency-bound SELECT and the REUSE gathers overlap
+    the HBM-bound FULL stream; only the last FULL layer's selection is exposed. Captured
+    into a CUDA graph the whole step is one replay.
+
+    schedule="sequential" instead runs the layers strictly in order on one stream (FULL +
+    SELECT or REUSE per layer), the order a real model's decode imposes when layer l+1's
+    query depends on layer l's output.
+    """
+
+    def __init__(self, policy, k_cache, v_cache, budget, *, q_heads, sel_group=1,
+                 refine=True, schedule="pipelined"):
+        super().__init__(policy, k_cache, v_cache, budget, q_heads=q_heads,
+                         sel_group=sel_group, refine=refine)
+        if schedule not in ("pipelined", "sequential"):
+            raise ConfigurationError(f"unknown schedule {schedule!r}")
+        self.schedule = schedule
+        L, B, Hkv, cap, d = k_cache.shape
+        from .attention import scores_row_stride
+        self.scores = torch.empty((len(self.full_layers), B, Hkv, scores_row_stride(cap)),
+                                  dtype=torch.float32, device=k_cache.device)
+        self.side = torch.cuda.Stream(device=k_cache.device)
+        self._events = [torch.cuda.Event() for _ in range(len(self.full_layers) + 2)]
+        # REUSE layers grouped by the FULL slot they inherit from
+        self.reuse_groups = [[l for l in range(L) if self.actions[l] is Action.REUSE
+                              and self.slot_of_layer[l] == s]
+                             for s in range(len(self.full_layers))]
+        self._ws = {}
+        n_reuse_launch = (sum(1 for g in self.reuse_groups if g) if schedule == "pipelined"
+                          else sum(len(g) for g in self.reuse_groups))
+        self.kernels_per_step = len(self.full_layers) * 2 + n_reuse_launch
+
+    def _buf(self, key, nbytes):
+        t = self._ws.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=self.k.device)
+            self._ws[key] = t
+        return t
+
+    def step(self, q: torch.Tensor, n_valid: int | None = None) -> StepResult:
+        lib = _abi.lib()
+        g = self._geometry(q)
+        n_valid = g.capacity if n_valid is None else int(n_valid)
+        k_eff = min(self.budget, n_valid)
+        B, Hkv = g.batch, g.kv_heads
+        groups = Hkv // self.sel_group
+        sc_slot = self.scores[0].numel()
+        idx_slot = self.idx[0].numel()
+        main = torch.cuda.current_stream(self.k.device)
+        side = self.side if self.schedule == "pipelined" else main
+        ws_f = self._buf("full", lib.hylra_attention_workspace_bytes(g, 1, n_valid))
+        sizes = {len(x) if self.schedule == "pipelined" else 1 for x in self.reuse_groups if x}
+        ws_r = self._buf("reuse", max([lib.hylra_attention_workspace_bytes(g, n, k_eff)
+                                       for n in sizes] or [256]))
+        flags = self.ws if self.ws.numel() >= 256 else self._buf("flags", 256)
+        if self.ws.numel() < 256:
+            self.ws = flags
+        qp, kp, vp = q.data_ptr(), self.k.data_ptr(), self.v.data_ptr()
+        outp = self.out.data_ptr()
+        refine_q = qp if self.refine else None
+        refine_k = kp if self.refine else None
+        if side is not main:
+            side.wait_stream(main)
+        for s, f in enumerate(self.full_layers):
+            ids = _abi.int32_array([f])
+            _abi.check(lib.hylra_full_decode(
+                g, qp, kp, vp, n_valid, 1, ids, outp, self.scores.data_ptr() + 4 * s * sc_slot,
+                ws_f.data_ptr(), ws_f.numel(), main.cuda_stream))
+            if side is not main:
+                self._events[s].record(main)
+                side.wait_event(self._events[s])
+            _abi.check(lib.hylra_topk_select(
+                g, self.scores.data_ptr() + 4 * s * sc_slot, 1, n_valid, self.budget,
+                self.sel_group, refine_q, refine_k, ids, self.idx.data_ptr() + 4 * s * idx_slot,
+                self.k_stride, None, flags.data_ptr(), flags.numel(), side.cuda_stream))
+            rg = self.reuse_groups[s]
+            # pipelined: one launch for the whole chain; sequential: one launch per layer
+            launches = [rg] if (rg and self.schedule == "pipelined") else [[l] for l in rg]
+            for grp in launches:
+                _abi.check(lib.hylra_reuse_decode(
+                    g, qp, kp, vp, n_valid, len(grp), _abi.int32_array(grp),
+                    _abi.int32_array([0] * len(grp)), self.idx.data_ptr() + 4 * s * idx_slot,
+                    self.k_stride, k_eff, self.sel_group, outp, ws_r.data_ptr(), ws_r.numel(),
+                    side.cuda_stream))
+        if side is not main:
+            main.wait_stream(side)
+        return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
 
 
 def decode_step(policy, k_cache, v_cache, q, budget: int, n_valid: int | None = None, *,

@@ -214,3 +214,34 @@ def test_policy_must_start_full():
     q, k, v, *_ = make_stack(2, 1, 4, 2, 64, 128, "bf16")
     with pytest.raises(InvalidInputError):
         HybridDecoder(("reuse", "full"), k, v, 8, q_heads=4)
+
+
+@pytest.mark.parametrize("schedule", ["pipelined", "sequential"])
+def test_pipelined_schedules_match_fused(schedule):
+    from paper_2602_00777_b200.engine import PipelinedDecoder
+    L, B, Hq, Hkv, d, cap, budget = 8, 2, 16, 4, 128, 4096, 256
+    q, k, v, qn, kn, vn = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=21, planted=64)
+    actions = ("full", "reuse", "full", "full", "reuse", "reuse", "full", "reuse")
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq).step(q, cap)
+    ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
+    dec = PipelinedDecoder(actions, k, v, budget, q_heads=Hq, schedule=schedule)
+    res = dec.step(q, cap)
+    torch.cuda.synchronize()
+    assert torch.equal(res.selections, ref_idx)
+    o, r = res.outputs.double().cpu().numpy(), ref_out.double().cpu().numpy()
+    assert max_head_err(o, r) < 1e-3
+    # graph capture of the two-stream DAG
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dec.step(q, cap)
+    torch.cuda.current_stream().wait_stream(s)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        dec.step(q, cap)
+    dec.out.zero_()
+    dec.idx.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(dec.idx[..., :budget], ref_idx)
+    assert max_head_err(dec.out.double().cpu().numpy(), r) < 1e-3
