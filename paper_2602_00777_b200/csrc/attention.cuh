@@ -44,6 +44,7 @@ struct AttnParams {
   int tiles_per_split;
   int k_stride, sel_group, n_groups;
   float scale_log2;     // log2(e) / sqrt(d)
+  int prefetch;         // REUSE: L2 prefetch distance in tiles
   float inv_sqrt_d;
   int layers[kMaxSlots];
   int src_slot[kMaxSlots];
@@ -231,6 +232,29 @@ __global__ void __launch_bounds__(160, 2)
         }
         return row;
       };
+      // L2 prefetch of the rows kPrefetch tiles ahead of the shared-memory pipeline: the
+      // scattered 2*D-byte rows have a long loaded latency and shared memory bounds the
+      // bytes in flight, so line prefetches (LSU path; one per 128-byte line) keep HBM
+      // busy beyond the smem ring
+      const int kPrefetch = p.prefetch;
+      auto prefetch_tile = [&](int tile) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int pos = tile * kTileRows + lane + 32 * rr;
+          if (pos < p.n_rows) {
+            int row = __ldg(ib + pos);
+            row = (row < 0 || row >= p.n_valid) ? 0 : row;
+#pragma unroll
+            for (int off = 0; off < D * 2; off += 128) {
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                  reinterpret_cast<const char*>(kbase + (int64_t)row * D) + off));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                  reinterpret_cast<const char*>(vbase + (int64_t)row * D) + off));
+            }
+          }
+        }
+      };
+      for (int t = 0; t < min(kPrefetch, n_my); ++t) prefetch_tile(t_begin + t);
       int nx0 = 0, nx1 = 0;
       if (n_my > 0) {
         nx0 = load_idx(t_begin, 0);
@@ -239,6 +263,7 @@ __global__ void __launch_bounds__(160, 2)
       for (int i = 0; i < n_my; ++i) {
         const int s = i % STAGES;
         const int cur0 = nx0, cur1 = nx1;
+        if (i + kPrefetch < n_my) prefetch_tile(t_begin + i + kPrefetch);
         if (i + 1 < n_my) {
           nx0 = load_idx(t_begin + i + 1, 0);
           nx1 = load_idx(t_begin + i + 1, 1);

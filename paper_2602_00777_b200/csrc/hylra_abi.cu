@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -24,6 +25,9 @@ namespace {
 
 constexpr int kNumSMs = 148;
 constexpr size_t kHeader = 256;
+// REUSE L2 prefetch distance in 64-row tiles (swept on B200 at cfg2: 0/2/3/4/6/8/12 tiles
+// -> 345/306/319/330/357/369/383 us; 2 is best)
+constexpr int kReusePrefetchTiles = 2;
 
 thread_local char g_err[512] = "";
 std::atomic<uint64_t> g_launches{0};
@@ -223,6 +227,7 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   p.n_groups = g->kv_heads / p.sel_group;
   p.inv_sqrt_d = (float)(1.0 / std::sqrt((double)g->head_dim));
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)g->head_dim));
+  p.prefetch = kReusePrefetchTiles;
   for (int i = 0; i < n_layers; ++i) {
     if (layer_ids[i] < 0 || layer_ids[i] >= g->num_layers)
       return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", layer_ids[i]);
