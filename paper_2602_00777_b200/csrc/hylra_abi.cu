@@ -323,7 +323,7 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
 struct StepLayout {
   std::vector<int32_t> full_ids, reuse_ids, reuse_src;
   int k_eff, n_groups;
-  size_t off_scores, off_attn, attn_bytes, total;
+  size_t off_scores, off_attn, attn_bytes, off_attn_r, attn_bytes_r, total;
 };
 
 int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, int budget,
@@ -355,12 +355,14 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   const size_t nf = s->full_ids.size();
   s->off_scores = kHeader;
   const size_t scores_b = sizeof(float) * nf * g->batch * g->kv_heads * scores_row_stride(g);
+  // FULL and REUSE get disjoint attention workspaces: each kernel's split-K counters must
+  // start at zero, and the other launch's partial buffers would otherwise overlap them.
   s->off_attn = align_up(s->off_scores + scores_b, 256);
-  size_t a = attn_layout(g, (int)nf, n_valid).total;
-  if (!s->reuse_ids.empty())
-    a = std::max(a, attn_layout(g, (int)s->reuse_ids.size(), s->k_eff).total);
-  s->attn_bytes = a;
-  s->total = s->off_attn + a;
+  s->attn_bytes = attn_layout(g, (int)nf, n_valid).total;
+  s->off_attn_r = align_up(s->off_attn + s->attn_bytes, 256);
+  s->attn_bytes_r =
+      s->reuse_ids.empty() ? 0 : attn_layout(g, (int)s->reuse_ids.size(), s->k_eff).total;
+  s->total = s->off_attn_r + s->attn_bytes_r;
   return HYLRA_OK;
 }
 
@@ -462,7 +464,7 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
   if (!s.reuse_ids.empty()) {
     if (int e = launch_attention(g, true, q, k, v, n_valid, s.k_eff, (int)s.reuse_ids.size(),
                                  s.reuse_ids.data(), s.reuse_src.data(), idx, k_stride, sel_group,
-                                 out, nullptr, aws, s.attn_bytes, flags, st))
+                                 out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags, st))
       return e;
   }
   return HYLRA_OK;

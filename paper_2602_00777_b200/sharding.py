@@ -74,9 +74,14 @@ def gather_outputs(out_local, plan: ShardPlan, group=None):
 
     if plan.world == 1:
         return out_local
-    buf = torch.empty((plan.world,) + tuple(out_local.shape), dtype=out_local.dtype,
-                      device=out_local.device)
-    dist.all_gather_into_tensor(buf, out_local.contiguous(), group=group)
+    src = out_local.contiguous()
+    if src.is_cuda:
+        buf = torch.empty((plan.world,) + tuple(src.shape), dtype=src.dtype, device=src.device)
+        dist.all_gather_into_tensor(buf, src, group=group)
+    else:  # gloo (CPU tests)
+        parts = [torch.empty_like(src) for _ in range(plan.world)]
+        dist.all_gather(parts, src, group=group)
+        buf = torch.stack(parts)
     if plan.mode == "kvhead":
         # [P, L, B, Hq/P, d] -> [L, B, P*Hq/P, d]
         return buf.permute(1, 2, 0, 3, 4).reshape(

@@ -1,0 +1,85 @@
+"""The C-ABI library loads without a GPU, exports every symbol include/hylra.h declares,
+and maps argument errors to the reference's exception classes (host-side validation runs
+before any CUDA call)."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2602_00777_b200 import _abi
+from paper_2602_00777_b200.errors import ConfigurationError, InvalidInputError
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_symbols():
+    text = (ROOT / "include" / "hylra.h").read_text()
+    # function declarations: "<return type> hylra_name(" at the start of a line
+    pat = r"^(?:const\s+)?\w+\s*\**\s*(hylra_[a-z0-9_]+)\s*\("
+    return sorted(set(re.findall(pat, text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.lib()
+    declared = header_symbols()
+    assert len(declared) >= 14
+    assert sorted(_abi.EXPORTED_SYMBOLS) == declared
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.hylra_abi_version() == 1
+    assert lib.hylra_status_string(3) == b"InvalidSelectionError"
+
+
+def _geom(**kw):
+    g = _abi.Geometry()
+    g.batch, g.q_heads, g.kv_heads, g.head_dim = 1, 8, 2, 64
+    g.capacity, g.dtype, g.num_layers = 2048, _abi.HYLRA_F32, 4
+    g.q_stride_layer, g.q_stride_batch = 8 * 64, 8 * 64
+    g.kv_stride_head = 2048 * 64
+    g.kv_stride_batch = 2 * 2048 * 64
+    g.kv_stride_layer = 2 * 2048 * 64
+    g.out_stride_layer, g.out_stride_batch = 8 * 64, 8 * 64
+    for k, v in kw.items():
+        setattr(g, k, v)
+    return g
+
+
+def test_workspace_queries_are_host_only():
+    lib = _abi.lib()
+    g = _geom()
+    assert lib.hylra_attention_workspace_bytes(g, 2, 2048) > 256
+    acts = _abi.uint8_array([1, 0, 1, 0])
+    assert lib.hylra_decode_step_workspace_bytes(g, acts, 2048, 128, 1) > 0
+    assert lib.hylra_decode_step_workspace_bytes(_geom(q_heads=7), acts, 2048, 128, 1) == 0
+
+
+def test_status_codes_map_to_reference_exceptions():
+    lib = _abi.lib()
+    acts = _abi.uint8_array([0, 1, 1, 0])  # first layer REUSE
+    with pytest.raises(InvalidInputError, match="first layer"):
+        _abi.check(lib.hylra_decode_step(_geom(), None, None, None, 2048, acts, 128, 1, 1,
+                                         None, None, 128, None, 0, None))
+    with pytest.raises(InvalidInputError, match="budget"):
+        _abi.check(lib.hylra_decode_step(_geom(), None, None, None, 2048,
+                                         _abi.uint8_array([1, 0, 1, 0]), 0, 1, 1, None, None,
+                                         128, None, 0, None))
+    with pytest.raises(ConfigurationError, match="multiple"):
+        _abi.check(lib.hylra_decode_step(_geom(q_heads=7), None, None, None, 2048,
+                                         _abi.uint8_array([1, 0, 1, 0]), 128, 1, 1, None, None,
+                                         128, None, 0, None))
+    with pytest.raises(ConfigurationError, match="head_dim"):
+        _abi.check(lib.hylra_full_decode(_geom(head_dim=80), None, None, None, 10, 1,
+                                         _abi.int32_array([0]), None, None, None, 0, None))
+    with pytest.raises(ConfigurationError, match="workspace"):
+        _abi.check(lib.hylra_decode_step(_geom(), 1, 1, 1, 2048,
+                                         _abi.uint8_array([1, 0, 1, 0]), 128, 1, 1, 1, 1, 128,
+                                         None, 0, None))
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    from paper_2602_00777_b200.errors import CudaError
+    monkeypatch.setattr(_abi, "LIB_PATH", tmp_path / "libhylra.so")
+    monkeypatch.setattr(_abi, "_lib", None)
+    with pytest.raises(CudaError, match="not been built"):
+        _abi.lib()

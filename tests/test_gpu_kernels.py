@@ -169,11 +169,16 @@ def test_overlap_counts_exact():
         np.testing.assert_array_equal(c[:, r], ref)
 
 
-@pytest.mark.parametrize("dtype,refine", [("bf16", True), ("f32", True), ("bf16", False)])
-def test_decode_step_matches_oracle(dtype, refine):
-    L, B, Hq, Hkv, d, cap, n_valid, budget = 6, 2, 16, 4, 128, 3000, 2900, 256
+@pytest.mark.parametrize("dtype,refine,actions", [
+    ("bf16", True, ("full", "reuse", "reuse", "full", "reuse", "full")),
+    ("f32", True, ("full", "reuse", "reuse", "full", "reuse", "full")),
+    ("bf16", False, ("full", "reuse", "reuse", "full", "reuse", "full")),
+    # many more REUSE than FULL (layer, b, head) pairs: disjoint split-K workspaces
+    ("bf16", True, ("full",) + ("reuse",) * 13),
+])
+def test_decode_step_matches_oracle(dtype, refine, actions):
+    L, B, Hq, Hkv, d, cap, n_valid, budget = len(actions), 2, 16, 4, 128, 3000, 2900, 256
     q, k, v, qn, kn, vn = make_stack(L, B, Hq, Hkv, d, cap, dtype, seed=5, planted=64)
-    actions = ("full", "reuse", "reuse", "full", "reuse", "full")
     dec = HybridDecoder(actions, k, v, budget, q_heads=Hq)
     dec.refine = refine
     res = dec.step(q, n_valid)
