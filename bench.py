@@ -189,6 +189,48 @@ def _ncu_traffic():
         return {}
 
 
+def _read_stream_gbs(torch):
+    """Context for the roofline: a read-only stream (torch.sum over 8 GiB of int64), the
+    ceiling a pure-read kernel can approach; the reported frac uses MEASURED_PEAKS.json."""
+    x = torch.ones(1 << 30, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        x.sum()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        x.sum()
+    e1.record()
+    torch.cuda.synchronize()
+    gbs = 10 * x.numel() * 8 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del x
+    torch.cuda.empty_cache()
+    return gbs
+
+
+def _sanity_check(torch, cfg, q, k, v, dec):
+    """Plain PyTorch fp32 attention for one FULL and one REUSE (layer, b, head) of the
+    replayed step, so a bench number never comes from a silently wrong step."""
+    dec.check_flags()
+    G = q.shape[2] // k.shape[2]
+    errs = {}
+    for l in (cfg.full_layers[0], next((x for x in range(cfg.layers)
+                                        if cfg.actions[x] == "reuse"), cfg.full_layers[0])):
+        b, hq = 0, q.shape[2] - 1
+        kh = hq // G
+        kk = k[l, b, kh, :cfg.context].float()
+        vv = v[l, b, kh, :cfg.context].float()
+        if cfg.actions[l] == "reuse":
+            sel = dec.idx[dec.slot_of_layer[l], b, kh].long()
+            kk, vv = kk[sel], vv[sel]
+        w = torch.softmax(kk @ q[l, b, hq].float() / (k.shape[-1] ** 0.5), dim=0)
+        ref = w @ vv
+        got = dec.out[l, b, hq]
+        errs[f"layer{l}_{cfg.actions[l]}"] = float((got - ref).norm() / ref.norm())
+    if max(errs.values()) > 2e-2:
+        raise RuntimeError(f"bench sanity check failed: {errs}")
+    return {"rel_err_vs_torch_fp32": errs, "flags": "clear"}
+
+
 def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     from paper_2602_00777_b200 import _abi
     from paper_2602_00777_b200.attention import geometry, scores_row_stride
@@ -267,6 +309,8 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
         del g2, d2
     dec = make(a.schedule)
     graph = capture(dec)
+
+    check = _sanity_check(torch, cfg, q, k, v, dec)
 
     clocks = ClockSampler(_env_int("LOCAL_RANK", 0))
     clocks.start()
@@ -401,7 +445,7 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                                "per launch)",
                      "traffic": ncu.get("full_traffic_bytes_per_launch")},
         "gpu_launches": dec.kernels_per_step * a.steps,
-        "schedules": schedules,
+        "schedules": schedules, "check": check,
         "e2e": e2e_line, "clocks": clk,
     }
     del graph, dec, q, k, v, scores
@@ -424,6 +468,8 @@ def run_ours(a):
     cfg = CONFIGS[a.config]
     batch = a.batch or cfg.batch
     main = measure_config(a, cfg, batch, rank, world, torch, dist)
+
+    read_peak = _read_stream_gbs(torch) if rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -460,9 +506,11 @@ def run_ours(a):
                     "10% drift; stands in for model traces)",
             "config": _config_dict(cfg, main["global_batch"], world),
             "step_hbm_gbs": main["step_gbs"],
+            "read_stream_gbs_torch_sum": read_peak,
             "roofline": main["roofline"], "kernels": main["kernels"],
             "cpu_baseline": cpu, "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
-            "clocks": main["clocks"], "schedules": main["schedules"], "extra": extra,
+            "clocks": main["clocks"], "schedules": main["schedules"], "check": main["check"],
+            "extra": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
