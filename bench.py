@@ -375,51 +375,42 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     reuse_bytes = len(reuse_ids) * B * Hkv * 2 * k_eff * d * es
     step_bytes = full_bytes + reuse_bytes
 
-    # ---- e2e through the public API with host buffers
+    # ---- e2e through the public API with host buffers: DecodeLoop = H2D(q, new K/V row)
+    #      -> append -> hybrid step -> D2H(outputs), one CUDA-graph launch + sync per step
     e2e_line = None
     if e2e:
+        from paper_2602_00777_b200.engine import DecodeLoop
         pos = cfg.context - 1
-        q_h = torch.empty(q.shape, dtype=q.dtype).pin_memory()
-        q_h.copy_(q.cpu())
-        kn_h = torch.empty((L, B, Hkv, d), dtype=k.dtype).pin_memory()
-        vn_h = torch.empty((L, B, Hkv, d), dtype=v.dtype).pin_memory()
-        kn_h.copy_(k[:, :, :, pos].cpu())
-        vn_h.copy_(v[:, :, :, pos].cpu())
-        out_h = torch.empty(dec.out.shape, dtype=torch.float32).pin_memory()
-        q_dev = torch.empty_like(q)
-
-        def e2e_step():
-            q_dev.copy_(q_h, non_blocking=True)
-            k[:, :, :, pos].copy_(kn_h, non_blocking=True)
-            v[:, :, :, pos].copy_(vn_h, non_blocking=True)
-            res = dec.step(q_dev, pos + 1)
-            out = gather_outputs(res.outputs, plan) if world > 1 else res.outputs
-            if world > 1:
-                out_h_full = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
-                out_h_full.copy_(out, non_blocking=True)
-            else:
-                out_h.copy_(out, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-
+        loop = DecodeLoop(dec, pos)
+        loop.q_host.copy_(q.cpu())
+        loop.k_host.copy_(k[:, :, :, pos].cpu())
+        loop.v_host.copy_(v[:, :, :, pos].cpu())
+        loop.capture()
         for _ in range(3):
-            e2e_step()
+            loop.run()
+            if world > 1:
+                gather_outputs(dec.out, plan)
         if world > 1:
             dist.barrier()
         n_e2e = max(10, a.steps)
         t0 = time.perf_counter()
         for _ in range(n_e2e):
-            e2e_step()
+            loop.run()
+            if world > 1:
+                gather_outputs(dec.out, plan)
+                torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / n_e2e
         if world > 1:
             tt = torch.tensor([t_e2e], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
-        h2d = q.numel() * q.element_size() + 2 * kn_h.numel() * kn_h.element_size()
-        d2h = dec.out.numel() * 4 * (world if world > 1 else 1)
         e2e_line = {"value": global_batch / t_e2e, "unit": "tok/s",
-                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "h2d_bytes_per_step": int(loop.h2d_bytes),
+                    "d2h_bytes_per_step": int(loop.d2h_bytes),
                     "ms_per_step": t_e2e * 1e3,
-                    "path": "HybridDecoder.step (eager C-ABI call) + pinned H2D/D2H, wall clock"}
+                    "path": "DecodeLoop.run(): pinned H2D (q + new K/V rows) -> append -> "
+                            "hybrid step -> D2H fp32 outputs, one graph launch + host sync "
+                            "per step, wall clock"}
     clk = clocks.stop()
 
     peaks = _peaks()

@@ -29,7 +29,7 @@ from .errors import ConfigurationError, InvalidInputError, InvalidSelectionError
 from .policy import Action, LayerPolicy, policy_from_actions
 from .profiling import overlap_counts, relative_l2_error, similarity_from_counts
 
-__all__ = ["HybridDecoder", "PipelinedDecoder", "StepResult", "decode_step", "DecodeRunResult", "FidelityTable",
+__all__ = ["HybridDecoder", "PipelinedDecoder", "DecodeLoop", "StepResult", "decode_step", "DecodeRunResult", "FidelityTable",
            "DecodeTrace", "hybrid_decode", "run_full_trace", "trace_overlap_counts"]
 
 
@@ -229,6 +229,66 @@ class PipelinedDecoder(HybridDecoder):
         if side is not main:
             main.wait_stream(side)
         return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
+
+
+class DecodeLoop:
+    """One decode step with host I/O as a single CUDA-graph launch.
+
+    Per step: the query [L, B, Hq, d] and the new token's key/value rows [L, B, Hkv, d]
+    are copied from pinned host buffers (`q_host`, `k_host`, `v_host`), the K/V rows are
+    appended at cache row `pos`, the hybrid step runs over `pos + 1` rows, and the fp32
+    outputs land in the pinned `out_host`. Fill the host buffers, call `run()`; it returns
+    `out_host` after the step completed.
+    """
+
+    def __init__(self, decoder: HybridDecoder, pos: int):
+        k = decoder.k
+        L, B, Hkv, cap, d = k.shape
+        if not 0 <= pos < cap:
+            raise InvalidInputError(f"pos {pos} outside the cache capacity {cap}")
+        self.dec, self.pos = decoder, int(pos)
+        dt = k.dtype
+        Hq = decoder.q_heads
+        self.q_host = torch.zeros((L, B, Hq, d), dtype=dt).pin_memory()
+        self.k_host = torch.zeros((L, B, Hkv, d), dtype=dt).pin_memory()
+        self.v_host = torch.zeros((L, B, Hkv, d), dtype=dt).pin_memory()
+        self.out_host = torch.zeros((L, B, Hq, d), dtype=torch.float32).pin_memory()
+        self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
+        self.kv_dev = torch.zeros((2, L, B, Hkv, d), dtype=dt, device=k.device)
+        self.graph = None
+        self.h2d_bytes = (self.q_host.numel() + 2 * self.k_host.numel()) * self.q_host.element_size()
+        self.d2h_bytes = self.out_host.numel() * 4
+
+    def _body(self):
+        dec, pos = self.dec, self.pos
+        self.q_dev.copy_(self.q_host, non_blocking=True)
+        self.kv_dev[0].copy_(self.k_host, non_blocking=True)
+        self.kv_dev[1].copy_(self.v_host, non_blocking=True)
+        dec.k[:, :, :, pos].copy_(self.kv_dev[0])
+        dec.v[:, :, :, pos].copy_(self.kv_dev[1])
+        dec.step(self.q_dev, pos + 1)
+        self.out_host.copy_(dec.out, non_blocking=True)
+
+    def capture(self):
+        """Warm up and capture the step (host copies included) into a CUDA graph."""
+        s = torch.cuda.Stream(device=self.dec.k.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                self._body()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._body()
+        return self
+
+    def run(self) -> torch.Tensor:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+        torch.cuda.current_stream().synchronize()
+        return self.out_host
 
 
 def decode_step(policy, k_cache, v_cache, q, budget: int, n_valid: int | None = None, *,

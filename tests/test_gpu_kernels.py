@@ -250,3 +250,30 @@ def test_pipelined_schedules_match_fused(schedule):
     torch.cuda.synchronize()
     assert torch.equal(dec.idx[..., :budget], ref_idx)
     assert max_head_err(dec.out.double().cpu().numpy(), r) < 1e-3
+
+
+def test_decode_loop_host_io_graph():
+    """DecodeLoop: H2D (q + new K/V row) -> append -> step -> D2H in one graph launch."""
+    from paper_2602_00777_b200.engine import DecodeLoop
+    L, B, Hq, Hkv, d, cap, budget = 4, 2, 8, 2, 128, 2048, 128
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=13, planted=16)
+    actions = ("full", "reuse", "full", "reuse")
+    dec = HybridDecoder(actions, k.clone(), v.clone(), budget, q_heads=Hq)
+    pos = 1500
+    loop = DecodeLoop(dec, pos)
+    g = torch.Generator().manual_seed(3)
+    for step in range(3):
+        qh = torch.randn((L, B, Hq, d), generator=g).to(torch.bfloat16)
+        kh = torch.randn((L, B, Hkv, d), generator=g).to(torch.bfloat16)
+        vh = torch.randn((L, B, Hkv, d), generator=g).to(torch.bfloat16)
+        loop.q_host.copy_(qh)
+        loop.k_host.copy_(kh)
+        loop.v_host.copy_(vh)
+        out = loop.run().clone()
+        # eager reference on a separate cache with the same appended row
+        k2, v2 = k.clone(), v.clone()
+        k2[:, :, :, pos] = kh.cuda()
+        v2[:, :, :, pos] = vh.cuda()
+        ref = HybridDecoder(actions, k2, v2, budget, q_heads=Hq).step(qh.cuda(), pos + 1)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref.outputs.cpu())
