@@ -486,6 +486,20 @@ def run_ours(a):
                                                         "kernels", "roofline", "schedules")}
         except Exception as exc:  # noqa: BLE001
             extra["cfg3_128k_b4"] = {"error": str(exc)}
+        c4 = CONFIGS["cfg4"]
+        try:
+            r4 = measure_config(a, c4, c4.batch, rank, world, torch, dist, e2e=False)
+            extra["cfg4_qwen_64k_b16"] = {k: r4[k] for k in ("value", "ms_per_step", "step_gbs",
+                                                             "kernels", "roofline", "schedules")}
+        except Exception as exc:  # noqa: BLE001
+            extra["cfg4_qwen_64k_b16"] = {"error": str(exc)}
+        for b_small in (1, 4):
+            try:
+                rb = measure_config(a, cfg, b_small, rank, world, torch, dist, e2e=False)
+                extra[f"{cfg.name}_b{b_small}"] = {k: rb[k] for k in ("value", "ms_per_step",
+                                                                     "step_gbs", "kernels")}
+            except Exception as exc:  # noqa: BLE001
+                extra[f"{cfg.name}_b{b_small}"] = {"error": str(exc)}
 
     if rank == 0:
         line = {

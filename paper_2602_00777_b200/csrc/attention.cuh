@@ -22,6 +22,7 @@ constexpr int kMaxSlots = 64;   // layer slots per launch
 constexpr int kTileRows = 64;   // rows per pipeline stage
 constexpr int kConsumerWarps = 4;
 constexpr int kMaxG = 16;
+constexpr int kIdxStage = 2048;  // REUSE: indices staged in shared memory per CTA
 
 struct AttnParams {
   const void* q;
@@ -222,15 +223,35 @@ __global__ void __launch_bounds__(160, 2)
       constexpr int RPI = 32 / CH;  // rows per instruction
       const int my_ch = lane % CH;
       const int my_sub = lane / CH;
-      // indices of the next tile are loaded one stage ahead (2 per lane: rows lane, lane+32)
-      auto load_idx = [&](int tile, int rr) -> int {
-        const int pos = tile * kTileRows + lane + 32 * rr;
-        int row = (pos < p.n_rows) ? __ldg(ib + pos) : 0;
+      // The CTA's whole index range is staged (validated) in shared memory once, so neither
+      // the copies nor the L2 prefetches wait on a dependent global index load.
+      int32_t* sidx = reinterpret_cast<int32_t*>(smem + STAGES * SM::kStageBytes + 256);
+      const int pos_begin = t_begin * kTileRows;
+      const int n_pos = min(p.n_rows, t_end * kTileRows) - pos_begin;
+      const bool staged = n_pos <= kIdxStage;
+      if (staged) {
+        for (int j = lane; j < n_pos; j += 32) {
+          int row = __ldg(ib + pos_begin + j);
+          if (row < 0 || row >= p.n_valid) {
+            atomicOr(p.flags, 1);
+            row = 0;
+          }
+          sidx[j] = row;
+        }
+        __syncwarp();
+      }
+      auto row_at = [&](int pos) -> int {  // pos < p.n_rows
+        if (staged) return sidx[pos - pos_begin];
+        int row = __ldg(ib + pos);
         if (row < 0 || row >= p.n_valid) {
-          if (pos < p.n_rows) atomicOr(p.flags, 1);
+          atomicOr(p.flags, 1);
           row = 0;
         }
         return row;
+      };
+      auto load_idx = [&](int tile, int rr) -> int {
+        const int pos = tile * kTileRows + lane + 32 * rr;
+        return (pos < p.n_rows) ? row_at(pos) : 0;
       };
       // L2 prefetch of the rows kPrefetch tiles ahead of the shared-memory pipeline: the
       // scattered 2*D-byte rows have a long loaded latency and shared memory bounds the
@@ -242,8 +263,7 @@ __global__ void __launch_bounds__(160, 2)
         for (int rr = 0; rr < 2; ++rr) {
           const int pos = tile * kTileRows + lane + 32 * rr;
           if (pos < p.n_rows) {
-            int row = __ldg(ib + pos);
-            row = (row < 0 || row >= p.n_valid) ? 0 : row;
+            const int row = row_at(pos);
 #pragma unroll
             for (int off = 0; off < D * 2; off += 128) {
               asm volatile("prefetch.global.L2 [%0];" ::"l"(
@@ -263,7 +283,7 @@ __global__ void __launch_bounds__(160, 2)
       for (int i = 0; i < n_my; ++i) {
         const int s = i % STAGES;
         const int cur0 = nx0, cur1 = nx1;
-        if (i + kPrefetch < n_my) prefetch_tile(t_begin + i + kPrefetch);
+        if (kPrefetch > 0 && i + kPrefetch < n_my) prefetch_tile(t_begin + i + kPrefetch);
         if (i + 1 < n_my) {
           nx0 = load_idx(t_begin + i + 1, 0);
           nx1 = load_idx(t_begin + i + 1, 1);

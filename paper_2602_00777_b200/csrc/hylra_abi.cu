@@ -25,9 +25,10 @@ namespace {
 
 constexpr int kNumSMs = 148;
 constexpr size_t kHeader = 256;
-// REUSE L2 prefetch distance in 64-row tiles (swept on B200 at cfg2: 0/2/3/4/6/8/12 tiles
-// -> 345/306/319/330/357/369/383 us; 2 is best)
-constexpr int kReusePrefetchTiles = 2;
+// REUSE L2 prefetch distance in 64-row tiles. Swept on B200 at cfg2 B=8 once the CTA's
+// indices are staged in shared memory: 0/1/2/3/4/6/8/12/16 tiles -> 305.6/307.0/311.1/
+// 314.8/318.5/329.8/338.5/346.9/347.9 us (before staging, 2 tiles won: 306 vs 345 us).
+constexpr int kReusePrefetchTiles = 0;
 
 thread_local char g_err[512] = "";
 std::atomic<uint64_t> g_launches{0};
@@ -146,7 +147,8 @@ constexpr int mma_stages() {
 }
 template <int D, bool GATHER, bool GBIG>
 size_t mma_smem_bytes() {
-  return (size_t)mma_stages<D, GATHER, GBIG>() * MmaSmem<D>::kStageBytes + 1024 + 256;
+  return (size_t)mma_stages<D, GATHER, GBIG>() * MmaSmem<D>::kStageBytes + 1024 + 256 +
+         (GATHER ? kIdxStage * sizeof(int32_t) : 0);
 }
 
 template <int D, bool GATHER, bool GBIG>

@@ -325,77 +325,138 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
   if (tid == 0) red.misc[3] = red.misc[5] = 0;
 
-  // ---- A. brackets [lo, hi] around the k-th rank from a sorted strided sample
-  float x = rd.at((int)(((int64_t)tid * n) / kSelThreads));
-  x = bitonic_desc(x, sm.xchg);
-  sm.xchg[tid] = x;
-  __syncthreads();
+  // ---- A. brackets [lo, hi] around the k-th rank from 4 x 256 strided samples: their
+  //         quantiles are read off a 1024-bin histogram over [sample min, sample max]
+  //         (no sort); edges are widened outward so the bracket stays conservative
+  constexpr int kS = 4 * kSelThreads;
+  float smp[4];
+  float smin = INFINITY, smax = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    smp[j] = rd.at((int)(((int64_t)(tid + j * kSelThreads) * n) / kS));
+    smin = fminf(smin, smp[j]);
+    smax = fmaxf(smax, smp[j]);
+  }
+  smax = block_max_float(smax, red);
+  smin = -block_max_float(-smin, red);
   float hi, lo;
   {
     const float pr = (float)k / (float)n;
-    const float delta = 3.0f * sqrtf(kSelThreads * pr * (1.0f - pr)) + 2.0f;
-    // clamp to the sample's extremes: for small k/n the sample max still has far fewer
-    // than k scores above it (rank ~ n / kSelThreads), and the bracket test below
-    // re-validates the assumption on the counted row
-    const int hi_i = max(0, (int)floorf(pr * kSelThreads - delta));
-    const int lo_i = min(kSelThreads - 1, (int)ceilf(pr * kSelThreads + delta));
-    hi = sm.xchg[hi_i];
-    lo = sm.xchg[lo_i];
+    const float delta = 3.0f * sqrtf(kS * pr * (1.0f - pr)) + 2.0f;
+    const int hi_i = max(0, (int)floorf(pr * kS - delta));        // ranks from the top
+    const int lo_i = min(kS - 1, (int)ceilf(pr * kS + delta));
+    const float sscale = (smax > smin) ? 1024.f / (smax - smin) : 0.f;
+    auto sbin = [&](float v) { return min(1023, max(0, (int)((v - smin) * sscale))); };
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (isfinite(smp[j])) atomicAdd(sm.hist + sbin(smp[j]), 1u);
+    __syncthreads();
+    // thread t scans bins 1023-4t .. 1020-4t (descending)
+    int hb[4], s4 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      hb[j] = (int)sm.hist[1023 - (tid * 4 + j)];
+      s4 += hb[j];
+    }
+    int tot;
+    const int ex = block_scan(s4, &tot, red);
+    int acc = ex;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int bin = 1023 - (tid * 4 + j);
+      // samples ranked [acc, acc + hb[j]) from the top live in this bin
+      if (acc <= hi_i && hi_i < acc + hb[j]) red.misc[12] = bin;
+      if (acc <= lo_i && lo_i < acc + hb[j]) red.misc[13] = bin;
+      acc += hb[j];
+    }
+    if (tid == 0) red.misc[3] = red.misc[5] = 0;
+    __syncthreads();
+    const int bh = red.misc[12], bl = red.misc[13];
+    // hi: upper edge of the hi_i-th sample's bin (the top sample's bin: the sample max);
+    // lo: lower edge of the lo_i-th sample's bin
+    hi = (bh >= 1023) ? smax : smin + (float)(bh + 1) / sscale;
+    lo = smin + (float)bl / sscale;
+    for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+    __syncthreads();
   }
-  const bool brackets = isfinite(lo) && isfinite(hi) && lo < hi;
-  if (!brackets) {
-    lo = -INFINITY;
-    hi = INFINITY;
-  }
-  const float scale = brackets ? (float)kBins / (hi - lo) : 0.f;
-  auto bin_of = [&](float v) { return min(kBins - 1, (int)((v - lo) * scale)); };
   const long long t1 = clock64();
 
   // ---- B. above-bits -> bitmap, [lo, hi] -> histogram, max|s|, non-finite check.
   // Thread t owns 32 consecutive tokens of each 8K chunk: 8 float4, one bitmap word.
+  // One retry with a bracket reaching the row's max (or min) if the sample bracket missed.
   const int nch = (n + kChunk - 1) / kChunk;
-  float mabs = 0.f, nanacc = 0.f;
-  int cgt = 0, cin = 0;
-  auto pass_b = [&](int c, bool full) {
-    const int w4 = (c * kChunk + tid * 32) >> 2;
-    float4 vv[8];
+  const int nfull = n / kChunk;
+  float mabs = 0.f, vmax = -INFINITY, vmin = INFINITY;
+  int cgt = 0, cin = 0, bad = 0;
+  bool brackets = false;
+  float scale = 0.f;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    brackets = isfinite(lo) && isfinite(hi) && lo < hi;
+    if (!brackets) {
+      lo = -INFINITY;
+      hi = INFINITY;
+    }
+    scale = brackets ? (float)kBins / (hi - lo) : 0.f;
+    const float blo = lo, bhi = hi, bsc = scale;
+    float nanacc = 0.f;
+    int cg = 0, ci = 0;
+    auto pass_b = [&](int c, bool full) {
+      const int w4 = (c * kChunk + tid * 32) >> 2;
+      float4 vv[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
-    uint32_t word = 0u;
+      for (int u = 0; u < 8; ++u)
+        vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+      uint32_t word = 0u;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 8; ++u) {
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const float v = lane4(vv[u], cc);
-        if (full || 4 * (w4 + u) + cc < n) {
-          nanacc = fmaf(v, 0.f, nanacc);  // NaN iff some score is NaN or inf
-          mabs = fmaxf(mabs, fabsf(v));
-          word |= (v > hi) ? (1u << (u * 4 + cc)) : 0u;
-          if (brackets && v >= lo && v <= hi) {
-            atomicAdd(sm.hist + bin_of(v), 1u);
-            ++cin;
+        for (int cc = 0; cc < 4; ++cc) {
+          const float v = lane4(vv[u], cc);
+          if (full || 4 * (w4 + u) + cc < n) {
+            nanacc = fmaf(v, 0.f, nanacc);  // NaN iff some score is NaN or inf
+            vmax = fmaxf(vmax, v);
+            vmin = fminf(vmin, v);
+            word |= (v > bhi) ? (1u << (u * 4 + cc)) : 0u;
+            if (brackets && v >= blo && v <= bhi) {
+              atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
+              ++ci;
+            }
           }
         }
       }
+      sm.bitmap[c * kSelThreads + tid] = word;
+      cg += __popc(word);
+    };
+    for (int c = 0; c < nfull; ++c) pass_b(c, true);
+    if (nfull < nch) pass_b(nfull, false);
+    vmax = block_max_float(vmax, red);
+    vmin = -block_max_float(-vmin, red);
+    bad = block_sum_int(nanacc != nanacc ? 1 : 0, red);
+    cgt = block_sum_int(cg, red);
+    cin = block_sum_int(ci, red);
+    mabs = fmaxf(fabsf(vmax), fabsf(vmin));
+    if (bad || !brackets || (cgt < k && k <= cgt + cin) || attempt == 1) break;
+    // retry once: the k-th value lies above hi (too many above) or below lo
+    if (cgt >= k) {
+      lo = hi;
+      hi = vmax;
+    } else {
+      hi = lo;
+      lo = vmin;
     }
-    sm.bitmap[c * kSelThreads + tid] = word;
-    cgt += __popc(word);
-  };
-  const int nfull = n / kChunk;
-  for (int c = 0; c < nfull; ++c) pass_b(c, true);
-  if (nfull < nch) pass_b(nfull, false);
-  mabs = block_max_float(mabs, red);
-  if (block_sum_int(nanacc != nanacc ? 1 : 0, red) && tid == 0) atomicOr(p.flags, 2);
-  cgt = block_sum_int(cgt, red);
-  cin = block_sum_int(cin, red);
+    for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+    __syncthreads();
+  }
+  if (bad && tid == 0) atomicOr(p.flags, 2);
+  auto bin_of = [&](float v) { return min(kBins - 1, (int)((v - lo) * scale)); };
   const long long t2 = clock64();
 
   const bool refine = p.q != nullptr;
   const float tau = fmaxf(p.tau_rel * mabs, 1e-30f);
   float T = 0.f, lo_w = 0.f, hi_w = 0.f;
-  int above_w = 0, nw = 0, mode = 0;
+  int above_w = 0, nw = 0, mode = 0, why = 0;
   bool fast = brackets && cgt < k && k <= cgt + cin;
+  if (!fast) why = !brackets ? 16 : (cgt >= k ? 32 : 48);
   if (fast) {
     // ---- C. bin b* holding rank r = k - cgt counted from the top
     const int r = k - cgt;
@@ -492,6 +553,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
     __syncthreads();
     const int nc = red.misc[3];
     fast = nc >= 1 && nc <= kCandCap;
+    if (!fast) why = 64;
     if (fast) {
       // exact T: rank r2 among the members of bin b*
       const int r2 = r - cum_above;
@@ -514,6 +576,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
       const int blw = lo_w >= lo ? bin_of(lo_w) : -1;
       const int bhw = hi_w <= hi ? bin_of(hi_w) : kBins;
       fast = blw >= b_lo && bhw <= b_hi;  // the window lies inside the candidate bins
+      if (!fast) why = 80;
     }
     if (fast) {
       // keep the window in place; candidates above it are selected outright
@@ -546,7 +609,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   }
   if (!fast) {
     // ---------------------------------------------------------------- generic path
-    mode = 1;
+    mode = 1 + why;
     int c_gt = 0;
     radix_select_row(rd, n, k, red, &T, &c_gt);
     lo_w = refine ? T - tau : T;
