@@ -51,6 +51,34 @@ struct AttnParams {
   int src_slot[kMaxSlots];
 };
 
+// Stage n selection indices from global into shared memory, validated (out-of-range ->
+// row 0 + HYLRA_FLAG_INDEX_OUT_OF_RANGE). One warp; 8 independent loads in flight per lane.
+__device__ __forceinline__ void stage_indices(const int32_t* __restrict__ src, int n, int n_valid,
+                                              int32_t* dst, int* flags, int lane) {
+  constexpr int U = 8;
+  for (int j0 = 0; j0 < n; j0 += 32 * U) {
+    int r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * 32 + lane;
+      r[u] = (j < n) ? __ldg(src + j) : 0;
+    }
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * 32 + lane;
+      if (j < n) {
+        if (r[u] < 0 || r[u] >= n_valid) {
+          bad = true;
+          r[u] = 0;
+        }
+        dst[j] = r[u];
+      }
+    }
+    if (bad) atomicOr(flags, 1);
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // Cross-warp merge + split-K combine (shared by both kernel families).
 // sm_m/sm_l: [4][16], sm_o: [4][16][D] partial states of the 4 consumer warps, with
@@ -230,14 +258,7 @@ __global__ void __launch_bounds__(160, 2)
       const int n_pos = min(p.n_rows, t_end * kTileRows) - pos_begin;
       const bool staged = n_pos <= kIdxStage;
       if (staged) {
-        for (int j = lane; j < n_pos; j += 32) {
-          int row = __ldg(ib + pos_begin + j);
-          if (row < 0 || row >= p.n_valid) {
-            atomicOr(p.flags, 1);
-            row = 0;
-          }
-          sidx[j] = row;
-        }
+        stage_indices(ib + pos_begin, n_pos, p.n_valid, sidx, p.flags, lane);
         __syncwarp();
       }
       auto row_at = [&](int pos) -> int {  // pos < p.n_rows

@@ -74,6 +74,10 @@ int choose_splits(int pairs, int tiles) {
   return (tiles + tps - 1) / tps;
 }
 
+bool use_mma_path(const hylra_geometry* g) {
+  return g->dtype == HYLRA_BF16 && (g->head_dim == 64 || g->head_dim == 128);
+}
+
 struct AttnLayout {
   int pairs, splits, tiles, tps;
   size_t off_counters, off_ml, off_o, total;
@@ -86,11 +90,12 @@ AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows) {
   a.tiles = std::max(1, (rows + kTileRows - 1) / kTileRows);
   a.splits = choose_splits(a.pairs, a.tiles);
   a.tps = (a.tiles + a.splits - 1) / a.splits;
+  const size_t parts = a.splits;  // partial slots per pair
   a.off_counters = kHeader;
   a.off_ml = align_up(a.off_counters + sizeof(int) * a.pairs, 256);
-  a.off_o = align_up(a.off_ml + sizeof(float) * 2 * (size_t)a.pairs * a.splits * G, 256);
-  a.total = align_up(a.off_o + sizeof(float) * (size_t)a.pairs * a.splits * G * g->head_dim, 256);
-  if (a.splits == 1) a.total = align_up(a.off_counters + sizeof(int) * a.pairs, 256);
+  a.off_o = align_up(a.off_ml + sizeof(float) * 2 * (size_t)a.pairs * parts * G, 256);
+  a.total = align_up(a.off_o + sizeof(float) * (size_t)a.pairs * parts * G * g->head_dim, 256);
+  if (parts == 1) a.total = align_up(a.off_counters + sizeof(int) * a.pairs, 256);
   return a;
 }
 
@@ -187,10 +192,6 @@ cudaError_t dispatch_simt(int D, int G, dim3 grid, cudaStream_t st, const AttnPa
   HY_SIMT_D(128)
 #undef HY_SIMT_D
   return cudaErrorInvalidValue;
-}
-
-bool use_mma_path(const hylra_geometry* g) {
-  return g->dtype == HYLRA_BF16 && (g->head_dim == 64 || g->head_dim == 128);
 }
 
 int launch_attention(const hylra_geometry* g, bool gather, const void* q, const void* k,

@@ -233,8 +233,9 @@ def test_pipelined_schedules_match_fused(schedule):
     res = dec.step(q, cap)
     torch.cuda.synchronize()
     assert torch.equal(res.selections, ref_idx)
+    # two bf16 evaluations with different split-K merges: each is ~1e-3 from float64
     o, r = res.outputs.double().cpu().numpy(), ref_out.double().cpu().numpy()
-    assert max_head_err(o, r) < 1e-3
+    assert max_head_err(o, r) < 4e-3
     # graph capture of the two-stream DAG
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -249,7 +250,7 @@ def test_pipelined_schedules_match_fused(schedule):
     gr.replay()
     torch.cuda.synchronize()
     assert torch.equal(dec.idx[..., :budget], ref_idx)
-    assert max_head_err(dec.out.double().cpu().numpy(), r) < 1e-3
+    assert max_head_err(dec.out.double().cpu().numpy(), r) < 4e-3
 
 
 def test_decode_loop_host_io_graph():
