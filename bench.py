@@ -350,7 +350,7 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
 
     def op_reuse():
         _abi.check(lib.hylra_reuse_decode(g, q.data_ptr(), k.data_ptr(), v.data_ptr(), n_valid,
-                                          len(reuse_ids), rids, rsrc, dec.idx.data_ptr(),
+                                          len(reuse_ids), rids, rsrc, dec.idx.data_ptr(), None,
                                           dec.k_stride, k_eff, 1, dec.out.data_ptr(),
                                           ws_r.data_ptr(), ws_r.numel(), st))
 

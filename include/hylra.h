@@ -19,6 +19,8 @@
  *                           layer's selection (engine.py:173,185-194)
  *   hylra_overlap_counts <- profiling.py:38-47 `overlap_ratio` numerators |S_i & S_j|
  *                           feeding profiling.py:126-145 `build_similarity_matrix`
+ *   hylra_block_select,  <- attention.py:287-313 block pooling / topk_blocks and
+ *   hylra_decode_step_blocks  engine.py:212-286 `hybrid_decode_blocks` (block mode)
  *
  * Conventions
  *   - Every pointer is caller-owned DEVICE memory unless stated otherwise; the
@@ -42,7 +44,7 @@
 extern "C" {
 #endif
 
-#define HYLRA_ABI_VERSION 1
+#define HYLRA_ABI_VERSION 2
 
 enum hylra_status {
   HYLRA_OK = 0,
@@ -59,8 +61,9 @@ enum hylra_dtype { HYLRA_BF16 = 0, HYLRA_F32 = 1 };
  * hylra_read_flags). Set by kernels; cleared by hylra_clear_flags. */
 enum hylra_flag {
   HYLRA_FLAG_INDEX_OUT_OF_RANGE = 1, /* a REUSE index >= n_valid  (attention.py:256-259) */
-  HYLRA_FLAG_NON_FINITE_SCORE = 2,   /* a NaN/inf selection score (attention.py:43-44)   */
-  HYLRA_FLAG_REFINE_SKIPPED = 4      /* boundary band exceeded the f64 refinement cap    */
+  HYLRA_FLAG_NON_FINITE_SCORE = 2,   /* a NaN/inf score or output (attention.py:43-44)   */
+  HYLRA_FLAG_REFINE_SKIPPED = 4,     /* boundary band exceeded the f64 refinement cap    */
+  HYLRA_FLAG_INTERNAL = 8            /* a kernel invariant failed (selection size != k)  */
 };
 
 /*
@@ -128,12 +131,31 @@ int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots,
  * REUSE attention for layers layer_ids[0..n_layers) (host array): layer i gathers the
  * k_eff rows idx[src_slots[i]][b][kh / sel_group][0..k_eff) of its own K/V and runs
  * the subset-renormalised softmax (attention.py:229-241). Indices >= n_valid are
- * masked and raise HYLRA_FLAG_INDEX_OUT_OF_RANGE.
+ * masked and raise HYLRA_FLAG_INDEX_OUT_OF_RANGE. counts (optional, same row indexing as
+ * idx) trims each selection row to its own length (block coverage).
  */
 int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, const void* v,
                        int n_valid, int n_layers, const int32_t* layer_ids,
-                       const int32_t* src_slots, const int32_t* idx, int k_stride, int k_eff,
-                       int sel_group, float* out, void* ws, size_t ws_bytes, void* stream);
+                       const int32_t* src_slots, const int32_t* idx, const int32_t* counts,
+                       int k_stride, int k_eff, int sel_group, float* out, void* ws,
+                       size_t ws_bytes, void* stream);
+
+/*
+ * Block-level selection (paper §3.5; engine.py:212-286): per (slot, b, group) row the
+ * token scores are max-pooled into ceil(n_valid / block_size) block scores
+ * (attention.py:287-295), the top min(block_budget, n_blocks) blocks are selected with
+ * the token rule (ties -> lower block, ascending; float64 refinement when q/k given, a
+ * block's exact score being the float64 max over its tokens), written to
+ * blocks[s][b][grp][bk_stride], and — if tokens != NULL — expanded to their ascending
+ * token coverage tokens[..][tok_stride] (final block truncated at n_valid) with the
+ * coverage length in counts[..] (attention.py:166-182). info: as hylra_topk_select.
+ * ws: 256 B + 4 * n_slots * B * (Hkv/sel_group) * round_up(n_blocks, 8) bytes.
+ */
+int hylra_block_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
+                       int block_budget, int block_size, int sel_group, const void* q,
+                       const void* k, const int32_t* layer_ids, int32_t* blocks, int bk_stride,
+                       int32_t* tokens, int tok_stride, int32_t* counts, int32_t* info,
+                       void* ws, size_t ws_bytes, void* stream);
 
 /* Workspace for hylra_decode_step (covers scores, select and attention workspaces). */
 size_t hylra_decode_step_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
@@ -151,6 +173,17 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                       int n_valid, const uint8_t* actions, int budget, int sel_group,
                       int refine, float* out, int32_t* idx, int k_stride, void* ws,
                       size_t ws_bytes, void* stream);
+
+/* Block-mode decode step (engine.py:212-286): budget counts blocks of block_size tokens;
+ * blocks[s][b][grp][bk_stride] receives each FULL layer's block selection. */
+size_t hylra_decode_step_blocks_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
+                                                int n_valid, int block_budget, int block_size,
+                                                int sel_group);
+int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void* k,
+                             const void* v, int n_valid, const uint8_t* actions,
+                             int block_budget, int block_size, int sel_group, int refine,
+                             float* out, int32_t* blocks, int bk_stride, void* ws,
+                             size_t ws_bytes, void* stream);
 
 /*
  * Pairwise selection overlaps: counts[t][r][j][i] = |S(t,i,r) & S(t,j,r)| where

@@ -222,3 +222,52 @@ def brute_force_dp(values, theta: float):
         if best_key is None or key < best_key:
             best_key, best = key, (acts, tuple(src), fulls, credit)
     return best
+
+
+# ----------------------------------------------------------------------------- blocks
+def block_max_of_logits(logits, block_size: int) -> np.ndarray:
+    """attention.py:287-295: max-pool into ceil(N / block_size) block scores."""
+    x = np.asarray(logits, dtype=np.float64)
+    return np.maximum.reduceat(x, np.arange(0, x.shape[0], block_size))
+
+
+def block_coverage(blocks, block_size: int, n: int) -> np.ndarray:
+    """attention.py:166-182 BlockSet.token_coverage: ascending tokens of the selected blocks,
+    the final block truncated at n."""
+    return np.concatenate([np.arange(b * block_size, min((b + 1) * block_size, n))
+                           for b in blocks]).astype(np.int64)
+
+
+def hybrid_step_blocks(q, k, v, n_valid: int, actions, block_budget: int, block_size: int,
+                       sel_group: int = 1):
+    """Block-mode decode step (engine.py:212-286): FULL layers keep the top
+    min(block_budget, n_blocks) blocks of the max-pooled head-summed logits (ties -> lower
+    block, ascending); REUSE layers attend over the inherited blocks' token coverage.
+    Returns (outputs [L, B, Hq, d], blocks {layer: int64 [B, groups, bb]})."""
+    L, B, Hq, d = q.shape
+    Hkv = k.shape[2]
+    G = Hq // Hkv
+    groups = Hkv // sel_group
+    nb = -(-n_valid // block_size)
+    bb = min(block_budget, nb)
+    out = np.zeros((L, B, Hq, d))
+    blocks, sel = {}, None
+    for l in range(L):
+        act = actions[l] if isinstance(actions[l], str) else actions[l].value
+        if act == "full":
+            for b in range(B):
+                for h in range(Hq):
+                    out[l, b, h], _ = full_attention(q[l, b, h], k[l, b, h // G, :n_valid],
+                                                     v[l, b, h // G, :n_valid])
+            sc = group_scores(q[l], k[l], n_valid, G, sel_group)
+            sel = np.stack([np.stack([topk_of_logits(block_max_of_logits(sc[b, g], block_size), bb)
+                                      for g in range(groups)]) for b in range(B)])
+        else:
+            for b in range(B):
+                for h in range(Hq):
+                    kh = h // G
+                    cov = block_coverage(sel[b, kh // sel_group], block_size, n_valid)
+                    out[l, b, h] = subset_attention(q[l, b, h], k[l, b, kh, :n_valid],
+                                                    v[l, b, kh, :n_valid], cov)
+        blocks[l] = sel
+    return out, blocks

@@ -21,17 +21,20 @@ __all__ = [
     "validate_policy", "SimilarityMatrix", "merge_similarity_matrices", "overlap_counts",
     "relative_l2_error", "similarity_from_counts", "LayerReuseError", "ConfigurationError",
     "NumericInputError", "InvalidSelectionError", "InvalidInputError", "CudaError",
-    "TopKSet", "full_attention", "topk_select", "sparse_attention", "HybridDecoder",
-    "decode_step", "hybrid_decode", "run_full_trace", "build_similarity_matrix",
+    "TopKSet", "BlockSet", "full_attention", "topk_select", "block_select", "sparse_attention",
+    "HybridDecoder", "PipelinedDecoder", "DecodeLoop", "decode_step", "hybrid_decode",
+    "hybrid_decode_blocks", "run_full_trace", "build_similarity_matrix",
 ]
 
 
 def __getattr__(name):
     # torch-dependent entry points load lazily so the host-only parts import without it
-    if name in ("TopKSet", "full_attention", "topk_select", "sparse_attention", "geometry"):
+    if name in ("TopKSet", "BlockSet", "full_attention", "topk_select", "block_select",
+                "sparse_attention", "geometry"):
         from . import attention
         return getattr(attention, name)
-    if name in ("HybridDecoder", "decode_step", "hybrid_decode", "run_full_trace",
+    if name in ("HybridDecoder", "decode_step", "hybrid_decode", "hybrid_decode_blocks",
+                "run_full_trace", "PipelinedDecoder", "DecodeLoop",
                 "build_similarity_matrix", "DecodeRunResult", "DecodeTrace", "StepResult"):
         from . import engine
         return getattr(engine, name)

@@ -19,6 +19,7 @@ HYLRA_F32 = 1
 FLAG_INDEX_OUT_OF_RANGE = 1
 FLAG_NON_FINITE_SCORE = 2
 FLAG_REFINE_SKIPPED = 4
+FLAG_INTERNAL = 8
 
 # Every symbol include/hylra.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
@@ -34,6 +35,9 @@ EXPORTED_SYMBOLS = (
     "hylra_decode_step_workspace_bytes",
     "hylra_decode_step",
     "hylra_overlap_counts",
+    "hylra_block_select",
+    "hylra_decode_step_blocks_workspace_bytes",
+    "hylra_decode_step_blocks",
     "hylra_read_flags",
     "hylra_clear_flags",
 )
@@ -91,8 +95,16 @@ def lib() -> ctypes.CDLL:
         l.hylra_topk_select.argtypes = [gp, vp, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp,
                                         sz, vp]
         l.hylra_reuse_decode.restype = i32
-        l.hylra_reuse_decode.argtypes = [gp, vp, vp, vp, i32, i32, vp, vp, vp, i32, i32, i32,
-                                         vp, vp, sz, vp]
+        l.hylra_reuse_decode.argtypes = [gp, vp, vp, vp, i32, i32, vp, vp, vp, vp, i32, i32,
+                                         i32, vp, vp, sz, vp]
+        l.hylra_block_select.restype = i32
+        l.hylra_block_select.argtypes = [gp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i32,
+                                         vp, i32, vp, vp, vp, sz, vp]
+        l.hylra_decode_step_blocks_workspace_bytes.restype = sz
+        l.hylra_decode_step_blocks_workspace_bytes.argtypes = [gp, vp, i32, i32, i32, i32]
+        l.hylra_decode_step_blocks.restype = i32
+        l.hylra_decode_step_blocks.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, vp,
+                                               vp, i32, vp, sz, vp]
         l.hylra_decode_step_workspace_bytes.restype = sz
         l.hylra_decode_step_workspace_bytes.argtypes = [gp, vp, i32, i32, i32]
         l.hylra_decode_step.restype = i32

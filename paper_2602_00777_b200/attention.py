@@ -19,8 +19,8 @@ import torch
 from . import _abi
 from .errors import ConfigurationError, InvalidInputError, InvalidSelectionError
 
-__all__ = ["TopKSet", "geometry", "full_attention", "topk_select", "sparse_attention",
-           "scores_row_stride"]
+__all__ = ["TopKSet", "BlockSet", "geometry", "full_attention", "topk_select", "block_select",
+           "sparse_attention", "scores_row_stride"]
 
 
 @dataclass(frozen=True)
@@ -48,6 +48,44 @@ class TopKSet:
     @property
     def size(self) -> int:
         return len(self.indices)
+
+
+@dataclass(frozen=True)
+class BlockSet:
+    """Canonical block selection (attention.py:143-182): distinct ascending block indices
+    plus the block width; token_coverage(n) truncates the final block at n."""
+
+    block_indices: tuple
+    block_size: int
+
+    def __post_init__(self) -> None:
+        blocks = tuple(int(b) for b in self.block_indices)
+        if self.block_size < 1:
+            raise InvalidInputError(f"block_size must be >= 1, got {self.block_size}")
+        if not blocks:
+            raise InvalidSelectionError("block selection must contain at least one block")
+        if any(b < 0 for b in blocks):
+            raise InvalidSelectionError("block indices must be non-negative")
+        if any(b2 <= b1 for b1, b2 in zip(blocks, blocks[1:])):
+            raise InvalidSelectionError("block indices must be strictly ascending")
+        object.__setattr__(self, "block_indices", blocks)
+
+    @property
+    def size(self) -> int:
+        return len(self.block_indices)
+
+    def token_coverage(self, n: int):
+        import numpy as np
+        if n < 1:
+            raise InvalidInputError(f"cache length must be >= 1, got {n}")
+        spans = []
+        for b in self.block_indices:
+            start = b * self.block_size
+            if start >= n:
+                raise InvalidSelectionError(
+                    f"block {b} starts at token {start}, beyond cache length {n}")
+            spans.append(np.arange(start, min(start + self.block_size, n), dtype=np.int64))
+        return np.concatenate(spans)
 
 
 _DTYPES = {torch.bfloat16: _abi.HYLRA_BF16, torch.float32: _abi.HYLRA_F32}
@@ -171,6 +209,53 @@ def topk_select(scores, budget: int, n_valid: int, *, sel_group: int = 1, q=None
     return (idx, inf) if info else idx
 
 
+def block_select(scores, block_budget: int, block_size: int, n_valid: int, *,
+                 sel_group: int = 1, q=None, k=None, layers=None, info: bool = False):
+    """Block-level top-k (attention.py:287-313): per row, max-pool the token scores into
+    blocks, keep the top min(block_budget, n_blocks) blocks (ties -> lower block,
+    ascending) and expand them to their token coverage.
+
+    Returns (blocks int32 [S,B,groups,bb], tokens int32 [S,B,groups,bb*block_size] (-1 past
+    the coverage), counts int32 [S,B,groups])."""
+    single = scores.dim() == 3
+    scores = _as_stack(scores, 4)
+    if scores.dtype != torch.float32 or not scores.is_cuda or not scores.is_contiguous():
+        raise ConfigurationError("scores must be a contiguous fp32 CUDA tensor")
+    if block_budget < 1:
+        raise InvalidInputError(f"block_budget must be >= 1, got {block_budget}")
+    if block_size < 1:
+        raise InvalidInputError(f"block_size must be >= 1, got {block_size}")
+    S, B, Hkv, rs = scores.shape
+    if q is not None and k is not None:
+        q4, k5 = _as_stack(q, 4), _as_stack(k, 5)
+        g = geometry(q4, k5, k5)
+        qp, kp = q4.data_ptr(), k5.data_ptr()
+        layer_ids = list(range(S)) if layers is None else list(layers)
+    else:
+        g = _abi.Geometry()
+        g.batch, g.q_heads, g.kv_heads, g.head_dim = B, Hkv, Hkv, 128
+        g.dtype, g.num_layers, g.capacity = _abi.HYLRA_F32, S, rs
+        qp = kp = None
+        layer_ids = list(range(S))
+    nb = -(-n_valid // block_size)
+    bb = min(block_budget, nb)
+    groups = Hkv // sel_group
+    blocks = torch.empty((S, B, groups, bb), dtype=torch.int32, device=scores.device)
+    tokens = torch.empty((S, B, groups, bb * block_size), dtype=torch.int32, device=scores.device)
+    counts = torch.empty((S, B, groups), dtype=torch.int32, device=scores.device)
+    inf = torch.zeros((S, B, groups, 8), dtype=torch.int32, device=scores.device)
+    ws = _workspace(256 + 4 * S * B * groups * ((nb + 7) & ~7), scores.device)
+    _abi.check(_abi.lib().hylra_block_select(
+        g, scores.data_ptr(), S, int(n_valid), int(block_budget), int(block_size), int(sel_group),
+        qp, kp, _abi.int32_array(layer_ids), blocks.data_ptr(), bb, tokens.data_ptr(),
+        bb * block_size, counts.data_ptr(), inf.data_ptr(), ws.data_ptr(), ws.numel(),
+        _stream(scores)))
+    _raise_flags(ws)
+    if single:
+        blocks, tokens, counts, inf = blocks[0], tokens[0], counts[0], inf[0]
+    return (blocks, tokens, counts, inf) if info else (blocks, tokens, counts)
+
+
 def sparse_attention(q, k, v, idx, n_valid: int | None = None, *, sel_group: int = 1,
                      check: bool = True):
     """Attention over the selected rows only, softmax renormalised over the subset.
@@ -205,7 +290,7 @@ def sparse_attention(q, k, v, idx, n_valid: int | None = None, *, sel_group: int
     ws = _workspace(ws_b, q.device)
     _abi.check(_abi.lib().hylra_reuse_decode(
         g, q.data_ptr(), k.data_ptr(), v.data_ptr(), n_valid, L, _abi.int32_array(range(L)),
-        _abi.int32_array(src), idx.data_ptr(), k_eff, k_eff, int(sel_group), out.data_ptr(),
+        _abi.int32_array(src), idx.data_ptr(), None, k_eff, k_eff, int(sel_group), out.data_ptr(),
         ws.data_ptr(), ws.numel(), _stream(q)))
     _raise_flags(ws)
     return out[0] if single else out
@@ -219,3 +304,6 @@ def _raise_flags(ws: torch.Tensor) -> None:
     if flags & _abi.FLAG_NON_FINITE_SCORE:
         from .errors import NumericInputError
         raise NumericInputError("selection scores contain non-finite entries")
+    if flags & _abi.FLAG_INTERNAL:
+        from .errors import CudaError
+        raise CudaError("a selection kernel invariant failed (internal error)")

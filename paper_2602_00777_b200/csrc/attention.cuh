@@ -31,6 +31,7 @@ struct AttnParams {
   float* out;
   float* scores;        // FULL: [slot][b][kh][cap] or null
   const int32_t* idx;   // REUSE: [src_slot][b][group][k_stride]
+  const int32_t* counts;  // REUSE: optional rows per selection row (block coverage)
   float* ws_o;          // [pair][split][G][D]
   float* ws_ml;         // [pair][split][G][2]
   int* counters;        // [pair]
@@ -107,7 +108,9 @@ __device__ __forceinline__ void merge_and_store(const AttnParams& p, int slot, i
         acc += sm_o[(w * 16 + g) * D + d] * s;
         L += sm_l[w * 16 + g] * s;
       }
-      out_base[g * D + d] = acc / L;
+      const float val = acc / L;
+      if (!isfinite(val)) atomicOr(p.flags, 2);  // NaN/inf in q, K or V
+      out_base[g * D + d] = val;
     }
     return;
   }
@@ -156,7 +159,9 @@ __device__ __forceinline__ void merge_and_store(const AttnParams& p, int slot, i
       acc += __ldcg(po + (int64_t)(s * G + g) * D + d) * sc;
       L += __ldcg(pml + (s * G + g) * 2 + 1) * sc;
     }
-    out_base[g * D + d] = acc / L;
+    const float val = acc / L;
+    if (!isfinite(val)) atomicOr(p.flags, 2);  // NaN/inf in q, K or V
+    out_base[g * D + d] = val;
   }
   if (tid == 0) p.counters[pair] = 0;  // leave the workspace zeroed for the next call
 }
@@ -204,6 +209,11 @@ __global__ void __launch_bounds__(160, 2)
   const int t_begin = split * p.tiles_per_split;
   const int t_end = min(n_tiles, t_begin + p.tiles_per_split);
   const int n_my = t_end - t_begin;
+  // rows of this pair: uniform, or the selection row's own length (block coverage)
+  const int n_rows = (GATHER && p.counts != nullptr)
+                         ? min(p.n_rows, __ldg(p.counts + (int64_t)(p.src_slot[slot] * p.B + b) *
+                                                              p.n_groups + kh / p.sel_group))
+                         : p.n_rows;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -255,13 +265,13 @@ __global__ void __launch_bounds__(160, 2)
       // the copies nor the L2 prefetches wait on a dependent global index load.
       int32_t* sidx = reinterpret_cast<int32_t*>(smem + STAGES * SM::kStageBytes + 256);
       const int pos_begin = t_begin * kTileRows;
-      const int n_pos = min(p.n_rows, t_end * kTileRows) - pos_begin;
+      const int n_pos = min(n_rows, t_end * kTileRows) - pos_begin;
       const bool staged = n_pos <= kIdxStage;
       if (staged) {
         stage_indices(ib + pos_begin, n_pos, p.n_valid, sidx, p.flags, lane);
         __syncwarp();
       }
-      auto row_at = [&](int pos) -> int {  // pos < p.n_rows
+      auto row_at = [&](int pos) -> int {  // pos < n_rows
         if (staged) return sidx[pos - pos_begin];
         int row = __ldg(ib + pos);
         if (row < 0 || row >= p.n_valid) {
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(160, 2)
       };
       auto load_idx = [&](int tile, int rr) -> int {
         const int pos = tile * kTileRows + lane + 32 * rr;
-        return (pos < p.n_rows) ? row_at(pos) : 0;
+        return (pos < n_rows) ? row_at(pos) : 0;
       };
       // L2 prefetch of the rows kPrefetch tiles ahead of the shared-memory pipeline: the
       // scattered 2*D-byte rows have a long loaded latency and shared memory bounds the
@@ -283,7 +293,7 @@ __global__ void __launch_bounds__(160, 2)
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int pos = tile * kTileRows + lane + 32 * rr;
-          if (pos < p.n_rows) {
+          if (pos < n_rows) {
             const int row = row_at(pos);
 #pragma unroll
             for (int off = 0; off < D * 2; off += 128) {
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(160, 2)
           const int r = it * RPI + my_sub;  // row of the tile this lane copies now
           // it*RPI < 32 is warp-uniform (RPI divides 32), so every lane offers the same half
           const int src = __shfl_sync(0xffffffffu, (it * RPI < 32) ? cur0 : cur1, r & 31);
-          const bool valid = pos0 + r < p.n_rows;
+          const bool valid = pos0 + r < n_rows;
           const uint32_t off = swz_addr(0, r, my_ch);
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kt + off),
                        "l"(kbase + (int64_t)src * D + my_ch * 8), "r"(valid ? 16 : 0)
@@ -392,13 +402,13 @@ __global__ void __launch_bounds__(160, 2)
     }
 
     // ---- mask rows past the end of the range
-    const bool tail = row0 + 16 > p.n_rows;
+    const bool tail = row0 + 16 > n_rows;
     if (tail) {
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          if (row0 + nt * 8 + 2 * t + e >= p.n_rows) {
+          if (row0 + nt * 8 + 2 * t + e >= n_rows) {
             sacc[nt][e] = -INFINITY;
             sacc[nt][2 + e] = -INFINITY;
           }
@@ -430,10 +440,10 @@ __global__ void __launch_bounds__(160, 2)
           *reinterpret_cast<float2*>(score_row + n1) =
               make_float2(v10 * p.inv_sqrt_d, v11 * p.inv_sqrt_d);
         } else {
-          if (n0 < p.n_rows) score_row[n0] = v00 * p.inv_sqrt_d;
-          if (n0 + 1 < p.n_rows) score_row[n0 + 1] = v01 * p.inv_sqrt_d;
-          if (n1 < p.n_rows) score_row[n1] = v10 * p.inv_sqrt_d;
-          if (n1 + 1 < p.n_rows) score_row[n1 + 1] = v11 * p.inv_sqrt_d;
+          if (n0 < n_rows) score_row[n0] = v00 * p.inv_sqrt_d;
+          if (n0 + 1 < n_rows) score_row[n0 + 1] = v01 * p.inv_sqrt_d;
+          if (n1 < n_rows) score_row[n1] = v10 * p.inv_sqrt_d;
+          if (n1 + 1 < n_rows) score_row[n1 + 1] = v11 * p.inv_sqrt_d;
         }
       }
     }
@@ -553,8 +563,12 @@ __global__ void __launch_bounds__(128)
   const int G = p.G;
   const float c = p.scale_log2;
 
+  const int n_rows = (GATHER && p.counts != nullptr)
+                         ? min(p.n_rows, __ldg(p.counts + (int64_t)(p.src_slot[slot] * p.B + b) *
+                                                              p.n_groups + kh / p.sel_group))
+                         : p.n_rows;
   const int r_begin = split * p.tiles_per_split * kTileRows;
-  const int r_end = min(p.n_rows, r_begin + p.tiles_per_split * kTileRows);
+  const int r_end = min(n_rows, r_begin + p.tiles_per_split * kTileRows);
 
   const T* qb = reinterpret_cast<const T*>(p.q) + layer * p.q_sl + b * p.q_sb +
                 (int64_t)(kh * G) * D;

@@ -16,6 +16,7 @@
 
 #include "../../include/hylra.h"
 #include "attention.cuh"
+#include "blocks.cuh"
 #include "overlap.cuh"
 #include "select.cuh"
 
@@ -197,8 +198,8 @@ cudaError_t dispatch_simt(int D, int G, dim3 grid, cudaStream_t st, const AttnPa
 int launch_attention(const hylra_geometry* g, bool gather, const void* q, const void* k,
                      const void* v, int n_valid, int n_rows, int n_layers,
                      const int32_t* layer_ids, const int32_t* src_slots, const int32_t* idx,
-                     int k_stride, int sel_group, float* out, float* scores, void* ws,
-                     size_t ws_bytes, int* flags, cudaStream_t st) {
+                     const int32_t* counts, int k_stride, int sel_group, float* out,
+                     float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st) {
   if (int e = check_geometry(g)) return e;
   if (n_layers < 1 || n_layers > kMaxSlots)
     return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", n_layers, kMaxSlots);
@@ -213,7 +214,7 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
     return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, lay.total);
   const int G = g->q_heads / g->kv_heads;
   AttnParams p{};
-  p.q = q; p.k = k; p.v = v; p.out = out; p.scores = scores; p.idx = idx;
+  p.q = q; p.k = k; p.v = v; p.out = out; p.scores = scores; p.idx = idx; p.counts = counts;
   uint8_t* w = static_cast<uint8_t*>(ws);
   p.counters = reinterpret_cast<int*>(w + lay.off_counters);
   p.ws_ml = reinterpret_cast<float*>(w + lay.off_ml);
@@ -270,10 +271,14 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
 
 size_t select_smem_bytes(int n_valid) { return sel_smem_bytes(n_valid); }
 
+struct BlockRows {  // block mode: rows are pooled block scores
+  int block_size = 1, n_tokens = 0, row_stride = 0;
+};
+
 int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
                   int budget, int sel_group, const void* q, const void* k,
                   const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
-                  int* flags, cudaStream_t st) {
+                  int* flags, cudaStream_t st, const BlockRows& br = BlockRows()) {
   if (int e = check_geometry(g)) return e;
   if (budget < 1) return fail(HYLRA_ERR_INVALID_INPUT, "budget must be >= 1, got %d", budget);
   if (n_slots < 1 || n_slots > kMaxSlots)
@@ -285,6 +290,7 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
     return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads %d", sel_group,
                 g->kv_heads);
   const int k_eff = std::min(budget, n_valid);
+  const bool blocks = br.block_size > 1;
   if (k_stride < k_eff)
     return fail(HYLRA_ERR_CONFIGURATION, "k_stride %d < selection size %d", k_stride, k_eff);
   if (n_valid > kSelMaxTokens)
@@ -300,7 +306,10 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
   p.B = g->batch; p.Hkv = g->kv_heads; p.G = g->q_heads / g->kv_heads; p.D = g->head_dim;
   p.sel_group = sel_group; p.n_groups = g->kv_heads / sel_group;
   p.n_valid = n_valid; p.k_eff = k_eff; p.k_stride = k_stride;
-  p.row_stride = scores_row_stride(g);
+  p.row_stride = blocks ? br.row_stride : scores_row_stride(g);
+  p.pre_grouped = blocks ? 1 : 0;
+  p.block_size = blocks ? br.block_size : 1;
+  p.n_tokens = blocks ? br.n_tokens : n_valid;
   p.tau_rel = 1.0f / 4096.0f;
   for (int i = 0; i < n_slots; ++i) {
     const int l = layer_ids ? layer_ids[i] : 0;
@@ -323,14 +332,57 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
   return cuda_check(cudaGetLastError(), "topk_select launch");
 }
 
+int nb_stride_of(int n_blocks) { return (n_blocks + 7) & ~7; }
+
+// pool -> select -> expand for n_slots layers (see blocks.cuh)
+int launch_block_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
+                        int block_budget, int block_size, int sel_group, const void* q,
+                        const void* k, const int32_t* layer_ids, float* bscores,
+                        int32_t* blocks_out, int bk_stride, int32_t* tokens_out,
+                        int tok_stride, int32_t* counts_out, int32_t* info, int* flags,
+                        cudaStream_t st) {
+  if (block_size < 1) return fail(HYLRA_ERR_INVALID_INPUT, "block_size must be >= 1");
+  if (block_budget < 1)
+    return fail(HYLRA_ERR_INVALID_INPUT, "block_budget must be >= 1, got %d", block_budget);
+  if (sel_group < 1 || g->kv_heads % sel_group != 0)
+    return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads", sel_group);
+  const int nb = (n_valid + block_size - 1) / block_size;
+  const int bb = std::min(block_budget, nb);
+  const int groups = g->kv_heads / sel_group;
+  if (bk_stride < bb || (tokens_out && tok_stride < bb * block_size))
+    return fail(HYLRA_ERR_CONFIGURATION, "block/token output strides too small");
+  dim3 grid(groups, g->batch, n_slots);
+  block_pool_kernel<<<grid, kPoolThreads, 0, st>>>(scores, g->batch, g->kv_heads, sel_group,
+                                                   scores_row_stride(g), n_valid, block_size,
+                                                   bscores, nb_stride_of(nb));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (int e = cuda_check(cudaGetLastError(), "block_pool launch")) return e;
+  BlockRows br;
+  br.block_size = block_size;
+  br.n_tokens = n_valid;
+  br.row_stride = nb_stride_of(nb);
+  if (int e = launch_select(g, bscores, n_slots, nb, block_budget, sel_group, q, k, layer_ids,
+                            blocks_out, bk_stride, info, flags, st, br))
+    return e;
+  if (tokens_out) {
+    block_expand_kernel<<<n_slots * g->batch * groups, kPoolThreads, 0, st>>>(
+        blocks_out, bk_stride, bb, block_size, n_valid, tokens_out, tok_stride, counts_out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (int e = cuda_check(cudaGetLastError(), "block_expand launch")) return e;
+  }
+  return HYLRA_OK;
+}
+
 struct StepLayout {
   std::vector<int32_t> full_ids, reuse_ids, reuse_src;
   int k_eff, n_groups;
+  int bb = 0, tok_stride = 0;                   // block mode
+  size_t off_bscores = 0, off_tokens = 0, off_counts = 0;
   size_t off_scores, off_attn, attn_bytes, off_attn_r, attn_bytes_r, total;
 };
 
 int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, int budget,
-                int sel_group, StepLayout* s) {
+                int sel_group, StepLayout* s, int block_size = 1) {
   if (int e = check_geometry(g)) return e;
   if (!actions) return fail(HYLRA_ERR_CONFIGURATION, "actions is NULL");
   if (actions[0] != 1)
@@ -353,14 +405,30 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   }
   if ((int)s->full_ids.size() > kMaxSlots || (int)s->reuse_ids.size() > kMaxSlots)
     return fail(HYLRA_ERR_CONFIGURATION, "more than %d layers of one kind", kMaxSlots);
-  s->k_eff = std::min(budget, n_valid);
   s->n_groups = g->kv_heads / sel_group;
   const size_t nf = s->full_ids.size();
   s->off_scores = kHeader;
   const size_t scores_b = sizeof(float) * nf * g->batch * g->kv_heads * scores_row_stride(g);
+  size_t off = align_up(s->off_scores + scores_b, 256);
+  if (block_size > 1) {
+    // budget counts blocks; REUSE layers read the coverage (<= bb * block_size tokens)
+    const int nb = (n_valid + block_size - 1) / block_size;
+    s->bb = std::min(budget, nb);
+    s->k_eff = s->bb * block_size;  // coverage upper bound; per-row counts trim it
+    s->tok_stride = s->bb * block_size;
+    const size_t rows = nf * g->batch * s->n_groups;
+    s->off_bscores = off;
+    off = align_up(off + sizeof(float) * rows * nb_stride_of(nb), 256);
+    s->off_tokens = off;
+    off = align_up(off + sizeof(int32_t) * rows * s->tok_stride, 256);
+    s->off_counts = off;
+    off = align_up(off + sizeof(int32_t) * rows, 256);
+  } else {
+    s->k_eff = std::min(budget, n_valid);
+  }
   // FULL and REUSE get disjoint attention workspaces: each kernel's split-K counters must
   // start at zero, and the other launch's partial buffers would otherwise overlap them.
-  s->off_attn = align_up(s->off_scores + scores_b, 256);
+  s->off_attn = off;
   s->attn_bytes = attn_layout(g, (int)nf, n_valid).total;
   s->off_attn_r = align_up(s->off_attn + s->attn_bytes, 256);
   s->attn_bytes_r =
@@ -406,7 +474,7 @@ int hylra_full_decode(const hylra_geometry* g, const void* q, const void* k, con
                       int n_valid, int n_layers, const int32_t* layer_ids, float* out,
                       float* scores, void* ws, size_t ws_bytes, void* stream) {
   return launch_attention(g, false, q, k, v, n_valid, n_valid, n_layers, layer_ids, nullptr,
-                          nullptr, 0, 1, out, scores, ws, ws_bytes, static_cast<int*>(ws),
+                          nullptr, nullptr, 0, 1, out, scores, ws, ws_bytes, static_cast<int*>(ws),
                           static_cast<cudaStream_t>(stream));
 }
 
@@ -421,8 +489,9 @@ int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots,
 
 int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, const void* v,
                        int n_valid, int n_layers, const int32_t* layer_ids,
-                       const int32_t* src_slots, const int32_t* idx, int k_stride, int k_eff,
-                       int sel_group, float* out, void* ws, size_t ws_bytes, void* stream) {
+                       const int32_t* src_slots, const int32_t* idx, const int32_t* counts,
+                       int k_stride, int k_eff, int sel_group, float* out, void* ws,
+                       size_t ws_bytes, void* stream) {
   if (!idx || !src_slots) return fail(HYLRA_ERR_CONFIGURATION, "NULL selection argument");
   if (k_eff < 1 || k_eff > k_stride)
     return fail(HYLRA_ERR_INVALID_SELECTION, "selection size %d not in [1, k_stride=%d]", k_eff,
@@ -430,8 +499,8 @@ int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, co
   if (sel_group < 1 || (g && g->kv_heads % sel_group != 0))
     return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads", sel_group);
   return launch_attention(g, true, q, k, v, n_valid, k_eff, n_layers, layer_ids, src_slots, idx,
-                          k_stride, sel_group, out, nullptr, ws, ws_bytes, static_cast<int*>(ws),
-                          static_cast<cudaStream_t>(stream));
+                          counts, k_stride, sel_group, out, nullptr, ws, ws_bytes,
+                          static_cast<int*>(ws), static_cast<cudaStream_t>(stream));
 }
 
 size_t hylra_decode_step_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
@@ -458,7 +527,7 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
   void* aws = w + s.off_attn;
   const int nf = (int)s.full_ids.size();
   if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, nf, s.full_ids.data(), nullptr,
-                               nullptr, 0, 1, out, scores, aws, s.attn_bytes, flags, st))
+                               nullptr, nullptr, 0, 1, out, scores, aws, s.attn_bytes, flags, st))
     return e;
   if (int e = launch_select(g, scores, nf, n_valid, budget, sel_group, refine ? q : nullptr,
                             refine ? k : nullptr, s.full_ids.data(), idx, k_stride, nullptr,
@@ -466,8 +535,83 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
     return e;
   if (!s.reuse_ids.empty()) {
     if (int e = launch_attention(g, true, q, k, v, n_valid, s.k_eff, (int)s.reuse_ids.size(),
-                                 s.reuse_ids.data(), s.reuse_src.data(), idx, k_stride, sel_group,
-                                 out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags, st))
+                                 s.reuse_ids.data(), s.reuse_src.data(), idx, nullptr, k_stride,
+                                 sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags,
+                                 st))
+      return e;
+  }
+  return HYLRA_OK;
+}
+
+int hylra_block_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
+                       int block_budget, int block_size, int sel_group, const void* q,
+                       const void* k, const int32_t* layer_ids, int32_t* blocks, int bk_stride,
+                       int32_t* tokens, int tok_stride, int32_t* counts, int32_t* info, void* ws,
+                       size_t ws_bytes, void* stream) {
+  if (int e = check_geometry(g)) return e;
+  if (!scores || !blocks || !ws) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  if (n_valid < 1 || n_valid > g->capacity)
+    return fail(HYLRA_ERR_INVALID_INPUT, "n_valid %d not in [1, capacity]", n_valid);
+  if (block_size < 1) return fail(HYLRA_ERR_INVALID_INPUT, "block_size must be >= 1");
+  if (sel_group < 1 || g->kv_heads % sel_group != 0)
+    return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads", sel_group);
+  if (n_slots < 1 || n_slots > kMaxSlots)
+    return fail(HYLRA_ERR_CONFIGURATION, "n_slots %d not in [1, %d]", n_slots, kMaxSlots);
+  const int nb = (n_valid + block_size - 1) / block_size;
+  const size_t need = kHeader + sizeof(float) * (size_t)n_slots * g->batch *
+                                    (g->kv_heads / sel_group) * nb_stride_of(nb);
+  if (ws_bytes < need)
+    return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, need);
+  return launch_block_select(g, scores, n_slots, n_valid, block_budget, block_size, sel_group, q,
+                             k, layer_ids, reinterpret_cast<float*>(static_cast<uint8_t*>(ws) +
+                                                                    kHeader),
+                             blocks, bk_stride, tokens, tok_stride, counts, info,
+                             static_cast<int*>(ws), static_cast<cudaStream_t>(stream));
+}
+
+size_t hylra_decode_step_blocks_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
+                                                int n_valid, int block_budget, int block_size,
+                                                int sel_group) {
+  StepLayout s;
+  if (block_size < 1 || step_layout(g, actions, n_valid, block_budget, sel_group, &s, block_size))
+    return 0;
+  return s.total;
+}
+
+int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void* k,
+                             const void* v, int n_valid, const uint8_t* actions,
+                             int block_budget, int block_size, int sel_group, int refine,
+                             float* out, int32_t* blocks, int bk_stride, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (block_size < 1) return fail(HYLRA_ERR_INVALID_INPUT, "block_size must be >= 1");
+  StepLayout s;
+  if (int e = step_layout(g, actions, n_valid, block_budget, sel_group, &s, block_size)) return e;
+  if (!ws || ws_bytes < s.total)
+    return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, s.total);
+  if (!blocks || bk_stride < s.bb)
+    return fail(HYLRA_ERR_CONFIGURATION, "block output stride %d < %d", bk_stride, s.bb);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int* flags = reinterpret_cast<int*>(w);
+  float* scores = reinterpret_cast<float*>(w + s.off_scores);
+  int32_t* toks = reinterpret_cast<int32_t*>(w + s.off_tokens);
+  int32_t* cnts = reinterpret_cast<int32_t*>(w + s.off_counts);
+  const int nf = (int)s.full_ids.size();
+  if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, nf, s.full_ids.data(), nullptr,
+                               nullptr, nullptr, 0, 1, out, scores, w + s.off_attn, s.attn_bytes,
+                               flags, st))
+    return e;
+  if (int e = launch_block_select(g, scores, nf, n_valid, block_budget, block_size, sel_group,
+                                  refine ? q : nullptr, refine ? k : nullptr, s.full_ids.data(),
+                                  reinterpret_cast<float*>(w + s.off_bscores), blocks, bk_stride,
+                                  s.reuse_ids.empty() ? nullptr : toks, s.tok_stride, cnts,
+                                  nullptr, flags, st))
+    return e;
+  if (!s.reuse_ids.empty()) {
+    if (int e = launch_attention(g, true, q, k, v, n_valid, s.k_eff, (int)s.reuse_ids.size(),
+                                 s.reuse_ids.data(), s.reuse_src.data(), toks, cnts, s.tok_stride,
+                                 sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags,
+                                 st))
       return e;
   }
   return HYLRA_OK;

@@ -47,6 +47,9 @@ struct SelectParams {
   int B, Hkv, G, D, sel_group, n_groups;
   int n_valid, k_eff, k_stride, row_stride;
   float tau_rel;
+  int pre_grouped;  // score rows already summed per group ([slot][b][grp][row_stride])
+  int block_size;   // 1: token selection; >1: rows are block scores over n_tokens tokens
+  int n_tokens;
   int layers[kMaxSlots];
 };
 
@@ -239,6 +242,41 @@ __device__ void rescore_f64(const SelectParams& p, int slot, int b, int grp, con
   }
 }
 
+// float64 score of candidate BLOCKS: the max over the block's tokens of the head-order
+// summed q.k/sqrt(d) (engine.py:256-262 + attention.py:287-295). One warp per block, one
+// lane per token.
+__device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int grp,
+                                   const int* blocks, double* vals, int n) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int layer = p.layers[slot];
+  const double sqd = sqrt((double)p.D);
+  for (int c = warp; c < n; c += kSelWarps) {
+    const int t0 = blocks[c] * p.block_size;
+    const int t1 = min(p.n_tokens, t0 + p.block_size);
+    double best = -INFINITY;
+    for (int tok = t0 + lane; tok < t1; tok += 32) {
+      double agg = 0.0;
+      for (int hh = 0; hh < p.sel_group; ++hh) {
+        const int kh = grp * p.sel_group + hh;
+        const int64_t koff = layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
+        for (int g = 0; g < p.G; ++g) {
+          const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D;
+          double dot = 0.0;
+          for (int i = 0; i < p.D; ++i)
+            dot += (p.dtype == 0 ? elem_f64<__nv_bfloat16>(p.q, qoff + i) *
+                                       elem_f64<__nv_bfloat16>(p.k, koff + i)
+                                 : elem_f64<float>(p.q, qoff + i) * elem_f64<float>(p.k, koff + i));
+          agg += dot / sqd;
+        }
+      }
+      best = fmax(best, agg);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) vals[c] = best;
+  }
+}
+
 // MSB-first 4 x 8-bit radix select of the rank-`rank` (1-based, descending) score of the
 // row: T, #(s > T). Degenerate-row fallback only.
 __device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, float* T_out,
@@ -301,9 +339,14 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   const long long t0 = clock64();
 
   RowReader rd;
-  rd.base = p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + grp * p.sel_group) * p.row_stride;
+  if (p.pre_grouped) {
+    rd.base = p.scores + ((int64_t)(slot * p.B + b) * p.n_groups + grp) * p.row_stride;
+    rd.sg = 1;
+  } else {
+    rd.base = p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + grp * p.sel_group) * p.row_stride;
+    rd.sg = p.sel_group;
+  }
   rd.hstride = p.row_stride;
-  rd.sg = p.sel_group;
 
   if (k >= n) {
     // the budget covers the cache: every index (after the non-finite check)
@@ -527,7 +570,8 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
           const bool ok = full || 4 * (w4 + u) + cc < n;
           // above hi: already set in pass B; [v_hi, hi]: set now
           word |= (ok && v >= v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
-          cand |= (ok && v >= v_lo && v < v_hi) ? (1u << (u * 4 + cc)) : 0u;
+          // inside the band only: scores above hi were counted (and set) by pass B
+          cand |= (ok && v >= v_lo && v < v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
         }
       }
       if (word) sm.bitmap[c * kSelThreads + tid] |= word;
@@ -664,7 +708,8 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   if (nw > 0) {
     __syncthreads();
     if (refine) {
-      rescore_f64(p, slot, b, grp, sm.ci, sm.cv, nw);
+      if (p.block_size > 1) rescore_f64_blocks(p, slot, b, grp, sm.ci, sm.cv, nw);
+      else rescore_f64(p, slot, b, grp, sm.ci, sm.cv, nw);
       __syncthreads();
     }
     const int take = k - above_w;
@@ -696,6 +741,8 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
     }
     run += tot;
   }
+  // invariant: exactly k indices were emitted
+  if (tid == 0 && run != k) atomicOr(p.flags, 8);
   if (info && tid == 0) {
     info[0] = k;
     info[1] = nw;

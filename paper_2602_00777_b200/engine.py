@@ -24,13 +24,14 @@ import numpy as np
 import torch
 
 from . import _abi
-from .attention import TopKSet, geometry
+from .attention import BlockSet, TopKSet, geometry
 from .errors import ConfigurationError, InvalidInputError, InvalidSelectionError, NumericInputError
 from .policy import Action, LayerPolicy, policy_from_actions
 from .profiling import overlap_counts, relative_l2_error, similarity_from_counts
 
-__all__ = ["HybridDecoder", "PipelinedDecoder", "DecodeLoop", "StepResult", "decode_step", "DecodeRunResult", "FidelityTable",
-           "DecodeTrace", "hybrid_decode", "run_full_trace", "trace_overlap_counts"]
+__all__ = ["HybridDecoder", "PipelinedDecoder", "DecodeLoop", "StepResult", "decode_step",
+           "DecodeRunResult", "FidelityTable", "DecodeTrace", "hybrid_decode",
+           "hybrid_decode_blocks", "run_full_trace", "trace_overlap_counts"]
 
 
 def _actions_of(policy) -> tuple:
@@ -64,7 +65,7 @@ class HybridDecoder:
     """
 
     def __init__(self, policy, k_cache: torch.Tensor, v_cache: torch.Tensor, budget: int, *,
-                 q_heads: int, sel_group: int = 1, refine: bool = True):
+                 q_heads: int, sel_group: int = 1, refine: bool = True, block_size: int = 1):
         self.actions = _actions_of(policy)
         if len(self.actions) != k_cache.shape[0]:
             raise ConfigurationError(
@@ -87,12 +88,18 @@ class HybridDecoder:
         self.slot_of_layer = tuple(slots)
         self.q_heads = q_heads
         self.out = torch.empty((L, B, q_heads, d), dtype=torch.float32, device=k_cache.device)
-        self.k_stride = min(self.budget, cap)
+        if block_size < 1:
+            raise InvalidInputError(f"block_size must be >= 1, got {block_size}")
+        self.block_size = int(block_size)
+        # token mode: k indices per row; block mode: budget counts blocks
+        self.k_stride = (min(self.budget, -(-cap // block_size)) if block_size > 1
+                         else min(self.budget, cap))
         self.idx = torch.zeros((len(self.full_layers), B, Hkv // sel_group, self.k_stride),
                                dtype=torch.int32, device=k_cache.device)
         self._acts = _abi.uint8_array(1 if a is Action.FULL else 0 for a in self.actions)
         self.ws = torch.zeros(256, dtype=torch.uint8, device=k_cache.device)
-        self.kernels_per_step = 2 + (1 if len(self.full_layers) < L else 0)
+        has_reuse = len(self.full_layers) < L
+        self.kernels_per_step = (2 + has_reuse) if block_size == 1 else (3 + 2 * has_reuse)
 
     def _geometry(self, q):
         return geometry(q, self.k, self.v, self.out)
@@ -105,17 +112,31 @@ class HybridDecoder:
     def step(self, q: torch.Tensor, n_valid: int | None = None) -> StepResult:
         g = self._geometry(q)
         n_valid = g.capacity if n_valid is None else int(n_valid)
-        need = int(_abi.lib().hylra_decode_step_workspace_bytes(
+        lib = _abi.lib()
+        st = torch.cuda.current_stream(self.k.device).cuda_stream
+        if self.block_size > 1:
+            need = int(lib.hylra_decode_step_blocks_workspace_bytes(
+                g, self._acts, n_valid, self.budget, self.block_size, self.sel_group))
+            if self.ws.numel() < need:
+                self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
+            _abi.check(lib.hylra_decode_step_blocks(
+                g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
+                self.budget, self.block_size, self.sel_group, int(self.refine),
+                self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(),
+                self.ws.numel(), st))
+            bb = min(self.budget, -(-n_valid // self.block_size))
+            return StepResult(self.out, self.idx[..., :bb], self.slot_of_layer,
+                              self.full_layers)
+        need = int(lib.hylra_decode_step_workspace_bytes(
             g, self._acts, n_valid, self.budget, self.sel_group))
         if need == 0:
-            _abi.check(_abi.lib().hylra_decode_step(
+            _abi.check(lib.hylra_decode_step(
                 g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
                 self.budget, self.sel_group, int(self.refine), self.out.data_ptr(),
                 self.idx.data_ptr(), self.k_stride, None, 0, 0))
         if self.ws.numel() < need:
             self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
-        st = torch.cuda.current_stream(self.k.device).cuda_stream
-        _abi.check(_abi.lib().hylra_decode_step(
+        _abi.check(lib.hylra_decode_step(
             g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
             self.budget, self.sel_group, int(self.refine), self.out.data_ptr(),
             self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(), self.ws.numel(), st))
@@ -132,6 +153,9 @@ class HybridDecoder:
             raise InvalidSelectionError("a selection index is out of range for the cache")
         if f & _abi.FLAG_NON_FINITE_SCORE:
             raise NumericInputError("selection scores contain non-finite entries")
+        if f & _abi.FLAG_INTERNAL:
+            from .errors import CudaError
+            raise CudaError("a selection kernel invariant failed (internal error)")
 
     def clear_flags(self) -> None:
         self.ws[:4].zero_()
@@ -223,7 +247,7 @@ class PipelinedDecoder(HybridDecoder):
             for grp in launches:
                 _abi.check(lib.hylra_reuse_decode(
                     g, qp, kp, vp, n_valid, len(grp), _abi.int32_array(grp),
-                    _abi.int32_array([0] * len(grp)), self.idx.data_ptr() + 4 * s * idx_slot,
+                    _abi.int32_array([0] * len(grp)), self.idx.data_ptr() + 4 * s * idx_slot, None,
                     self.k_stride, k_eff, self.sel_group, outp, ws_r.data_ptr(), ws_r.numel(),
                     side.cuda_stream))
         if side is not main:
@@ -444,6 +468,62 @@ def hybrid_decode(model, policy, budget: int, steps: int, *, include_sinks: int 
     outputs.setflags(write=False)
     return DecodeRunResult(
         policy=pol, budget=budget, block_size=1, outputs=outputs,
+        selections=tuple(selections),
+        fidelity=FidelityTable(table, per_layer, float(table.mean())),
+        full_score_computations=tuple(full_counts), reuse_full_scans=0,
+        reuse_gathered_rows=tuple(gathered))
+
+
+def hybrid_decode_blocks(model, policy, block_budget: int, block_size: int, steps: int, *,
+                         device="cuda", refine: bool = True) -> DecodeRunResult:
+    """Drop-in for the reference `hybrid_decode_blocks` (engine.py:212-286): FULL layers keep
+    the top min(block_budget, n_blocks) blocks of block_size tokens (max-pooled summed
+    logits), REUSE layers attend over the inherited blocks' token coverage."""
+    actions = _actions_of(policy)
+    pol = policy if isinstance(policy, LayerPolicy) else policy_from_actions(actions)
+    _check_model_args(model, actions, steps, block_budget)
+    if block_size < 1:
+        raise InvalidInputError(f"block_size must be >= 1, got {block_size}")
+    cfg = model.config
+    q, k, v = _model_tensors(model, steps, device)
+    H = cfg.heads
+    dec = HybridDecoder(actions, k, v, block_budget, q_heads=H, sel_group=H, refine=refine,
+                        block_size=block_size)
+    outs, sels = [], []
+    for t in range(steps):
+        res = dec.step(q[t], cfg.context_len + t)
+        dec.check_flags()
+        outs.append(res.outputs[:, 0].double().cpu().numpy())
+        sels.append(res.selections[:, 0, 0].cpu().numpy())
+    outputs = np.stack(outs)
+    baseline_budget = min(max(block_budget * block_size, 1), cfg.context_len)
+    baseline = run_full_trace(model, steps, baseline_budget, device=device, refine=refine)
+    L = cfg.layers
+    selections, full_counts, gathered = [], [], []
+    for t in range(steps):
+        n_t = cfg.context_len + t
+        step_sel, step_g, cur = [], [], None
+        for l, a in enumerate(actions):
+            if a is Action.FULL:
+                slot = sum(1 for x in actions[:l] if x is Action.FULL)
+                cur = BlockSet(tuple(int(i) for i in sels[t][slot]), block_size)
+                step_g.append(None)
+            else:
+                step_g.append(int(cur.token_coverage(n_t).shape[0]))
+            step_sel.append(cur)
+        selections.append(tuple(step_sel))
+        gathered.append(tuple(step_g))
+        full_counts.append(pol.full_count)
+    table = np.empty((steps, L))
+    for t in range(steps):
+        for l in range(L):
+            table[t, l] = relative_l2_error(outputs[t, l].ravel(), baseline.outputs[t, l].ravel())
+    table.setflags(write=False)
+    per_layer = table.mean(axis=0)
+    per_layer.setflags(write=False)
+    outputs.setflags(write=False)
+    return DecodeRunResult(
+        policy=pol, budget=block_budget, block_size=block_size, outputs=outputs,
         selections=tuple(selections),
         fidelity=FidelityTable(table, per_layer, float(table.mean())),
         full_score_computations=tuple(full_counts), reuse_full_scans=0,

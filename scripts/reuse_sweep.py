@@ -27,7 +27,7 @@ st = torch.cuda.current_stream().cuda_stream
 def op():
     _abi.check(_abi.lib().hylra_reuse_decode(g, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                              cfg.context, len(rl), _abi.int32_array(rl),
-                                             _abi.int32_array(src), dec.idx.data_ptr(),
+                                             _abi.int32_array(src), dec.idx.data_ptr(), None,
                                              dec.k_stride, ke, 1, dec.out.data_ptr(),
                                              ws.data_ptr(), ws.numel(), st))
 

@@ -77,7 +77,7 @@ def point(N, ratio, B):
         g, sc.data_ptr(), len(fl), N, k, 1, q.data_ptr(), kk.data_ptr(), fid, dec.idx.data_ptr(),
         dec.k_stride, None, wss.data_ptr(), wss.numel(), st)))
     t_reuse = time_ms(lambda: _abi.check(lib.hylra_reuse_decode(
-        g, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), N, len(rl), rid, rsrc, dec.idx.data_ptr(),
+        g, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), N, len(rl), rid, rsrc, dec.idx.data_ptr(), None,
         dec.k_stride, min(k, N), 1, dec.out.data_ptr(), wsr.data_ptr(), wsr.numel(), st))) \
         if rl else 0.0
     t_step = time_ms(lambda: dec.step(q, N))

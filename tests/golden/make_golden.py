@@ -93,6 +93,27 @@ def overlap_fixture():
     print("overlap fixture: adjacent", repr(adjacent))
 
 
+def block_fixture():
+    """tests/test_engine.py:34-38,196-206 BLOCK_FIXTURE (L5 d32 N512 seed33 rho0.8 H2):
+    block mode, static_jump_policy(5, 2), 2 blocks of 128, 2 steps; golden aggregate
+    0.4524886792120594."""
+    cfg = lr.SynthModelConfig(layers=5, head_dim=32, context_len=512, seed=33,
+                              inter_layer_correlation=0.8, heads=2)
+    model = lr.generate_model(cfg)
+    keys, values = model.grown_arrays(2)
+    queries = model.queries(2)
+    policy = lr.static_jump_policy(5, 2)
+    run = lr.hybrid_decode_blocks(model, policy, 2, 128, 2)
+    blocks = np.array([[list(s.block_indices) for s in row] for row in run.selections])
+    gathered = np.array([[-1 if g is None else g for g in row] for row in run.reuse_gathered_rows])
+    np.savez_compressed(HERE / "block_reference.npz", keys=keys, values=values, queries=queries,
+                        actions=np.array([a.value for a in policy.actions]),
+                        outputs=run.outputs, blocks=blocks, gathered=gathered,
+                        aggregate=run.fidelity.aggregate, context_len=512, block_budget=2,
+                        block_size=128)
+    print("block fixture: agg", repr(run.fidelity.aggregate))
+
+
 def mha_fixture():
     cfg = lr.SynthModelConfig(layers=4, head_dim=32, context_len=128, seed=5,
                               inter_layer_correlation=0.7, heads=2)
@@ -202,6 +223,7 @@ if __name__ == "__main__":
     engine_fixture()
     overlap_fixture()
     mha_fixture()
+    block_fixture()
     cfg1_fixture()
     topk_cases()
     dp_cases()

@@ -278,3 +278,17 @@ def test_decode_loop_host_io_graph():
         ref = HybridDecoder(actions, k2, v2, budget, q_heads=Hq).step(qh.cuda(), pos + 1)
         torch.cuda.synchronize()
         assert torch.equal(out, ref.outputs.cpu())
+
+
+@pytest.mark.parametrize("where", ["k", "v", "q"])
+def test_non_finite_inputs_raise_numeric_error(where):
+    """Non-finite cache or query values -> NumericInputError (attention.py:43-44,205-206)."""
+    from paper_2602_00777_b200 import NumericInputError
+    L, B, Hq, Hkv, d, cap = 2, 1, 8, 2, 128, 1024
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=2)
+    {"k": k, "v": v}.get(where, q).view(-1)[777] = float("nan") if where != "k" else float("inf")
+    dec = HybridDecoder(("full", "reuse"), k, v, 64, q_heads=Hq)
+    dec.step(q, cap)
+    torch.cuda.synchronize()
+    with pytest.raises(NumericInputError):
+        dec.check_flags()

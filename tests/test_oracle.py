@@ -103,3 +103,30 @@ def test_cfg1_gqa_adapter_golden(golden_dir):
     for s, l in enumerate(cfg.full_layers):
         assert np.array_equal(sets[l], z["sets"][s])
         np.testing.assert_allclose(scores[l], z["scores"][s], rtol=1e-12, atol=1e-12)
+
+
+def test_block_mode_golden(golden_dir):
+    """Block-level selection (engine.py:212-286) vs the reference's BLOCK_FIXTURE run:
+    golden aggregate 0.4524886792120594 (tests/test_engine.py:34-38,196-206)."""
+    z = load_npz(golden_dir / "block_reference.npz")
+    assert float(z["aggregate"]) == pytest.approx(0.4524886792120594, rel=1e-12)
+    N, bb, bs = int(z["context_len"]), int(z["block_budget"]), int(z["block_size"])
+    acts = tuple(z["actions"])
+    for t in range(2):
+        n_t = N + t
+        q = np.asarray(z["queries"][t])[:, None]
+        k = np.asarray(z["keys"])[:, None]
+        v = np.asarray(z["values"])[:, None]
+        H = k.shape[2]
+        out, blocks = orc.hybrid_step_blocks(q, k, v, n_t, acts, bb, bs, sel_group=H)
+        np.testing.assert_allclose(out[:, 0], z["outputs"][t], rtol=1e-12, atol=1e-14)
+        for l in range(len(acts)):
+            assert list(blocks[l][0, 0]) == list(z["blocks"][t][l])
+            if acts[l] == "reuse":
+                cov = orc.block_coverage(blocks[l][0, 0], bs, n_t)
+                assert cov.shape[0] == int(z["gathered"][t][l])
+    # reference known answers (tests/test_attention.py:245-270)
+    assert list(orc.block_max_of_logits([1.0, 9.0, 2.0, 3.0], 2)) == [9.0, 3.0]
+    assert list(orc.block_max_of_logits([1.0, 9.0, 2.0], 8)) == [9.0]
+    assert list(orc.topk_of_logits(np.array([0.5, 3.0, 1.0]), 2)) == [1, 2]
+    assert list(orc.block_coverage([0, 2], 4, 10)) == [0, 1, 2, 3, 8, 9]
