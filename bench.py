@@ -189,6 +189,45 @@ def _ncu_traffic():
         return {}
 
 
+def _block_mode_line(a, cfg, torch):
+    """cfg2 at B=8 in block mode: block_size 128, block budget 16 (2048 tokens covered)."""
+    from paper_2602_00777_b200.engine import HybridDecoder
+    from paper_2602_00777_b200.synthetic import generate_torch
+
+    bs, bb = 128, cfg.budget // 128
+    q, k, v = generate_torch(cfg, "cuda")
+    dec = HybridDecoder(cfg.actions, k, v, bb, q_heads=cfg.q_heads, block_size=bs)
+    for _ in range(3):
+        dec.step(q, cfg.context)
+    torch.cuda.synchronize()
+    dec.check_flags()
+    gr = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dec.step(q, cfg.context)
+    torch.cuda.current_stream().wait_stream(s)
+    with torch.cuda.graph(gr):
+        dec.step(q, cfg.context)
+    for _ in range(3):
+        gr.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    L, B = q.shape[0], q.shape[1]
+    nf = len(cfg.full_layers)
+    by = (nf * cfg.context + (L - nf) * bb * bs) * B * k.shape[2] * 2 * cfg.head_dim * 2
+    del gr, dec, q, k, v
+    torch.cuda.empty_cache()
+    return {"value": B / (ms * 1e-3), "ms_per_step": ms, "block_size": bs, "block_budget": bb,
+            "step_gbs": by / (ms * 1e-3) / 1e9, "kernels_per_step": 5}
+
+
 def _read_stream_gbs(torch):
     """Context for the roofline: a read-only stream (torch.sum over 8 GiB of int64), the
     ceiling a pure-read kernel can approach; the reported frac uses MEASURED_PEAKS.json."""
@@ -493,6 +532,11 @@ def run_ours(a):
                                                              "kernels", "roofline", "schedules")}
         except Exception as exc:  # noqa: BLE001
             extra["cfg4_qwen_64k_b16"] = {"error": str(exc)}
+        # block mode (paper §3.5): 16 blocks of 128 tokens = the same 2048-token coverage
+        try:
+            extra["cfg2_blocks_b8"] = _block_mode_line(a, cfg, torch)
+        except Exception as exc:  # noqa: BLE001
+            extra["cfg2_blocks_b8"] = {"error": str(exc)}
         for b_small in (1, 4):
             try:
                 rb = measure_config(a, cfg, b_small, rank, world, torch, dist, e2e=False)

@@ -159,7 +159,8 @@ int hylra_block_select(const hylra_geometry* g, const float* scores, int n_slots
 
 /* Workspace for hylra_decode_step (covers scores, select and attention workspaces). */
 size_t hylra_decode_step_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
-                                         int n_valid, int budget, int sel_group);
+                                         int n_valid, int budget, int sel_group, int sinks,
+                                         int recent);
 
 /*
  * One hybrid decode step over all g->num_layers layers (Algorithm 2).
@@ -167,12 +168,20 @@ size_t hylra_decode_step_workspace_bytes(const hylra_geometry* g, const uint8_t*
  * idx    : int32 [n_full][B][Hkv/sel_group][k_stride]; slot s holds the selection of
  *          the s-th FULL layer; a REUSE layer's selection is its source slot's.
  * All FULL layers are scored in one launch, all selections made in one launch and all
- * REUSE layers gathered in one launch: 3 kernels per step whatever L is.
+ * REUSE layers gathered in one launch: 3 kernels per step whatever L is. sinks / recent
+ * (engine.py:122-126, off = 0) add the first `sinks` and last `recent` tokens to the sets
+ * REUSE layers read (one more launch); idx keeps the FULL layers' own sets.
  */
 int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, const void* v,
                       int n_valid, const uint8_t* actions, int budget, int sel_group,
-                      int refine, float* out, int32_t* idx, int k_stride, void* ws,
-                      size_t ws_bytes, void* stream);
+                      int refine, int sinks, int recent, float* out, int32_t* idx,
+                      int k_stride, void* ws, size_t ws_bytes, void* stream);
+
+/* Sink / recent augmentation (engine.py:122-126): out[r] = sorted(idx[r][0..k_eff) |
+ * [0, sinks) | [n_valid - recent, n_valid)), counts[r] its length. */
+int hylra_augment_selection(const int32_t* idx, int rows, int k_eff, int k_stride, int n_valid,
+                            int sinks, int recent, int32_t* out, int out_stride,
+                            int32_t* counts, void* stream);
 
 /* Block-mode decode step (engine.py:212-286): budget counts blocks of block_size tokens;
  * blocks[s][b][grp][bk_stride] receives each FULL layer's block selection. */

@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = (
     "hylra_decode_step_workspace_bytes",
     "hylra_decode_step",
     "hylra_overlap_counts",
+    "hylra_augment_selection",
     "hylra_block_select",
     "hylra_decode_step_blocks_workspace_bytes",
     "hylra_decode_step_blocks",
@@ -106,10 +107,12 @@ def lib() -> ctypes.CDLL:
         l.hylra_decode_step_blocks.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, vp,
                                                vp, i32, vp, sz, vp]
         l.hylra_decode_step_workspace_bytes.restype = sz
-        l.hylra_decode_step_workspace_bytes.argtypes = [gp, vp, i32, i32, i32]
+        l.hylra_decode_step_workspace_bytes.argtypes = [gp, vp, i32, i32, i32, i32, i32]
         l.hylra_decode_step.restype = i32
-        l.hylra_decode_step.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, vp, vp, i32,
-                                        vp, sz, vp]
+        l.hylra_decode_step.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, i32, vp,
+                                        vp, i32, vp, sz, vp]
+        l.hylra_augment_selection.restype = i32
+        l.hylra_augment_selection.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp]
         l.hylra_overlap_counts.restype = i32
         l.hylra_overlap_counts.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, vp]
         l.hylra_read_flags.restype = i32

@@ -17,29 +17,30 @@ namespace hylra {
 
 constexpr int kPoolThreads = 256;
 
-// grid (groups, B, slots); scores [slot][b][kh][row_stride] -> bscores [slot][b][grp][nb_stride]
+// grid (groups * B * slots, ceil(n_blocks / 8)); one warp per block, coalesced loads:
+// scores [slot][b][kh][row_stride] -> bscores [slot][b][grp][nb_stride]
 __global__ void __launch_bounds__(kPoolThreads)
     block_pool_kernel(const float* __restrict__ scores, int B, int Hkv, int sel_group,
                       int row_stride, int n_tokens, int block_size, float* __restrict__ bscores,
                       int nb_stride) {
-  const int grp = blockIdx.x, b = blockIdx.y, slot = blockIdx.z;
   const int n_groups = Hkv / sel_group;
-  const float* base = scores + ((int64_t)(slot * B + b) * Hkv + grp * sel_group) * row_stride;
-  float* outr = bscores + ((int64_t)(slot * B + b) * n_groups + grp) * nb_stride;
+  const int row = blockIdx.x;  // (slot * B + b) * n_groups + grp
+  const int grp = row % n_groups, sb = row / n_groups;
+  const float* base = scores + ((int64_t)sb * Hkv + grp * sel_group) * row_stride;
+  float* outr = bscores + (int64_t)row * nb_stride;
   const int nb = (n_tokens + block_size - 1) / block_size;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // one warp per block: lanes stride over the block's tokens (coalesced), then max-reduce
-  for (int blk = warp; blk < nb; blk += kPoolThreads / 32) {
-    const int t0 = blk * block_size, t1 = min(n_tokens, t0 + block_size);
-    float m = -INFINITY;
-    for (int t = t0 + lane; t < t1; t += 32) {
-      float s = __ldg(base + t);
-      for (int h = 1; h < sel_group; ++h) s += __ldg(base + (int64_t)h * row_stride + t);
-      m = fmaxf(m, s);
-    }
-    m = warp_max(m);
-    if (lane == 0) outr[blk] = m;
+  const int lane = threadIdx.x & 31;
+  const int blk = blockIdx.y * (kPoolThreads / 32) + (threadIdx.x >> 5);
+  if (blk >= nb) return;
+  const int t0 = blk * block_size, t1 = min(n_tokens, t0 + block_size);
+  float m = -INFINITY;
+  for (int t = t0 + lane; t < t1; t += 32) {
+    float s = __ldg(base + t);
+    for (int h = 1; h < sel_group; ++h) s += __ldg(base + (int64_t)h * row_stride + t);
+    m = fmaxf(m, s);
   }
+  m = warp_max(m);
+  if (lane == 0) outr[blk] = m;
 }
 
 // grid (rows): blocks [row][bk_stride] (ascending, bb valid) -> tokens [row][tok_stride],
@@ -61,6 +62,46 @@ __global__ void __launch_bounds__(kPoolThreads)
     const int last = br[bb - 1];
     counts[row] = (bb - 1) * block_size + min(block_size, n_tokens - last * block_size);
   }
+}
+
+}  // namespace hylra
+
+namespace hylra {
+
+// Sink / recent augmentation of REUSE selections (engine.py:122-126 _augment_selection):
+// out = sorted(sel | [0, sinks) | [n - recent, n)). grid (rows); idx rows are ascending.
+__global__ void __launch_bounds__(kPoolThreads)
+    augment_kernel(const int32_t* __restrict__ idx, int k_stride, int k_eff, int n, int sinks,
+                   int recent, int32_t* __restrict__ out, int out_stride,
+                   int32_t* __restrict__ counts) {
+  const int row = blockIdx.x;
+  const int32_t* src = idx + (int64_t)row * k_stride;
+  int32_t* dst = out + (int64_t)row * out_stride;
+  const int s = min(sinks, n);
+  const int u0 = max(n - recent, 0);
+  if (u0 <= s) {  // the two ranges already cover every token
+    for (int i = threadIdx.x; i < n; i += kPoolThreads) dst[i] = i;
+    if (threadIdx.x == 0) counts[row] = n;
+    return;
+  }
+  // selected tokens strictly between the ranges: [lower_bound(s), lower_bound(u0))
+  __shared__ int s_lb[2];
+  if (threadIdx.x < 2) {
+    const int key = threadIdx.x == 0 ? s : u0;
+    int a = 0, z = k_eff;
+    while (a < z) {
+      const int m = (a + z) >> 1;
+      if (src[m] < key) a = m + 1;
+      else z = m;
+    }
+    s_lb[threadIdx.x] = a;
+  }
+  __syncthreads();
+  const int mid0 = s_lb[0], mid = s_lb[1] - s_lb[0];
+  for (int i = threadIdx.x; i < s; i += kPoolThreads) dst[i] = i;
+  for (int i = threadIdx.x; i < mid; i += kPoolThreads) dst[s + i] = src[mid0 + i];
+  for (int i = threadIdx.x; i < n - u0; i += kPoolThreads) dst[s + mid + i] = u0 + i;
+  if (threadIdx.x == 0) counts[row] = s + mid + (n - u0);
 }
 
 }  // namespace hylra

@@ -351,7 +351,7 @@ int launch_block_select(const hylra_geometry* g, const float* scores, int n_slot
   const int groups = g->kv_heads / sel_group;
   if (bk_stride < bb || (tokens_out && tok_stride < bb * block_size))
     return fail(HYLRA_ERR_CONFIGURATION, "block/token output strides too small");
-  dim3 grid(groups, g->batch, n_slots);
+  dim3 grid(n_slots * g->batch * groups, (nb + kPoolThreads / 32 - 1) / (kPoolThreads / 32));
   block_pool_kernel<<<grid, kPoolThreads, 0, st>>>(scores, g->batch, g->kv_heads, sel_group,
                                                    scores_row_stride(g), n_valid, block_size,
                                                    bscores, nb_stride_of(nb));
@@ -378,11 +378,14 @@ struct StepLayout {
   int k_eff, n_groups;
   int bb = 0, tok_stride = 0;                   // block mode
   size_t off_bscores = 0, off_tokens = 0, off_counts = 0;
+  int aug_stride = 0;                           // sink / recent augmentation
+  size_t off_aug = 0, off_aug_counts = 0;
   size_t off_scores, off_attn, attn_bytes, off_attn_r, attn_bytes_r, total;
 };
 
 int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, int budget,
-                int sel_group, StepLayout* s, int block_size = 1) {
+                int sel_group, StepLayout* s, int block_size = 1, int sinks = 0,
+                int recent = 0) {
   if (int e = check_geometry(g)) return e;
   if (!actions) return fail(HYLRA_ERR_CONFIGURATION, "actions is NULL");
   if (actions[0] != 1)
@@ -425,6 +428,16 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
     off = align_up(off + sizeof(int32_t) * rows, 256);
   } else {
     s->k_eff = std::min(budget, n_valid);
+    if (sinks < 0 || recent < 0)
+      return fail(HYLRA_ERR_INVALID_INPUT, "include_sinks and include_recent must be >= 0");
+    if ((sinks > 0 || recent > 0) && !s->reuse_ids.empty()) {
+      const size_t rows = nf * g->batch * s->n_groups;
+      s->aug_stride = std::min(n_valid, s->k_eff + sinks + recent);
+      s->off_aug = off;
+      off = align_up(off + sizeof(int32_t) * rows * s->aug_stride, 256);
+      s->off_aug_counts = off;
+      off = align_up(off + sizeof(int32_t) * rows, 256);
+    }
   }
   // FULL and REUSE get disjoint attention workspaces: each kernel's split-K counters must
   // start at zero, and the other launch's partial buffers would otherwise overlap them.
@@ -432,7 +445,10 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   s->attn_bytes = attn_layout(g, (int)nf, n_valid).total;
   s->off_attn_r = align_up(s->off_attn + s->attn_bytes, 256);
   s->attn_bytes_r =
-      s->reuse_ids.empty() ? 0 : attn_layout(g, (int)s->reuse_ids.size(), s->k_eff).total;
+      s->reuse_ids.empty()
+          ? 0
+          : attn_layout(g, (int)s->reuse_ids.size(), s->aug_stride ? s->aug_stride : s->k_eff)
+                .total;
   s->total = s->off_attn_r + s->attn_bytes_r;
   return HYLRA_OK;
 }
@@ -504,18 +520,19 @@ int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, co
 }
 
 size_t hylra_decode_step_workspace_bytes(const hylra_geometry* g, const uint8_t* actions,
-                                         int n_valid, int budget, int sel_group) {
+                                         int n_valid, int budget, int sel_group, int sinks,
+                                         int recent) {
   StepLayout s;
-  if (step_layout(g, actions, n_valid, budget, sel_group, &s)) return 0;
+  if (step_layout(g, actions, n_valid, budget, sel_group, &s, 1, sinks, recent)) return 0;
   return s.total;
 }
 
 int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, const void* v,
                       int n_valid, const uint8_t* actions, int budget, int sel_group,
-                      int refine, float* out, int32_t* idx, int k_stride, void* ws,
-                      size_t ws_bytes, void* stream) {
+                      int refine, int sinks, int recent, float* out, int32_t* idx,
+                      int k_stride, void* ws, size_t ws_bytes, void* stream) {
   StepLayout s;
-  if (int e = step_layout(g, actions, n_valid, budget, sel_group, &s)) return e;
+  if (int e = step_layout(g, actions, n_valid, budget, sel_group, &s, 1, sinks, recent)) return e;
   if (!ws || ws_bytes < s.total)
     return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, s.total);
   if (k_stride < s.k_eff)
@@ -534,13 +551,44 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                             flags, st))
     return e;
   if (!s.reuse_ids.empty()) {
-    if (int e = launch_attention(g, true, q, k, v, n_valid, s.k_eff, (int)s.reuse_ids.size(),
-                                 s.reuse_ids.data(), s.reuse_src.data(), idx, nullptr, k_stride,
+    const int32_t* ridx = idx;
+    const int32_t* rcnt = nullptr;
+    int rstride = k_stride, rk = s.k_eff;
+    if (s.aug_stride) {
+      int32_t* aug = reinterpret_cast<int32_t*>(w + s.off_aug);
+      int32_t* acnt = reinterpret_cast<int32_t*>(w + s.off_aug_counts);
+      const int rows = nf * g->batch * s.n_groups;
+      augment_kernel<<<rows, kPoolThreads, 0, st>>>(idx, k_stride, s.k_eff, n_valid, sinks,
+                                                    recent, aug, s.aug_stride, acnt);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      if (int e = cuda_check(cudaGetLastError(), "augment launch")) return e;
+      ridx = aug;
+      rcnt = acnt;
+      rstride = rk = s.aug_stride;
+    }
+    if (int e = launch_attention(g, true, q, k, v, n_valid, rk, (int)s.reuse_ids.size(),
+                                 s.reuse_ids.data(), s.reuse_src.data(), ridx, rcnt, rstride,
                                  sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags,
                                  st))
       return e;
   }
   return HYLRA_OK;
+}
+
+int hylra_augment_selection(const int32_t* idx, int rows, int k_eff, int k_stride, int n_valid,
+                            int sinks, int recent, int32_t* out, int out_stride,
+                            int32_t* counts, void* stream) {
+  if (!idx || !out || !counts) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  if (sinks < 0 || recent < 0)
+    return fail(HYLRA_ERR_INVALID_INPUT, "include_sinks and include_recent must be >= 0");
+  if (rows < 1 || k_eff < 1 || k_eff > k_stride || n_valid < 1)
+    return fail(HYLRA_ERR_INVALID_INPUT, "invalid augmentation dimensions");
+  if (out_stride < std::min(n_valid, k_eff + sinks + recent))
+    return fail(HYLRA_ERR_CONFIGURATION, "out_stride %d too small", out_stride);
+  augment_kernel<<<rows, kPoolThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      idx, k_stride, k_eff, n_valid, sinks, recent, out, out_stride, counts);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_check(cudaGetLastError(), "augment launch");
 }
 
 int hylra_block_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,

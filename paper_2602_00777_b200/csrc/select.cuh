@@ -57,7 +57,10 @@ struct SelectParams {
 __host__ __device__ constexpr size_t sel_bitmap_bytes(int n) {
   return (size_t)((n + kChunk - 1) / kChunk) * kChunk / 8;
 }
-constexpr size_t kSelFixedBytes = kBins * 4 + kCandCap * (8 + 4) + kSelThreads * 4;
+// block refinement: the group's queries staged as floats (exact for bf16/fp32 inputs)
+constexpr int kQsFloats = 4096;
+constexpr size_t kSelFixedBytes = kBins * 4 + kCandCap * (8 + 4) + kSelThreads * 4 +
+                                  kQsFloats * 4;
 __host__ __device__ constexpr size_t sel_smem_bytes(int n) {
   return sel_bitmap_bytes(n) + kSelFixedBytes;
 }
@@ -68,6 +71,7 @@ struct SelSmem {
   double* cv;        // [kCandCap] window scores (fp32 value, then float64 re-score)
   int* ci;           // [kCandCap] window token indices
   float* xchg;       // [kSelThreads]
+  float* qs;         // [kQsFloats]
 };
 
 __device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
@@ -78,6 +82,7 @@ __device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
   m.cv = reinterpret_cast<double*>(base + bb + kBins * 4);
   m.ci = reinterpret_cast<int*>(base + bb + kBins * 4 + kCandCap * 8);
   m.xchg = reinterpret_cast<float*>(m.ci + kCandCap);
+  m.qs = m.xchg + kSelThreads;
   return m;
 }
 
@@ -243,13 +248,36 @@ __device__ void rescore_f64(const SelectParams& p, int slot, int b, int grp, con
 }
 
 // float64 score of candidate BLOCKS: the max over the block's tokens of the head-order
-// summed q.k/sqrt(d) (engine.py:256-262 + attention.py:287-295). One warp per block, one
-// lane per token.
-__device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int grp,
-                                   const int* blocks, double* vals, int n) {
+// summed q.k/sqrt(d) (engine.py:256-262 + attention.py:287-295). The group's queries are
+// staged in shared memory as doubles (qs: sel_group * G * D); one warp per block, one lane
+// per token, each K row read once with 16-byte loads.
+template <typename T>
+__device__ __forceinline__ void load8_f64(const T* src, double* dst);
+template <>
+__device__ __forceinline__ void load8_f64<__nv_bfloat16>(const __nv_bfloat16* src, double* dst) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    dst[2 * j] = (double)__uint_as_float(w[j] << 16);
+    dst[2 * j + 1] = (double)__uint_as_float(w[j] & 0xffff0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void load8_f64<float>(const float* src, double* dst) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+  const float4 c = __ldg(reinterpret_cast<const float4*>(src) + 1);
+  dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
+  dst[4] = c.x; dst[5] = c.y; dst[6] = c.z; dst[7] = c.w;
+}
+
+template <typename T, bool QS>
+__device__ void rescore_blocks_t(const SelectParams& p, int slot, int b, int grp, const int* blocks,
+                                 double* vals, int n, const float* qs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int layer = p.layers[slot];
   const double sqd = sqrt((double)p.D);
+  const int G = p.G, D = p.D;
   for (int c = warp; c < n; c += kSelWarps) {
     const int t0 = blocks[c] * p.block_size;
     const int t1 = min(p.n_tokens, t0 + p.block_size);
@@ -258,22 +286,56 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
       double agg = 0.0;
       for (int hh = 0; hh < p.sel_group; ++hh) {
         const int kh = grp * p.sel_group + hh;
-        const int64_t koff = layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
-        for (int g = 0; g < p.G; ++g) {
-          const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D;
-          double dot = 0.0;
-          for (int i = 0; i < p.D; ++i)
-            dot += (p.dtype == 0 ? elem_f64<__nv_bfloat16>(p.q, qoff + i) *
-                                       elem_f64<__nv_bfloat16>(p.k, koff + i)
-                                 : elem_f64<float>(p.q, qoff + i) * elem_f64<float>(p.k, koff + i));
-          agg += dot / sqd;
+        const T* kr = reinterpret_cast<const T*>(p.k) + layer * p.kv_sl + b * p.kv_sb +
+                      kh * p.kv_sh + (int64_t)tok * D;
+        const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * G) * D;
+        double acc[kMaxG];
+#pragma unroll
+        for (int g = 0; g < kMaxG; ++g) acc[g] = 0.0;
+        for (int d0 = 0; d0 < D; d0 += 8) {
+          double kx[8];
+          load8_f64<T>(kr + d0, kx);
+#pragma unroll
+          for (int g = 0; g < kMaxG; ++g) {
+            if (g < G) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const double qv = QS ? (double)qs[(hh * G + g) * D + d0 + j]
+                                     : elem_f64<T>(p.q, qoff + g * D + d0 + j);
+                acc[g] += qv * kx[j];
+              }
+            }
+          }
         }
+        for (int g = 0; g < G; ++g) agg += acc[g] / sqd;
       }
       best = fmax(best, agg);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) vals[c] = best;
+  }
+}
+
+__device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int grp,
+                                   const int* blocks, double* vals, int n, float* qs) {
+  // stage the group's queries (sel_group kv heads x G query heads x D) when they fit
+  const int layer = p.layers[slot];
+  const int nq = p.sel_group * p.G * p.D;
+  const bool fits = nq <= kQsFloats;
+  if (fits) {
+    const int64_t base = layer * p.q_sl + b * p.q_sb + (int64_t)(grp * p.sel_group * p.G) * p.D;
+    for (int e = threadIdx.x; e < nq; e += kSelThreads)
+      qs[e] = p.dtype == 0 ? (float)elem_f64<__nv_bfloat16>(p.q, base + e)
+                           : (float)elem_f64<float>(p.q, base + e);
+  }
+  __syncthreads();
+  if (p.dtype == 0) {
+    if (fits) rescore_blocks_t<__nv_bfloat16, true>(p, slot, b, grp, blocks, vals, n, qs);
+    else rescore_blocks_t<__nv_bfloat16, false>(p, slot, b, grp, blocks, vals, n, qs);
+  } else {
+    if (fits) rescore_blocks_t<float, true>(p, slot, b, grp, blocks, vals, n, qs);
+    else rescore_blocks_t<float, false>(p, slot, b, grp, blocks, vals, n, qs);
   }
 }
 
@@ -708,7 +770,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   if (nw > 0) {
     __syncthreads();
     if (refine) {
-      if (p.block_size > 1) rescore_f64_blocks(p, slot, b, grp, sm.ci, sm.cv, nw);
+      if (p.block_size > 1) rescore_f64_blocks(p, slot, b, grp, sm.ci, sm.cv, nw, sm.qs);
       else rescore_f64(p, slot, b, grp, sm.ci, sm.cv, nw);
       __syncthreads();
     }

@@ -65,7 +65,8 @@ class HybridDecoder:
     """
 
     def __init__(self, policy, k_cache: torch.Tensor, v_cache: torch.Tensor, budget: int, *,
-                 q_heads: int, sel_group: int = 1, refine: bool = True, block_size: int = 1):
+                 q_heads: int, sel_group: int = 1, refine: bool = True, block_size: int = 1,
+                 include_sinks: int = 0, include_recent: int = 0):
         self.actions = _actions_of(policy)
         if len(self.actions) != k_cache.shape[0]:
             raise ConfigurationError(
@@ -90,7 +91,12 @@ class HybridDecoder:
         self.out = torch.empty((L, B, q_heads, d), dtype=torch.float32, device=k_cache.device)
         if block_size < 1:
             raise InvalidInputError(f"block_size must be >= 1, got {block_size}")
+        if include_sinks < 0 or include_recent < 0:
+            raise InvalidInputError("include_sinks and include_recent must be >= 0")
+        if block_size > 1 and (include_sinks or include_recent):
+            raise ConfigurationError("sink/recent augmentation applies to token selection only")
         self.block_size = int(block_size)
+        self.sinks, self.recent = int(include_sinks), int(include_recent)
         # token mode: k indices per row; block mode: budget counts blocks
         self.k_stride = (min(self.budget, -(-cap // block_size)) if block_size > 1
                          else min(self.budget, cap))
@@ -99,7 +105,8 @@ class HybridDecoder:
         self._acts = _abi.uint8_array(1 if a is Action.FULL else 0 for a in self.actions)
         self.ws = torch.zeros(256, dtype=torch.uint8, device=k_cache.device)
         has_reuse = len(self.full_layers) < L
-        self.kernels_per_step = (2 + has_reuse) if block_size == 1 else (3 + 2 * has_reuse)
+        self.kernels_per_step = ((2 + has_reuse + (has_reuse and bool(include_sinks or include_recent)))
+                                 if block_size == 1 else (3 + 2 * has_reuse))
 
     def _geometry(self, q):
         return geometry(q, self.k, self.v, self.out)
@@ -107,7 +114,7 @@ class HybridDecoder:
     def workspace_bytes(self, q, n_valid: int) -> int:
         g = self._geometry(q)
         return int(_abi.lib().hylra_decode_step_workspace_bytes(
-            g, self._acts, int(n_valid), self.budget, self.sel_group))
+            g, self._acts, int(n_valid), self.budget, self.sel_group, self.sinks, self.recent))
 
     def step(self, q: torch.Tensor, n_valid: int | None = None) -> StepResult:
         g = self._geometry(q)
@@ -128,18 +135,19 @@ class HybridDecoder:
             return StepResult(self.out, self.idx[..., :bb], self.slot_of_layer,
                               self.full_layers)
         need = int(lib.hylra_decode_step_workspace_bytes(
-            g, self._acts, n_valid, self.budget, self.sel_group))
+            g, self._acts, n_valid, self.budget, self.sel_group, self.sinks, self.recent))
         if need == 0:
             _abi.check(lib.hylra_decode_step(
                 g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
-                self.budget, self.sel_group, int(self.refine), self.out.data_ptr(),
-                self.idx.data_ptr(), self.k_stride, None, 0, 0))
+                self.budget, self.sel_group, int(self.refine), self.sinks, self.recent,
+                self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, None, 0, 0))
         if self.ws.numel() < need:
             self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
         _abi.check(lib.hylra_decode_step(
             g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
-            self.budget, self.sel_group, int(self.refine), self.out.data_ptr(),
-            self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(), self.ws.numel(), st))
+            self.budget, self.sel_group, int(self.refine), self.sinks, self.recent,
+            self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(),
+            self.ws.numel(), st))
         k_eff = min(self.budget, n_valid)
         return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
 
@@ -409,11 +417,13 @@ def _check_model_args(model, actions, steps: int, budget: int) -> None:
         raise InvalidInputError(f"budget must be >= 1, got {budget}")
 
 
-def _run(model, actions, budget: int, steps: int, device, refine: bool):
+def _run(model, actions, budget: int, steps: int, device, refine: bool, sinks: int = 0,
+         recent: int = 0):
     cfg = model.config
     q, k, v = _model_tensors(model, steps, device)
     H = cfg.heads
-    dec = HybridDecoder(actions, k, v, budget, q_heads=H, sel_group=H, refine=refine)
+    dec = HybridDecoder(actions, k, v, budget, q_heads=H, sel_group=H, refine=refine,
+                        include_sinks=sinks, include_recent=recent)
     outs, sels = [], []
     for t in range(steps):
         n_t = cfg.context_len + t
@@ -436,10 +446,9 @@ def hybrid_decode(model, policy, budget: int, steps: int, *, include_sinks: int 
     _check_model_args(model, actions, steps, budget)
     if include_sinks < 0 or include_recent < 0:
         raise InvalidInputError("include_sinks and include_recent must be >= 0")
-    if include_sinks or include_recent:
-        raise ConfigurationError("sink/recent augmentation is not implemented on the GPU path")
     cfg = model.config
-    outputs, sel_arrays, _ = _run(model, actions, budget, steps, device, refine)
+    outputs, sel_arrays, _ = _run(model, actions, budget, steps, device, refine,
+                                  include_sinks, include_recent)
     baseline = run_full_trace(model, steps, min(budget, cfg.context_len), device=device,
                               refine=refine)
     L = cfg.layers
@@ -453,7 +462,13 @@ def hybrid_decode(model, policy, budget: int, steps: int, *, include_sinks: int 
                 cur = TopKSet(tuple(int(i) for i in sel_arrays[t][slot]), budget)
                 step_g.append(None)
             else:
-                step_g.append(min(budget, n_t))
+                if include_sinks or include_recent:  # engine.py:122-126,187-188
+                    extra = set(range(min(include_sinks, n_t))) | \
+                        set(range(max(n_t - include_recent, 0), n_t))
+                    merged = tuple(sorted(set(cur.indices) | extra))
+                    if merged != cur.indices or cur.budget != len(merged):
+                        cur = TopKSet(merged, len(merged))
+                step_g.append(cur.size)
             step_sel.append(cur)
         selections.append(tuple(step_sel))
         gathered.append(tuple(step_g))

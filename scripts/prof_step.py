@@ -21,13 +21,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--block-size", type=int, default=1)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 if a.batch:
     cfg = cfg.with_(batch=a.batch)
 q, k, v = generate_torch(cfg, "cuda")
 torch.cuda.synchronize()
-dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
+bs = a.block_size
+dec = HybridDecoder(cfg.actions, k, v, cfg.budget // bs if bs > 1 else cfg.budget,
+                    q_heads=cfg.q_heads, block_size=bs)
 for _ in range(a.steps):
     dec.step(q, cfg.context)
 torch.cuda.synchronize()

@@ -50,31 +50,35 @@ def test_workspace_queries_are_host_only():
     g = _geom()
     assert lib.hylra_attention_workspace_bytes(g, 2, 2048) > 256
     acts = _abi.uint8_array([1, 0, 1, 0])
-    assert lib.hylra_decode_step_workspace_bytes(g, acts, 2048, 128, 1) > 0
-    assert lib.hylra_decode_step_workspace_bytes(_geom(q_heads=7), acts, 2048, 128, 1) == 0
+    assert lib.hylra_decode_step_workspace_bytes(g, acts, 2048, 128, 1, 0, 0) > 0
+    assert lib.hylra_decode_step_workspace_bytes(_geom(q_heads=7), acts, 2048, 128, 1, 0, 0) == 0
 
 
 def test_status_codes_map_to_reference_exceptions():
     lib = _abi.lib()
     acts = _abi.uint8_array([0, 1, 1, 0])  # first layer REUSE
     with pytest.raises(InvalidInputError, match="first layer"):
-        _abi.check(lib.hylra_decode_step(_geom(), None, None, None, 2048, acts, 128, 1, 1,
+        _abi.check(lib.hylra_decode_step(_geom(), None, None, None, 2048, acts, 128, 1, 1, 0, 0,
                                          None, None, 128, None, 0, None))
     with pytest.raises(InvalidInputError, match="budget"):
         _abi.check(lib.hylra_decode_step(_geom(), None, None, None, 2048,
-                                         _abi.uint8_array([1, 0, 1, 0]), 0, 1, 1, None, None,
-                                         128, None, 0, None))
+                                         _abi.uint8_array([1, 0, 1, 0]), 0, 1, 1, 0, 0, None,
+                                         None, 128, None, 0, None))
     with pytest.raises(ConfigurationError, match="multiple"):
         _abi.check(lib.hylra_decode_step(_geom(q_heads=7), None, None, None, 2048,
-                                         _abi.uint8_array([1, 0, 1, 0]), 128, 1, 1, None, None,
-                                         128, None, 0, None))
+                                         _abi.uint8_array([1, 0, 1, 0]), 128, 1, 1, 0, 0, None,
+                                         None, 128, None, 0, None))
+    with pytest.raises(InvalidInputError, match="sinks"):
+        _abi.check(lib.hylra_decode_step(_geom(), None, None, None, 2048,
+                                         _abi.uint8_array([1, 0, 1, 0]), 128, 1, 1, -1, 0, None,
+                                         None, 128, None, 0, None))
     with pytest.raises(ConfigurationError, match="head_dim"):
         _abi.check(lib.hylra_full_decode(_geom(head_dim=80), None, None, None, 10, 1,
                                          _abi.int32_array([0]), None, None, None, 0, None))
     with pytest.raises(ConfigurationError, match="workspace"):
         _abi.check(lib.hylra_decode_step(_geom(), 1, 1, 1, 2048,
-                                         _abi.uint8_array([1, 0, 1, 0]), 128, 1, 1, 1, 1, 128,
-                                         None, 0, None))
+                                         _abi.uint8_array([1, 0, 1, 0]), 128, 1, 1, 0, 0, 1, 1,
+                                         128, None, 0, None))
 
 
 def test_missing_library_fails_loudly(tmp_path, monkeypatch):

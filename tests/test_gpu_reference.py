@@ -196,3 +196,28 @@ def test_config5_profile_policy_matches_oracle():
         po = dp_optimize(SimilarityMatrix(values=omerged, budget=cfg.budget), theta)
         assert p.actions == po.actions and p.sources == po.sources
         assert p.cum_similarity == po.cum_similarity
+
+
+def test_sink_and_recent_augmentation(golden_dir):
+    """tests/test_engine.py:146-158: REUSE sets = selection | first sinks | last recent;
+    FULL layers untouched (engine.py:122-126,187-188)."""
+    z = load_npz(golden_dir / "fixture_engine.npz")
+    model = FixtureModel(z["keys"], z["values"], z["queries"], int(z["context_len"]))
+    pol = policy_from_actions(("full", "reuse", "reuse", "full", "reuse", "reuse"))
+    plain = hybrid_decode(model, pol, 8, 2)
+    aug = hybrid_decode(model, pol, 8, 2, include_sinks=4, include_recent=4)
+    for t in range(2):
+        n_t = int(z["context_len"]) + t
+        for l in (1, 2, 4, 5):
+            base = set(plain.selections[t][l].indices)
+            want = base | set(range(4)) | set(range(n_t - 4, n_t))
+            assert set(aug.selections[t][l].indices) == want
+            assert aug.reuse_gathered_rows[t][l] == len(want)
+            # the oracle on the augmented set
+            qn = np.asarray(z["queries"][t][l, 0])
+            kn = np.asarray(z["keys"][l, 0, :n_t])
+            vn = np.asarray(z["values"][l, 0, :n_t])
+            ref = orc.subset_attention(qn, kn, vn, sorted(want))
+            assert rel(aug.outputs[t, l, 0], ref) < 1e-3
+        for l in (0, 3):
+            np.testing.assert_array_equal(plain.outputs[t, l], aug.outputs[t, l])
