@@ -43,6 +43,52 @@ __global__ void __launch_bounds__(kPoolThreads)
   if (lane == 0) outr[blk] = m;
 }
 
+// Vectorised pooling for block_size = 4 * W, W a power of two <= 32: each lane owns a
+// float4 of tokens, W lanes cover one block (a warp is block-aligned because W | 32), four
+// float4 loads in flight per thread. grid (groups * B * slots, ceil(n / (4 * 4 * 256))).
+constexpr int kPoolVec = 4;
+template <int W>
+__global__ void __launch_bounds__(kPoolThreads)
+    block_pool_vec_kernel(const float* __restrict__ scores, int Hkv, int sel_group,
+                          int row_stride, int n_tokens, float* __restrict__ bscores,
+                          int nb_stride) {
+  const int n_groups = Hkv / sel_group;
+  const int row = blockIdx.x;
+  const int grp = row % n_groups, sb = row / n_groups;
+  const float* base = scores + ((int64_t)sb * Hkv + grp * sel_group) * row_stride;
+  float* outr = bscores + (int64_t)row * nb_stride;
+  const int j0 = blockIdx.y * (kPoolThreads * kPoolVec) + threadIdx.x;  // float4 index
+  float4 v[kPoolVec];
+#pragma unroll
+  for (int u = 0; u < kPoolVec; ++u) {
+    const int j = j0 + u * kPoolThreads;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * j < n_tokens) {
+      for (int h = 0; h < sel_group; ++h) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(base + (int64_t)h * row_stride) + j);
+        v[u].x += x.x;
+        v[u].y += x.y;
+        v[u].z += x.z;
+        v[u].w += x.w;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < kPoolVec; ++u) {
+    const int j = j0 + u * kPoolThreads;
+    const int t = 4 * j;
+    float m = -INFINITY;
+    if (t < n_tokens) m = v[u].x;
+    if (t + 1 < n_tokens) m = fmaxf(m, v[u].y);
+    if (t + 2 < n_tokens) m = fmaxf(m, v[u].z);
+    if (t + 3 < n_tokens) m = fmaxf(m, v[u].w);
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((lane & (W - 1)) == 0 && t < n_tokens) outr[t / (4 * W)] = m;
+  }
+}
+
 // grid (rows): blocks [row][bk_stride] (ascending, bb valid) -> tokens [row][tok_stride],
 // counts[row] = number of covered tokens (< n_tokens).
 __global__ void __launch_bounds__(kPoolThreads)

@@ -273,6 +273,7 @@ size_t select_smem_bytes(int n_valid) { return sel_smem_bytes(n_valid); }
 
 struct BlockRows {  // block mode: rows are pooled block scores
   int block_size = 1, n_tokens = 0, row_stride = 0;
+  const float* tok_scores = nullptr;  // the token scores they were pooled from
 };
 
 int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
@@ -310,6 +311,8 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
   p.pre_grouped = blocks ? 1 : 0;
   p.block_size = blocks ? br.block_size : 1;
   p.n_tokens = blocks ? br.n_tokens : n_valid;
+  p.tok_scores = blocks ? br.tok_scores : nullptr;
+  p.tok_row_stride = scores_row_stride(g);
   p.tau_rel = 1.0f / 4096.0f;
   for (int i = 0; i < n_slots; ++i) {
     const int l = layer_ids ? layer_ids[i] : 0;
@@ -351,16 +354,31 @@ int launch_block_select(const hylra_geometry* g, const float* scores, int n_slot
   const int groups = g->kv_heads / sel_group;
   if (bk_stride < bb || (tokens_out && tok_stride < bb * block_size))
     return fail(HYLRA_ERR_CONFIGURATION, "block/token output strides too small");
-  dim3 grid(n_slots * g->batch * groups, (nb + kPoolThreads / 32 - 1) / (kPoolThreads / 32));
-  block_pool_kernel<<<grid, kPoolThreads, 0, st>>>(scores, g->batch, g->kv_heads, sel_group,
-                                                   scores_row_stride(g), n_valid, block_size,
-                                                   bscores, nb_stride_of(nb));
+  const int rows = n_slots * g->batch * groups;
+  const int rs = scores_row_stride(g), nbs = nb_stride_of(nb);
+  const int w = block_size / 4;
+  if (block_size % 4 == 0 && w <= 32 && (w & (w - 1)) == 0) {
+    dim3 grid(rows, (n_valid + 4 * kPoolVec * kPoolThreads - 1) / (4 * kPoolVec * kPoolThreads));
+    auto kern = w == 1    ? block_pool_vec_kernel<1>
+                : w == 2  ? block_pool_vec_kernel<2>
+                : w == 4  ? block_pool_vec_kernel<4>
+                : w == 8  ? block_pool_vec_kernel<8>
+                : w == 16 ? block_pool_vec_kernel<16>
+                          : block_pool_vec_kernel<32>;
+    kern<<<grid, kPoolThreads, 0, st>>>(scores, g->kv_heads, sel_group, rs, n_valid, bscores,
+                                        nbs);
+  } else {
+    dim3 grid(rows, (nb + kPoolThreads / 32 - 1) / (kPoolThreads / 32));
+    block_pool_kernel<<<grid, kPoolThreads, 0, st>>>(scores, g->batch, g->kv_heads, sel_group,
+                                                     rs, n_valid, block_size, bscores, nbs);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (int e = cuda_check(cudaGetLastError(), "block_pool launch")) return e;
   BlockRows br;
   br.block_size = block_size;
   br.n_tokens = n_valid;
   br.row_stride = nb_stride_of(nb);
+  br.tok_scores = scores;
   if (int e = launch_select(g, bscores, n_slots, nb, block_budget, sel_group, q, k, layer_ids,
                             blocks_out, bk_stride, info, flags, st, br))
     return e;

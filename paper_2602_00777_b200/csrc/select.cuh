@@ -32,6 +32,7 @@ constexpr int kSelThreads = 256;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kBins = 2048;
 constexpr int kCandCap = 1024;            // scores collected around the k-th bin
+constexpr int kSmallN = 2048;             // rows sorted outright (small-row path)
 constexpr int kSelMaxTokens = 262144;     // longest row (bitmap = 32 KB)
 constexpr int kChunk = kSelThreads * 32;  // tokens per bitmap chunk (one word per thread)
 
@@ -50,6 +51,8 @@ struct SelectParams {
   int pre_grouped;  // score rows already summed per group ([slot][b][grp][row_stride])
   int block_size;   // 1: token selection; >1: rows are block scores over n_tokens tokens
   int n_tokens;
+  const float* tok_scores;  // block mode: token scores [slot][b][kh][tok_row_stride] or null
+  int tok_row_stride;
   int layers[kMaxSlots];
 };
 
@@ -57,10 +60,8 @@ struct SelectParams {
 __host__ __device__ constexpr size_t sel_bitmap_bytes(int n) {
   return (size_t)((n + kChunk - 1) / kChunk) * kChunk / 8;
 }
-// block refinement: the group's queries staged as floats (exact for bf16/fp32 inputs)
-constexpr int kQsFloats = 4096;
 constexpr size_t kSelFixedBytes = kBins * 4 + kCandCap * (8 + 4) + kSelThreads * 4 +
-                                  kQsFloats * 4;
+                                  kSmallN * 8;
 __host__ __device__ constexpr size_t sel_smem_bytes(int n) {
   return sel_bitmap_bytes(n) + kSelFixedBytes;
 }
@@ -71,7 +72,7 @@ struct SelSmem {
   double* cv;        // [kCandCap] window scores (fp32 value, then float64 re-score)
   int* ci;           // [kCandCap] window token indices
   float* xchg;       // [kSelThreads]
-  float* qs;         // [kQsFloats]
+  uint64_t* keys;    // [kSmallN] small-row sort keys
 };
 
 __device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
@@ -82,7 +83,7 @@ __device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
   m.cv = reinterpret_cast<double*>(base + bb + kBins * 4);
   m.ci = reinterpret_cast<int*>(base + bb + kBins * 4 + kCandCap * 8);
   m.xchg = reinterpret_cast<float*>(m.ci + kCandCap);
-  m.qs = m.xchg + kSelThreads;
+  m.keys = reinterpret_cast<uint64_t*>(m.xchg + kSelThreads);
   return m;
 }
 
@@ -209,134 +210,118 @@ __device__ __forceinline__ double elem_f64(const void* p, int64_t i) {
   return (double)to_f32(reinterpret_cast<const T*>(p)[i]);
 }
 
-// float64 selection score of tokens toks[0..n): agg = sum over (kv head of the group,
-// query head g) of (q . k) / sqrt(d) in the reference's head order. One warp per token.
+// float64 selection score of a token: agg = sum over (kv head of the group, query head g)
+// of (q . k) / sqrt(d) in the reference's head order (engine.py:177-181). kLpt lanes share a
+// token (lane sub handles dims sub, sub + kLpt, ...), so a warp scores kTpw tokens at once;
+// every lane of the warp must call it (sub-group shuffles).
+constexpr int kLpt = 8, kTpw = 32 / kLpt;
+__device__ double token_score_f64(const SelectParams& p, int layer, int b, int grp, int tok) {
+  const int sub = threadIdx.x & (kLpt - 1);
+  const double sqd = sqrt((double)p.D);
+  double agg = 0.0;
+  for (int hh = 0; hh < p.sel_group; ++hh) {
+    const int kh = grp * p.sel_group + hh;
+    const int64_t koff = layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
+    for (int g = 0; g < p.G; ++g) {
+      const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D;
+      double part0 = 0.0, part1 = 0.0;
+      if (p.dtype == 0) {
+#pragma unroll 4
+        for (int i = sub; i < p.D; i += 2 * kLpt) {
+          part0 += elem_f64<__nv_bfloat16>(p.q, qoff + i) * elem_f64<__nv_bfloat16>(p.k, koff + i);
+          part1 += elem_f64<__nv_bfloat16>(p.q, qoff + i + kLpt) *
+                   elem_f64<__nv_bfloat16>(p.k, koff + i + kLpt);
+        }
+      } else {
+#pragma unroll 4
+        for (int i = sub; i < p.D; i += 2 * kLpt) {
+          part0 += elem_f64<float>(p.q, qoff + i) * elem_f64<float>(p.k, koff + i);
+          part1 += elem_f64<float>(p.q, qoff + i + kLpt) * elem_f64<float>(p.k, koff + i + kLpt);
+        }
+      }
+      double part = part0 + part1;
+#pragma unroll
+      for (int o = kLpt / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      agg += part / sqd;
+    }
+  }
+  return agg;
+}
+
+// float64 scores of candidate tokens toks[0..n); kTpw tokens per warp.
 __device__ void rescore_f64(const SelectParams& p, int slot, int b, int grp, const int* toks,
                             double* vals, int n) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int layer = p.layers[slot];
-  const double sqd = sqrt((double)p.D);
-  for (int c = warp; c < n; c += kSelWarps) {
-    const int tok = toks[c];
-    double agg = 0.0;
-    for (int hh = 0; hh < p.sel_group; ++hh) {
-      const int kh = grp * p.sel_group + hh;
-      const int64_t koff = layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
-      double kx[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = lane + 32 * j;
-        kx[j] = (i < p.D) ? (p.dtype == 0 ? elem_f64<__nv_bfloat16>(p.k, koff + i)
-                                          : elem_f64<float>(p.k, koff + i))
-                          : 0.0;
-      }
-      for (int g = 0; g < p.G; ++g) {
-        const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D;
-        double part = 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int i = lane + 32 * j;
-          if (i < p.D)
-            part += (p.dtype == 0 ? elem_f64<__nv_bfloat16>(p.q, qoff + i)
-                                  : elem_f64<float>(p.q, qoff + i)) * kx[j];
-        }
-        agg += warp_sum_f64(part) / sqd;
-      }
-    }
-    if (lane == 0) vals[c] = agg;
+  const int warp = threadIdx.x >> 5, sub = threadIdx.x & (kLpt - 1);
+  const int slot_in_warp = (threadIdx.x & 31) / kLpt;
+  for (int c0 = warp * kTpw; c0 < n; c0 += kSelWarps * kTpw) {  // warp-uniform trip count
+    const int c = c0 + slot_in_warp;
+    const double agg = token_score_f64(p, p.layers[slot], b, grp, toks[min(c, n - 1)]);
+    if (sub == 0 && c < n) vals[c] = agg;
   }
 }
 
-// float64 score of candidate BLOCKS: the max over the block's tokens of the head-order
-// summed q.k/sqrt(d) (engine.py:256-262 + attention.py:287-295). The group's queries are
-// staged in shared memory as doubles (qs: sel_group * G * D); one warp per block, one lane
-// per token, each K row read once with 16-byte loads.
-template <typename T>
-__device__ __forceinline__ void load8_f64(const T* src, double* dst);
-template <>
-__device__ __forceinline__ void load8_f64<__nv_bfloat16>(const __nv_bfloat16* src, double* dst) {
-  const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    dst[2 * j] = (double)__uint_as_float(w[j] << 16);
-    dst[2 * j + 1] = (double)__uint_as_float(w[j] & 0xffff0000u);
-  }
+__device__ __forceinline__ unsigned long long f64_key(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
-template <>
-__device__ __forceinline__ void load8_f64<float>(const float* src, double* dst) {
-  const float4 a = __ldg(reinterpret_cast<const float4*>(src));
-  const float4 c = __ldg(reinterpret_cast<const float4*>(src) + 1);
-  dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
-  dst[4] = c.x; dst[5] = c.y; dst[6] = c.z; dst[7] = c.w;
+__device__ __forceinline__ double key_f64(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
 }
 
-template <typename T, bool QS>
-__device__ void rescore_blocks_t(const SelectParams& p, int slot, int b, int grp, const int* blocks,
-                                 double* vals, int n, const float* qs) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int layer = p.layers[slot];
-  const double sqd = sqrt((double)p.D);
-  const int G = p.G, D = p.D;
-  for (int c = warp; c < n; c += kSelWarps) {
-    const int t0 = blocks[c] * p.block_size;
-    const int t1 = min(p.n_tokens, t0 + p.block_size);
-    double best = -INFINITY;
-    for (int tok = t0 + lane; tok < t1; tok += 32) {
-      double agg = 0.0;
-      for (int hh = 0; hh < p.sel_group; ++hh) {
-        const int kh = grp * p.sel_group + hh;
-        const T* kr = reinterpret_cast<const T*>(p.k) + layer * p.kv_sl + b * p.kv_sb +
-                      kh * p.kv_sh + (int64_t)tok * D;
-        const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * G) * D;
-        double acc[kMaxG];
-#pragma unroll
-        for (int g = 0; g < kMaxG; ++g) acc[g] = 0.0;
-        for (int d0 = 0; d0 < D; d0 += 8) {
-          double kx[8];
-          load8_f64<T>(kr + d0, kx);
-#pragma unroll
-          for (int g = 0; g < kMaxG; ++g) {
-            if (g < G) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const double qv = QS ? (double)qs[(hh * G + g) * D + d0 + j]
-                                     : elem_f64<T>(p.q, qoff + g * D + d0 + j);
-                acc[g] += qv * kx[j];
-              }
-            }
-          }
-        }
-        for (int g = 0; g < G; ++g) agg += acc[g] / sqd;
-      }
-      best = fmax(best, agg);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (lane == 0) vals[c] = best;
-  }
-}
-
+// float64 scores of candidate BLOCKS blocks[0..n): the max over the block's tokens of the
+// token score (engine.py:256-262 + attention.py:287-295); the per-block max goes through
+// ordered 64-bit keys in place of vals. vals[c] holds the block's fp32 score on entry.
+// Only tokens whose fp32 score is >= that score - tau are re-scored: with fp32 scores within
+// tau/2 of float64 (the premise of the refinement window), the float64 maximiser t* obeys
+// s32(t*) >= s64(t*) - tau/2 >= s64(t_max32) - tau/2 >= s32(t_max32) - tau. If more than
+// kSmallN tokens qualify (or token scores are absent) every token is re-scored.
 __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int grp,
-                                   const int* blocks, double* vals, int n, float* qs) {
-  // stage the group's queries (sel_group kv heads x G query heads x D) when they fit
-  const int layer = p.layers[slot];
-  const int nq = p.sel_group * p.G * p.D;
-  const bool fits = nq <= kQsFloats;
-  if (fits) {
-    const int64_t base = layer * p.q_sl + b * p.q_sb + (int64_t)(grp * p.sel_group * p.G) * p.D;
-    for (int e = threadIdx.x; e < nq; e += kSelThreads)
-      qs[e] = p.dtype == 0 ? (float)elem_f64<__nv_bfloat16>(p.q, base + e)
-                           : (float)elem_f64<float>(p.q, base + e);
+                                   const int* blocks, double* vals, int n, float tau,
+                                   uint64_t* list) {
+  __shared__ int s_cnt;
+  const int warp = threadIdx.x >> 5, sub = threadIdx.x & (kLpt - 1);
+  const int slot_in_warp = (threadIdx.x & 31) / kLpt;
+  const int bs = p.block_size;
+  const int total = n * bs;
+  if (threadIdx.x == 0) s_cnt = p.tok_scores ? 0 : kSmallN + 1;
+  __syncthreads();
+  if (p.tok_scores) {
+    const float* trow = p.tok_scores +
+                        ((int64_t)(slot * p.B + b) * p.Hkv + grp * p.sel_group) * p.tok_row_stride;
+    for (int e = threadIdx.x; e < total; e += kSelThreads) {
+      const int c = e / bs;
+      const int tok = blocks[c] * bs + (e - c * bs);
+      if (tok >= p.n_tokens) continue;
+      float s = trow[tok];  // the pooling kernel's fp32 head-order sum
+      for (int h = 1; h < p.sel_group; ++h) s += trow[(int64_t)h * p.tok_row_stride + tok];
+      if (s >= (float)vals[c] - tau) {
+        const int pos = atomicAdd(&s_cnt, 1);
+        if (pos < kSmallN) list[pos] = ((uint64_t)c << 32) | (uint32_t)tok;
+      }
+    }
   }
   __syncthreads();
-  if (p.dtype == 0) {
-    if (fits) rescore_blocks_t<__nv_bfloat16, true>(p, slot, b, grp, blocks, vals, n, qs);
-    else rescore_blocks_t<__nv_bfloat16, false>(p, slot, b, grp, blocks, vals, n, qs);
-  } else {
-    if (fits) rescore_blocks_t<float, true>(p, slot, b, grp, blocks, vals, n, qs);
-    else rescore_blocks_t<float, false>(p, slot, b, grp, blocks, vals, n, qs);
+  const bool listed = s_cnt <= kSmallN;
+  const int items = listed ? s_cnt : total;
+  unsigned long long* vk = reinterpret_cast<unsigned long long*>(vals);
+  for (int c = threadIdx.x; c < n; c += kSelThreads) vk[c] = 0ull;
+  __syncthreads();
+  for (int e0 = warp * kTpw; e0 < items; e0 += kSelWarps * kTpw) {  // warp-uniform trips
+    const int e = min(e0 + slot_in_warp, items - 1);
+    int c, tok;
+    if (listed) {
+      c = (int)(list[e] >> 32);
+      tok = (int)(uint32_t)list[e];
+    } else {
+      c = e / bs;
+      tok = blocks[c] * bs + (e - c * bs);
+    }
+    const bool ok = e0 + slot_in_warp < items && tok < p.n_tokens;
+    const double agg = token_score_f64(p, p.layers[slot], b, grp, ok ? tok : blocks[c] * bs);
+    if (ok && sub == 0) atomicMax(vk + c, f64_key(agg));
   }
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += kSelThreads) vals[c] = key_f64(vk[c]);
 }
 
 // MSB-first 4 x 8-bit radix select of the rank-`rank` (1-based, descending) score of the
@@ -382,6 +367,85 @@ __device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, f
   }
   *T_out = key_float(prefix);
   *gt_out = rank - krem;
+}
+
+// Descending bitonic sort of np (power of two) 64-bit keys in shared memory.
+__device__ void bitonic_sort_desc(uint64_t* a, int np) {
+  for (int size = 2; size <= np; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (np >> 1); t += kSelThreads) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const uint64_t x = a[i], y = a[j];
+        if ((x < y) == ((i & size) == 0)) {
+          a[i] = y;
+          a[j] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Rows of at most kSmallN scores (block rows, short caches): one exact sort of
+// (score desc, index asc) keys replaces phases A-D. Tokens ranked above the window are set
+// in the bitmap; the window [T - tau, T + tau] (refine) goes to cv/ci for the shared
+// re-score + rank step. Without refinement (or with non-finite scores, or a window larger
+// than kCandCap, flagged 4) the first k sorted entries are the answer.
+__device__ void small_row_select(const SelectParams& p, const RowReader& rd, int n, int k,
+                                 bool refine, const SelSmem& sm, Red& red, int* above_w,
+                                 int* nw_out, float* tau_out) {
+  const int tid = threadIdx.x;
+  uint64_t* keys = sm.keys;
+  int np = 64;
+  while (np < n) np <<= 1;
+  float nanacc = 0.f, mx = 0.f;
+  for (int i = tid; i < np; i += kSelThreads) {
+    uint64_t key = 0ull;  // padding sorts after every real entry
+    if (i < n) {
+      const float v = rd.at(i);
+      nanacc = fmaf(v, 0.f, nanacc);
+      mx = fmaxf(mx, fabsf(v));
+      key = ((uint64_t)float_key(v) << 32) | (uint32_t)(~(uint32_t)i);
+    }
+    keys[i] = key;
+  }
+  const int bad = block_sum_int(nanacc != nanacc ? 1 : 0, red);
+  mx = block_max_float(mx, red);
+  if (bad && tid == 0) atomicOr(p.flags, 2);
+  __syncthreads();
+  bitonic_sort_desc(keys, np);
+  auto val = [&](int pos) { return key_float((uint32_t)(keys[pos] >> 32)); };
+  auto tok = [&](int pos) { return (int)(~(uint32_t)keys[pos]); };
+  int a = k, z = k;
+  if (refine && !bad) {
+    const float T = val(k - 1);
+    const float tau = *tau_out = fmaxf(p.tau_rel * mx, 1e-30f);
+    const float lo_w = T - tau, hi_w = T + tau;
+    int ca = 0, cz = 0;
+    for (int pos = tid; pos < n; pos += kSelThreads) {
+      const float v = val(pos);
+      ca += v > hi_w;
+      cz += v >= lo_w;
+    }
+    a = block_sum_int(ca, red);
+    z = block_sum_int(cz, red);
+    if (z - a > kCandCap) {
+      if (tid == 0) atomicOr(p.flags, 4);
+      a = z = k;
+    }
+  }
+  for (int pos = tid; pos < z; pos += kSelThreads) {
+    const int i = tok(pos);
+    if (pos < a) {
+      atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+    } else {
+      sm.cv[pos - a] = (double)val(pos);
+      sm.ci[pos - a] = i;
+    }
+  }
+  *above_w = a;
+  *nw_out = z - a;
 }
 
 // ----------------------------------------------------------------------------- kernel
@@ -430,347 +494,357 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
   if (tid == 0) red.misc[3] = red.misc[5] = 0;
 
-  // ---- A. brackets [lo, hi] around the k-th rank from 4 x 256 strided samples: their
-  //         quantiles are read off a 1024-bin histogram over [sample min, sample max]
-  //         (no sort); edges are widened outward so the bracket stays conservative
-  constexpr int kS = 4 * kSelThreads;
-  float smp[4];
-  float smin = INFINITY, smax = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    smp[j] = rd.at((int)(((int64_t)(tid + j * kSelThreads) * n) / kS));
-    smin = fminf(smin, smp[j]);
-    smax = fmaxf(smax, smp[j]);
-  }
-  smax = block_max_float(smax, red);
-  smin = -block_max_float(-smin, red);
-  float hi, lo;
-  {
-    const float pr = (float)k / (float)n;
-    const float delta = 3.0f * sqrtf(kS * pr * (1.0f - pr)) + 2.0f;
-    const int hi_i = max(0, (int)floorf(pr * kS - delta));        // ranks from the top
-    const int lo_i = min(kS - 1, (int)ceilf(pr * kS + delta));
-    const float sscale = (smax > smin) ? 1024.f / (smax - smin) : 0.f;
-    auto sbin = [&](float v) { return min(1023, max(0, (int)((v - smin) * sscale))); };
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (isfinite(smp[j])) atomicAdd(sm.hist + sbin(smp[j]), 1u);
-    __syncthreads();
-    // thread t scans bins 1023-4t .. 1020-4t (descending)
-    int hb[4], s4 = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      hb[j] = (int)sm.hist[1023 - (tid * 4 + j)];
-      s4 += hb[j];
-    }
-    int tot;
-    const int ex = block_scan(s4, &tot, red);
-    int acc = ex;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int bin = 1023 - (tid * 4 + j);
-      // samples ranked [acc, acc + hb[j]) from the top live in this bin
-      if (acc <= hi_i && hi_i < acc + hb[j]) red.misc[12] = bin;
-      if (acc <= lo_i && lo_i < acc + hb[j]) red.misc[13] = bin;
-      acc += hb[j];
-    }
-    if (tid == 0) red.misc[3] = red.misc[5] = 0;
-    __syncthreads();
-    const int bh = red.misc[12], bl = red.misc[13];
-    // hi: upper edge of the hi_i-th sample's bin (the top sample's bin: the sample max);
-    // lo: lower edge of the lo_i-th sample's bin
-    hi = (bh >= 1023) ? smax : smin + (float)(bh + 1) / sscale;
-    lo = smin + (float)bl / sscale;
-    for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
-    __syncthreads();
-  }
-  const long long t1 = clock64();
-
-  // ---- B. above-bits -> bitmap, [lo, hi] -> histogram, max|s|, non-finite check.
-  // Thread t owns 32 consecutive tokens of each 8K chunk: 8 float4, one bitmap word.
-  // One retry with a bracket reaching the row's max (or min) if the sample bracket missed.
+  const bool refine = p.q != nullptr;
   const int nch = (n + kChunk - 1) / kChunk;
-  const int nfull = n / kChunk;
-  float mabs = 0.f, vmax = -INFINITY, vmin = INFINITY;
-  int cgt = 0, cin = 0, bad = 0;
-  bool brackets = false;
-  float scale = 0.f;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    brackets = isfinite(lo) && isfinite(hi) && lo < hi;
-    if (!brackets) {
-      lo = -INFINITY;
-      hi = INFINITY;
+  int above_w = 0, nw = 0, mode = 0, cin = 0;
+  float tau_w = 0.f;  // refinement half-width
+  long long t1, t2, t3;
+  if (n <= kSmallN) {
+    small_row_select(p, rd, n, k, refine, sm, red, &above_w, &nw, &tau_w);
+    mode = 3;
+    t1 = t2 = t3 = clock64();
+  } else {
+    // ---- A. brackets [lo, hi] around the k-th rank from 4 x 256 strided samples: their
+    //         quantiles are read off a 1024-bin histogram over [sample min, sample max]
+    //         (no sort); edges are widened outward so the bracket stays conservative
+    constexpr int kS = 4 * kSelThreads;
+    float smp[4];
+    float smin = INFINITY, smax = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      smp[j] = rd.at((int)(((int64_t)(tid + j * kSelThreads) * n) / kS));
+      smin = fminf(smin, smp[j]);
+      smax = fmaxf(smax, smp[j]);
     }
-    scale = brackets ? (float)kBins / (hi - lo) : 0.f;
-    const float blo = lo, bhi = hi, bsc = scale;
-    float nanacc = 0.f;
-    int cg = 0, ci = 0;
-    auto pass_b = [&](int c, bool full) {
-      const int w4 = (c * kChunk + tid * 32) >> 2;
-      float4 vv[8];
+    smax = block_max_float(smax, red);
+    smin = -block_max_float(-smin, red);
+    float hi, lo;
+    {
+      const float pr = (float)k / (float)n;
+      const float delta = 3.0f * sqrtf(kS * pr * (1.0f - pr)) + 2.0f;
+      const int hi_i = max(0, (int)floorf(pr * kS - delta));        // ranks from the top
+      const int lo_i = min(kS - 1, (int)ceilf(pr * kS + delta));
+      const float sscale = (smax > smin) ? 1024.f / (smax - smin) : 0.f;
+      auto sbin = [&](float v) { return min(1023, max(0, (int)((v - smin) * sscale))); };
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
-      uint32_t word = 0u;
+      for (int j = 0; j < 4; ++j)
+        if (isfinite(smp[j])) atomicAdd(sm.hist + sbin(smp[j]), 1u);
+      __syncthreads();
+      // thread t scans bins 1023-4t .. 1020-4t (descending)
+      int hb[4], s4 = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int j = 0; j < 4; ++j) {
+        hb[j] = (int)sm.hist[1023 - (tid * 4 + j)];
+        s4 += hb[j];
+      }
+      int tot;
+      const int ex = block_scan(s4, &tot, red);
+      int acc = ex;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const float v = lane4(vv[u], cc);
-          if (full || 4 * (w4 + u) + cc < n) {
-            nanacc = fmaf(v, 0.f, nanacc);  // NaN iff some score is NaN or inf
-            vmax = fmaxf(vmax, v);
-            vmin = fminf(vmin, v);
-            word |= (v > bhi) ? (1u << (u * 4 + cc)) : 0u;
-            if (brackets && v >= blo && v <= bhi) {
-              atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
-              ++ci;
+      for (int j = 0; j < 4; ++j) {
+        const int bin = 1023 - (tid * 4 + j);
+        // samples ranked [acc, acc + hb[j]) from the top live in this bin
+        if (acc <= hi_i && hi_i < acc + hb[j]) red.misc[12] = bin;
+        if (acc <= lo_i && lo_i < acc + hb[j]) red.misc[13] = bin;
+        acc += hb[j];
+      }
+      if (tid == 0) red.misc[3] = red.misc[5] = 0;
+      __syncthreads();
+      const int bh = red.misc[12], bl = red.misc[13];
+      // hi: upper edge of the hi_i-th sample's bin (the top sample's bin: the sample max);
+      // lo: lower edge of the lo_i-th sample's bin
+      hi = (bh >= 1023) ? smax : smin + (float)(bh + 1) / sscale;
+      lo = smin + (float)bl / sscale;
+      for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+      __syncthreads();
+    }
+    t1 = clock64();
+
+    // ---- B. above-bits -> bitmap, [lo, hi] -> histogram, max|s|, non-finite check.
+    // Thread t owns 32 consecutive tokens of each 8K chunk: 8 float4, one bitmap word.
+    // One retry with a bracket reaching the row's max (or min) if the sample bracket missed.
+    const int nfull = n / kChunk;
+    float mabs = 0.f, vmax = -INFINITY, vmin = INFINITY;
+    int cgt = 0, bad = 0;
+    bool brackets = false;
+    float scale = 0.f;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      brackets = isfinite(lo) && isfinite(hi) && lo < hi;
+      if (!brackets) {
+        lo = -INFINITY;
+        hi = INFINITY;
+      }
+      scale = brackets ? (float)kBins / (hi - lo) : 0.f;
+      const float blo = lo, bhi = hi, bsc = scale;
+      float nanacc = 0.f;
+      int cg = 0, ci = 0;
+      auto pass_b = [&](int c, bool full) {
+        const int w4 = (c * kChunk + tid * 32) >> 2;
+        float4 vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+        uint32_t word = 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const float v = lane4(vv[u], cc);
+            if (full || 4 * (w4 + u) + cc < n) {
+              nanacc = fmaf(v, 0.f, nanacc);  // NaN iff some score is NaN or inf
+              vmax = fmaxf(vmax, v);
+              vmin = fminf(vmin, v);
+              word |= (v > bhi) ? (1u << (u * 4 + cc)) : 0u;
+              if (brackets && v >= blo && v <= bhi) {
+                atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
+                ++ci;
+              }
             }
           }
         }
+        sm.bitmap[c * kSelThreads + tid] = word;
+        cg += __popc(word);
+      };
+      for (int c = 0; c < nfull; ++c) pass_b(c, true);
+      if (nfull < nch) pass_b(nfull, false);
+      vmax = block_max_float(vmax, red);
+      vmin = -block_max_float(-vmin, red);
+      bad = block_sum_int(nanacc != nanacc ? 1 : 0, red);
+      cgt = block_sum_int(cg, red);
+      cin = block_sum_int(ci, red);
+      mabs = fmaxf(fabsf(vmax), fabsf(vmin));
+      if (bad || !brackets || (cgt < k && k <= cgt + cin) || attempt == 1) break;
+      // retry once: the k-th value lies above hi (too many above) or below lo
+      if (cgt >= k) {
+        lo = hi;
+        hi = vmax;
+      } else {
+        hi = lo;
+        lo = vmin;
       }
-      sm.bitmap[c * kSelThreads + tid] = word;
-      cg += __popc(word);
-    };
-    for (int c = 0; c < nfull; ++c) pass_b(c, true);
-    if (nfull < nch) pass_b(nfull, false);
-    vmax = block_max_float(vmax, red);
-    vmin = -block_max_float(-vmin, red);
-    bad = block_sum_int(nanacc != nanacc ? 1 : 0, red);
-    cgt = block_sum_int(cg, red);
-    cin = block_sum_int(ci, red);
-    mabs = fmaxf(fabsf(vmax), fabsf(vmin));
-    if (bad || !brackets || (cgt < k && k <= cgt + cin) || attempt == 1) break;
-    // retry once: the k-th value lies above hi (too many above) or below lo
-    if (cgt >= k) {
-      lo = hi;
-      hi = vmax;
-    } else {
-      hi = lo;
-      lo = vmin;
+      for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+      __syncthreads();
     }
-    for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
-    __syncthreads();
-  }
-  if (bad && tid == 0) atomicOr(p.flags, 2);
-  auto bin_of = [&](float v) { return min(kBins - 1, (int)((v - lo) * scale)); };
-  const long long t2 = clock64();
+    if (bad && tid == 0) atomicOr(p.flags, 2);
+    auto bin_of = [&](float v) { return min(kBins - 1, (int)((v - lo) * scale)); };
+    t2 = clock64();
 
-  const bool refine = p.q != nullptr;
-  const float tau = fmaxf(p.tau_rel * mabs, 1e-30f);
-  float T = 0.f, lo_w = 0.f, hi_w = 0.f;
-  int above_w = 0, nw = 0, mode = 0, why = 0;
-  bool fast = brackets && cgt < k && k <= cgt + cin;
-  if (!fast) why = !brackets ? 16 : (cgt >= k ? 32 : 48);
-  if (fast) {
-    // ---- C. bin b* holding rank r = k - cgt counted from the top
-    const int r = k - cgt;
-    constexpr int PER = kBins / kSelThreads;  // bins per thread, descending order
-    int hb[PER], s = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      hb[j] = (int)sm.hist[kBins - 1 - (tid * PER + j)];
-      s += hb[j];
-    }
-    int tot;
-    const int ex = block_scan(s, &tot, red);
-    if (ex < r && r <= ex + s) {
-      int acc = ex;
+    const float tau = tau_w = fmaxf(p.tau_rel * mabs, 1e-30f);
+    float T = 0.f, lo_w = 0.f, hi_w = 0.f;
+    int why = 0;
+    bool fast = brackets && cgt < k && k <= cgt + cin;
+    if (!fast) why = !brackets ? 16 : (cgt >= k ? 32 : 48);
+    if (fast) {
+      // ---- C. bin b* holding rank r = k - cgt counted from the top
+      const int r = k - cgt;
+      constexpr int PER = kBins / kSelThreads;  // bins per thread, descending order
+      int hb[PER], s = 0;
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
-        if (acc < r && r <= acc + hb[j]) {
-          red.misc[1] = kBins - 1 - (tid * PER + j);
-          red.misc[2] = acc;
-        }
-        acc += hb[j];
+        hb[j] = (int)sm.hist[kBins - 1 - (tid * PER + j)];
+        s += hb[j];
       }
-    }
-    __syncthreads();
-    const int bstar = red.misc[1], cum_above = red.misc[2];
-    // candidate bins [b_lo, b_hi]: b* widened by the refinement tolerance
-    const int wb = refine ? (int)ceilf(tau * scale) + 1 : 0;
-    const int b_lo = max(0, bstar - wb), b_hi = min(kBins - 1, bstar + wb);
-    int above_bins = 0;
+      int tot;
+      const int ex = block_scan(s, &tot, red);
+      if (ex < r && r <= ex + s) {
+        int acc = ex;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) above_bins += (kBins - 1 - (tid * PER + j) > b_hi) ? hb[j] : 0;
-    above_bins = block_sum_int(above_bins, red);
-
-    // ---- D. second pass (L2): higher bins join the bitmap, candidate bins are collected.
-    // bin_of is monotone, so "bin > b_hi" and "bin >= b_lo" are exact value thresholds,
-    // found once by bisection over the ordered float keys.
-    if (tid < 2) {
-      const int target = (tid == 0) ? b_hi + 1 : b_lo;  // smallest v with bin_of(v) >= target
-      uint32_t a = float_key(lo), z = float_key(hi);     // bin_of(lo)=0, bin_of(hi)=kBins-1
-      if (target <= 0) {
-        red.misc[6 + tid] = __float_as_int(lo);
-      } else if (target > kBins - 1 || bin_of(hi) < target) {
-        red.misc[6 + tid] = __float_as_int(INFINITY);
-      } else {
-        while (a < z) {  // invariant: bin_of(key_float(z)) >= target
-          const uint32_t mid = a + (z - a) / 2;
-          if (bin_of(key_float(mid)) >= target) z = mid;
-          else a = mid + 1;
+        for (int j = 0; j < PER; ++j) {
+          if (acc < r && r <= acc + hb[j]) {
+            red.misc[1] = kBins - 1 - (tid * PER + j);
+            red.misc[2] = acc;
+          }
+          acc += hb[j];
         }
-        red.misc[6 + tid] = __float_as_int(key_float(z));
-      }
-    }
-    __syncthreads();
-    const float v_hi = __int_as_float(red.misc[6]);  // v >= v_hi  <=>  bin > b_hi
-    const float v_lo = __int_as_float(red.misc[7]);  // v >= v_lo  <=>  bin >= b_lo
-    auto pass_d = [&](int c, bool full) {
-      const int w4 = (c * kChunk + tid * 32) >> 2;
-      float4 vv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
-      uint32_t word = 0u, cand = 0u;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const float v = lane4(vv[u], cc);
-          const bool ok = full || 4 * (w4 + u) + cc < n;
-          // above hi: already set in pass B; [v_hi, hi]: set now
-          word |= (ok && v >= v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
-          // inside the band only: scores above hi were counted (and set) by pass B
-          cand |= (ok && v >= v_lo && v < v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
-        }
-      }
-      if (word) sm.bitmap[c * kSelThreads + tid] |= word;
-      int pos = warp_append(__popc(cand), &red.misc[3]);
-      while (cand) {
-        const int bit = __ffs(cand) - 1;
-        cand &= cand - 1;
-        if (pos < kCandCap) {
-          float e = vv[0].x;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
-              if (u * 4 + cc == bit) e = lane4(vv[u], cc);
-          sm.cv[pos] = (double)e;
-          sm.ci[pos] = 4 * w4 + bit;
-        }
-        ++pos;
-      }
-    };
-    for (int c = 0; c < nfull; ++c) pass_d(c, true);
-    if (nfull < nch) pass_d(nfull, false);
-    __syncthreads();
-    const int nc = red.misc[3];
-    fast = nc >= 1 && nc <= kCandCap;
-    if (!fast) why = 64;
-    if (fast) {
-      // exact T: rank r2 among the members of bin b*
-      const int r2 = r - cum_above;
-      for (int j = tid; j < nc; j += kSelThreads) {
-        const float vj = (float)sm.cv[j];
-        if (bin_of(vj) != bstar) continue;
-        int gt = 0, ge = 0;
-        for (int i = 0; i < nc; ++i) {
-          const float vi = (float)sm.cv[i];
-          if (bin_of(vi) != bstar) continue;
-          gt += vi > vj;
-          ge += vi >= vj;
-        }
-        if (gt < r2 && r2 <= ge) red.misc[4] = __float_as_int(vj);
       }
       __syncthreads();
-      T = __int_as_float(red.misc[4]);
-      lo_w = refine ? T - tau : T;
-      hi_w = refine ? T + tau : T;
-      const int blw = lo_w >= lo ? bin_of(lo_w) : -1;
-      const int bhw = hi_w <= hi ? bin_of(hi_w) : kBins;
-      fast = blw >= b_lo && bhw <= b_hi;  // the window lies inside the candidate bins
-      if (!fast) why = 80;
-    }
-    if (fast) {
-      // keep the window in place; candidates above it are selected outright
-      int abv = 0;
-      for (int base = 0; base < nc; base += kSelThreads) {
-        const int j = base + tid;
-        double v = 0.0;
-        int ii = 0;
-        bool in = false;
-        if (j < nc) {
-          v = sm.cv[j];
-          ii = sm.ci[j];
-          in = (float)v >= lo_w && (float)v <= hi_w;
-          if ((float)v > hi_w) {
-            atomicOr(sm.bitmap + (ii >> 5), 1u << (ii & 31));
-            ++abv;
+      const int bstar = red.misc[1], cum_above = red.misc[2];
+      // candidate bins [b_lo, b_hi]: b* widened by the refinement tolerance
+      const int wb = refine ? (int)ceilf(tau * scale) + 1 : 0;
+      const int b_lo = max(0, bstar - wb), b_hi = min(kBins - 1, bstar + wb);
+      int above_bins = 0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) above_bins += (kBins - 1 - (tid * PER + j) > b_hi) ? hb[j] : 0;
+      above_bins = block_sum_int(above_bins, red);
+
+      // ---- D. second pass (L2): higher bins join the bitmap, candidate bins are collected.
+      // bin_of is monotone, so "bin > b_hi" and "bin >= b_lo" are exact value thresholds,
+      // found once by bisection over the ordered float keys.
+      if (tid < 2) {
+        const int target = (tid == 0) ? b_hi + 1 : b_lo;  // smallest v with bin_of(v) >= target
+        uint32_t a = float_key(lo), z = float_key(hi);     // bin_of(lo)=0, bin_of(hi)=kBins-1
+        if (target <= 0) {
+          red.misc[6 + tid] = __float_as_int(lo);
+        } else if (target > kBins - 1 || bin_of(hi) < target) {
+          red.misc[6 + tid] = __float_as_int(INFINITY);
+        } else {
+          while (a < z) {  // invariant: bin_of(key_float(z)) >= target
+            const uint32_t mid = a + (z - a) / 2;
+            if (bin_of(key_float(mid)) >= target) z = mid;
+            else a = mid + 1;
+          }
+          red.misc[6 + tid] = __float_as_int(key_float(z));
+        }
+      }
+      __syncthreads();
+      const float v_hi = __int_as_float(red.misc[6]);  // v >= v_hi  <=>  bin > b_hi
+      const float v_lo = __int_as_float(red.misc[7]);  // v >= v_lo  <=>  bin >= b_lo
+      auto pass_d = [&](int c, bool full) {
+        const int w4 = (c * kChunk + tid * 32) >> 2;
+        float4 vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+        uint32_t word = 0u, cand = 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const float v = lane4(vv[u], cc);
+            const bool ok = full || 4 * (w4 + u) + cc < n;
+            // above hi: already set in pass B; [v_hi, hi]: set now
+            word |= (ok && v >= v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
+            // inside the band only: scores above hi were counted (and set) by pass B
+            cand |= (ok && v >= v_lo && v < v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
           }
         }
-        __syncthreads();
-        const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
-        if (in) {
-          sm.cv[pos] = v;
-          sm.ci[pos] = ii;
+        if (word) sm.bitmap[c * kSelThreads + tid] |= word;
+        int pos = warp_append(__popc(cand), &red.misc[3]);
+        while (cand) {
+          const int bit = __ffs(cand) - 1;
+          cand &= cand - 1;
+          if (pos < kCandCap) {
+            float e = vv[0].x;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc)
+                if (u * 4 + cc == bit) e = lane4(vv[u], cc);
+            sm.cv[pos] = (double)e;
+            sm.ci[pos] = 4 * w4 + bit;
+          }
+          ++pos;
         }
-      }
-      above_w = cgt + above_bins + block_sum_int(abv, red);
-      nw = red.misc[5];
-      mode = refine ? 2 : 0;
-    }
-  }
-  if (!fast) {
-    // ---------------------------------------------------------------- generic path
-    mode = 1 + why;
-    int c_gt = 0;
-    radix_select_row(rd, n, k, red, &T, &c_gt);
-    lo_w = refine ? T - tau : T;
-    hi_w = refine ? T + tau : T;
-    for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
-    if (tid == 0) red.misc[5] = 0;
-    __syncthreads();
-    int abv = 0;
-    for (int base = 0; base < n; base += kSelThreads) {
-      const int i = base + tid;
-      const float v = (i < n) ? rd.at(i) : -INFINITY;
-      const bool in = i < n && v >= lo_w && v <= hi_w;
-      if (i < n && v > hi_w) {
-        atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
-        ++abv;
-      }
-      const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
-      if (in && pos < kCandCap) {
-        sm.cv[pos] = (double)v;
-        sm.ci[pos] = i;
-      }
-    }
-    above_w = block_sum_int(abv, red);
-    nw = red.misc[5];
-    if (nw > kCandCap) {
-      // the window cannot be held: resolve the exact fp32 ties at T by index order
-      if (refine && tid == 0) atomicOr(p.flags, 4);
-      if (refine) {
-        for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
-        __syncthreads();
-        for (int base = 0; base < n; base += kSelThreads) {
-          const int i = base + tid;
-          if (i < n && rd.at(i) > T) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+      };
+      for (int c = 0; c < nfull; ++c) pass_d(c, true);
+      if (nfull < nch) pass_d(nfull, false);
+      __syncthreads();
+      const int nc = red.misc[3];
+      fast = nc >= 1 && nc <= kCandCap;
+      if (!fast) why = 64;
+      if (fast) {
+        // exact T: rank r2 among the members of bin b*
+        const int r2 = r - cum_above;
+        for (int j = tid; j < nc; j += kSelThreads) {
+          const float vj = (float)sm.cv[j];
+          if (bin_of(vj) != bstar) continue;
+          int gt = 0, ge = 0;
+          for (int i = 0; i < nc; ++i) {
+            const float vi = (float)sm.cv[i];
+            if (bin_of(vi) != bstar) continue;
+            gt += vi > vj;
+            ge += vi >= vj;
+          }
+          if (gt < r2 && r2 <= ge) red.misc[4] = __float_as_int(vj);
         }
+        __syncthreads();
+        T = __int_as_float(red.misc[4]);
+        lo_w = refine ? T - tau : T;
+        hi_w = refine ? T + tau : T;
+        const int blw = lo_w >= lo ? bin_of(lo_w) : -1;
+        const int bhw = hi_w <= hi ? bin_of(hi_w) : kBins;
+        fast = blw >= b_lo && bhw <= b_hi;  // the window lies inside the candidate bins
+        if (!fast) why = 80;
       }
-      int taken = refine ? c_gt : above_w;
+      if (fast) {
+        // keep the window in place; candidates above it are selected outright
+        int abv = 0;
+        for (int base = 0; base < nc; base += kSelThreads) {
+          const int j = base + tid;
+          double v = 0.0;
+          int ii = 0;
+          bool in = false;
+          if (j < nc) {
+            v = sm.cv[j];
+            ii = sm.ci[j];
+            in = (float)v >= lo_w && (float)v <= hi_w;
+            if ((float)v > hi_w) {
+              atomicOr(sm.bitmap + (ii >> 5), 1u << (ii & 31));
+              ++abv;
+            }
+          }
+          __syncthreads();
+          const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
+          if (in) {
+            sm.cv[pos] = v;
+            sm.ci[pos] = ii;
+          }
+        }
+        above_w = cgt + above_bins + block_sum_int(abv, red);
+        nw = red.misc[5];
+        mode = refine ? 2 : 0;
+      }
+    }
+    if (!fast) {
+      // ---------------------------------------------------------------- generic path
+      mode = 1 + why;
+      int c_gt = 0;
+      radix_select_row(rd, n, k, red, &T, &c_gt);
+      lo_w = refine ? T - tau : T;
+      hi_w = refine ? T + tau : T;
+      for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
+      if (tid == 0) red.misc[5] = 0;
+      __syncthreads();
+      int abv = 0;
       for (int base = 0; base < n; base += kSelThreads) {
         const int i = base + tid;
-        const bool tie = i < n && rd.at(i) == T;
-        int tot;
-        const int pre = block_scan(tie ? 1 : 0, &tot, red);
-        if (tie && taken + pre < k) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
-        taken += tot;
+        const float v = (i < n) ? rd.at(i) : -INFINITY;
+        const bool in = i < n && v >= lo_w && v <= hi_w;
+        if (i < n && v > hi_w) {
+          atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+          ++abv;
+        }
+        const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
+        if (in && pos < kCandCap) {
+          sm.cv[pos] = (double)v;
+          sm.ci[pos] = i;
+        }
       }
-      nw = 0;
-      mode = 5;
+      above_w = block_sum_int(abv, red);
+      nw = red.misc[5];
+      if (nw > kCandCap) {
+        // the window cannot be held: resolve the exact fp32 ties at T by index order
+        if (refine && tid == 0) atomicOr(p.flags, 4);
+        if (refine) {
+          for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
+          __syncthreads();
+          for (int base = 0; base < n; base += kSelThreads) {
+            const int i = base + tid;
+            if (i < n && rd.at(i) > T) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+          }
+        }
+        int taken = refine ? c_gt : above_w;
+        for (int base = 0; base < n; base += kSelThreads) {
+          const int i = base + tid;
+          const bool tie = i < n && rd.at(i) == T;
+          int tot;
+          const int pre = block_scan(tie ? 1 : 0, &tot, red);
+          if (tie && taken + pre < k) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+          taken += tot;
+        }
+        nw = 0;
+        mode = 5;
+      }
     }
+    t3 = clock64();
   }
-  const long long t3 = clock64();
 
   // ---- window: re-score (refine) and keep the top k - above_w by (score desc, index asc)
   if (nw > 0) {
     __syncthreads();
     if (refine) {
-      if (p.block_size > 1) rescore_f64_blocks(p, slot, b, grp, sm.ci, sm.cv, nw, sm.qs);
+      if (p.block_size > 1)
+        rescore_f64_blocks(p, slot, b, grp, sm.ci, sm.cv, nw, tau_w, sm.keys);
       else rescore_f64(p, slot, b, grp, sm.ci, sm.cv, nw);
       __syncthreads();
     }

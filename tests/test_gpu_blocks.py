@@ -10,7 +10,7 @@ torch = pytest.importorskip("torch")
 
 from oracle import hylra_oracle as orc  # noqa: E402
 from paper_2602_00777_b200 import policy_from_actions  # noqa: E402
-from paper_2602_00777_b200.attention import block_select  # noqa: E402
+from paper_2602_00777_b200.attention import block_select, full_attention, topk_select  # noqa: E402
 from paper_2602_00777_b200.engine import (HybridDecoder, hybrid_decode,  # noqa: E402
                                           hybrid_decode_blocks)
 from refmodel import FixtureModel, load_npz  # noqa: E402
@@ -53,27 +53,56 @@ def test_block_size_one_equals_token_mode(golden_dir):
                 list(tok.selections[t][l].indices)
 
 
-@pytest.mark.parametrize("n,bb,bs,kind", [(4000, 16, 128, "normal"), (4000, 40, 64, "ties"),
-                                          (32768, 16, 128, "normal"), (1000, 3, 300, "normal")])
-def test_block_select_matches_oracle(n, bb, bs, kind):
+@pytest.mark.parametrize("n,bb,bs,kind,sg", [
+    (4000, 16, 128, "normal", 1), (4000, 40, 64, "ties", 1), (32768, 16, 128, "normal", 1),
+    (1000, 3, 300, "normal", 1), (4001, 10, 4, "normal", 1), (5003, 7, 32, "ties", 1),
+    (777, 5, 8, "normal", 2), (3001, 20, 16, "ties", 2), (3000, 20, 2, "ties", 1),
+    (70001, 9, 128, "normal", 2), (65, 2, 64, "normal", 1)])
+def test_block_select_matches_oracle(n, bb, bs, kind, sg):
     rng = np.random.default_rng(n + bb)
-    S, B, H = 2, 2, 2
+    S, B, H = 2, 2, 4
     x = (rng.standard_normal((S, B, H, n)) if kind == "normal"
          else rng.integers(-5, 5, size=(S, B, H, n))).astype(np.float32)
     x[0, 0, 0, -5:] += 9.0  # make the truncated final block win somewhere
     buf = np.zeros((S, B, H, (n + 7) & ~7), dtype=np.float32)
     buf[..., :n] = x
-    blocks, tokens, counts = block_select(torch.from_numpy(buf).cuda(), bb, bs, n)
+    buf[..., n:] = 1e9  # padding past n must never be pooled
+    blocks, tokens, counts = block_select(torch.from_numpy(buf).cuda(), bb, bs, n, sel_group=sg)
     blocks, tokens, counts = blocks.cpu().numpy(), tokens.cpu().numpy(), counts.cpu().numpy()
     for s in range(S):
         for b in range(B):
-            for h in range(H):
-                want = orc.topk_of_logits(orc.block_max_of_logits(x[s, b, h].astype(np.float64), bs),
-                                          bb)
-                assert np.array_equal(blocks[s, b, h], want)
+            for grp in range(H // sg):
+                agg = np.zeros(n, dtype=np.float32)
+                for h in range(grp * sg, (grp + 1) * sg):
+                    agg += x[s, b, h]  # fp32 head-order sum, as the pooling kernel adds
+                want = orc.topk_of_logits(orc.block_max_of_logits(agg.astype(np.float64), bs), bb)
+                assert np.array_equal(blocks[s, b, grp], want)
                 cov = orc.block_coverage(want, bs, n)
-                assert counts[s, b, h] == cov.shape[0]
-                assert np.array_equal(tokens[s, b, h, :cov.shape[0]], cov)
+                assert counts[s, b, grp] == cov.shape[0]
+                assert np.array_equal(tokens[s, b, grp, :cov.shape[0]], cov)
+
+
+@pytest.mark.parametrize("n,k", [(2048, 100), (2049, 100), (300, 17), (64, 63), (1500, 1)])
+def test_small_row_select_ties_and_refinement(n, k):
+    """Rows of <= 2048 scores take the sorted small-row path: exact (score desc, index asc)
+    without refinement; with q/k the float64 re-score decides near-ties."""
+    rng = np.random.default_rng(n * 7 + k)
+    x = rng.integers(-3, 3, size=(1, 2, 2, n)).astype(np.float32)
+    buf = np.zeros((1, 2, 2, (n + 7) & ~7), dtype=np.float32)
+    buf[..., :n] = x
+    idx = topk_select(torch.from_numpy(buf).cuda(), k, n).cpu().numpy()
+    for b in range(2):
+        for h in range(2):
+            assert np.array_equal(idx[0, b, h], orc.topk_of_logits(x[0, b, h].astype(np.float64), k))
+    # refinement on real scores: GPU FULL scores + refined select == float64 oracle sets
+    L, B, Hq, Hkv, d = 1, 2, 8, 2, 64
+    q, kk, v, qn, kn, vn = make_stack(L, B, Hq, Hkv, d, n, "bf16", seed=n + k, planted=min(k, 8))
+    _, sc = full_attention(q, kk, v, n)
+    got = topk_select(sc, k, n, q=q, k=kk).cpu().numpy()
+    sc64 = orc.group_scores(qn[0], kn[0], n, Hq // Hkv, 1)
+    for b in range(B):
+        for h in range(Hkv):
+            assert np.array_equal(got[0, b, h], orc.topk_of_logits(sc64[b, h], k))
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
@@ -91,3 +120,23 @@ def test_block_decode_step_matches_oracle(dtype):
         assert np.array_equal(sel[res.slot_of_layer[l]], ref_blocks[l])
     tol = 2e-2 if dtype == "bf16" else 1e-3
     assert max_head_err(res.outputs.double().cpu().numpy(), ref_out) < tol
+
+
+@pytest.mark.parametrize("n,bs,bb", [(4096, 64, 8), (3000, 16, 5)])
+def test_block_refinement_all_tied(n, bs, bb):
+    """Every key identical: all blocks tie, every token qualifies for the float64 re-score
+    (more than the filtered list holds at n=4096), and ties go to the lowest blocks."""
+    L, B, Hq, Hkv, d = 2, 1, 8, 2, 128
+    q, k, v, qn, kn, vn = make_stack(L, B, Hq, Hkv, d, n, "bf16", seed=5)
+    k[:] = k[:, :, :, :1, :]
+    kn[:] = kn[:, :, :, :1, :]
+    actions = ("full", "reuse")
+    dec = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs)
+    res = dec.step(q, n)
+    torch.cuda.synchronize()
+    dec.check_flags()
+    ref_out, ref_blocks = orc.hybrid_step_blocks(qn, kn, vn, n, actions, bb, bs)
+    sel = res.selections.cpu().numpy()
+    assert np.array_equal(sel[res.slot_of_layer[0]], ref_blocks[0])
+    assert list(ref_blocks[0][0, 0]) == list(range(bb))
+    assert max_head_err(res.outputs.double().cpu().numpy(), ref_out) < 2e-2
