@@ -11,8 +11,12 @@ from .errors import (ConfigurationError, CudaError, InvalidInputError, InvalidSe
                      LayerReuseError, NumericInputError)
 from .policy import (Action, LayerPolicy, dp_optimize, policy_from_actions, static_jump_policy,
                      validate_policy)
-from .profiling import (SimilarityMatrix, merge_similarity_matrices, overlap_counts,
-                        relative_l2_error, similarity_from_counts)
+from .profiling import (LayerSensitivity, SensitivityReport, SimilarityMatrix, kl_extended,
+                        merge_similarity_matrices, overlap_counts, relative_l2_error,
+                        sensitivity_profile, similarity_from_counts)
+from .results import (CostModelReport, DecodeRunResult, DecodeTrace, FidelityReport,
+                      FidelityTable, cost_model, fidelity_report)
+from .sets import BlockSet, TopKSet
 
 __version__ = "0.1.0"
 
@@ -23,19 +27,22 @@ __all__ = [
     "NumericInputError", "InvalidSelectionError", "InvalidInputError", "CudaError",
     "TopKSet", "BlockSet", "full_attention", "topk_select", "block_select", "sparse_attention",
     "HybridDecoder", "PipelinedDecoder", "DecodeLoop", "decode_step", "hybrid_decode",
-    "hybrid_decode_blocks", "run_full_trace", "build_similarity_matrix",
+    "hybrid_decode_blocks", "run_full_trace", "build_similarity_matrix", "kl_extended",
+    "LayerSensitivity", "SensitivityReport", "sensitivity_profile", "CostModelReport",
+    "cost_model", "FidelityReport", "fidelity_report", "FidelityTable", "DecodeRunResult",
+    "DecodeTrace",
 ]
 
 
 def __getattr__(name):
     # torch-dependent entry points load lazily so the host-only parts import without it
-    if name in ("TopKSet", "BlockSet", "full_attention", "topk_select", "block_select",
-                "sparse_attention", "geometry"):
+    if name in ("full_attention", "topk_select", "block_select", "sparse_attention",
+                "geometry"):
         from . import attention
         return getattr(attention, name)
     if name in ("HybridDecoder", "decode_step", "hybrid_decode", "hybrid_decode_blocks",
                 "run_full_trace", "PipelinedDecoder", "DecodeLoop",
-                "build_similarity_matrix", "DecodeRunResult", "DecodeTrace", "StepResult"):
+                "build_similarity_matrix", "StepResult"):
         from . import engine
         return getattr(engine, name)
     raise AttributeError(name)

@@ -24,14 +24,19 @@ import numpy as np
 import torch
 
 from . import _abi
-from .attention import BlockSet, TopKSet, geometry
+from .attention import block_select, full_attention, geometry, topk_select
 from .errors import ConfigurationError, InvalidInputError, InvalidSelectionError, NumericInputError
 from .policy import Action, LayerPolicy, policy_from_actions
-from .profiling import overlap_counts, relative_l2_error, similarity_from_counts
+from .profiling import overlap_counts, similarity_from_counts
+from .results import (CostModelReport, DecodeRunResult, DecodeTrace, FidelityReport,
+                      FidelityTable, cost_model, fidelity_report, fidelity_tables)
+from .sets import BlockSet, TopKSet
 
 __all__ = ["HybridDecoder", "PipelinedDecoder", "DecodeLoop", "StepResult", "decode_step",
            "DecodeRunResult", "FidelityTable", "DecodeTrace", "hybrid_decode",
-           "hybrid_decode_blocks", "run_full_trace", "trace_overlap_counts"]
+           "hybrid_decode_blocks", "run_full_trace", "trace_overlap_counts",
+           "build_similarity_matrix", "CostModelReport", "cost_model", "FidelityReport",
+           "fidelity_report"]
 
 
 def _actions_of(policy) -> tuple:
@@ -334,60 +339,6 @@ def decode_step(policy, k_cache, v_cache, q, budget: int, n_valid: int | None = 
 
 
 # --------------------------------------------------------------------------- drop-ins
-@dataclass(frozen=True)
-class FidelityTable:
-    """Relative L2 error of hybrid outputs against the all-FULL baseline (engine.py:47-57)."""
-
-    per_step_layer: np.ndarray
-    per_layer: np.ndarray
-    aggregate: float
-
-
-@dataclass(frozen=True)
-class DecodeRunResult:
-    """Outputs, selections, fidelity and counters of one hybrid run (engine.py:60-92)."""
-
-    policy: LayerPolicy
-    budget: int
-    block_size: int
-    outputs: np.ndarray
-    selections: tuple
-    fidelity: FidelityTable
-    full_score_computations: tuple
-    reuse_full_scans: int
-    reuse_gathered_rows: tuple
-
-    @property
-    def full_layer_count(self) -> int:
-        return self.policy.full_count
-
-    @property
-    def reuse_layer_count(self) -> int:
-        return self.policy.num_layers - self.policy.full_count
-
-    @property
-    def steps(self) -> int:
-        return self.outputs.shape[0]
-
-
-@dataclass(frozen=True)
-class DecodeTrace:
-    """All-FULL decode record (synthetic.py:214-234): queries/outputs [T, L, H, d] and
-    topk[t][l] TopKSet per layer (layer-wide selection, summed over all heads)."""
-
-    config: object
-    budget: int
-    block_size: int
-    queries: np.ndarray
-    outputs: np.ndarray
-    topk: tuple
-    idx_device: torch.Tensor | None = None   # int32 [T, L, 1, budget] on the GPU
-
-    @property
-    def steps(self) -> int:
-        return self.queries.shape[0]
-
-
 def _model_tensors(model, steps: int, device):
     """Reference model arrays -> fp32 device tensors in the ABI layout.
 
@@ -473,18 +424,11 @@ def hybrid_decode(model, policy, budget: int, steps: int, *, include_sinks: int 
         selections.append(tuple(step_sel))
         gathered.append(tuple(step_g))
         full_counts.append(pol.full_count)
-    table = np.empty((steps, L))
-    for t in range(steps):
-        for l in range(L):
-            table[t, l] = relative_l2_error(outputs[t, l].ravel(), baseline.outputs[t, l].ravel())
-    table.setflags(write=False)
-    per_layer = table.mean(axis=0)
-    per_layer.setflags(write=False)
     outputs.setflags(write=False)
     return DecodeRunResult(
         policy=pol, budget=budget, block_size=1, outputs=outputs,
         selections=tuple(selections),
-        fidelity=FidelityTable(table, per_layer, float(table.mean())),
+        fidelity=fidelity_tables(baseline.outputs, outputs),
         full_score_computations=tuple(full_counts), reuse_full_scans=0,
         reuse_gathered_rows=tuple(gathered))
 
@@ -529,53 +473,53 @@ def hybrid_decode_blocks(model, policy, block_budget: int, block_size: int, step
         selections.append(tuple(step_sel))
         gathered.append(tuple(step_g))
         full_counts.append(pol.full_count)
-    table = np.empty((steps, L))
-    for t in range(steps):
-        for l in range(L):
-            table[t, l] = relative_l2_error(outputs[t, l].ravel(), baseline.outputs[t, l].ravel())
-    table.setflags(write=False)
-    per_layer = table.mean(axis=0)
-    per_layer.setflags(write=False)
     outputs.setflags(write=False)
     return DecodeRunResult(
         policy=pol, budget=block_budget, block_size=block_size, outputs=outputs,
         selections=tuple(selections),
-        fidelity=FidelityTable(table, per_layer, float(table.mean())),
+        fidelity=fidelity_tables(baseline.outputs, outputs),
         full_score_computations=tuple(full_counts), reuse_full_scans=0,
         reuse_gathered_rows=tuple(gathered))
 
 
 def run_full_trace(model, steps: int, budget: int, block_size: int = 1, *, device="cuda",
                    refine: bool = True) -> DecodeTrace:
-    """Drop-in for the reference `run_full_trace` (synthetic.py:237-301): every layer FULL,
-    one layer-wide TopKSet per (step, layer); the int32 sets stay on the device for the
-    OVERLAP kernel (idx_device [T, L, 1, budget])."""
+    """Drop-in for the reference `run_full_trace` (synthetic.py:237-301): every layer FULL;
+    per (step, layer) one layer-wide TopKSet of `budget` tokens and one BlockSet of the top
+    min(ceil(budget / block_size), n_blocks) blocks, both from the same FULL-kernel scores
+    (summed over all heads). The int32 token sets stay on the device for the OVERLAP kernel
+    (idx_device [T, L, 1, budget])."""
     cfg = model.config
     if steps < 1:
         raise InvalidInputError(f"steps must be >= 1, got {steps}")
     if budget < 1 or budget > cfg.context_len:
         raise InvalidInputError(
             f"budget must lie in [1, context_len={cfg.context_len}], got {budget}")
-    if block_size != 1:
-        raise ConfigurationError("block-level selection is not implemented on the GPU path")
-    actions = (Action.FULL,) * cfg.layers
+    if block_size < 1:
+        raise InvalidInputError(f"block_size must be >= 1, got {block_size}")
     q, k, v = _model_tensors(model, steps, device)
-    H = cfg.heads
-    dec = HybridDecoder(actions, k, v, budget, q_heads=H, sel_group=H, refine=refine)
-    outs, topk = [], []
-    idx_dev = torch.empty((steps, cfg.layers, 1, budget), dtype=torch.int32, device=device)
+    H, L = cfg.heads, cfg.layers
+    block_budget = -(-budget // block_size)
+    outs, topk, blocks = [], [], []
+    idx_dev = torch.empty((steps, L, 1, budget), dtype=torch.int32, device=device)
+    rq, rk = (q, k) if refine else (None, None)
     for t in range(steps):
-        res = dec.step(q[t], cfg.context_len + t)
-        dec.check_flags()
-        idx_dev[t].copy_(res.selections[:, 0, :, :budget])
-        outs.append(res.outputs[:, 0].double().cpu().numpy())
-        sel = res.selections[:, 0, 0].cpu().numpy()
-        topk.append(tuple(TopKSet(tuple(int(i) for i in sel[l]), budget)
-                          for l in range(cfg.layers)))
+        n_t = cfg.context_len + t
+        out, sc = full_attention(q[t], k, v, n_t)
+        idx = topk_select(sc, budget, n_t, sel_group=H, q=rq[t] if refine else None, k=rk)
+        blk, _, _ = block_select(sc, block_budget, block_size, n_t, sel_group=H,
+                                 q=rq[t] if refine else None, k=rk)
+        idx_dev[t].copy_(idx[:, 0])
+        outs.append(out[:, 0].double().cpu().numpy())
+        sel, bsel = idx[:, 0, 0].cpu().numpy(), blk[:, 0, 0].cpu().numpy()
+        topk.append(tuple(TopKSet(tuple(int(i) for i in sel[l]), budget) for l in range(L)))
+        blocks.append(tuple(BlockSet(tuple(int(i) for i in bsel[l]), block_size)
+                            for l in range(L)))
     outputs = np.stack(outs)
     outputs.setflags(write=False)
     queries = np.asarray(model.queries(steps))
-    return DecodeTrace(cfg, budget, block_size, queries, outputs, tuple(topk), idx_dev)
+    return DecodeTrace(cfg, budget, block_size, queries, outputs, tuple(topk), tuple(blocks),
+                       idx_dev)
 
 
 def trace_overlap_counts(trace: DecodeTrace) -> np.ndarray:

@@ -20,6 +20,12 @@ Fixtures
                        and the summed logits.
   topk_cases.json      topk_of_logits on random, tied and saturated logit vectors.
   dp_cases.json        dp_optimize on random similarity matrices x theta grid.
+  artifacts/           versioned JSON artifacts WRITTEN BY THE REFERENCE (formats.py) for an
+                       H=2 model (L6 d32 N96 seed21 rho0.85): decode-trace (+ sidecars,
+                       block_size 4), similarity-matrix, layer-policy, decode-run (token and
+                       block mode), cost-report, sensitivity-report.
+  artifacts_reference.npz  the same model's arrays, the sensitivity probe noise, both hybrid
+                       runs' outputs/selections and the reference fidelity_report values.
 """
 from __future__ import annotations
 
@@ -219,6 +225,52 @@ def dp_cases():
     print("dp matrices:", len(out))
 
 
+def artifacts_fixture():
+    from layerreuse import formats as fm
+    from layerreuse.synthetic import _S_PROBE, _rng
+
+    adir = HERE / "artifacts"
+    adir.mkdir(exist_ok=True)
+    cfg = lr.SynthModelConfig(layers=6, head_dim=32, context_len=96, seed=21,
+                              inter_layer_correlation=0.85, heads=2)
+    model = lr.generate_model(cfg)
+    T, k, bs = 3, 12, 4
+    keys, values = model.grown_arrays(T)
+    queries = model.queries(T)
+    trace = lr.run_full_trace(model, T, k, block_size=bs)
+    fm.write_trace(trace, str(adir / "trace.json"))
+    matrix = lr.build_similarity_matrix(trace)
+    fm.write_similarity_matrix(matrix, str(adir / "matrix.json"))
+    policy = lr.dp_optimize(matrix, 0.6)
+    fm.write_policy(policy, str(adir / "policy.json"))
+    run = lr.hybrid_decode(model, policy, k, T)
+    fm.write_run_result(run, str(adir / "run.json"))
+    runb = lr.hybrid_decode_blocks(model, policy, 3, bs, T)
+    fm.write_run_result(runb, str(adir / "run_blocks.json"))
+    cost = lr.cost_model(policy, 32768, 2048, head_dim=1024, bytes_per_elem=2)
+    fm.write_cost_report(cost, str(adir / "cost.json"), contextLen=32768, budget=2048)
+    costb = lr.cost_model(policy, 1000, 7, block_size=128, head_dim=64)
+    fm.write_cost_report(costb, str(adir / "cost_blocks.json"))
+    sens_step = 1
+    sens = lr.sensitivity_profile(model, sens_step, k)
+    fm.write_sensitivity_report(sens, str(adir / "sensitivity.json"))
+    probe = np.stack([np.stack([_rng(cfg.seed, _S_PROBE, nl, h, sens_step).standard_normal(32)
+                                for h in range(2)]) for nl in range(7)])
+    fid = lr.fidelity_report(trace, run)
+    fidb = lr.fidelity_report(trace, runb)
+    np.savez_compressed(
+        HERE / "artifacts_reference.npz", keys=keys, values=values, queries=queries,
+        probe=probe, sens_step=sens_step, rho=0.85, context_len=96, budget=k, block_size=bs,
+        run_outputs=run.outputs, run_sets=sets_array(run.selections),
+        runb_outputs=runb.outputs,
+        runb_blocks=np.array([[list(s.block_indices) for s in row] for row in runb.selections]),
+        fid_overlap=fid.selection_overlap, fid_per_layer=fid.per_layer_overlap,
+        fid_rnmse=fid.rnmse.per_step_layer, fid_aggregate=fid.rnmse.aggregate,
+        fidb_overlap=fidb.selection_overlap, fidb_rnmse=fidb.rnmse.per_step_layer,
+        sens_rnmse=sens.rnmse, sens_kl=sens.kl)
+    print("artifacts: policy", [a.value for a in policy.actions], "sens", sens.rnmse)
+
+
 if __name__ == "__main__":
     engine_fixture()
     overlap_fixture()
@@ -227,3 +279,4 @@ if __name__ == "__main__":
     cfg1_fixture()
     topk_cases()
     dp_cases()
+    artifacts_fixture()
