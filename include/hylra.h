@@ -21,6 +21,9 @@
  *                           feeding profiling.py:126-145 `build_similarity_matrix`
  *   hylra_block_select,  <- attention.py:287-313 block pooling / topk_blocks and
  *   hylra_decode_step_blocks  engine.py:212-286 `hybrid_decode_blocks` (block mode)
+ *   hylra_decode_step_offload <- index-guided offload (the offload mirror
+ *                           of engine.py:314-368 `cost_model`): REUSE layers' K/V in
+ *                           page-locked host memory, only the selected rows cross the link
  *
  * Conventions
  *   - Every pointer is caller-owned DEVICE memory unless stated otherwise; the
@@ -44,7 +47,7 @@
 extern "C" {
 #endif
 
-#define HYLRA_ABI_VERSION 2
+#define HYLRA_ABI_VERSION 3
 
 enum hylra_status {
   HYLRA_OK = 0,
@@ -176,6 +179,22 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                       int n_valid, const uint8_t* actions, int budget, int sel_group,
                       int refine, int sinks, int recent, float* out, int32_t* idx,
                       int k_stride, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * hylra_decode_step with the cache split by action (index-guided offload). k_full/v_full:
+ * [n_full][B][Hkv][cap][d] DEVICE memory holding the FULL layers in layer order; k_reuse /
+ * v_reuse: [n_reuse][B][Hkv][cap][d] holding the REUSE layers in layer order, in
+ * page-locked host memory (cudaHostAlloc / cudaHostRegister; read in place over the link
+ * through its device mapping) or in device memory. Both use g->kv_stride_* (the layer
+ * stride is per compact buffer); g->num_layers = L still sizes q and out. REUSE kernels
+ * read only the selected rows, so the link carries B*Hkv*2*k_eff*d*e bytes per REUSE
+ * layer. Pageable host memory -> ConfigurationError. Workspace: as hylra_decode_step.
+ */
+int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void* k_full,
+                              const void* v_full, const void* k_reuse, const void* v_reuse,
+                              int n_valid, const uint8_t* actions, int budget, int sel_group,
+                              int refine, int sinks, int recent, float* out, int32_t* idx,
+                              int k_stride, void* ws, size_t ws_bytes, void* stream);
 
 /* Sink / recent augmentation (engine.py:122-126): out[r] = sorted(idx[r][0..k_eff) |
  * [0, sinks) | [n_valid - recent, n_valid)), counts[r] its length. */

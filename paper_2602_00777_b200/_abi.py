@@ -16,6 +16,14 @@ LIB_PATH = Path(__file__).resolve().parent / "libhylra.so"
 HYLRA_BF16 = 0
 HYLRA_F32 = 1
 
+# status codes (include/hylra.h)
+HYLRA_OK = 0
+HYLRA_ERR_CONFIGURATION = 1
+HYLRA_ERR_INVALID_INPUT = 2
+HYLRA_ERR_INVALID_SELECTION = 3
+HYLRA_ERR_NUMERIC_INPUT = 4
+HYLRA_ERR_CUDA = 5
+
 FLAG_INDEX_OUT_OF_RANGE = 1
 FLAG_NON_FINITE_SCORE = 2
 FLAG_REFINE_SKIPPED = 4
@@ -34,6 +42,7 @@ EXPORTED_SYMBOLS = (
     "hylra_reuse_decode",
     "hylra_decode_step_workspace_bytes",
     "hylra_decode_step",
+    "hylra_decode_step_offload",
     "hylra_overlap_counts",
     "hylra_augment_selection",
     "hylra_block_select",
@@ -111,6 +120,9 @@ def lib() -> ctypes.CDLL:
         l.hylra_decode_step.restype = i32
         l.hylra_decode_step.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, i32, vp,
                                         vp, i32, vp, sz, vp]
+        l.hylra_decode_step_offload.restype = i32
+        l.hylra_decode_step_offload.argtypes = [gp, vp, vp, vp, vp, vp, i32, vp, i32, i32, i32,
+                                                i32, i32, vp, vp, i32, vp, sz, vp]
         l.hylra_augment_selection.restype = i32
         l.hylra_augment_selection.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp]
         l.hylra_overlap_counts.restype = i32

@@ -48,7 +48,8 @@ struct AttnParams {
   float scale_log2;     // log2(e) / sqrt(d)
   int prefetch;         // REUSE: L2 prefetch distance in tiles
   float inv_sqrt_d;
-  int layers[kMaxSlots];
+  int layers[kMaxSlots];     // q / out layer of each slot
+  int kv_layers[kMaxSlots];  // K / V layer of each slot (differs for split caches)
   int src_slot[kMaxSlots];
 };
 
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(160, 2)
   const int slot = blockIdx.z / p.B;
   const int b = blockIdx.z % p.B;
   const int layer = p.layers[slot];
+  const int kvl = p.kv_layers[slot];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -240,9 +242,9 @@ __global__ void __launch_bounds__(160, 2)
           const int row = (t_begin + i) * kTileRows;
 #pragma unroll
           for (int bx = 0; bx < SM::kBoxes; ++bx) {
-            tma_load_5d(kt + bx * kTileRows * 128, &tmk, full_bar + s, bx * 64, row, kh, b, layer,
+            tma_load_5d(kt + bx * kTileRows * 128, &tmk, full_bar + s, bx * 64, row, kh, b, kvl,
                         pol);
-            tma_load_5d(vt + bx * kTileRows * 128, &tmv, full_bar + s, bx * 64, row, kh, b, layer,
+            tma_load_5d(vt + bx * kTileRows * 128, &tmv, full_bar + s, bx * 64, row, kh, b, kvl,
                         pol);
           }
         }
@@ -250,9 +252,9 @@ __global__ void __launch_bounds__(160, 2)
     } else {
       // gather: every lane copies 2 rows (K and V) per stage with 16-byte cp.async
       const __nv_bfloat16* kbase = reinterpret_cast<const __nv_bfloat16*>(p.k) +
-                                   layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+                                   kvl * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
       const __nv_bfloat16* vbase = reinterpret_cast<const __nv_bfloat16*>(p.v) +
-                                   layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+                                   kvl * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
       const int32_t* ib = p.idx + ((int64_t)(p.src_slot[slot] * p.B + b) * p.n_groups +
                                    kh / p.sel_group) * p.k_stride;
       // Lane roles: a row of D bf16 is D/8 16-byte chunks; CH = D/8 consecutive lanes copy
@@ -558,6 +560,7 @@ __global__ void __launch_bounds__(128)
   const int slot = blockIdx.z / p.B;
   const int b = blockIdx.z % p.B;
   const int layer = p.layers[slot];
+  const int kvl = p.kv_layers[slot];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int G = p.G;
@@ -572,8 +575,8 @@ __global__ void __launch_bounds__(128)
 
   const T* qb = reinterpret_cast<const T*>(p.q) + layer * p.q_sl + b * p.q_sb +
                 (int64_t)(kh * G) * D;
-  const T* kb = reinterpret_cast<const T*>(p.k) + layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
-  const T* vb = reinterpret_cast<const T*>(p.v) + layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+  const T* kb = reinterpret_cast<const T*>(p.k) + kvl * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
+  const T* vb = reinterpret_cast<const T*>(p.v) + kvl * p.kv_sl + b * p.kv_sb + kh * p.kv_sh;
   const int32_t* ib = nullptr;
   if (GATHER)
     ib = p.idx + ((int64_t)(p.src_slot[slot] * p.B + b) * p.n_groups + kh / p.sel_group) *

@@ -120,19 +120,19 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-int encode_kv_map(CUtensorMap* map, const hylra_geometry* g, const void* base) {
+int encode_kv_map(CUtensorMap* map, const hylra_geometry* g, const void* base, int kv_layers) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return fail(HYLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int D = g->head_dim;
   const cuuint64_t es = 2;  // bf16
   cuuint64_t dims[5] = {(cuuint64_t)D, (cuuint64_t)g->capacity, (cuuint64_t)g->kv_heads,
-                        (cuuint64_t)g->batch, (cuuint64_t)g->num_layers};
+                        (cuuint64_t)g->batch, (cuuint64_t)kv_layers};
   // strides of dims 1..4 in bytes; size-1 dims get a harmless dense stride
   cuuint64_t st[4];
   st[0] = (cuuint64_t)D * es;
   st[1] = g->kv_heads > 1 ? (cuuint64_t)g->kv_stride_head * es : st[0] * g->capacity;
   st[2] = g->batch > 1 ? (cuuint64_t)g->kv_stride_batch * es : st[1] * g->kv_heads;
-  st[3] = g->num_layers > 1 ? (cuuint64_t)g->kv_stride_layer * es : st[2] * g->batch;
+  st[3] = kv_layers > 1 ? (cuuint64_t)g->kv_stride_layer * es : st[2] * g->batch;
   for (int i = 0; i < 4; ++i)
     if (st[i] % 16 != 0 || st[i] >= (1ull << 40))
       return fail(HYLRA_ERR_CONFIGURATION, "KV stride %d (%llu B) not TMA-compatible", i,
@@ -199,7 +199,8 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
                      const void* v, int n_valid, int n_rows, int n_layers,
                      const int32_t* layer_ids, const int32_t* src_slots, const int32_t* idx,
                      const int32_t* counts, int k_stride, int sel_group, float* out,
-                     float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st) {
+                     float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st,
+                     const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0) {
   if (int e = check_geometry(g)) return e;
   if (n_layers < 1 || n_layers > kMaxSlots)
     return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", n_layers, kMaxSlots);
@@ -232,10 +233,14 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   p.inv_sqrt_d = (float)(1.0 / std::sqrt((double)g->head_dim));
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)g->head_dim));
   p.prefetch = kReusePrefetchTiles;
+  const int n_kv = kv_layer_ids ? kv_layer_count : g->num_layers;
   for (int i = 0; i < n_layers; ++i) {
     if (layer_ids[i] < 0 || layer_ids[i] >= g->num_layers)
       return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", layer_ids[i]);
     p.layers[i] = layer_ids[i];
+    p.kv_layers[i] = kv_layer_ids ? kv_layer_ids[i] : layer_ids[i];
+    if (p.kv_layers[i] < 0 || p.kv_layers[i] >= n_kv)
+      return fail(HYLRA_ERR_CONFIGURATION, "KV layer %d out of range", p.kv_layers[i]);
     p.src_slot[i] = src_slots ? src_slots[i] : 0;
   }
   dim3 grid(lay.splits, g->kv_heads, g->batch * n_layers);
@@ -243,8 +248,8 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   if (use_mma_path(g)) {
     CUtensorMap tk{}, tv{};
     if (!gather) {
-      if (int e = encode_kv_map(&tk, g, k)) return e;
-      if (int e = encode_kv_map(&tv, g, v)) return e;
+      if (int e = encode_kv_map(&tk, g, k, n_kv)) return e;
+      if (int e = encode_kv_map(&tv, g, v, n_kv)) return e;
     }
     const bool big = G > 8;
     if (g->head_dim == 128) {
@@ -279,7 +284,8 @@ struct BlockRows {  // block mode: rows are pooled block scores
 int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
                   int budget, int sel_group, const void* q, const void* k,
                   const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
-                  int* flags, cudaStream_t st, const BlockRows& br = BlockRows()) {
+                  int* flags, cudaStream_t st, const BlockRows& br = BlockRows(),
+                  const int32_t* kv_layer_ids = nullptr) {
   if (int e = check_geometry(g)) return e;
   if (budget < 1) return fail(HYLRA_ERR_INVALID_INPUT, "budget must be >= 1, got %d", budget);
   if (n_slots < 1 || n_slots > kMaxSlots)
@@ -319,6 +325,7 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
     if (l < 0 || l >= g->num_layers)
       return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", l);
     p.layers[i] = l;
+    p.kv_layers[i] = kv_layer_ids ? kv_layer_ids[i] : l;
   }
   const size_t smem = select_smem_bytes(n_valid);
   static std::once_flag once;
@@ -471,6 +478,85 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   return HYLRA_OK;
 }
 
+// Device address of caller memory that kernels may read: device memory as is, page-locked
+// host memory through its mapping (UVA). Pageable host memory is rejected.
+int device_view(const void* ptr, const void** dev, const char* what) {
+  if (!ptr) return fail(HYLRA_ERR_CONFIGURATION, "%s is NULL", what);
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HYLRA_ERR_CONFIGURATION, "%s: not a CUDA-visible pointer", what);
+  }
+  if (a.type == cudaMemoryTypeUnregistered)
+    return fail(HYLRA_ERR_CONFIGURATION,
+                "%s must be device memory or page-locked (pinned) host memory", what);
+  *dev = a.devicePointer ? a.devicePointer : ptr;
+  return HYLRA_OK;
+}
+
+// One decode step: FULL layers (+ scores) -> SELECT -> [augment] -> REUSE layers. With
+// `split`, FULL layers read a compact device cache and REUSE layers a compact cache that
+// may live in page-locked host memory (index-guided offload: only selected rows cross the
+// link); otherwise both read the one [L][B][Hkv][cap][d] cache.
+struct SplitKv {
+  const void *kf, *vf, *kr, *vr;
+};
+
+int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                     int n_valid, const uint8_t* actions, int budget, int sel_group, int refine,
+                     int sinks, int recent, float* out, int32_t* idx, int k_stride, void* ws,
+                     size_t ws_bytes, void* stream, const SplitKv* split) {
+  StepLayout s;
+  if (int e = step_layout(g, actions, n_valid, budget, sel_group, &s, 1, sinks, recent)) return e;
+  if (!ws || ws_bytes < s.total)
+    return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, s.total);
+  if (k_stride < s.k_eff)
+    return fail(HYLRA_ERR_CONFIGURATION, "k_stride %d < selection size %d", k_stride, s.k_eff);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int* flags = reinterpret_cast<int*>(w);
+  float* scores = reinterpret_cast<float*>(w + s.off_scores);
+  void* aws = w + s.off_attn;
+  const int nf = (int)s.full_ids.size();
+  const int nr = (int)s.reuse_ids.size();
+  std::vector<int32_t> fkv(nf), rkv(nr);  // compact KV layer index of each slot
+  for (int i = 0; i < nf; ++i) fkv[i] = i;
+  for (int i = 0; i < nr; ++i) rkv[i] = i;
+  const void* kf = split ? split->kf : k;
+  const void* vf = split ? split->vf : v;
+  if (int e = launch_attention(g, false, q, kf, vf, n_valid, n_valid, nf, s.full_ids.data(),
+                               nullptr, nullptr, nullptr, 0, 1, out, scores, aws, s.attn_bytes,
+                               flags, st, split ? fkv.data() : nullptr, nf))
+    return e;
+  if (int e = launch_select(g, scores, nf, n_valid, budget, sel_group, refine ? q : nullptr,
+                            refine ? kf : nullptr, s.full_ids.data(), idx, k_stride, nullptr,
+                            flags, st, BlockRows(), split ? fkv.data() : nullptr))
+    return e;
+  if (!s.reuse_ids.empty()) {
+    const int32_t* ridx = idx;
+    const int32_t* rcnt = nullptr;
+    int rstride = k_stride, rk = s.k_eff;
+    if (s.aug_stride) {
+      int32_t* aug = reinterpret_cast<int32_t*>(w + s.off_aug);
+      int32_t* acnt = reinterpret_cast<int32_t*>(w + s.off_aug_counts);
+      const int rows = nf * g->batch * s.n_groups;
+      augment_kernel<<<rows, kPoolThreads, 0, st>>>(idx, k_stride, s.k_eff, n_valid, sinks,
+                                                    recent, aug, s.aug_stride, acnt);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      if (int e = cuda_check(cudaGetLastError(), "augment launch")) return e;
+      ridx = aug;
+      rcnt = acnt;
+      rstride = rk = s.aug_stride;
+    }
+    if (int e = launch_attention(g, true, q, split ? split->kr : k, split ? split->vr : v,
+                                 n_valid, rk, nr, s.reuse_ids.data(), s.reuse_src.data(), ridx,
+                                 rcnt, rstride, sel_group, out, nullptr, w + s.off_attn_r,
+                                 s.attn_bytes_r, flags, st, split ? rkv.data() : nullptr, nr))
+      return e;
+  }
+  return HYLRA_OK;
+}
+
 }  // namespace
 
 // ======================================================================== extern "C"
@@ -549,48 +635,28 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                       int n_valid, const uint8_t* actions, int budget, int sel_group,
                       int refine, int sinks, int recent, float* out, int32_t* idx,
                       int k_stride, void* ws, size_t ws_bytes, void* stream) {
-  StepLayout s;
-  if (int e = step_layout(g, actions, n_valid, budget, sel_group, &s, 1, sinks, recent)) return e;
-  if (!ws || ws_bytes < s.total)
-    return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, s.total);
-  if (k_stride < s.k_eff)
-    return fail(HYLRA_ERR_CONFIGURATION, "k_stride %d < selection size %d", k_stride, s.k_eff);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  int* flags = reinterpret_cast<int*>(w);
-  float* scores = reinterpret_cast<float*>(w + s.off_scores);
-  void* aws = w + s.off_attn;
-  const int nf = (int)s.full_ids.size();
-  if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, nf, s.full_ids.data(), nullptr,
-                               nullptr, nullptr, 0, 1, out, scores, aws, s.attn_bytes, flags, st))
-    return e;
-  if (int e = launch_select(g, scores, nf, n_valid, budget, sel_group, refine ? q : nullptr,
-                            refine ? k : nullptr, s.full_ids.data(), idx, k_stride, nullptr,
-                            flags, st))
-    return e;
-  if (!s.reuse_ids.empty()) {
-    const int32_t* ridx = idx;
-    const int32_t* rcnt = nullptr;
-    int rstride = k_stride, rk = s.k_eff;
-    if (s.aug_stride) {
-      int32_t* aug = reinterpret_cast<int32_t*>(w + s.off_aug);
-      int32_t* acnt = reinterpret_cast<int32_t*>(w + s.off_aug_counts);
-      const int rows = nf * g->batch * s.n_groups;
-      augment_kernel<<<rows, kPoolThreads, 0, st>>>(idx, k_stride, s.k_eff, n_valid, sinks,
-                                                    recent, aug, s.aug_stride, acnt);
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      if (int e = cuda_check(cudaGetLastError(), "augment launch")) return e;
-      ridx = aug;
-      rcnt = acnt;
-      rstride = rk = s.aug_stride;
-    }
-    if (int e = launch_attention(g, true, q, k, v, n_valid, rk, (int)s.reuse_ids.size(),
-                                 s.reuse_ids.data(), s.reuse_src.data(), ridx, rcnt, rstride,
-                                 sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags,
-                                 st))
-      return e;
+  return decode_step_impl(g, q, k, v, n_valid, actions, budget, sel_group, refine, sinks, recent,
+                          out, idx, k_stride, ws, ws_bytes, stream, nullptr);
+}
+
+int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void* k_full,
+                              const void* v_full, const void* k_reuse, const void* v_reuse,
+                              int n_valid, const uint8_t* actions, int budget, int sel_group,
+                              int refine, int sinks, int recent, float* out, int32_t* idx,
+                              int k_stride, void* ws, size_t ws_bytes, void* stream) {
+  if (int e = check_geometry(g)) return e;
+  if (!actions) return fail(HYLRA_ERR_CONFIGURATION, "actions is NULL");
+  bool any_reuse = false;
+  for (int l = 0; l < g->num_layers; ++l) any_reuse |= actions[l] == 0;
+  SplitKv sp{};
+  if (int e = device_view(k_full, &sp.kf, "k_full")) return e;
+  if (int e = device_view(v_full, &sp.vf, "v_full")) return e;
+  if (any_reuse) {
+    if (int e = device_view(k_reuse, &sp.kr, "k_reuse")) return e;
+    if (int e = device_view(v_reuse, &sp.vr, "v_reuse")) return e;
   }
-  return HYLRA_OK;
+  return decode_step_impl(g, q, nullptr, nullptr, n_valid, actions, budget, sel_group, refine,
+                          sinks, recent, out, idx, k_stride, ws, ws_bytes, stream, &sp);
 }
 
 int hylra_augment_selection(const int32_t* idx, int rows, int k_eff, int k_stride, int n_valid,

@@ -53,7 +53,8 @@ struct SelectParams {
   int n_tokens;
   const float* tok_scores;  // block mode: token scores [slot][b][kh][tok_row_stride] or null
   int tok_row_stride;
-  int layers[kMaxSlots];
+  int layers[kMaxSlots];     // q layer of each slot
+  int kv_layers[kMaxSlots];  // K layer of each slot (refinement)
 };
 
 // Dynamic shared memory: the bitmap sized for the row, then fixed arrays.
@@ -215,13 +216,14 @@ __device__ __forceinline__ double elem_f64(const void* p, int64_t i) {
 // token (lane sub handles dims sub, sub + kLpt, ...), so a warp scores kTpw tokens at once;
 // every lane of the warp must call it (sub-group shuffles).
 constexpr int kLpt = 8, kTpw = 32 / kLpt;
-__device__ double token_score_f64(const SelectParams& p, int layer, int b, int grp, int tok) {
+__device__ double token_score_f64(const SelectParams& p, int layer, int kvl, int b, int grp,
+                                  int tok) {
   const int sub = threadIdx.x & (kLpt - 1);
   const double sqd = sqrt((double)p.D);
   double agg = 0.0;
   for (int hh = 0; hh < p.sel_group; ++hh) {
     const int kh = grp * p.sel_group + hh;
-    const int64_t koff = layer * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
+    const int64_t koff = kvl * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
     for (int g = 0; g < p.G; ++g) {
       const int64_t qoff = layer * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D;
       double part0 = 0.0, part1 = 0.0;
@@ -255,7 +257,8 @@ __device__ void rescore_f64(const SelectParams& p, int slot, int b, int grp, con
   const int slot_in_warp = (threadIdx.x & 31) / kLpt;
   for (int c0 = warp * kTpw; c0 < n; c0 += kSelWarps * kTpw) {  // warp-uniform trip count
     const int c = c0 + slot_in_warp;
-    const double agg = token_score_f64(p, p.layers[slot], b, grp, toks[min(c, n - 1)]);
+    const double agg = token_score_f64(p, p.layers[slot], p.kv_layers[slot], b, grp,
+                                       toks[min(c, n - 1)]);
     if (sub == 0 && c < n) vals[c] = agg;
   }
 }
@@ -317,7 +320,8 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
       tok = blocks[c] * bs + (e - c * bs);
     }
     const bool ok = e0 + slot_in_warp < items && tok < p.n_tokens;
-    const double agg = token_score_f64(p, p.layers[slot], b, grp, ok ? tok : blocks[c] * bs);
+    const double agg = token_score_f64(p, p.layers[slot], p.kv_layers[slot], b, grp,
+                                       ok ? tok : blocks[c] * bs);
     if (ok && sub == 0) atomicMax(vk + c, f64_key(agg));
   }
   __syncthreads();

@@ -32,7 +32,7 @@ from .results import (CostModelReport, DecodeRunResult, DecodeTrace, FidelityRep
                       FidelityTable, cost_model, fidelity_report, fidelity_tables)
 from .sets import BlockSet, TopKSet
 
-__all__ = ["HybridDecoder", "PipelinedDecoder", "DecodeLoop", "StepResult", "decode_step",
+__all__ = ["HybridDecoder", "OffloadDecoder", "PipelinedDecoder", "DecodeLoop", "StepResult", "decode_step",
            "DecodeRunResult", "FidelityTable", "DecodeTrace", "hybrid_decode",
            "hybrid_decode_blocks", "run_full_trace", "trace_overlap_counts",
            "build_similarity_matrix", "CostModelReport", "cost_model", "FidelityReport",
@@ -172,6 +172,81 @@ class HybridDecoder:
 
     def clear_flags(self) -> None:
         self.ws[:4].zero_()
+
+
+class OffloadDecoder(HybridDecoder):
+    """Index-guided offload (the offload mirror of engine.py:314-368): the
+    FULL layers' K/V stay in HBM, the REUSE layers' K/V live in page-locked host memory and
+    each step the REUSE kernel reads only the selected rows of them across the link
+    (hylra_decode_step_offload; same three kernels as HybridDecoder).
+
+    k_full / v_full: [n_full, B, Hkv, cap, d] CUDA tensors (FULL layers in layer order);
+    k_reuse / v_reuse: [n_reuse, B, Hkv, cap, d] pinned CPU tensors (REUSE layers in layer
+    order) — or CUDA tensors. Use `split_cache` to build them from one [L, ...] cache.
+    Token selection only (optionally with sinks / recent)."""
+
+    def __init__(self, policy, k_full, v_full, k_reuse, v_reuse, budget: int, *, q_heads: int,
+                 sel_group: int = 1, refine: bool = True, include_sinks: int = 0,
+                 include_recent: int = 0):
+        actions = _actions_of(policy)
+        n_full = sum(a is Action.FULL for a in actions)
+        n_reuse = len(actions) - n_full
+        if k_full.shape[0] != n_full or (n_reuse and k_reuse.shape[0] != n_reuse):
+            raise ConfigurationError(
+                f"policy has {n_full} FULL / {n_reuse} REUSE layers, caches hold "
+                f"{k_full.shape[0]} / {0 if k_reuse is None else k_reuse.shape[0]}")
+        if n_reuse:
+            for t in (k_reuse, v_reuse):
+                if t.shape[1:] != k_full.shape[1:] or t.stride()[1:] != k_full.stride()[1:] \
+                        or t.dtype != k_full.dtype:
+                    raise ConfigurationError("offloaded and resident caches must share a layout")
+                if not t.is_cuda and not t.is_pinned():
+                    raise ConfigurationError("an offloaded cache must be in pinned host memory")
+        # the base class sees an L-layer cache view only for shapes; kernels get the split
+        full_view = k_full[:1].expand((len(actions),) + tuple(k_full.shape[1:]))
+        super().__init__(actions, full_view, full_view, budget, q_heads=q_heads,
+                         sel_group=sel_group, refine=refine, include_sinks=include_sinks,
+                         include_recent=include_recent)
+        self.k_full, self.v_full, self.k_reuse, self.v_reuse = k_full, v_full, k_reuse, v_reuse
+        self.reuse_layers = tuple(l for l, a in enumerate(actions) if a is Action.REUSE)
+
+    @staticmethod
+    def split_cache(policy, k_cache, v_cache, device="cuda"):
+        """[L, B, Hkv, cap, d] cache -> (k_full, v_full) on `device`, (k_reuse, v_reuse)
+        pinned on the host."""
+        actions = _actions_of(policy)
+        fl = [l for l, a in enumerate(actions) if a is Action.FULL]
+        rl = [l for l, a in enumerate(actions) if a is Action.REUSE]
+        kf = k_cache[fl].to(device).contiguous()
+        vf = v_cache[fl].to(device).contiguous()
+        kr = k_cache[rl].cpu().contiguous().pin_memory() if rl else None
+        vr = v_cache[rl].cpu().contiguous().pin_memory() if rl else None
+        return kf, vf, kr, vr
+
+    def _geometry(self, q):
+        g = geometry(q, self.k, self.v, self.out)
+        g.kv_stride_layer = self.k_full.stride(0) if self.k_full.shape[0] > 1 else \
+            self.k_full.stride(1) * self.k_full.shape[1]
+        return g
+
+    def step(self, q: torch.Tensor, n_valid: int | None = None) -> StepResult:
+        g = self._geometry(q)
+        n_valid = g.capacity if n_valid is None else int(n_valid)
+        lib = _abi.lib()
+        st = torch.cuda.current_stream(self.k_full.device).cuda_stream
+        need = int(lib.hylra_decode_step_workspace_bytes(
+            g, self._acts, n_valid, self.budget, self.sel_group, self.sinks, self.recent))
+        if self.ws.numel() < need:
+            self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k_full.device)
+        kr = self.k_reuse.data_ptr() if self.k_reuse is not None else None
+        vr = self.v_reuse.data_ptr() if self.v_reuse is not None else None
+        _abi.check(lib.hylra_decode_step_offload(
+            g, q.data_ptr(), self.k_full.data_ptr(), self.v_full.data_ptr(), kr, vr, n_valid,
+            self._acts, self.budget, self.sel_group, int(self.refine), self.sinks, self.recent,
+            self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(),
+            self.ws.numel(), st))
+        k_eff = min(self.budget, n_valid)
+        return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
 
 
 class PipelinedDecoder(HybridDecoder):
