@@ -447,9 +447,12 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                     "h2d_bytes_per_step": int(loop.h2d_bytes),
                     "d2h_bytes_per_step": int(loop.d2h_bytes),
                     "ms_per_step": t_e2e * 1e3,
-                    "path": "DecodeLoop.run(): pinned H2D (q + new K/V rows) -> append -> "
-                            "hybrid step -> D2H fp32 outputs, one graph launch + host sync "
-                            "per step, wall clock"}
+                    "path": "DecodeLoop.run() per step: pinned host q (H2D copies; REUSE "
+                            "layers' on a side stream behind the FULL kernel) + new K/V rows "
+                            "(appended by hylra_append_kv reading pinned host memory in place)"
+                            " -> hybrid step -> fp32 outputs stored by the kernels straight "
+                            "into pinned host memory; one graph launch + host sync per step, "
+                            "wall clock" + ("" if loop.overlap else " (serialised copies)")}
     clk = clocks.stop()
 
     peaks = _peaks()

@@ -21,6 +21,9 @@
  *                           feeding profiling.py:126-145 `build_similarity_matrix`
  *   hylra_block_select,  <- attention.py:287-313 block pooling / topk_blocks and
  *   hylra_decode_step_blocks  engine.py:212-286 `hybrid_decode_blocks` (block mode)
+ *   hylra_decode_step_events  <- hylra_decode_step with per-layer completion events (the
+ *                           caller overlaps H2D of queries / D2H of outputs with the step)
+ *   hylra_append_kv      <- synthetic.py:154-187 (the cache grows one row per step)
  *   hylra_decode_step_offload <- index-guided offload (the offload mirror
  *                           of engine.py:314-368 `cost_model`): REUSE layers' K/V in
  *                           page-locked host memory, only the selected rows cross the link
@@ -47,7 +50,7 @@
 extern "C" {
 #endif
 
-#define HYLRA_ABI_VERSION 3
+#define HYLRA_ABI_VERSION 4
 
 enum hylra_status {
   HYLRA_OK = 0,
@@ -181,6 +184,22 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                       int k_stride, void* ws, size_t ws_bytes, void* stream);
 
 /*
+ * hylra_decode_step that lets the caller overlap host transfers with the step (same
+ * kernels, same results). layer_events (optional, L entries, NULL entries allowed): event
+ * layer_events[l] is recorded on `stream` as soon as out[l] is final — FULL layers right
+ * after the FULL launch, REUSE layers after the REUSE launch that covers them; the REUSE
+ * layers are launched in chunks that end at each REUSE layer carrying an event, so a
+ * caller streams finished layers to the host while later chunks run. reuse_wait_event
+ * (optional): the stream waits on it before the first REUSE launch (e.g. the REUSE
+ * layers' queries still arriving over the link). Workspace: as hylra_decode_step.
+ */
+int hylra_decode_step_events(const hylra_geometry* g, const void* q, const void* k,
+                             const void* v, int n_valid, const uint8_t* actions, int budget,
+                             int sel_group, int refine, int sinks, int recent, float* out,
+                             int32_t* idx, int k_stride, void* ws, size_t ws_bytes, void* stream,
+                             void* reuse_wait_event, void* const* layer_events);
+
+/*
  * hylra_decode_step with the cache split by action (index-guided offload). k_full/v_full:
  * [n_full][B][Hkv][cap][d] DEVICE memory holding the FULL layers in layer order; k_reuse /
  * v_reuse: [n_reuse][B][Hkv][cap][d] holding the REUSE layers in layer order, in
@@ -195,6 +214,18 @@ int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void
                               int n_valid, const uint8_t* actions, int budget, int sel_group,
                               int refine, int sinks, int recent, float* out, int32_t* idx,
                               int k_stride, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Append one decode step's new K/V rows (synthetic.py:154-187 grows the cache one row per
+ * step): k_rows / v_rows are [L][B][Hkv][d] (dtype of g, contiguous) in device memory OR
+ * page-locked host memory (read in place across the link: no separate H2D copy); row `pos`
+ * of every (layer, b, kh) block of k / v receives them. layer_ids (host array of n_layers,
+ * NULL = all g->num_layers layers) limits the append to some layers (rows stay indexed by
+ * layer id), so an append can be split around the kernels that need it first.
+ */
+int hylra_append_kv(const hylra_geometry* g, void* k, void* v, const void* k_rows,
+                    const void* v_rows, int pos, int n_layers, const int32_t* layer_ids,
+                    void* stream);
 
 /* Sink / recent augmentation (engine.py:122-126): out[r] = sorted(idx[r][0..k_eff) |
  * [0, sinks) | [n_valid - recent, n_valid)), counts[r] its length. */

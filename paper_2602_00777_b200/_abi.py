@@ -43,6 +43,8 @@ EXPORTED_SYMBOLS = (
     "hylra_decode_step_workspace_bytes",
     "hylra_decode_step",
     "hylra_decode_step_offload",
+    "hylra_decode_step_events",
+    "hylra_append_kv",
     "hylra_overlap_counts",
     "hylra_augment_selection",
     "hylra_block_select",
@@ -123,6 +125,11 @@ def lib() -> ctypes.CDLL:
         l.hylra_decode_step_offload.restype = i32
         l.hylra_decode_step_offload.argtypes = [gp, vp, vp, vp, vp, vp, i32, vp, i32, i32, i32,
                                                 i32, i32, vp, vp, i32, vp, sz, vp]
+        l.hylra_decode_step_events.restype = i32
+        l.hylra_decode_step_events.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, i32,
+                                               vp, vp, i32, vp, sz, vp, vp, vp]
+        l.hylra_append_kv.restype = i32
+        l.hylra_append_kv.argtypes = [gp, vp, vp, vp, vp, i32, i32, vp, vp]
         l.hylra_augment_selection.restype = i32
         l.hylra_augment_selection.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp]
         l.hylra_overlap_counts.restype = i32
@@ -152,6 +159,12 @@ def launch_count() -> int:
 def int32_array(values) -> ctypes.Array:
     values = list(values)
     return (ctypes.c_int32 * max(len(values), 1))(*values)
+
+
+def pointer_array(values) -> ctypes.Array:
+    """void* [n] (None -> NULL), e.g. per-layer cudaEvent_t handles."""
+    values = list(values)
+    return (ctypes.c_void_p * max(len(values), 1))(*values)
 
 
 def uint8_array(values) -> ctypes.Array:

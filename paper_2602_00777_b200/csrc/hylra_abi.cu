@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/hylra.h"
+#include "append.cuh"
 #include "attention.cuh"
 #include "blocks.cuh"
 #include "overlap.cuh"
@@ -66,10 +67,65 @@ int check_geometry(const hylra_geometry* g) {
   return HYLRA_OK;
 }
 
-int choose_splits(int pairs, int tiles) {
-  const int target = kNumSMs * 2 * 8;  // ~8 waves of 2 CTAs per SM
-  int s = (target + pairs - 1) / pairs;
-  s = std::min(s, std::max(1, tiles / 4));
+// Split-K sizing: how many CTAs (splits) share one (layer, b, kv-head) pair's rows.
+// Rules from B200 sweeps of cfg2 shapes at B = 1/4/8 (scripts/split_sweep.py; 2 CTAs of
+// the attention kernel are resident per SM, S = 296 slots):
+//  * a CTA pays a fixed cost (pipeline fill, q load, split merge), and with ~25 GB/s per
+//    CTA (3-stage ring) a partial last wave runs almost as long as a full one;
+//  * REUSE, at most one wave of pairs: split only up to one wave of >= 8-tile splits
+//    (B=1 24 layers: 65.7 us at 8 splits/pair -> 45.3 at 1; B=1 5 layers: 16.6 at 4);
+//  * REUSE, 1-4 waves of pairs: unsplit unless that leaves a nearly empty last wave
+//    (B=4 24 layers: 145 us unsplit vs 155 at 4; B=8 5 layers, 1.08 waves: 83 us
+//    unsplit -> 76 at 4 splits);
+//  * REUSE, >= 4 waves of pairs: ~8 waves of >= 4-tile splits (B=8 24 layers: 283 vs
+//    295 us unsplit — the tail of a many-wave grid is short); "pairs" above count
+//    32-tile units of a pair (longer selections start out split);
+//  * FULL: ~4 waves of >= 32-tile splits, at least one wave (B=1: 186.5 -> 168.8 us).
+// HYLRA_{FULL,REUSE}_{WAVES,MIN_TILES} replace a rule by "waves x S CTAs, >= min tiles
+// per split" for tuning experiments.
+constexpr int kSlots = kNumSMs * 2;
+
+int splits_by_waves(int pairs, int tiles, int waves, int min_tiles) {
+  int s = (kSlots * waves + pairs - 1) / pairs;
+  return std::min(s, std::max(1, tiles / min_tiles));
+}
+
+int choose_splits(int pairs, int tiles, bool gather) {
+  static int env[2][2];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* n) {
+      const char* v = std::getenv(n);
+      return (v && *v) ? std::max(1, atoi(v)) : 0;
+    };
+    env[0][0] = get("HYLRA_FULL_WAVES");
+    env[0][1] = get("HYLRA_FULL_MIN_TILES");
+    env[1][0] = get("HYLRA_REUSE_WAVES");
+    env[1][1] = get("HYLRA_REUSE_MIN_TILES");
+  });
+  const int* e = env[gather ? 1 : 0];
+  int s;
+  if (e[0] || e[1]) {
+    s = splits_by_waves(pairs, tiles, e[0] ? e[0] : 8, e[1] ? e[1] : 4);
+  } else if (!gather) {
+    s = splits_by_waves(pairs, tiles, 4, 32);
+    const int fill = (kSlots + pairs - 1) / pairs;  // at least one wave when rows allow
+    s = std::max(s, std::min(fill, std::max(1, tiles / 4)));
+  } else {
+    // REUSE: CTAs of at most 32 tiles (1 MiB of K/V at d=128) — the 128K config's 4096-row
+    // selections at 64-tile CTAs left a long tail (300 -> 368 us)
+    const int s0 = std::max(1, (tiles + 31) / 32);
+    const long units = (long)pairs * s0;
+    if (units >= 4l * kSlots) {
+      s = splits_by_waves(pairs, tiles, 8, 4);
+    } else if (units <= kSlots) {
+      s = std::max(s0, std::min(kSlots / pairs, tiles / 8));
+    } else {
+      const long full_waves = units / kSlots, rest = units % kSlots;
+      s = (full_waves >= 2 || 2 * rest >= kSlots) ? s0
+                                                  : std::max(s0, splits_by_waves(pairs, tiles, 4, 8));
+    }
+  }
   s = std::max(1, std::min(s, tiles));
   const int tps = (tiles + s - 1) / s;
   return (tiles + tps - 1) / tps;
@@ -84,12 +140,12 @@ struct AttnLayout {
   size_t off_counters, off_ml, off_o, total;
 };
 
-AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows) {
+AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows, bool gather) {
   AttnLayout a{};
   const int G = g->q_heads / g->kv_heads;
   a.pairs = n_layers * g->batch * g->kv_heads;
   a.tiles = std::max(1, (rows + kTileRows - 1) / kTileRows);
-  a.splits = choose_splits(a.pairs, a.tiles);
+  a.splits = choose_splits(a.pairs, a.tiles, gather);
   a.tps = (a.tiles + a.splits - 1) / a.splits;
   const size_t parts = a.splits;  // partial slots per pair
   a.off_counters = kHeader;
@@ -210,7 +266,7 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   if (n_rows < 1) return fail(HYLRA_ERR_INVALID_INPUT, "no rows to attend over");
   if (!q || !k || !v || !out || !ws || !layer_ids)
     return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
-  const AttnLayout lay = attn_layout(g, n_layers, n_rows);
+  const AttnLayout lay = attn_layout(g, n_layers, n_rows, gather);
   if (ws_bytes < lay.total)
     return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, lay.total);
   const int G = g->q_heads / g->kv_heads;
@@ -467,13 +523,14 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   // FULL and REUSE get disjoint attention workspaces: each kernel's split-K counters must
   // start at zero, and the other launch's partial buffers would otherwise overlap them.
   s->off_attn = off;
-  s->attn_bytes = attn_layout(g, (int)nf, n_valid).total;
+  s->attn_bytes = attn_layout(g, (int)nf, n_valid, false).total;
   s->off_attn_r = align_up(s->off_attn + s->attn_bytes, 256);
-  s->attn_bytes_r =
-      s->reuse_ids.empty()
-          ? 0
-          : attn_layout(g, (int)s->reuse_ids.size(), s->aug_stride ? s->aug_stride : s->k_eff)
-                .total;
+  // REUSE layers may be launched in chunks (hylra_decode_step_events): size for the
+  // largest workspace any chunk length needs (fewer pairs can mean more splits).
+  s->attn_bytes_r = 0;
+  for (int n = 1; n <= (int)s->reuse_ids.size(); ++n)
+    s->attn_bytes_r = std::max(
+        s->attn_bytes_r, attn_layout(g, n, s->aug_stride ? s->aug_stride : s->k_eff, true).total);
   s->total = s->off_attn_r + s->attn_bytes_r;
   return HYLRA_OK;
 }
@@ -505,7 +562,8 @@ struct SplitKv {
 int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, const void* v,
                      int n_valid, const uint8_t* actions, int budget, int sel_group, int refine,
                      int sinks, int recent, float* out, int32_t* idx, int k_stride, void* ws,
-                     size_t ws_bytes, void* stream, const SplitKv* split) {
+                     size_t ws_bytes, void* stream, const SplitKv* split,
+                     void* reuse_wait = nullptr, void* const* layer_events = nullptr) {
   StepLayout s;
   if (int e = step_layout(g, actions, n_valid, budget, sel_group, &s, 1, sinks, recent)) return e;
   if (!ws || ws_bytes < s.total)
@@ -528,6 +586,13 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                nullptr, nullptr, nullptr, 0, 1, out, scores, aws, s.attn_bytes,
                                flags, st, split ? fkv.data() : nullptr, nf))
     return e;
+  // FULL layers' outputs are final once the FULL launch retires
+  if (layer_events)
+    for (int l : s.full_ids)
+      if (layer_events[l])
+        if (int e = cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l]), st),
+                               "event record"))
+          return e;
   if (int e = launch_select(g, scores, nf, n_valid, budget, sel_group, refine ? q : nullptr,
                             refine ? kf : nullptr, s.full_ids.data(), idx, k_stride, nullptr,
                             flags, st, BlockRows(), split ? fkv.data() : nullptr))
@@ -548,11 +613,27 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
       rcnt = acnt;
       rstride = rk = s.aug_stride;
     }
-    if (int e = launch_attention(g, true, q, split ? split->kr : k, split ? split->vr : v,
-                                 n_valid, rk, nr, s.reuse_ids.data(), s.reuse_src.data(), ridx,
-                                 rcnt, rstride, sel_group, out, nullptr, w + s.off_attn_r,
-                                 s.attn_bytes_r, flags, st, split ? rkv.data() : nullptr, nr))
-      return e;
+    if (reuse_wait)
+      if (int e = cuda_check(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(reuse_wait), 0),
+                             "stream wait event"))
+        return e;
+    // one launch, or one per chunk of REUSE layers ending at a layer that carries an event
+    int c0 = 0;
+    for (int i = 0; i < nr; ++i) {
+      const int l = s.reuse_ids[i];
+      cudaEvent_t ev = layer_events ? static_cast<cudaEvent_t>(layer_events[l]) : nullptr;
+      if (!(ev || i == nr - 1)) continue;
+      const int n = i + 1 - c0;
+      if (int e = launch_attention(g, true, q, split ? split->kr : k, split ? split->vr : v,
+                                   n_valid, rk, n, s.reuse_ids.data() + c0,
+                                   s.reuse_src.data() + c0, ridx, rcnt, rstride, sel_group, out,
+                                   nullptr, w + s.off_attn_r, s.attn_bytes_r, flags, st,
+                                   split ? rkv.data() + c0 : nullptr, nr))
+        return e;
+      if (ev)
+        if (int e = cuda_check(cudaEventRecord(ev, st), "event record")) return e;
+      c0 = i + 1;
+    }
   }
   return HYLRA_OK;
 }
@@ -582,7 +663,9 @@ uint64_t hylra_launch_count(void) { return g_launches.load(); }
 
 size_t hylra_attention_workspace_bytes(const hylra_geometry* g, int n_layers, int rows) {
   if (check_geometry(g) || n_layers < 1) return 0;
-  return attn_layout(g, n_layers, std::max(rows, 1)).total;
+  // either op (FULL or REUSE) may use the workspace
+  return std::max(attn_layout(g, n_layers, std::max(rows, 1), false).total,
+                  attn_layout(g, n_layers, std::max(rows, 1), true).total);
 }
 
 size_t hylra_select_workspace_bytes(const hylra_geometry* g, int n_slots, int sel_group) {
@@ -639,6 +722,16 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                           out, idx, k_stride, ws, ws_bytes, stream, nullptr);
 }
 
+int hylra_decode_step_events(const hylra_geometry* g, const void* q, const void* k,
+                             const void* v, int n_valid, const uint8_t* actions, int budget,
+                             int sel_group, int refine, int sinks, int recent, float* out,
+                             int32_t* idx, int k_stride, void* ws, size_t ws_bytes, void* stream,
+                             void* reuse_wait_event, void* const* layer_events) {
+  return decode_step_impl(g, q, k, v, n_valid, actions, budget, sel_group, refine, sinks, recent,
+                          out, idx, k_stride, ws, ws_bytes, stream, nullptr, reuse_wait_event,
+                          layer_events);
+}
+
 int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void* k_full,
                               const void* v_full, const void* k_reuse, const void* v_reuse,
                               int n_valid, const uint8_t* actions, int budget, int sel_group,
@@ -657,6 +750,50 @@ int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void
   }
   return decode_step_impl(g, q, nullptr, nullptr, n_valid, actions, budget, sel_group, refine,
                           sinks, recent, out, idx, k_stride, ws, ws_bytes, stream, &sp);
+}
+
+int hylra_append_kv(const hylra_geometry* g, void* k, void* v, const void* k_rows,
+                    const void* v_rows, int pos, int n_layers, const int32_t* layer_ids,
+                    void* stream) {
+  if (int e = check_geometry(g)) return e;
+  if (!k || !v) return fail(HYLRA_ERR_CONFIGURATION, "NULL cache pointer");
+  if (pos < 0 || pos >= g->capacity)
+    return fail(HYLRA_ERR_INVALID_INPUT, "pos %d not in [0, capacity=%d)", pos, g->capacity);
+  const int L = layer_ids ? n_layers : g->num_layers;
+  if (L < 1 || L > kMaxSlots)
+    return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", L, kMaxSlots);
+  AppendParams p{};
+  if (int e = device_view(k_rows, reinterpret_cast<const void**>(&p.k_rows), "k_rows")) return e;
+  if (int e = device_view(v_rows, reinterpret_cast<const void**>(&p.v_rows), "v_rows")) return e;
+  const int es = g->dtype == HYLRA_BF16 ? 2 : 4;
+  const int64_t row_bytes = (int64_t)g->head_dim * es;
+  if (row_bytes % 16 != 0 || (g->kv_stride_layer * es) % 16 != 0 ||
+      (g->kv_stride_batch * es) % 16 != 0 || (g->kv_stride_head * es) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(k) % 16 != 0 || reinterpret_cast<uintptr_t>(v) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(p.k_rows) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(p.v_rows) % 16 != 0)
+    return fail(HYLRA_ERR_CONFIGURATION, "append needs 16-byte aligned rows and strides");
+  p.k = static_cast<uint8_t*>(k);
+  p.v = static_cast<uint8_t*>(v);
+  p.kv_sl = g->kv_stride_layer * es;
+  p.kv_sb = g->kv_stride_batch * es;
+  p.kv_sh = g->kv_stride_head * es;
+  p.pos_bytes = (int64_t)pos * row_bytes;
+  p.B = g->batch;
+  p.Hkv = g->kv_heads;
+  p.chunks = (int)(row_bytes / 16);
+  p.n_layers = L;
+  for (int i = 0; i < L; ++i) {
+    const int l = layer_ids ? layer_ids[i] : i;
+    if (l < 0 || l >= g->num_layers)
+      return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", l);
+    p.layers[i] = l;
+  }
+  const int64_t total = 2ll * L * g->batch * g->kv_heads * p.chunks;
+  const unsigned blocks = (unsigned)((total + kAppendThreads - 1) / kAppendThreads);
+  append_kv_kernel<<<blocks, kAppendThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_check(cudaGetLastError(), "append launch");
 }
 
 int hylra_augment_selection(const int32_t* idx, int rows, int k_eff, int k_stride, int n_valid,

@@ -121,11 +121,48 @@ class HybridDecoder:
         return int(_abi.lib().hylra_decode_step_workspace_bytes(
             g, self._acts, int(n_valid), self.budget, self.sel_group, self.sinks, self.recent))
 
-    def step(self, q: torch.Tensor, n_valid: int | None = None) -> StepResult:
+    def step(self, q: torch.Tensor, n_valid: int | None = None, *, layer_events=None,
+             reuse_wait=None, out: torch.Tensor | None = None) -> StepResult:
+        """Enqueue one decode step. layer_events (optional, L torch.cuda.Event or None):
+        event l is recorded once out[l] is final, REUSE layers being launched in chunks
+        that end at the evented layers; reuse_wait (optional event): the REUSE launches
+        wait on it (hylra_decode_step_events). Token mode only. out (optional): fp32
+        [L, B, Hq, d] destination instead of the decoder's own buffer — device memory or
+        pinned host memory, which the kernels then write across the link directly."""
+        if out is not None:
+            if out.shape != self.out.shape or out.dtype != torch.float32 \
+                    or not out.is_contiguous() or not (out.is_cuda or out.is_pinned()):
+                raise ConfigurationError("out must be a contiguous fp32 [L, B, Hq, d] device "
+                                         "or pinned host tensor")
+            own = self.out
+            self.out = out
+            try:
+                return self.step(q, n_valid, layer_events=layer_events, reuse_wait=reuse_wait)
+            finally:
+                self.out = own
         g = self._geometry(q)
         n_valid = g.capacity if n_valid is None else int(n_valid)
         lib = _abi.lib()
         st = torch.cuda.current_stream(self.k.device).cuda_stream
+        if layer_events is not None or reuse_wait is not None:
+            if self.block_size > 1:
+                raise ConfigurationError("per-layer events apply to token selection only")
+            evs = list(layer_events) if layer_events is not None else [None] * len(self.actions)
+            if len(evs) != len(self.actions):
+                raise ConfigurationError(f"{len(evs)} layer events for {len(self.actions)} layers")
+            need = int(lib.hylra_decode_step_workspace_bytes(
+                g, self._acts, n_valid, self.budget, self.sel_group, self.sinks, self.recent))
+            if self.ws.numel() < need:
+                self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
+            _abi.check(lib.hylra_decode_step_events(
+                g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
+                self.budget, self.sel_group, int(self.refine), self.sinks, self.recent,
+                self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(),
+                self.ws.numel(), st, reuse_wait.cuda_event if reuse_wait is not None else None,
+                _abi.pointer_array(e.cuda_event if e is not None else None for e in evs)))
+            k_eff = min(self.budget, n_valid)
+            return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer,
+                              self.full_layers)
         if self.block_size > 1:
             need = int(lib.hylra_decode_step_blocks_workspace_bytes(
                 g, self._acts, n_valid, self.budget, self.block_size, self.sel_group))
@@ -155,6 +192,27 @@ class HybridDecoder:
             self.ws.numel(), st))
         k_eff = min(self.budget, n_valid)
         return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
+
+    def append(self, k_rows: torch.Tensor, v_rows: torch.Tensor, pos: int, layers=None) -> None:
+        """Write one step's new K/V rows [L, B, Hkv, d] (device or pinned host tensors, the
+        cache dtype) at cache row `pos` of the given layers (default all), on the current
+        stream (hylra_append_kv; host rows are read across the link in place)."""
+        L, B, Hkv, cap, d = self.k.shape
+        for t in (k_rows, v_rows):
+            if t.shape != (L, B, Hkv, d) or t.dtype != self.k.dtype or not t.is_contiguous() \
+                    or not (t.is_cuda or t.is_pinned()):
+                raise ConfigurationError("new rows must be contiguous [L, B, Hkv, d] device or "
+                                         "pinned host tensors of the cache dtype")
+        ids = list(range(L)) if layers is None else list(layers)
+        g = _abi.Geometry()
+        g.batch, g.q_heads, g.kv_heads, g.head_dim = B, self.q_heads, Hkv, d
+        g.capacity, g.num_layers = cap, L
+        g.dtype = _abi.HYLRA_BF16 if self.k.dtype == torch.bfloat16 else _abi.HYLRA_F32
+        g.kv_stride_layer, g.kv_stride_batch, g.kv_stride_head = self.k.stride()[:3]
+        _abi.check(_abi.lib().hylra_append_kv(
+            g, self.k.data_ptr(), self.v.data_ptr(), k_rows.data_ptr(), v_rows.data_ptr(),
+            int(pos), len(ids), _abi.int32_array(ids),
+            torch.cuda.current_stream(self.k.device).cuda_stream))
 
     def flags(self) -> int:
         """Device flag word (synchronises)."""
@@ -343,17 +401,36 @@ class PipelinedDecoder(HybridDecoder):
         return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
 
 
+def _runs(layers):
+    """Ascending layer ids -> [(first, last + 1)] runs of consecutive layers."""
+    runs = []
+    for l in layers:
+        if runs and runs[-1][1] == l:
+            runs[-1][1] = l + 1
+        else:
+            runs.append([l, l + 1])
+    return [tuple(r) for r in runs]
+
+
 class DecodeLoop:
     """One decode step with host I/O as a single CUDA-graph launch.
 
     Per step: the query [L, B, Hq, d] and the new token's key/value rows [L, B, Hkv, d]
-    are copied from pinned host buffers (`q_host`, `k_host`, `v_host`), the K/V rows are
+    come from pinned host buffers (`q_host`, `k_host`, `v_host`), the K/V rows are
     appended at cache row `pos`, the hybrid step runs over `pos + 1` rows, and the fp32
     outputs land in the pinned `out_host`. Fill the host buffers, call `run()`; it returns
     `out_host` after the step completed.
+
+    overlap=True (token-mode HybridDecoder): the FULL layers' queries are copied and their
+    new rows appended first (hylra_append_kv reads the pinned rows across the link in
+    place); the REUSE layers' queries and rows follow on a side stream behind the FULL
+    kernel (the REUSE launch waits on them: hylra_decode_step_events); the kernels store
+    the outputs straight into the pinned `out_host` as each (layer, KV head) completes,
+    so no device-to-host copy follows the step. overlap=False: plain H2D copies, append,
+    step, D2H copy, serialised.
     """
 
-    def __init__(self, decoder: HybridDecoder, pos: int):
+    def __init__(self, decoder: HybridDecoder, pos: int, *, overlap: bool = True):
         k = decoder.k
         L, B, Hkv, cap, d = k.shape
         if not 0 <= pos < cap:
@@ -366,20 +443,47 @@ class DecodeLoop:
         self.v_host = torch.zeros((L, B, Hkv, d), dtype=dt).pin_memory()
         self.out_host = torch.zeros((L, B, Hq, d), dtype=torch.float32).pin_memory()
         self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
-        self.kv_dev = torch.zeros((2, L, B, Hkv, d), dtype=dt, device=k.device)
         self.graph = None
         self.h2d_bytes = (self.q_host.numel() + 2 * self.k_host.numel()) * self.q_host.element_size()
         self.d2h_bytes = self.out_host.numel() * 4
+        self.overlap = bool(overlap) and type(decoder) is HybridDecoder \
+            and decoder.block_size == 1
+        acts = decoder.actions
+        self.full_layers = [l for l in range(L) if acts[l] is Action.FULL]
+        self.reuse_layers = [l for l in range(L) if acts[l] is Action.REUSE]
+        if self.overlap:
+            self.side = torch.cuda.Stream(device=k.device)
+            # torch creates events lazily: record once so the handle exists for the ABI
+            self.ev_side = torch.cuda.Event()
+            self.ev_side.record()
+        else:
+            self.kv_dev = torch.zeros((2, L, B, Hkv, d), dtype=dt, device=k.device)
 
     def _body(self):
         dec, pos = self.dec, self.pos
-        self.q_dev.copy_(self.q_host, non_blocking=True)
-        self.kv_dev[0].copy_(self.k_host, non_blocking=True)
-        self.kv_dev[1].copy_(self.v_host, non_blocking=True)
-        dec.k[:, :, :, pos].copy_(self.kv_dev[0])
-        dec.v[:, :, :, pos].copy_(self.kv_dev[1])
-        dec.step(self.q_dev, pos + 1)
-        self.out_host.copy_(dec.out, non_blocking=True)
+        if not self.overlap:
+            self.q_dev.copy_(self.q_host, non_blocking=True)
+            self.kv_dev[0].copy_(self.k_host, non_blocking=True)
+            self.kv_dev[1].copy_(self.v_host, non_blocking=True)
+            dec.append(self.kv_dev[0], self.kv_dev[1], pos)
+            dec.step(self.q_dev, pos + 1)
+            self.out_host.copy_(dec.out, non_blocking=True)
+            return
+        main = torch.cuda.current_stream(dec.k.device)
+        if self.reuse_layers:
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                for a, b in _runs(self.reuse_layers):
+                    self.q_dev[a:b].copy_(self.q_host[a:b], non_blocking=True)
+                dec.append(self.k_host, self.v_host, pos, self.reuse_layers)
+                self.ev_side.record(self.side)
+        for a, b in _runs(self.full_layers):
+            self.q_dev[a:b].copy_(self.q_host[a:b], non_blocking=True)
+        dec.append(self.k_host, self.v_host, pos, self.full_layers)
+        dec.step(self.q_dev, pos + 1, out=self.out_host,
+                 reuse_wait=self.ev_side if self.reuse_layers else None)
+        if self.reuse_layers:
+            main.wait_stream(self.side)
 
     def capture(self):
         """Warm up and capture the step (host copies included) into a CUDA graph."""

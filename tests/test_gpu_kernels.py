@@ -253,15 +253,18 @@ def test_pipelined_schedules_match_fused(schedule):
     assert max_head_err(dec.out.double().cpu().numpy(), r) < 4e-3
 
 
-def test_decode_loop_host_io_graph():
-    """DecodeLoop: H2D (q + new K/V row) -> append -> step -> D2H in one graph launch."""
+@pytest.mark.parametrize("overlap", [False, True])
+def test_decode_loop_host_io_graph(overlap):
+    """DecodeLoop: H2D (q + new K/V row) -> append -> step -> D2H in one graph launch;
+    overlap=True: REUSE inputs on a side stream, rows appended from pinned host memory in
+    place, outputs stored by the kernels straight into pinned host memory."""
     from paper_2602_00777_b200.engine import DecodeLoop
-    L, B, Hq, Hkv, d, cap, budget = 4, 2, 8, 2, 128, 2048, 128
+    L, B, Hq, Hkv, d, cap, budget = 9, 2, 8, 2, 128, 2048, 128
     q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=13, planted=16)
-    actions = ("full", "reuse", "full", "reuse")
+    actions = ("full", "reuse", "full", "reuse", "reuse", "full", "reuse", "reuse", "reuse")
     dec = HybridDecoder(actions, k.clone(), v.clone(), budget, q_heads=Hq)
     pos = 1500
-    loop = DecodeLoop(dec, pos)
+    loop = DecodeLoop(dec, pos, overlap=overlap)
     g = torch.Generator().manual_seed(3)
     for step in range(3):
         qh = torch.randn((L, B, Hq, d), generator=g).to(torch.bfloat16)
@@ -275,9 +278,54 @@ def test_decode_loop_host_io_graph():
         k2, v2 = k.clone(), v.clone()
         k2[:, :, :, pos] = kh.cuda()
         v2[:, :, :, pos] = vh.cuda()
+        assert torch.equal(dec.k[:, :, :, pos].cpu(), kh) and torch.equal(dec.v, v2)
         ref = HybridDecoder(actions, k2, v2, budget, q_heads=Hq).step(qh.cuda(), pos + 1)
         torch.cuda.synchronize()
+        assert torch.equal(dec.idx, ref.selections)
         assert torch.equal(out, ref.outputs.cpu())
+
+
+def test_step_layer_events_chunks_reuse():
+    """hylra_decode_step_events: per-layer completion events split the REUSE launch into
+    chunks; selections identical, outputs within split-K rounding; events fire."""
+    L, B, Hq, Hkv, d, cap, budget = 9, 2, 8, 2, 128, 2048, 128
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=14, planted=16)
+    actions = ("full", "reuse", "full", "reuse", "reuse", "full", "reuse", "reuse", "reuse")
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq).step(q, cap)
+    ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq)
+    evs = [torch.cuda.Event() if l in (0, 1, 4, 7, 8) else None for l in range(L)]
+    for e in evs:
+        if e is not None:
+            e.record()
+    wait = torch.cuda.Event()
+    wait.record()
+    res = dec.step(q, cap, layer_events=evs, reuse_wait=wait)
+    torch.cuda.synchronize()
+    assert all(e.query() for e in evs if e is not None)
+    assert torch.equal(res.selections, ref_idx)
+    o, r = res.outputs.double().cpu().numpy(), ref_out.double().cpu().numpy()
+    assert max_head_err(o, r) < 4e-3
+
+
+def test_append_kv_from_device_and_pinned_host():
+    """hylra_append_kv writes [L, B, Hkv, d] rows at cache row pos of the chosen layers."""
+    L, B, Hq, Hkv, d, cap = 3, 2, 8, 2, 64, 100
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=5)
+    dec = HybridDecoder(("full", "reuse", "full"), k, v, 8, q_heads=Hq)
+    k0, v0 = k.clone(), v.clone()
+    rows_k = torch.randn((L, B, Hkv, d)).to(torch.bfloat16)
+    rows_v = torch.randn((L, B, Hkv, d)).to(torch.bfloat16)
+    dec.append(rows_k.cuda(), rows_v.cuda(), 7, layers=[1])
+    dec.append(rows_k.pin_memory(), rows_v.pin_memory(), 99, layers=[0, 2])
+    torch.cuda.synchronize()
+    k0[1, :, :, 7] = rows_k[1].cuda()
+    v0[1, :, :, 7] = rows_v[1].cuda()
+    k0[[0, 2], :, :, 99] = rows_k[[0, 2]].cuda()
+    v0[[0, 2], :, :, 99] = rows_v[[0, 2]].cuda()
+    assert torch.equal(k, k0) and torch.equal(v, v0)
+    with pytest.raises(InvalidInputError):
+        dec.append(rows_k.cuda(), rows_v.cuda(), cap)
 
 
 @pytest.mark.parametrize("where", ["k", "v", "q"])
