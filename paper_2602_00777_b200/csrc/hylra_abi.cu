@@ -77,10 +77,11 @@ int check_geometry(const hylra_geometry* g) {
 //  * REUSE, 1-4 waves of pairs: unsplit unless that leaves a nearly empty last wave
 //    (B=4 24 layers: 145 us unsplit vs 155 at 4; B=8 5 layers, 1.08 waves: 83 us
 //    unsplit -> 76 at 4 splits);
-//  * REUSE, >= 4 waves of pairs: ~8 waves of >= 4-tile splits (B=8 24 layers: 283 vs
+//  * REUSE, >= 4 waves of pairs: ~8 waves of >= 8-tile splits (B=8 24 layers: 283 vs
 //    295 us unsplit — the tail of a many-wave grid is short); "pairs" above count
 //    32-tile units of a pair (longer selections start out split);
-//  * FULL: ~4 waves of >= 32-tile splits, at least one wave (B=1: 186.5 -> 168.8 us).
+//  * FULL: ~4 waves of >= 32-tile splits, or up to one wave of shorter splits when
+//    rows are few (B=1: 186.5 -> 168.8 us).
 // HYLRA_{FULL,REUSE}_{WAVES,MIN_TILES} replace a rule by "waves x S CTAs, >= min tiles
 // per split" for tuning experiments.
 constexpr int kSlots = kNumSMs * 2;
@@ -109,7 +110,9 @@ int choose_splits(int pairs, int tiles, bool gather) {
     s = splits_by_waves(pairs, tiles, e[0] ? e[0] : 8, e[1] ? e[1] : 4);
   } else if (!gather) {
     s = splits_by_waves(pairs, tiles, 4, 32);
-    const int fill = (kSlots + pairs - 1) / pairs;  // at least one wave when rows allow
+    // up to one full wave when the rows allow (never just over one: N=8K B=1 at 5 splits
+    // = 320 CTAs took 60.7 us, at 4 = 256 CTAs 47.9 us)
+    const int fill = std::max(1, kSlots / pairs);
     s = std::max(s, std::min(fill, std::max(1, tiles / 4)));
   } else {
     // REUSE: CTAs of at most 32 tiles (1 MiB of K/V at d=128) — the 128K config's 4096-row
@@ -117,7 +120,8 @@ int choose_splits(int pairs, int tiles, bool gather) {
     const int s0 = std::max(1, (tiles + 31) / 32);
     const long units = (long)pairs * s0;
     if (units >= 4l * kSlots) {
-      s = splits_by_waves(pairs, tiles, 8, 4);
+      // >= 8-tile splits: N=8K k=512 B=8 (8 tiles/pair) took 117 us at 4-tile splits, 87 unsplit
+      s = std::max(s0, splits_by_waves(pairs, tiles, 8, 8));
     } else if (units <= kSlots) {
       s = std::max(s0, std::min(kSlots / pairs, tiles / 8));
     } else {
@@ -330,7 +334,36 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   return cuda_check(ce, gather ? "reuse_decode launch" : "full_decode launch");
 }
 
-size_t select_smem_bytes(int n_valid) { return sel_smem_bytes(n_valid); }
+// SELECT CTA width: one CTA per row; few rows (small batch) get wide CTAs so each row's
+// passes finish sooner, many rows keep 256-thread CTAs (4 per SM, all rows resident).
+// HYLRA_SELECT_THREADS overrides (256 / 512 / 1024) for tuning.
+int select_threads(int rows) {
+  static int forced = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* v = std::getenv("HYLRA_SELECT_THREADS");
+    const int t = (v && *v) ? atoi(v) : 0;
+    forced = (t == 256 || t == 512 || t == 1024) ? t : 0;
+  });
+  if (forced) return forced;
+  if (rows <= kNumSMs) return 1024;
+  if (rows <= 2 * kNumSMs) return 512;
+  return 256;
+}
+
+template <int NT>
+cudaError_t launch_select_nt(dim3 grid, size_t smem, cudaStream_t st, const SelectParams& p) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(topk_select_kernel<NT>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sel_smem_bytes(kSelMaxTokens, NT));
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  topk_select_kernel<NT><<<grid, NT, smem, st>>>(p);
+  return cudaGetLastError();
+}
 
 struct BlockRows {  // block mode: rows are pooled block scores
   int block_size = 1, n_tokens = 0, row_stride = 0;
@@ -383,17 +416,13 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
     p.layers[i] = l;
     p.kv_layers[i] = kv_layer_ids ? kv_layer_ids[i] : l;
   }
-  const size_t smem = select_smem_bytes(n_valid);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(topk_select_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)select_smem_bytes(kSelMaxTokens));
-  });
-  if (attr_err != cudaSuccess) return cuda_check(attr_err, "select attribute");
   dim3 grid(p.n_groups, g->batch, n_slots);
-  topk_select_kernel<<<grid, kSelThreads, smem, st>>>(p);
+  const int nt = select_threads(p.n_groups * g->batch * n_slots);
+  cudaError_t ce;
+  if (nt == 1024) ce = launch_select_nt<1024>(grid, sel_smem_bytes(n_valid, 1024), st, p);
+  else if (nt == 512) ce = launch_select_nt<512>(grid, sel_smem_bytes(n_valid, 512), st, p);
+  else ce = launch_select_nt<256>(grid, sel_smem_bytes(n_valid, 256), st, p);
+  if (ce != cudaSuccess) return cuda_check(ce, "topk_select launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_check(cudaGetLastError(), "topk_select launch");
 }

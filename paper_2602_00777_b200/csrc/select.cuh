@@ -5,10 +5,10 @@
 // ascending; engine.py:169 clamps the budget per step; engine.py:177-183 scores are the
 // head-order sum of per-head scaled logits.
 //
-// One 256-thread CTA per row with ~29 KB of shared memory (4 CTAs per SM), so all rows of
-// a step are resident at once; no global atomics. Fast path:
-//   A. sort a strided sample of 256 scores (bitonic: shuffles + 6 shared-memory stages)
-//      and bracket the k-th rank with [lo, hi];
+// One CTA per row (256 threads and ~29 KB of shared memory when rows are many: 4 CTAs per
+// SM, all rows of a step resident at once; 512 / 1024 threads when rows are few); no
+// global atomics. Fast path:
+//   A. bracket the k-th rank with [lo, hi] from the quantiles of 1024 strided samples;
 //   B. one vectorised pass: "definitely selected" bits (s > hi) go straight into a shared
 //      bitmap, scores inside [lo, hi] into a 2048-bin linear histogram; max|s| and the
 //      non-finite check ride along;
@@ -28,13 +28,17 @@
 
 namespace hylra {
 
-constexpr int kSelThreads = 256;
-constexpr int kSelWarps = kSelThreads / 32;
+// Threads per CTA (one CTA per row) is a template parameter NT in {256, 512, 1024}: rows
+// are few at small batch (64 at cfg2 B=1), so a wider CTA shortens each row's passes;
+// with many rows 256-thread CTAs keep every row resident at once (4 per SM).
+constexpr int kSelMaxThreads = 1024;
+constexpr int kSelMaxWarps = kSelMaxThreads / 32;
 constexpr int kBins = 2048;
 constexpr int kCandCap = 1024;            // scores collected around the k-th bin
 constexpr int kSmallN = 2048;             // rows sorted outright (small-row path)
 constexpr int kSelMaxTokens = 262144;     // longest row (bitmap = 32 KB)
-constexpr int kChunk = kSelThreads * 32;  // tokens per bitmap chunk (one word per thread)
+template <int NT>
+__host__ __device__ constexpr int sel_chunk() { return NT * 32; }  // tokens per bitmap chunk (one word per thread)
 
 struct SelectParams {
   const float* scores;  // [slot][b][kh][row_stride]
@@ -58,45 +62,48 @@ struct SelectParams {
 };
 
 // Dynamic shared memory: the bitmap sized for the row, then fixed arrays.
-__host__ __device__ constexpr size_t sel_bitmap_bytes(int n) {
-  return (size_t)((n + kChunk - 1) / kChunk) * kChunk / 8;
+__host__ __device__ constexpr size_t sel_bitmap_bytes(int n, int nt) {
+  return (size_t)((n + nt * 32 - 1) / (nt * 32)) * (nt * 32) / 8;
 }
-constexpr size_t kSelFixedBytes = kBins * 4 + kCandCap * (8 + 4) + kSelThreads * 4 +
-                                  kSmallN * 8;
-__host__ __device__ constexpr size_t sel_smem_bytes(int n) {
-  return sel_bitmap_bytes(n) + kSelFixedBytes;
+__host__ __device__ constexpr size_t sel_fixed_bytes(int nt) {
+  return kBins * 4 + kCandCap * (8 + 4) + nt * 4 + kSmallN * 8;
+}
+__host__ __device__ constexpr size_t sel_smem_bytes(int n, int nt) {
+  return sel_bitmap_bytes(n, nt) + sel_fixed_bytes(nt);
 }
 
 struct SelSmem {
-  uint32_t* bitmap;  // [chunks * kSelThreads]
+  uint32_t* bitmap;  // [chunks * NT]
   unsigned* hist;    // [kBins]
   double* cv;        // [kCandCap] window scores (fp32 value, then float64 re-score)
   int* ci;           // [kCandCap] window token indices
-  float* xchg;       // [kSelThreads]
+  float* xchg;       // [NT]
   uint64_t* keys;    // [kSmallN] small-row sort keys
 };
 
+template <int NT>
 __device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
   SelSmem m;
-  const size_t bb = sel_bitmap_bytes(n);
+  const size_t bb = sel_bitmap_bytes(n, NT);
   m.bitmap = reinterpret_cast<uint32_t*>(base);
   m.hist = reinterpret_cast<unsigned*>(base + bb);
   m.cv = reinterpret_cast<double*>(base + bb + kBins * 4);
   m.ci = reinterpret_cast<int*>(base + bb + kBins * 4 + kCandCap * 8);
   m.xchg = reinterpret_cast<float*>(m.ci + kCandCap);
-  m.keys = reinterpret_cast<uint64_t*>(m.xchg + kSelThreads);
+  m.keys = reinterpret_cast<uint64_t*>(m.xchg + NT);
   return m;
 }
 
 // ----------------------------------------------------------------------------- helpers
 struct Red {
-  int i[kSelWarps];
-  float f[kSelWarps];
-  int wt[kSelWarps];
+  int i[kSelMaxWarps];
+  float f[kSelMaxWarps];
+  int wt[kSelMaxWarps];
   int misc[16];
   unsigned hist256[256];
 };
 
+template <int NT>
 __device__ __forceinline__ int block_sum_int(int v, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -106,9 +113,10 @@ __device__ __forceinline__ int block_sum_int(int v, Red& r) {
   __syncthreads();
   int x = 0;
 #pragma unroll
-  for (int w = 0; w < kSelWarps; ++w) x += r.i[w];
+  for (int w = 0; w < NT / 32; ++w) x += r.i[w];
   return x;
 }
+template <int NT>
 __device__ __forceinline__ float block_max_float(float v, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_max(v);
@@ -117,11 +125,12 @@ __device__ __forceinline__ float block_max_float(float v, Red& r) {
   __syncthreads();
   float x = -INFINITY;
 #pragma unroll
-  for (int w = 0; w < kSelWarps; ++w) x = fmaxf(x, r.f[w]);
+  for (int w = 0; w < NT / 32; ++w) x = fmaxf(x, r.f[w]);
   return x;
 }
 
 // Block exclusive scan of one int; returns the exclusive prefix, *total = block sum.
+template <int NT>
 __device__ __forceinline__ int block_scan(int v, int* total, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = v;
@@ -135,7 +144,7 @@ __device__ __forceinline__ int block_scan(int v, int* total, Red& r) {
   __syncthreads();
   int pre = 0, all = 0;
 #pragma unroll
-  for (int w = 0; w < kSelWarps; ++w) {
+  for (int w = 0; w < NT / 32; ++w) {
     const int t = r.wt[w];
     pre += (w < warp) ? t : 0;
     all += t;
@@ -157,30 +166,6 @@ __device__ __forceinline__ int warp_append(int cnt, int* counter) {
   if (lane == 31 && incl > 0) base = atomicAdd(counter, incl);
   base = __shfl_sync(0xffffffffu, base, 31);
   return base + incl - cnt;
-}
-
-// Descending bitonic sort of one float per thread (kSelThreads values), fully unrolled.
-__device__ __forceinline__ float bitonic_desc(float x, float* xchg) {
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int kk = 2; kk <= kSelThreads; kk <<= 1) {
-#pragma unroll
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      float y;
-      if (j >= 32) {
-        __syncthreads();
-        xchg[tid] = x;
-        __syncthreads();
-        y = xchg[tid ^ j];
-      } else {
-        y = __shfl_xor_sync(0xffffffffu, x, j);
-      }
-      const bool keep_max = ((tid & kk) == 0) == ((tid & j) == 0);
-      x = keep_max ? fmaxf(x, y) : fminf(x, y);
-    }
-  }
-  __syncthreads();
-  return x;
 }
 
 struct RowReader {
@@ -251,11 +236,12 @@ __device__ double token_score_f64(const SelectParams& p, int layer, int kvl, int
 }
 
 // float64 scores of candidate tokens toks[0..n); kTpw tokens per warp.
+template <int NT>
 __device__ void rescore_f64(const SelectParams& p, int slot, int b, int grp, const int* toks,
                             double* vals, int n) {
   const int warp = threadIdx.x >> 5, sub = threadIdx.x & (kLpt - 1);
   const int slot_in_warp = (threadIdx.x & 31) / kLpt;
-  for (int c0 = warp * kTpw; c0 < n; c0 += kSelWarps * kTpw) {  // warp-uniform trip count
+  for (int c0 = warp * kTpw; c0 < n; c0 += (NT / 32) * kTpw) {  // warp-uniform trip count
     const int c = c0 + slot_in_warp;
     const double agg = token_score_f64(p, p.layers[slot], p.kv_layers[slot], b, grp,
                                        toks[min(c, n - 1)]);
@@ -278,6 +264,7 @@ __device__ __forceinline__ double key_f64(unsigned long long k) {
 // tau/2 of float64 (the premise of the refinement window), the float64 maximiser t* obeys
 // s32(t*) >= s64(t*) - tau/2 >= s64(t_max32) - tau/2 >= s32(t_max32) - tau. If more than
 // kSmallN tokens qualify (or token scores are absent) every token is re-scored.
+template <int NT>
 __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int grp,
                                    const int* blocks, double* vals, int n, float tau,
                                    uint64_t* list) {
@@ -291,7 +278,7 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
   if (p.tok_scores) {
     const float* trow = p.tok_scores +
                         ((int64_t)(slot * p.B + b) * p.Hkv + grp * p.sel_group) * p.tok_row_stride;
-    for (int e = threadIdx.x; e < total; e += kSelThreads) {
+    for (int e = threadIdx.x; e < total; e += NT) {
       const int c = e / bs;
       const int tok = blocks[c] * bs + (e - c * bs);
       if (tok >= p.n_tokens) continue;
@@ -307,9 +294,9 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
   const bool listed = s_cnt <= kSmallN;
   const int items = listed ? s_cnt : total;
   unsigned long long* vk = reinterpret_cast<unsigned long long*>(vals);
-  for (int c = threadIdx.x; c < n; c += kSelThreads) vk[c] = 0ull;
+  for (int c = threadIdx.x; c < n; c += NT) vk[c] = 0ull;
   __syncthreads();
-  for (int e0 = warp * kTpw; e0 < items; e0 += kSelWarps * kTpw) {  // warp-uniform trips
+  for (int e0 = warp * kTpw; e0 < items; e0 += (NT / 32) * kTpw) {  // warp-uniform trips
     const int e = min(e0 + slot_in_warp, items - 1);
     int c, tok;
     if (listed) {
@@ -325,20 +312,21 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
     if (ok && sub == 0) atomicMax(vk + c, f64_key(agg));
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < n; c += kSelThreads) vals[c] = key_f64(vk[c]);
+  for (int c = threadIdx.x; c < n; c += NT) vals[c] = key_f64(vk[c]);
 }
 
 // MSB-first 4 x 8-bit radix select of the rank-`rank` (1-based, descending) score of the
 // row: T, #(s > T). Degenerate-row fallback only.
+template <int NT>
 __device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, float* T_out,
                                  int* gt_out) {
   const int tid = threadIdx.x, lane = tid & 31;
   uint32_t prefix = 0, mask = 0;
   int krem = rank;
   for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int j = tid; j < 256; j += kSelThreads) r.hist256[j] = 0;
+    for (int j = tid; j < 256; j += NT) r.hist256[j] = 0;
     __syncthreads();
-    for (int base = 0; base < n; base += kSelThreads) {
+    for (int base = 0; base < n; base += NT) {
       const int j = base + tid;
       bool act = false;
       unsigned dig = 0;
@@ -374,10 +362,11 @@ __device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, f
 }
 
 // Descending bitonic sort of np (power of two) 64-bit keys in shared memory.
+template <int NT>
 __device__ void bitonic_sort_desc(uint64_t* a, int np) {
   for (int size = 2; size <= np; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < (np >> 1); t += kSelThreads) {
+      for (int t = threadIdx.x; t < (np >> 1); t += NT) {
         const int i = 2 * t - (t & (stride - 1));
         const int j = i + stride;
         const uint64_t x = a[i], y = a[j];
@@ -396,6 +385,7 @@ __device__ void bitonic_sort_desc(uint64_t* a, int np) {
 // in the bitmap; the window [T - tau, T + tau] (refine) goes to cv/ci for the shared
 // re-score + rank step. Without refinement (or with non-finite scores, or a window larger
 // than kCandCap, flagged 4) the first k sorted entries are the answer.
+template <int NT>
 __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int n, int k,
                                  bool refine, const SelSmem& sm, Red& red, int* above_w,
                                  int* nw_out, float* tau_out) {
@@ -404,7 +394,7 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
   int np = 64;
   while (np < n) np <<= 1;
   float nanacc = 0.f, mx = 0.f;
-  for (int i = tid; i < np; i += kSelThreads) {
+  for (int i = tid; i < np; i += NT) {
     uint64_t key = 0ull;  // padding sorts after every real entry
     if (i < n) {
       const float v = rd.at(i);
@@ -414,11 +404,11 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
     }
     keys[i] = key;
   }
-  const int bad = block_sum_int(nanacc != nanacc ? 1 : 0, red);
-  mx = block_max_float(mx, red);
+  const int bad = block_sum_int<NT>(nanacc != nanacc ? 1 : 0, red);
+  mx = block_max_float<NT>(mx, red);
   if (bad && tid == 0) atomicOr(p.flags, 2);
   __syncthreads();
-  bitonic_sort_desc(keys, np);
+  bitonic_sort_desc<NT>(keys, np);
   auto val = [&](int pos) { return key_float((uint32_t)(keys[pos] >> 32)); };
   auto tok = [&](int pos) { return (int)(~(uint32_t)keys[pos]); };
   int a = k, z = k;
@@ -427,19 +417,19 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
     const float tau = *tau_out = fmaxf(p.tau_rel * mx, 1e-30f);
     const float lo_w = T - tau, hi_w = T + tau;
     int ca = 0, cz = 0;
-    for (int pos = tid; pos < n; pos += kSelThreads) {
+    for (int pos = tid; pos < n; pos += NT) {
       const float v = val(pos);
       ca += v > hi_w;
       cz += v >= lo_w;
     }
-    a = block_sum_int(ca, red);
-    z = block_sum_int(cz, red);
+    a = block_sum_int<NT>(ca, red);
+    z = block_sum_int<NT>(cz, red);
     if (z - a > kCandCap) {
       if (tid == 0) atomicOr(p.flags, 4);
       a = z = k;
     }
   }
-  for (int pos = tid; pos < z; pos += kSelThreads) {
+  for (int pos = tid; pos < z; pos += NT) {
     const int i = tok(pos);
     if (pos < a) {
       atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
@@ -453,7 +443,9 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
 }
 
 // ----------------------------------------------------------------------------- kernel
-__global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const SelectParams p) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const SelectParams p) {
+  constexpr int kChunk = sel_chunk<NT>();
   extern __shared__ __align__(16) uint8_t sraw[];
   __shared__ Red red;
 
@@ -465,7 +457,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   const int row_id = (slot * p.B + b) * p.n_groups + grp;
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
   int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
-  const SelSmem sm = carve(sraw, n);
+  const SelSmem sm = carve<NT>(sraw, n);
   const long long t0 = clock64();
 
   RowReader rd;
@@ -481,11 +473,11 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   if (k >= n) {
     // the budget covers the cache: every index (after the non-finite check)
     float nanacc = 0.f;
-    for (int i = tid; i < n; i += kSelThreads) {
+    for (int i = tid; i < n; i += NT) {
       nanacc = fmaf(rd.at(i), 0.f, nanacc);
       out[i] = i;
     }
-    if (block_sum_int(nanacc != nanacc ? 1 : 0, red) && tid == 0) atomicOr(p.flags, 2);
+    if (block_sum_int<NT>(nanacc != nanacc ? 1 : 0, red) && tid == 0) atomicOr(p.flags, 2);
     if (info && tid == 0) {
       for (int j = 0; j < 8; ++j) info[j] = 0;
       info[0] = k;
@@ -493,9 +485,9 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
     return;
   }
 
-  const int nwords = (int)(sel_bitmap_bytes(n) / 4);
-  for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
-  for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+  const int nwords = (int)(sel_bitmap_bytes(n, NT) / 4);
+  for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
+  for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
   if (tid == 0) red.misc[3] = red.misc[5] = 0;
 
   const bool refine = p.q != nullptr;
@@ -504,24 +496,25 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   float tau_w = 0.f;  // refinement half-width
   long long t1, t2, t3;
   if (n <= kSmallN) {
-    small_row_select(p, rd, n, k, refine, sm, red, &above_w, &nw, &tau_w);
+    small_row_select<NT>(p, rd, n, k, refine, sm, red, &above_w, &nw, &tau_w);
     mode = 3;
     t1 = t2 = t3 = clock64();
   } else {
-    // ---- A. brackets [lo, hi] around the k-th rank from 4 x 256 strided samples: their
-    //         quantiles are read off a 1024-bin histogram over [sample min, sample max]
-    //         (no sort); edges are widened outward so the bracket stays conservative
-    constexpr int kS = 4 * kSelThreads;
-    float smp[4];
+    // ---- A. brackets [lo, hi] around the k-th rank from 1024 strided samples (1024 / NT
+    //         per thread): their quantiles are read off a 1024-bin histogram over
+    //         [sample min, sample max] (no sort); edges are widened outward so the bracket
+    //         stays conservative
+    constexpr int kS = 1024, SPT = kS / NT;
+    float smp[SPT];
     float smin = INFINITY, smax = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      smp[j] = rd.at((int)(((int64_t)(tid + j * kSelThreads) * n) / kS));
+    for (int j = 0; j < SPT; ++j) {
+      smp[j] = rd.at((int)(((int64_t)(tid + j * NT) * n) / kS));
       smin = fminf(smin, smp[j]);
       smax = fmaxf(smax, smp[j]);
     }
-    smax = block_max_float(smax, red);
-    smin = -block_max_float(-smin, red);
+    smax = block_max_float<NT>(smax, red);
+    smin = -block_max_float<NT>(-smin, red);
     float hi, lo;
     {
       const float pr = (float)k / (float)n;
@@ -531,22 +524,22 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
       const float sscale = (smax > smin) ? 1024.f / (smax - smin) : 0.f;
       auto sbin = [&](float v) { return min(1023, max(0, (int)((v - smin) * sscale))); };
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < SPT; ++j)
         if (isfinite(smp[j])) atomicAdd(sm.hist + sbin(smp[j]), 1u);
       __syncthreads();
-      // thread t scans bins 1023-4t .. 1020-4t (descending)
-      int hb[4], s4 = 0;
+      // thread t scans bins 1023 - SPT t .. 1024 - SPT (t + 1) (descending)
+      int hb[SPT], s4 = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        hb[j] = (int)sm.hist[1023 - (tid * 4 + j)];
+      for (int j = 0; j < SPT; ++j) {
+        hb[j] = (int)sm.hist[1023 - (tid * SPT + j)];
         s4 += hb[j];
       }
       int tot;
-      const int ex = block_scan(s4, &tot, red);
+      const int ex = block_scan<NT>(s4, &tot, red);
       int acc = ex;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int bin = 1023 - (tid * 4 + j);
+      for (int j = 0; j < SPT; ++j) {
+        const int bin = 1023 - (tid * SPT + j);
         // samples ranked [acc, acc + hb[j]) from the top live in this bin
         if (acc <= hi_i && hi_i < acc + hb[j]) red.misc[12] = bin;
         if (acc <= lo_i && lo_i < acc + hb[j]) red.misc[13] = bin;
@@ -559,7 +552,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
       // lo: lower edge of the lo_i-th sample's bin
       hi = (bh >= 1023) ? smax : smin + (float)(bh + 1) / sscale;
       lo = smin + (float)bl / sscale;
-      for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+      for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
       __syncthreads();
     }
     t1 = clock64();
@@ -606,16 +599,16 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
             }
           }
         }
-        sm.bitmap[c * kSelThreads + tid] = word;
+        sm.bitmap[c * NT + tid] = word;
         cg += __popc(word);
       };
       for (int c = 0; c < nfull; ++c) pass_b(c, true);
       if (nfull < nch) pass_b(nfull, false);
-      vmax = block_max_float(vmax, red);
-      vmin = -block_max_float(-vmin, red);
-      bad = block_sum_int(nanacc != nanacc ? 1 : 0, red);
-      cgt = block_sum_int(cg, red);
-      cin = block_sum_int(ci, red);
+      vmax = block_max_float<NT>(vmax, red);
+      vmin = -block_max_float<NT>(-vmin, red);
+      bad = block_sum_int<NT>(nanacc != nanacc ? 1 : 0, red);
+      cgt = block_sum_int<NT>(cg, red);
+      cin = block_sum_int<NT>(ci, red);
       mabs = fmaxf(fabsf(vmax), fabsf(vmin));
       if (bad || !brackets || (cgt < k && k <= cgt + cin) || attempt == 1) break;
       // retry once: the k-th value lies above hi (too many above) or below lo
@@ -626,7 +619,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
         hi = lo;
         lo = vmin;
       }
-      for (int j = tid; j < kBins; j += kSelThreads) sm.hist[j] = 0u;
+      for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
       __syncthreads();
     }
     if (bad && tid == 0) atomicOr(p.flags, 2);
@@ -641,7 +634,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
     if (fast) {
       // ---- C. bin b* holding rank r = k - cgt counted from the top
       const int r = k - cgt;
-      constexpr int PER = kBins / kSelThreads;  // bins per thread, descending order
+      constexpr int PER = kBins / NT;  // bins per thread, descending order
       int hb[PER], s = 0;
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
@@ -649,7 +642,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
         s += hb[j];
       }
       int tot;
-      const int ex = block_scan(s, &tot, red);
+      const int ex = block_scan<NT>(s, &tot, red);
       if (ex < r && r <= ex + s) {
         int acc = ex;
 #pragma unroll
@@ -669,7 +662,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
       int above_bins = 0;
 #pragma unroll
       for (int j = 0; j < PER; ++j) above_bins += (kBins - 1 - (tid * PER + j) > b_hi) ? hb[j] : 0;
-      above_bins = block_sum_int(above_bins, red);
+      above_bins = block_sum_int<NT>(above_bins, red);
 
       // ---- D. second pass (L2): higher bins join the bitmap, candidate bins are collected.
       // bin_of is monotone, so "bin > b_hi" and "bin >= b_lo" are exact value thresholds,
@@ -712,7 +705,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
             cand |= (ok && v >= v_lo && v < v_hi && v <= hi) ? (1u << (u * 4 + cc)) : 0u;
           }
         }
-        if (word) sm.bitmap[c * kSelThreads + tid] |= word;
+        if (word) sm.bitmap[c * NT + tid] |= word;
         int pos = warp_append(__popc(cand), &red.misc[3]);
         while (cand) {
           const int bit = __ffs(cand) - 1;
@@ -739,7 +732,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
       if (fast) {
         // exact T: rank r2 among the members of bin b*
         const int r2 = r - cum_above;
-        for (int j = tid; j < nc; j += kSelThreads) {
+        for (int j = tid; j < nc; j += NT) {
           const float vj = (float)sm.cv[j];
           if (bin_of(vj) != bstar) continue;
           int gt = 0, ge = 0;
@@ -763,7 +756,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
       if (fast) {
         // keep the window in place; candidates above it are selected outright
         int abv = 0;
-        for (int base = 0; base < nc; base += kSelThreads) {
+        for (int base = 0; base < nc; base += NT) {
           const int j = base + tid;
           double v = 0.0;
           int ii = 0;
@@ -784,7 +777,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
             sm.ci[pos] = ii;
           }
         }
-        above_w = cgt + above_bins + block_sum_int(abv, red);
+        above_w = cgt + above_bins + block_sum_int<NT>(abv, red);
         nw = red.misc[5];
         mode = refine ? 2 : 0;
       }
@@ -793,14 +786,14 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
       // ---------------------------------------------------------------- generic path
       mode = 1 + why;
       int c_gt = 0;
-      radix_select_row(rd, n, k, red, &T, &c_gt);
+      radix_select_row<NT>(rd, n, k, red, &T, &c_gt);
       lo_w = refine ? T - tau : T;
       hi_w = refine ? T + tau : T;
-      for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
+      for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
       if (tid == 0) red.misc[5] = 0;
       __syncthreads();
       int abv = 0;
-      for (int base = 0; base < n; base += kSelThreads) {
+      for (int base = 0; base < n; base += NT) {
         const int i = base + tid;
         const float v = (i < n) ? rd.at(i) : -INFINITY;
         const bool in = i < n && v >= lo_w && v <= hi_w;
@@ -814,25 +807,25 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
           sm.ci[pos] = i;
         }
       }
-      above_w = block_sum_int(abv, red);
+      above_w = block_sum_int<NT>(abv, red);
       nw = red.misc[5];
       if (nw > kCandCap) {
         // the window cannot be held: resolve the exact fp32 ties at T by index order
         if (refine && tid == 0) atomicOr(p.flags, 4);
         if (refine) {
-          for (int w = tid; w < nwords; w += kSelThreads) sm.bitmap[w] = 0u;
+          for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
           __syncthreads();
-          for (int base = 0; base < n; base += kSelThreads) {
+          for (int base = 0; base < n; base += NT) {
             const int i = base + tid;
             if (i < n && rd.at(i) > T) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
           }
         }
         int taken = refine ? c_gt : above_w;
-        for (int base = 0; base < n; base += kSelThreads) {
+        for (int base = 0; base < n; base += NT) {
           const int i = base + tid;
           const bool tie = i < n && rd.at(i) == T;
           int tot;
-          const int pre = block_scan(tie ? 1 : 0, &tot, red);
+          const int pre = block_scan<NT>(tie ? 1 : 0, &tot, red);
           if (tie && taken + pre < k) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
           taken += tot;
         }
@@ -848,12 +841,12 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
     __syncthreads();
     if (refine) {
       if (p.block_size > 1)
-        rescore_f64_blocks(p, slot, b, grp, sm.ci, sm.cv, nw, tau_w, sm.keys);
-      else rescore_f64(p, slot, b, grp, sm.ci, sm.cv, nw);
+        rescore_f64_blocks<NT>(p, slot, b, grp, sm.ci, sm.cv, nw, tau_w, sm.keys);
+      else rescore_f64<NT>(p, slot, b, grp, sm.ci, sm.cv, nw);
       __syncthreads();
     }
     const int take = k - above_w;
-    for (int j = tid; j < nw; j += kSelThreads) {
+    for (int j = tid; j < nw; j += NT) {
       const double vj = sm.cv[j];
       const int ij = sm.ci[j];
       int rank = 0;
@@ -869,9 +862,9 @@ __global__ void __launch_bounds__(kSelThreads, 4) topk_select_kernel(const Selec
   // ---- E. index-ordered compaction of the bitmap
   int run = 0;
   for (int c = 0; c < nch; ++c) {
-    const uint32_t w = sm.bitmap[c * kSelThreads + tid];
+    const uint32_t w = sm.bitmap[c * NT + tid];
     int tot;
-    int pos = run + block_scan(__popc(w), &tot, red);
+    int pos = run + block_scan<NT>(__popc(w), &tot, red);
     uint32_t m = w;
     while (m) {
       const int bit = __ffs(m) - 1;

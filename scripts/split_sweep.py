@@ -28,8 +28,10 @@ def worker():
     lib = _abi.lib()
     st = torch.cuda.current_stream().cuda_stream
     res = {}
-    for B in (1, 4, 8):
-        cfg = CONFIGS["cfg2"].with_(batch=B)
+    N = int(os.environ.get("SWEEP_N", CONFIGS["cfg2"].context))
+    K = int(os.environ.get("SWEEP_K", CONFIGS["cfg2"].budget))
+    for B in [int(x) for x in os.environ.get("SWEEP_B", "1,4,8").split(",")]:
+        cfg = CONFIGS["cfg2"].with_(batch=B, context=N, budget=K)
         q, k, v = generate_torch(cfg, "cuda")
         dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
         dec.step(q, cfg.context)
@@ -70,10 +72,11 @@ def worker():
             return e0.elapsed_time(e1) / n * 1e3
 
         row = 2 * ke * cfg.head_dim * 2 * B * cfg.kv_heads  # bytes per REUSE layer
+        fl_bytes = len(fl) * B * cfg.kv_heads * 2 * cfg.context * cfg.head_dim * 2
         t24 = t(lambda: reuse(rl))
         t5 = t(lambda: reuse(rl[:5]))
         tf = t(full)
-        fb = len(fl) * B * cfg.kv_heads * 2 * cfg.context * cfg.head_dim * 2
+        fb = fl_bytes
         res[f"B{B}"] = {"reuse24_us": round(t24, 1), "reuse24_gbs": round(24 * row / t24 / 1e3),
                         "reuse5_us": round(t5, 1), "reuse5_gbs": round(5 * row / t5 / 1e3),
                         "full_us": round(tf, 1), "full_gbs": round(fb / tf / 1e3)}
