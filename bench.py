@@ -60,7 +60,11 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--schedule", default="fused3",
-                    choices=["pipelined", "fused3", "sequential"])
+                    choices=["fused3", "dual", "pipelined", "sequential"],
+                    help="fused3: FULL -> SELECT -> REUSE on one stream (default); dual: "
+                         "selects on a high-priority side stream under the FULL / REUSE "
+                         "launches (measured no faster: the split FULL launch costs what the "
+                         "hidden select latency saves)")
     return ap.parse_args()
 
 
@@ -289,8 +293,9 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     n_valid = cfg.context
 
     def make(kind):
-        if kind == "fused3":
-            return HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1)
+        if kind in ("dual", "fused3"):
+            return HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1,
+                                 dual_stream=kind == "dual")
         return PipelinedDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1,
                                 schedule=kind)
 
@@ -340,7 +345,7 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
 
     # the other schedules, timed the same way (reported, not the headline)
     schedules = {}
-    for kind in ("fused3", "sequential"):
+    for kind in [x for x in ("fused3", "dual", "sequential") if x != a.schedule]:
         d2 = make(kind)
         g2 = capture(d2)
         schedules[kind] = {"ms_per_step": time_replays(g2, d2, max(10, a.steps // 2)),

@@ -21,8 +21,8 @@
  *                           feeding profiling.py:126-145 `build_similarity_matrix`
  *   hylra_block_select,  <- attention.py:287-313 block pooling / topk_blocks and
  *   hylra_decode_step_blocks  engine.py:212-286 `hybrid_decode_blocks` (block mode)
- *   hylra_decode_step_events  <- hylra_decode_step with per-layer completion events (the
- *                           caller overlaps H2D of queries / D2H of outputs with the step)
+ *   hylra_decode_step_ex <- hylra_decode_step with a side stream (selects and REUSE
+ *                           gathers overlap FULL streaming) and per-layer completion events
  *   hylra_append_kv      <- synthetic.py:154-187 (the cache grows one row per step)
  *   hylra_decode_step_offload <- index-guided offload (the offload mirror
  *                           of engine.py:314-368 `cost_model`): REUSE layers' K/V in
@@ -184,20 +184,38 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                       int k_stride, void* ws, size_t ws_bytes, void* stream);
 
 /*
- * hylra_decode_step that lets the caller overlap host transfers with the step (same
- * kernels, same results). layer_events (optional, L entries, NULL entries allowed): event
- * layer_events[l] is recorded on `stream` as soon as out[l] is final — FULL layers right
- * after the FULL launch, REUSE layers after the REUSE launch that covers them; the REUSE
- * layers are launched in chunks that end at each REUSE layer carrying an event, so a
- * caller streams finished layers to the host while later chunks run. reuse_wait_event
- * (optional): the stream waits on it before the first REUSE launch (e.g. the REUSE
- * layers' queries still arriving over the link). Workspace: as hylra_decode_step.
+ * hylra_decode_step with scheduling options (same kernels and results; NULL opt = plain
+ * hylra_decode_step). Every field is optional (NULL):
+ *   side_stream + fork_event, select_event, full_event, join_event: a second stream (best
+ *     created with a higher priority than `stream`) that takes the latency-bound selects
+ *     off the critical path. FULL layers some REUSE layer inherits from (A) are scored
+ *     first, then the others (B), then the REUSE launch, all on `stream`; SELECT(A) runs on
+ *     side_stream under FULL(B) and SELECT(B) under the REUSE launch; `stream` finally
+ *     waits for side_stream. Ignored without REUSE layers, when every FULL layer feeds a
+ *     REUSE layer, or with sinks / recent.
+ *   reuse_wait_event: the REUSE launches wait on it (e.g. REUSE layers' queries arriving).
+ *   layer_events: L entries (NULL allowed); layer_events[l] is recorded as soon as out[l] is
+ *     final — FULL layers right after their FULL launch, REUSE layers after the REUSE
+ *     launch that covers them: REUSE layers are launched in chunks ending at each REUSE
+ *     layer that carries an event, so a caller can stream finished layers out while later
+ *     chunks run.
+ * Workspace: as hylra_decode_step.
  */
-int hylra_decode_step_events(const hylra_geometry* g, const void* q, const void* k,
-                             const void* v, int n_valid, const uint8_t* actions, int budget,
-                             int sel_group, int refine, int sinks, int recent, float* out,
-                             int32_t* idx, int k_stride, void* ws, size_t ws_bytes, void* stream,
-                             void* reuse_wait_event, void* const* layer_events);
+typedef struct hylra_step_options {
+  void* side_stream;
+  void* fork_event;   /* stream -> side: FULL(A) done   */
+  void* select_event; /* side -> stream: SELECT(A) done */
+  void* full_event;   /* stream -> side: FULL(B) done   */
+  void* join_event;   /* side -> stream: SELECT(B) done */
+  void* reuse_wait_event;
+  void* const* layer_events;
+} hylra_step_options;
+
+int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                         int n_valid, const uint8_t* actions, int budget, int sel_group,
+                         int refine, int sinks, int recent, float* out, int32_t* idx,
+                         int k_stride, void* ws, size_t ws_bytes, void* stream,
+                         const hylra_step_options* opt);
 
 /*
  * hylra_decode_step with the cache split by action (index-guided offload). k_full/v_full:

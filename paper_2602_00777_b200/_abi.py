@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = (
     "hylra_decode_step_workspace_bytes",
     "hylra_decode_step",
     "hylra_decode_step_offload",
-    "hylra_decode_step_events",
+    "hylra_decode_step_ex",
     "hylra_append_kv",
     "hylra_overlap_counts",
     "hylra_augment_selection",
@@ -74,6 +74,20 @@ class Geometry(ctypes.Structure):
         ("kv_stride_head", ctypes.c_int64),
         ("out_stride_layer", ctypes.c_int64),
         ("out_stride_batch", ctypes.c_int64),
+    ]
+
+
+class StepOptions(ctypes.Structure):
+    """Mirror of `hylra_step_options` (include/hylra.h)."""
+
+    _fields_ = [
+        ("side_stream", ctypes.c_void_p),
+        ("fork_event", ctypes.c_void_p),
+        ("select_event", ctypes.c_void_p),
+        ("full_event", ctypes.c_void_p),
+        ("join_event", ctypes.c_void_p),
+        ("reuse_wait_event", ctypes.c_void_p),
+        ("layer_events", ctypes.c_void_p),
     ]
 
 
@@ -125,9 +139,9 @@ def lib() -> ctypes.CDLL:
         l.hylra_decode_step_offload.restype = i32
         l.hylra_decode_step_offload.argtypes = [gp, vp, vp, vp, vp, vp, i32, vp, i32, i32, i32,
                                                 i32, i32, vp, vp, i32, vp, sz, vp]
-        l.hylra_decode_step_events.restype = i32
-        l.hylra_decode_step_events.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, i32,
-                                               vp, vp, i32, vp, sz, vp, vp, vp]
+        l.hylra_decode_step_ex.restype = i32
+        l.hylra_decode_step_ex.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, i32,
+                                           vp, vp, i32, vp, sz, vp, ctypes.POINTER(StepOptions)]
         l.hylra_append_kv.restype = i32
         l.hylra_append_kv.argtypes = [gp, vp, vp, vp, vp, i32, i32, vp, vp]
         l.hylra_augment_selection.restype = i32

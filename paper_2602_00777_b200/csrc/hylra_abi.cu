@@ -374,7 +374,7 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
                   int budget, int sel_group, const void* q, const void* k,
                   const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
                   int* flags, cudaStream_t st, const BlockRows& br = BlockRows(),
-                  const int32_t* kv_layer_ids = nullptr) {
+                  const int32_t* kv_layer_ids = nullptr, const int32_t* out_slots = nullptr) {
   if (int e = check_geometry(g)) return e;
   if (budget < 1) return fail(HYLRA_ERR_INVALID_INPUT, "budget must be >= 1, got %d", budget);
   if (n_slots < 1 || n_slots > kMaxSlots)
@@ -415,6 +415,7 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
       return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", l);
     p.layers[i] = l;
     p.kv_layers[i] = kv_layer_ids ? kv_layer_ids[i] : l;
+    p.out_slot[i] = out_slots ? out_slots[i] : i;
   }
   dim3 grid(p.n_groups, g->batch, n_slots);
   const int nt = select_threads(p.n_groups * g->batch * n_slots);
@@ -552,7 +553,10 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   // FULL and REUSE get disjoint attention workspaces: each kernel's split-K counters must
   // start at zero, and the other launch's partial buffers would otherwise overlap them.
   s->off_attn = off;
-  s->attn_bytes = attn_layout(g, (int)nf, n_valid, false).total;
+  // FULL layers may be launched in two groups (hylra_decode_step_ex with a side stream)
+  s->attn_bytes = 0;
+  for (int n = 1; n <= (int)nf; ++n)
+    s->attn_bytes = std::max(s->attn_bytes, attn_layout(g, n, n_valid, false).total);
   s->off_attn_r = align_up(s->off_attn + s->attn_bytes, 256);
   // REUSE layers may be launched in chunks (hylra_decode_step_events): size for the
   // largest workspace any chunk length needs (fewer pairs can mean more splits).
@@ -588,11 +592,24 @@ struct SplitKv {
   const void *kf, *vf, *kr, *vr;
 };
 
+// Options of hylra_decode_step_ex (all optional; see include/hylra.h).
+struct StepOpts {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, select = nullptr, full = nullptr, join = nullptr;
+  cudaEvent_t reuse_wait = nullptr;
+  void* const* layer_events = nullptr;
+};
+
+int record(void* const* evs, int l, cudaStream_t st) {
+  if (!evs || !evs[l]) return HYLRA_OK;
+  return cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(evs[l]), st), "event record");
+}
+
 int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, const void* v,
                      int n_valid, const uint8_t* actions, int budget, int sel_group, int refine,
                      int sinks, int recent, float* out, int32_t* idx, int k_stride, void* ws,
                      size_t ws_bytes, void* stream, const SplitKv* split,
-                     void* reuse_wait = nullptr, void* const* layer_events = nullptr) {
+                     const StepOpts& o = StepOpts()) {
   StepLayout s;
   if (int e = step_layout(g, actions, n_valid, budget, sel_group, &s, 1, sinks, recent)) return e;
   if (!ws || ws_bytes < s.total)
@@ -606,27 +623,58 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   void* aws = w + s.off_attn;
   const int nf = (int)s.full_ids.size();
   const int nr = (int)s.reuse_ids.size();
-  std::vector<int32_t> fkv(nf), rkv(nr);  // compact KV layer index of each slot
-  for (int i = 0; i < nf; ++i) fkv[i] = i;
-  for (int i = 0; i < nr; ++i) rkv[i] = i;
   const void* kf = split ? split->kf : k;
   const void* vf = split ? split->vf : v;
-  if (int e = launch_attention(g, false, q, kf, vf, n_valid, n_valid, nf, s.full_ids.data(),
-                               nullptr, nullptr, nullptr, 0, 1, out, scores, aws, s.attn_bytes,
-                               flags, st, split ? fkv.data() : nullptr, nf))
-    return e;
-  // FULL layers' outputs are final once the FULL launch retires
-  if (layer_events)
-    for (int l : s.full_ids)
-      if (layer_events[l])
-        if (int e = cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l]), st),
-                               "event record"))
-          return e;
-  if (int e = launch_select(g, scores, nf, n_valid, budget, sel_group, refine ? q : nullptr,
-                            refine ? kf : nullptr, s.full_ids.data(), idx, k_stride, nullptr,
-                            flags, st, BlockRows(), split ? fkv.data() : nullptr))
-    return e;
-  if (!s.reuse_ids.empty()) {
+  const size_t score_slot = (size_t)g->batch * g->kv_heads * scores_row_stride(g);
+
+  // FULL layer groups: A = the FULL layers some REUSE layer inherits from (the selection the
+  // REUSE launch waits for), B = the others. With a side stream the selects leave the
+  // critical path:  stream: FULL(A) -> FULL(B) -> REUSE;  side: SELECT(A) under FULL(B),
+  // SELECT(B) under REUSE. The selects are latency-bound (one CTA per row, ~30 us at any
+  // row count), the FULL and REUSE launches HBM-bound; the side stream has the higher
+  // priority so select CTAs are dispatched ahead of queued streaming CTAs.
+  std::vector<int32_t> a_ids, a_slot, a_kv, b_ids, b_slot, b_kv;
+  for (int i = 0; i < nf; ++i) {
+    const int l = s.full_ids[i];
+    const bool feeds = l + 1 < g->num_layers && actions[l + 1] == 0;
+    (feeds ? a_ids : b_ids).push_back(l);
+    (feeds ? a_slot : b_slot).push_back(i);
+    (feeds ? a_kv : b_kv).push_back(i);  // compact KV index (split caches) = FULL slot
+  }
+  const bool dual = o.side && !a_ids.empty() && !b_ids.empty() && !s.aug_stride;
+  if (o.side && !(o.fork && o.select && o.full && o.join))
+    return fail(HYLRA_ERR_CONFIGURATION, "a side stream needs its four events");
+  // groups of FULL layers: one launch (all FULL layers) or two (A then B)
+  struct Group {
+    const std::vector<int32_t>* ids;
+    const std::vector<int32_t>* slots;
+    const std::vector<int32_t>* kv;
+    int score_base;
+  };
+  std::vector<int32_t> all_slot(nf), all_kv(nf);
+  for (int i = 0; i < nf; ++i) all_slot[i] = all_kv[i] = i;
+  const Group g_all{&s.full_ids, &all_slot, &all_kv, 0};
+  const Group g_a{&a_ids, &a_slot, &a_kv, 0};
+  const Group g_b{&b_ids, &b_slot, &b_kv, (int)a_ids.size()};
+  auto full = [&](const Group& gr, cudaStream_t sx) -> int {
+    const int n = (int)gr.ids->size();
+    if (int e = launch_attention(g, false, q, kf, vf, n_valid, n_valid, n, gr.ids->data(),
+                                 nullptr, nullptr, nullptr, 0, 1, out,
+                                 scores + gr.score_base * score_slot, aws, s.attn_bytes, flags, sx,
+                                 split ? gr.kv->data() : nullptr, nf))
+      return e;
+    for (int l : *gr.ids)
+      if (int e = record(o.layer_events, l, sx)) return e;
+    return HYLRA_OK;
+  };
+  auto select = [&](const Group& gr, cudaStream_t sx) -> int {
+    return launch_select(g, scores + gr.score_base * score_slot, (int)gr.ids->size(), n_valid,
+                         budget, sel_group, refine ? q : nullptr, refine ? kf : nullptr,
+                         gr.ids->data(), idx, k_stride, nullptr, flags, sx, BlockRows(),
+                         split ? gr.kv->data() : nullptr, gr.slots->data());
+  };
+  auto reuse = [&](cudaStream_t sx) -> int {
+    if (s.reuse_ids.empty()) return HYLRA_OK;
     const int32_t* ridx = idx;
     const int32_t* rcnt = nullptr;
     int rstride = k_stride, rk = s.k_eff;
@@ -634,7 +682,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
       int32_t* aug = reinterpret_cast<int32_t*>(w + s.off_aug);
       int32_t* acnt = reinterpret_cast<int32_t*>(w + s.off_aug_counts);
       const int rows = nf * g->batch * s.n_groups;
-      augment_kernel<<<rows, kPoolThreads, 0, st>>>(idx, k_stride, s.k_eff, n_valid, sinks,
+      augment_kernel<<<rows, kPoolThreads, 0, sx>>>(idx, k_stride, s.k_eff, n_valid, sinks,
                                                     recent, aug, s.aug_stride, acnt);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       if (int e = cuda_check(cudaGetLastError(), "augment launch")) return e;
@@ -642,29 +690,56 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
       rcnt = acnt;
       rstride = rk = s.aug_stride;
     }
-    if (reuse_wait)
-      if (int e = cuda_check(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(reuse_wait), 0),
-                             "stream wait event"))
+    if (o.reuse_wait)
+      if (int e = cuda_check(cudaStreamWaitEvent(sx, o.reuse_wait, 0), "stream wait event"))
         return e;
+    std::vector<int32_t> rkv(nr);  // compact KV layer index of each REUSE slot
+    for (int i = 0; i < nr; ++i) rkv[i] = i;
     // one launch, or one per chunk of REUSE layers ending at a layer that carries an event
     int c0 = 0;
     for (int i = 0; i < nr; ++i) {
       const int l = s.reuse_ids[i];
-      cudaEvent_t ev = layer_events ? static_cast<cudaEvent_t>(layer_events[l]) : nullptr;
-      if (!(ev || i == nr - 1)) continue;
+      const bool mark = o.layer_events && o.layer_events[l];
+      if (!(mark || i == nr - 1)) continue;
       const int n = i + 1 - c0;
       if (int e = launch_attention(g, true, q, split ? split->kr : k, split ? split->vr : v,
                                    n_valid, rk, n, s.reuse_ids.data() + c0,
                                    s.reuse_src.data() + c0, ridx, rcnt, rstride, sel_group, out,
-                                   nullptr, w + s.off_attn_r, s.attn_bytes_r, flags, st,
+                                   nullptr, w + s.off_attn_r, s.attn_bytes_r, flags, sx,
                                    split ? rkv.data() + c0 : nullptr, nr))
         return e;
-      if (ev)
-        if (int e = cuda_check(cudaEventRecord(ev, st), "event record")) return e;
+      if (int e = record(o.layer_events, l, sx)) return e;
       c0 = i + 1;
     }
+    return HYLRA_OK;
+  };
+
+  if (!dual) {
+    if (int e = full(g_all, st)) return e;
+    if (int e = select(g_all, st)) return e;
+    return reuse(st);
   }
-  return HYLRA_OK;
+  auto rec = [](cudaEvent_t ev, cudaStream_t sx) {
+    return cuda_check(cudaEventRecord(ev, sx), "event record");
+  };
+  auto wait = [](cudaStream_t sx, cudaEvent_t ev) {
+    return cuda_check(cudaStreamWaitEvent(sx, ev, 0), "stream wait event");
+  };
+  // side: SELECT(A) once FULL(A) is done, SELECT(B) once FULL(B) is done
+  if (int e = full(g_a, st)) return e;
+  if (int e = rec(o.fork, st)) return e;
+  if (int e = wait(o.side, o.fork)) return e;
+  if (int e = select(g_a, o.side)) return e;
+  if (int e = rec(o.select, o.side)) return e;
+  if (int e = full(g_b, st)) return e;
+  if (int e = rec(o.full, st)) return e;
+  if (int e = wait(o.side, o.full)) return e;
+  if (int e = select(g_b, o.side)) return e;
+  if (int e = rec(o.join, o.side)) return e;
+  // stream: REUSE once SELECT(A) is done (long before FULL(B) ends), then join
+  if (int e = wait(st, o.select)) return e;
+  if (int e = reuse(st)) return e;
+  return wait(st, o.join);
 }
 
 }  // namespace
@@ -751,14 +826,23 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
                           out, idx, k_stride, ws, ws_bytes, stream, nullptr);
 }
 
-int hylra_decode_step_events(const hylra_geometry* g, const void* q, const void* k,
-                             const void* v, int n_valid, const uint8_t* actions, int budget,
-                             int sel_group, int refine, int sinks, int recent, float* out,
-                             int32_t* idx, int k_stride, void* ws, size_t ws_bytes, void* stream,
-                             void* reuse_wait_event, void* const* layer_events) {
+int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                         int n_valid, const uint8_t* actions, int budget, int sel_group,
+                         int refine, int sinks, int recent, float* out, int32_t* idx,
+                         int k_stride, void* ws, size_t ws_bytes, void* stream,
+                         const hylra_step_options* opt) {
+  StepOpts o;
+  if (opt) {
+    o.side = static_cast<cudaStream_t>(opt->side_stream);
+    o.fork = static_cast<cudaEvent_t>(opt->fork_event);
+    o.select = static_cast<cudaEvent_t>(opt->select_event);
+    o.full = static_cast<cudaEvent_t>(opt->full_event);
+    o.join = static_cast<cudaEvent_t>(opt->join_event);
+    o.reuse_wait = static_cast<cudaEvent_t>(opt->reuse_wait_event);
+    o.layer_events = opt->layer_events;
+  }
   return decode_step_impl(g, q, k, v, n_valid, actions, budget, sel_group, refine, sinks, recent,
-                          out, idx, k_stride, ws, ws_bytes, stream, nullptr, reuse_wait_event,
-                          layer_events);
+                          out, idx, k_stride, ws, ws_bytes, stream, nullptr, o);
 }
 
 int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void* k_full,

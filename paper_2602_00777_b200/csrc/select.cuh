@@ -59,6 +59,7 @@ struct SelectParams {
   int tok_row_stride;
   int layers[kMaxSlots];     // q layer of each slot
   int kv_layers[kMaxSlots];  // K layer of each slot (refinement)
+  int out_slot[kMaxSlots];   // idx / info slot each score slot's selection is written to
 };
 
 // Dynamic shared memory: the bitmap sized for the row, then fixed arrays.
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
   const int n = p.n_valid;
   const int k = p.k_eff;
   const int n4 = (n + 3) >> 2;
-  const int row_id = (slot * p.B + b) * p.n_groups + grp;
+  const int row_id = (p.out_slot[slot] * p.B + b) * p.n_groups + grp;
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
   int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
   const SelSmem sm = carve<NT>(sraw, n);

@@ -18,6 +18,8 @@ recent FULL layer's selection of the same step (engine.py:173,176,185-194).
 """
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -71,7 +73,7 @@ class HybridDecoder:
 
     def __init__(self, policy, k_cache: torch.Tensor, v_cache: torch.Tensor, budget: int, *,
                  q_heads: int, sel_group: int = 1, refine: bool = True, block_size: int = 1,
-                 include_sinks: int = 0, include_recent: int = 0):
+                 include_sinks: int = 0, include_recent: int = 0, dual_stream: bool = False):
         self.actions = _actions_of(policy)
         if len(self.actions) != k_cache.shape[0]:
             raise ConfigurationError(
@@ -110,8 +112,21 @@ class HybridDecoder:
         self._acts = _abi.uint8_array(1 if a is Action.FULL else 0 for a in self.actions)
         self.ws = torch.zeros(256, dtype=torch.uint8, device=k_cache.device)
         has_reuse = len(self.full_layers) < L
+        # dual stream (token mode): the FULL layers that feed REUSE layers are scored first,
+        # then the other FULL layers, then the REUSE launch, on the caller's stream; the
+        # selects run on a high-priority side stream under the next streaming launch
+        # (hylra_decode_step_ex)
+        feeds = [l for l in self.full_layers if l + 1 < L and self.actions[l + 1] is Action.REUSE]
+        self.dual = (bool(dual_stream) and block_size == 1 and not (include_sinks or include_recent)
+                     and 0 < len(feeds) < len(self.full_layers))
         self.kernels_per_step = ((2 + has_reuse + (has_reuse and bool(include_sinks or include_recent)))
-                                 if block_size == 1 else (3 + 2 * has_reuse))
+                                 if block_size == 1 else (3 + 2 * has_reuse)) + 2 * self.dual
+        if self.dual:
+            # high priority: select CTAs are dispatched ahead of the queued FULL / REUSE CTAs
+            self._side = torch.cuda.Stream(device=k_cache.device, priority=-8)
+            self._events = [torch.cuda.Event() for _ in range(4)]
+            for e in self._events:  # torch creates events lazily
+                e.record(torch.cuda.current_stream(k_cache.device))
 
     def _geometry(self, q):
         return geometry(q, self.k, self.v, self.out)
@@ -126,7 +141,7 @@ class HybridDecoder:
         """Enqueue one decode step. layer_events (optional, L torch.cuda.Event or None):
         event l is recorded once out[l] is final, REUSE layers being launched in chunks
         that end at the evented layers; reuse_wait (optional event): the REUSE launches
-        wait on it (hylra_decode_step_events). Token mode only. out (optional): fp32
+        wait on it (hylra_decode_step_ex). Token mode only. out (optional): fp32
         [L, B, Hq, d] destination instead of the decoder's own buffer — device memory or
         pinned host memory, which the kernels then write across the link directly."""
         if out is not None:
@@ -144,25 +159,36 @@ class HybridDecoder:
         n_valid = g.capacity if n_valid is None else int(n_valid)
         lib = _abi.lib()
         st = torch.cuda.current_stream(self.k.device).cuda_stream
-        if layer_events is not None or reuse_wait is not None:
-            if self.block_size > 1:
-                raise ConfigurationError("per-layer events apply to token selection only")
-            evs = list(layer_events) if layer_events is not None else [None] * len(self.actions)
-            if len(evs) != len(self.actions):
-                raise ConfigurationError(f"{len(evs)} layer events for {len(self.actions)} layers")
+        if self.block_size == 1:
+            if layer_events is not None and len(layer_events) != len(self.actions):
+                raise ConfigurationError(
+                    f"{len(layer_events)} layer events for {len(self.actions)} layers")
             need = int(lib.hylra_decode_step_workspace_bytes(
                 g, self._acts, n_valid, self.budget, self.sel_group, self.sinks, self.recent))
             if self.ws.numel() < need:
                 self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
-            _abi.check(lib.hylra_decode_step_events(
+            opt = _abi.StepOptions()
+            if self.dual:
+                opt.side_stream = self._side.cuda_stream
+                (opt.fork_event, opt.select_event, opt.full_event,
+                 opt.join_event) = (e.cuda_event for e in self._events)
+            if reuse_wait is not None:
+                opt.reuse_wait_event = reuse_wait.cuda_event
+            evs = None
+            if layer_events is not None:
+                evs = _abi.pointer_array(e.cuda_event if e is not None else None
+                                         for e in layer_events)
+                opt.layer_events = ctypes.cast(evs, ctypes.c_void_p)
+            _abi.check(lib.hylra_decode_step_ex(
                 g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
                 self.budget, self.sel_group, int(self.refine), self.sinks, self.recent,
                 self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(),
-                self.ws.numel(), st, reuse_wait.cuda_event if reuse_wait is not None else None,
-                _abi.pointer_array(e.cuda_event if e is not None else None for e in evs)))
+                self.ws.numel(), st, ctypes.byref(opt)))
             k_eff = min(self.budget, n_valid)
             return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer,
                               self.full_layers)
+        if layer_events is not None or reuse_wait is not None:
+            raise ConfigurationError("per-layer events apply to token selection only")
         if self.block_size > 1:
             need = int(lib.hylra_decode_step_blocks_workspace_bytes(
                 g, self._acts, n_valid, self.budget, self.block_size, self.sel_group))
@@ -176,22 +202,6 @@ class HybridDecoder:
             bb = min(self.budget, -(-n_valid // self.block_size))
             return StepResult(self.out, self.idx[..., :bb], self.slot_of_layer,
                               self.full_layers)
-        need = int(lib.hylra_decode_step_workspace_bytes(
-            g, self._acts, n_valid, self.budget, self.sel_group, self.sinks, self.recent))
-        if need == 0:
-            _abi.check(lib.hylra_decode_step(
-                g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
-                self.budget, self.sel_group, int(self.refine), self.sinks, self.recent,
-                self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, None, 0, 0))
-        if self.ws.numel() < need:
-            self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
-        _abi.check(lib.hylra_decode_step(
-            g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
-            self.budget, self.sel_group, int(self.refine), self.sinks, self.recent,
-            self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(),
-            self.ws.numel(), st))
-        k_eff = min(self.budget, n_valid)
-        return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
 
     def append(self, k_rows: torch.Tensor, v_rows: torch.Tensor, pos: int, layers=None) -> None:
         """Write one step's new K/V rows [L, B, Hkv, d] (device or pinned host tensors, the
@@ -264,7 +274,7 @@ class OffloadDecoder(HybridDecoder):
         full_view = k_full[:1].expand((len(actions),) + tuple(k_full.shape[1:]))
         super().__init__(actions, full_view, full_view, budget, q_heads=q_heads,
                          sel_group=sel_group, refine=refine, include_sinks=include_sinks,
-                         include_recent=include_recent)
+                         include_recent=include_recent, dual_stream=False)
         self.k_full, self.v_full, self.k_reuse, self.v_reuse = k_full, v_full, k_reuse, v_reuse
         self.reuse_layers = tuple(l for l, a in enumerate(actions) if a is Action.REUSE)
 
@@ -325,7 +335,7 @@ class PipelinedDecoder(HybridDecoder):
     def __init__(self, policy, k_cache, v_cache, budget, *, q_heads, sel_group=1,
                  refine=True, schedule="pipelined"):
         super().__init__(policy, k_cache, v_cache, budget, q_heads=q_heads,
-                         sel_group=sel_group, refine=refine)
+                         sel_group=sel_group, refine=refine, dual_stream=False)
         if schedule not in ("pipelined", "sequential"):
             raise ConfigurationError(f"unknown schedule {schedule!r}")
         self.schedule = schedule

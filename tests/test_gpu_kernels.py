@@ -285,6 +285,43 @@ def test_decode_loop_host_io_graph(overlap):
         assert torch.equal(out, ref.outputs.cpu())
 
 
+@pytest.mark.parametrize("actions", [
+    ("full", "reuse", "full", "full", "reuse", "reuse", "full", "reuse", "full", "full"),
+    ("full", "full", "reuse", "reuse"),
+])
+def test_dual_stream_step_matches_single_stream(actions):
+    """hylra_decode_step_ex with a side stream: FULL layers feeding REUSE layers first, their
+    SELECT + REUSE on the side stream under the other FULL layers. Same selections; outputs
+    within split-K rounding of the one-stream step; also under CUDA-graph capture."""
+    L = len(actions)
+    B, Hq, Hkv, d, cap, budget = 2, 16, 4, 128, 4096, 256
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=31, planted=64)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq).step(q, cap)
+    ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, dual_stream=True)
+    assert dec.dual
+    res = dec.step(q, cap)
+    torch.cuda.synchronize()
+    dec.check_flags()
+    assert torch.equal(res.selections, ref_idx)
+    r = ref_out.double().cpu().numpy()
+    assert max_head_err(res.outputs.double().cpu().numpy(), r) < 4e-3
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dec.step(q, cap)
+    torch.cuda.current_stream().wait_stream(s)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        dec.step(q, cap)
+    dec.out.zero_()
+    dec.idx.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(dec.idx[..., :budget], ref_idx)
+    assert max_head_err(dec.out.double().cpu().numpy(), r) < 4e-3
+
+
 def test_step_layer_events_chunks_reuse():
     """hylra_decode_step_events: per-layer completion events split the REUSE launch into
     chunks; selections identical, outputs within split-K rounding; events fire."""
