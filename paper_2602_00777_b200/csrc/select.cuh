@@ -66,8 +66,15 @@ struct SelectParams {
 __host__ __device__ constexpr size_t sel_bitmap_bytes(int n, int nt) {
   return (size_t)((n + nt * 32 - 1) / (nt * 32)) * (nt * 32) / 8;
 }
+// Band list: indices of the scores inside the bracket [lo, hi], collected by pass B so the
+// second pass reads only them (4096 entries per 256 threads; it shares the small-row keys
+// region, which the large-row path does not otherwise use before the window step).
+__host__ __device__ constexpr int sel_band_cap(int nt) { return 16 * nt; }
+__host__ __device__ constexpr size_t sel_keys_bytes(int nt) {
+  return (size_t)(kSmallN * 8 > sel_band_cap(nt) * 4 ? kSmallN * 8 : sel_band_cap(nt) * 4);
+}
 __host__ __device__ constexpr size_t sel_fixed_bytes(int nt) {
-  return kBins * 4 + kCandCap * (8 + 4) + nt * 4 + kSmallN * 8;
+  return kBins * 4 + kCandCap * (8 + 4) + nt * 4 + sel_keys_bytes(nt);
 }
 __host__ __device__ constexpr size_t sel_smem_bytes(int n, int nt) {
   return sel_bitmap_bytes(n, nt) + sel_fixed_bytes(nt);
@@ -80,6 +87,7 @@ struct SelSmem {
   int* ci;           // [kCandCap] window token indices
   float* xchg;       // [NT]
   uint64_t* keys;    // [kSmallN] small-row sort keys
+  int* band;         // [sel_band_cap(NT)] pass-B band list (aliases keys)
 };
 
 template <int NT>
@@ -92,6 +100,7 @@ __device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
   m.ci = reinterpret_cast<int*>(base + bb + kBins * 4 + kCandCap * 8);
   m.xchg = reinterpret_cast<float*>(m.ci + kCandCap);
   m.keys = reinterpret_cast<uint64_t*>(m.xchg + NT);
+  m.band = reinterpret_cast<int*>(m.keys);
   return m;
 }
 
@@ -501,11 +510,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
     mode = 3;
     t1 = t2 = t3 = clock64();
   } else {
-    // ---- A. brackets [lo, hi] around the k-th rank from 1024 strided samples (1024 / NT
-    //         per thread): their quantiles are read off a 1024-bin histogram over
-    //         [sample min, sample max] (no sort); edges are widened outward so the bracket
-    //         stays conservative
-    constexpr int kS = 1024, SPT = kS / NT;
+    // ---- A. brackets [lo, hi] around the k-th rank from 4 NT strided samples: their
+    //         quantiles are read off a 1024-bin histogram over [sample min, sample max]
+    //         (no sort); edges are widened outward so the bracket stays conservative.
+    //         Wider CTAs take more samples: a narrower band for pass D.
+    constexpr int SPT = 4, kS = SPT * NT, BPT = 1024 / NT;
     float smp[SPT];
     float smin = INFINITY, smax = -INFINITY;
 #pragma unroll
@@ -528,19 +537,19 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
       for (int j = 0; j < SPT; ++j)
         if (isfinite(smp[j])) atomicAdd(sm.hist + sbin(smp[j]), 1u);
       __syncthreads();
-      // thread t scans bins 1023 - SPT t .. 1024 - SPT (t + 1) (descending)
-      int hb[SPT], s4 = 0;
+      // thread t scans sample bins 1023 - BPT t .. 1024 - BPT (t + 1) (descending)
+      int hb[BPT], s4 = 0;
 #pragma unroll
-      for (int j = 0; j < SPT; ++j) {
-        hb[j] = (int)sm.hist[1023 - (tid * SPT + j)];
+      for (int j = 0; j < BPT; ++j) {
+        hb[j] = (int)sm.hist[1023 - (tid * BPT + j)];
         s4 += hb[j];
       }
       int tot;
       const int ex = block_scan<NT>(s4, &tot, red);
       int acc = ex;
 #pragma unroll
-      for (int j = 0; j < SPT; ++j) {
-        const int bin = 1023 - (tid * SPT + j);
+      for (int j = 0; j < BPT; ++j) {
+        const int bin = 1023 - (tid * BPT + j);
         // samples ranked [acc, acc + hb[j]) from the top live in this bin
         if (acc <= hi_i && hi_i < acc + hb[j]) red.misc[12] = bin;
         if (acc <= lo_i && lo_i < acc + hb[j]) red.misc[13] = bin;
@@ -576,13 +585,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
       const float blo = lo, bhi = hi, bsc = scale;
       float nanacc = 0.f;
       int cg = 0, ci = 0;
+      if (tid == 0) red.misc[10] = 0;  // band list length
+      __syncthreads();
       auto pass_b = [&](int c, bool full) {
         const int w4 = (c * kChunk + tid * 32) >> 2;
         float4 vv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
-        uint32_t word = 0u;
+        uint32_t word = 0u, band = 0u;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
 #pragma unroll
@@ -595,13 +606,23 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
               word |= (v > bhi) ? (1u << (u * 4 + cc)) : 0u;
               if (brackets && v >= blo && v <= bhi) {
                 atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
-                ++ci;
+                band |= 1u << (u * 4 + cc);
               }
             }
           }
         }
         sm.bitmap[c * NT + tid] = word;
         cg += __popc(word);
+        ci += __popc(band);
+        // band members' indices -> the band list (dropped past its capacity: pass D then
+        // falls back to re-reading the row)
+        int pos = warp_append(__popc(band), &red.misc[10]);
+        while (band) {
+          const int bit = __ffs(band) - 1;
+          band &= band - 1;
+          if (pos < sel_band_cap(NT)) sm.band[pos] = 4 * w4 + bit;
+          ++pos;
+        }
       };
       for (int c = 0; c < nfull; ++c) pass_b(c, true);
       if (nfull < nch) pass_b(nfull, false);
@@ -724,8 +745,26 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
           ++pos;
         }
       };
-      for (int c = 0; c < nfull; ++c) pass_d(c, true);
-      if (nfull < nch) pass_d(nfull, false);
+      const int nband = red.misc[10];
+      if (nband <= sel_band_cap(NT)) {
+        // the band list holds every score in [lo, hi]: only those are re-read
+        for (int base = 0; base < nband; base += NT) {
+          const int j = base + tid;
+          const int i = j < nband ? sm.band[j] : 0;
+          const float v = j < nband ? rd.at(i) : -INFINITY;
+          const bool in = j < nband;
+          if (in && v >= v_hi) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+          const bool cand = in && v >= v_lo && v < v_hi;
+          int pos = warp_append(cand ? 1 : 0, &red.misc[3]);
+          if (cand && pos < kCandCap) {
+            sm.cv[pos] = (double)v;
+            sm.ci[pos] = i;
+          }
+        }
+      } else {
+        for (int c = 0; c < nfull; ++c) pass_d(c, true);
+        if (nfull < nch) pass_d(nfull, false);
+      }
       __syncthreads();
       const int nc = red.misc[3];
       fast = nc >= 1 && nc <= kCandCap;
