@@ -47,8 +47,8 @@ def geometry(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
             f"query shape {tuple(q.shape)} does not match cache shape {tuple(k.shape)}")
     if q.dtype != k.dtype or k.dtype != v.dtype or q.dtype not in _DTYPES:
         raise ConfigurationError("q, k, v must share dtype bfloat16 or float32")
-    if not (q.is_cuda and k.is_cuda and v.is_cuda):
-        raise ConfigurationError("inputs must be CUDA tensors")
+    if not (k.is_cuda and v.is_cuda and (q.is_cuda or q.is_pinned())):
+        raise ConfigurationError("k / v must be CUDA tensors, q a CUDA or pinned host tensor")
     if q.stride(3) != 1 or q.stride(2) != d or k.stride(4) != 1 or k.stride(3) != d:
         raise ConfigurationError("rows must be d-contiguous (q heads and KV rows packed)")
     g = _abi.Geometry()

@@ -58,8 +58,13 @@ def ev_time(g, n=30):
     return round(e0.elapsed_time(e1) / n * 1e3, 1)
 
 
+k_rows = kv_host[0]
+v_rows = kv_host[1]
 parts = {
     "step": lambda: dec.step(q_dev, pos + 1),
+    "step_out_pinned": lambda: dec.step(q_dev, pos + 1, out=out_host),
+    "append_zero_copy": lambda: dec.append(k_rows, v_rows, pos),
+    "step_q_out_pinned": lambda: dec.step(q_host, pos + 1, out=out_host),
     "h2d": lambda: (q_dev.copy_(q_host, non_blocking=True), kv_dev.copy_(kv_host, non_blocking=True)),
     "append": lambda: (dec.k[:, :, :, pos].copy_(kv_dev[0]), dec.v[:, :, :, pos].copy_(kv_dev[1])),
     "d2h": lambda: out_host.copy_(dec.out, non_blocking=True),
@@ -70,6 +75,8 @@ for name, fn in parts.items():
 combos = {
     "h2d+step": ("h2d", "step"), "append+step": ("append", "step"), "step+d2h": ("step", "d2h"),
     "all": ("h2d", "append", "step", "d2h"),
+    "zc_all": ("h2d", "append_zero_copy", "step_out_pinned"),
+    "zc_all_q": ("append_zero_copy", "step_q_out_pinned"),
 }
 for name, names in combos.items():
     res[name] = ev_time(graph_of(lambda names=names: [parts[n]() for n in names]))
