@@ -21,6 +21,14 @@ namespace hylra {
 constexpr int kMaxSlots = 64;   // layer slots per launch
 constexpr int kTileRows = 64;   // rows per pipeline stage
 constexpr int kConsumerWarps = 4;
+// REUSE producer warps: the gather's cp.async rows of a stage are split between them
+// (HYLRA_GATHER_PRODUCERS in {1, 2, 4} at build time; FULL always has one TMA warp).
+#ifndef HYLRA_GATHER_PRODUCERS
+#define HYLRA_GATHER_PRODUCERS 2
+#endif
+constexpr int kGatherProducers = HYLRA_GATHER_PRODUCERS;
+template <bool GATHER>
+constexpr int attn_threads() { return 32 * (kConsumerWarps + (GATHER ? kGatherProducers : 1)); }
 constexpr int kMaxG = 16;
 constexpr int kIdxStage = 2048;  // REUSE: indices staged in shared memory per CTA
 
@@ -188,7 +196,7 @@ __device__ __forceinline__ uint32_t swz_addr(uint32_t tile_base, int r, int chun
 }
 
 template <int D, bool GATHER, bool GBIG, int STAGES>
-__global__ void __launch_bounds__(160, 2)
+__global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     attn_mma_kernel(const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv, const AttnParams p) {
   using SM = MmaSmem<D>;
@@ -219,14 +227,14 @@ __global__ void __launch_bounds__(160, 2)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar + s, GATHER ? 32 : 1);
+      mbar_init(full_bar + s, GATHER ? 32 * kGatherProducers : 1);
       mbar_init(empty_bar + s, kConsumerWarps);
     }
     mbar_fence_init();
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
+  if (warp >= kConsumerWarps) {
     // ------------------------------------------------------------- producer warp
     if constexpr (!GATHER) {
       if (lane == 0) {
@@ -325,8 +333,12 @@ __global__ void __launch_bounds__(160, 2)
         const uint32_t kt = smem_u32(smem + s * SM::kStageBytes);
         const uint32_t vt = kt + SM::kTileBytes;
         const int pos0 = (t_begin + i) * kTileRows;
+        // producer warp pw copies rows [pw, pw + 1) * kTileRows / kGatherProducers
+        constexpr int ITP = kTileRows / RPI / kGatherProducers;
+        const int it0 = (warp - kConsumerWarps) * ITP;
 #pragma unroll
-        for (int it = 0; it < kTileRows / RPI; ++it) {
+        for (int iu = 0; iu < ITP; ++iu) {
+          const int it = it0 + iu;
           const int r = it * RPI + my_sub;  // row of the tile this lane copies now
           // it*RPI < 32 is warp-uniform (RPI divides 32), so every lane offers the same half
           const int src = __shfl_sync(0xffffffffu, (it * RPI < 32) ? cur0 : cur1, r & 31);

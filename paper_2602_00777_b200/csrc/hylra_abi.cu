@@ -229,7 +229,7 @@ cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const 
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  kern<<<grid, 160, smem, st>>>(tk, tv, p);
+  kern<<<grid, attn_threads<GATHER>(), smem, st>>>(tk, tv, p);
   return cudaGetLastError();
 }
 
