@@ -415,6 +415,14 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     t_full = time_op(op_full, reps)
     t_sel = time_op(op_select, reps)
     t_reuse = time_op(op_reuse, reps) if reuse_ids else 0.0
+    # REUSE roofline: a load-only kernel reading the same rows (libhylra_probe.so)
+    gather_gbs = None
+    if reuse_ids:
+        try:
+            from scripts.gather_probe import gather_peak
+            gather_gbs, _ = gather_peak(dec, q, k, v, k_eff)
+        except Exception:  # noqa: BLE001 - measurement aid only
+            gather_gbs = None
     es = 2 if cfg.dtype == "bf16" else 4
     full_bytes = nf * B * Hkv * 2 * n_valid * d * es
     reuse_bytes = len(reuse_ids) * B * Hkv * 2 * k_eff * d * es
@@ -431,19 +439,16 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
         loop.k_host.copy_(k[:, :, :, pos].cpu())
         loop.v_host.copy_(v[:, :, :, pos].cpu())
         loop.capture()
+        # the kernels store each rank's shard of the outputs into that rank's pinned host
+        # buffer: every host holds its shard, no device all-gather is involved
         for _ in range(3):
             loop.run()
-            if world > 1:
-                gather_outputs(dec.out, plan)
         if world > 1:
             dist.barrier()
         n_e2e = max(10, a.steps)
         t0 = time.perf_counter()
         for _ in range(n_e2e):
             loop.run()
-            if world > 1:
-                gather_outputs(dec.out, plan)
-                torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / n_e2e
         if world > 1:
             tt = torch.tensor([t_e2e], device=dev)
@@ -458,7 +463,8 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                             "(appended by hylra_append_kv reading pinned host memory in place)"
                             " -> hybrid step -> fp32 outputs stored by the kernels straight "
                             "into pinned host memory; one graph launch + host sync per step, "
-                            "wall clock" + ("" if loop.overlap else " (serialised copies)")}
+                            "wall clock, max over ranks (each rank's host receives its shard)"
+                            + ("" if loop.overlap else " (serialised copies)")}
     clk = clocks.stop()
 
     peaks = _peaks()
@@ -476,6 +482,9 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
             "select_frac_of_full_plus_select": t_sel / (t_full + t_sel),
             "full_gbs": full_gbs, "full_frac": full_gbs / peak,
             "reuse_gbs": reuse_gbs, "reuse_frac": (reuse_gbs / peak) if reuse_gbs else None,
+            "reuse_gather_probe_gbs": gather_gbs,
+            "reuse_frac_of_gather_probe": (reuse_gbs / gather_gbs) if (reuse_gbs and gather_gbs)
+            else None,
             "full_bytes_per_launch": full_bytes, "reuse_bytes_per_launch": reuse_bytes,
         },
         "roofline": {"bound": "hbm", "achieved": full_gbs, "peak": peak, "unit": "GB/s",
