@@ -8,6 +8,7 @@
 // REUSE kernel's achieved GB/s is judged against (bench.py "reuse_gather_peak_gbs").
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace {
 
@@ -94,6 +95,12 @@ extern "C" int hylra_probe_gather(const void* k, const void* v, const int32_t* i
   const int pairs = n_layers * B * Hkv;
   dim3 grid(blocks_per_sm, pairs);
   if ((k_rows + blocks_per_sm - 1) / blocks_per_sm > kMaxStage) return 1;
-  gather_probe_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  // HYLRA_PROBE_SMEM (bytes of unused dynamic shared memory per CTA) caps CTAs per SM, i.e.
+  // the bytes in flight: the experiment that tells whether in-flight bytes bound a gather
+  const char* e = getenv("HYLRA_PROBE_SMEM");
+  const int smem = (e && *e) ? atoi(e) : 0;
+  if (smem + (int)sizeof(int32_t) * kMaxStage > 48 * 1024)
+    cudaFuncSetAttribute(gather_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  gather_probe_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

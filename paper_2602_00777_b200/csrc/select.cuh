@@ -109,22 +109,29 @@ struct Red {
   int i[kSelMaxWarps];
   float f[kSelMaxWarps];
   int wt[kSelMaxWarps];
+  float pf[kSelMaxWarps];
+  int pi[kSelMaxWarps];
   int misc[16];
   unsigned hist256[256];
 };
 
+// Block reductions: warps reduce with shuffles, the NT/32 warp partials go through shared
+// memory and every warp reduces them again with shuffles (one shared load per lane instead
+// of NT/32 per thread — the 1024-thread CTAs spent ~20% of their instructions there).
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int NT>
 __device__ __forceinline__ int block_sum_int(int v, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  v = warp_sum_int(v);
   __syncthreads();
   if (lane == 0) r.i[warp] = v;
   __syncthreads();
-  int x = 0;
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) x += r.i[w];
-  return x;
+  return warp_sum_int(lane < NT / 32 ? r.i[lane] : 0);
 }
 template <int NT>
 __device__ __forceinline__ float block_max_float(float v, Red& r) {
@@ -133,10 +140,34 @@ __device__ __forceinline__ float block_max_float(float v, Red& r) {
   __syncthreads();
   if (lane == 0) r.f[warp] = v;
   __syncthreads();
-  float x = -INFINITY;
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) x = fmaxf(x, r.f[w]);
-  return x;
+  return warp_max(lane < NT / 32 ? r.f[lane] : -INFINITY);
+}
+
+// Pass B's five reductions in one round: max, max, sum, sum, sum.
+template <int NT>
+__device__ __forceinline__ void block_reduce_pass_b(float& a, float& b, int& c, int& d, int& e,
+                                                    Red& r) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_max(a);
+  b = warp_max(b);
+  c = warp_sum_int(c);
+  d = warp_sum_int(d);
+  e = warp_sum_int(e);
+  __syncthreads();
+  if (lane == 0) {
+    r.f[warp] = a;
+    r.pf[warp] = b;
+    r.i[warp] = c;
+    r.wt[warp] = d;
+    r.pi[warp] = e;
+  }
+  __syncthreads();
+  const bool in = lane < NT / 32;
+  a = warp_max(in ? r.f[lane] : -INFINITY);
+  b = warp_max(in ? r.pf[lane] : -INFINITY);
+  c = warp_sum_int(in ? r.i[lane] : 0);
+  d = warp_sum_int(in ? r.wt[lane] : 0);
+  e = warp_sum_int(in ? r.pi[lane] : 0);
 }
 
 // Block exclusive scan of one int; returns the exclusive prefix, *total = block sum.
@@ -152,15 +183,16 @@ __device__ __forceinline__ int block_scan(int v, int* total, Red& r) {
   __syncthreads();
   if (lane == 31) r.wt[warp] = x;
   __syncthreads();
-  int pre = 0, all = 0;
+  // lane l scans the warp totals 0..l
+  int t = lane < NT / 32 ? r.wt[lane] : 0;
 #pragma unroll
-  for (int w = 0; w < NT / 32; ++w) {
-    const int t = r.wt[w];
-    pre += (w < warp) ? t : 0;
-    all += t;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, t, o);
+    if (lane >= o) t += y;
   }
-  *total = all;
-  return pre + x - v;
+  *total = __shfl_sync(0xffffffffu, t, 31);
+  const int pre = __shfl_sync(0xffffffffu, t, (warp + 31) & 31);  // inclusive of warp-1
+  return (warp > 0 ? pre : 0) + x - v;
 }
 
 // Warp-aggregated append: each thread adds `cnt` items; returns its first slot.
@@ -626,11 +658,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
       };
       for (int c = 0; c < nfull; ++c) pass_b(c, true);
       if (nfull < nch) pass_b(nfull, false);
-      vmax = block_max_float<NT>(vmax, red);
-      vmin = -block_max_float<NT>(-vmin, red);
-      bad = block_sum_int<NT>(nanacc != nanacc ? 1 : 0, red);
-      cgt = block_sum_int<NT>(cg, red);
-      cin = block_sum_int<NT>(ci, red);
+      {
+        float nmin = -vmin;
+        int nb = nanacc != nanacc ? 1 : 0;
+        block_reduce_pass_b<NT>(vmax, nmin, nb, cg, ci, red);
+        vmin = -nmin;
+        bad = nb;
+        cgt = cg;
+        cin = ci;
+      }
       mabs = fmaxf(fabsf(vmax), fabsf(vmin));
       if (bad || !brackets || (cgt < k && k <= cgt + cin) || attempt == 1) break;
       // retry once: the k-th value lies above hi (too many above) or below lo

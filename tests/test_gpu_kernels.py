@@ -109,6 +109,38 @@ def test_topk_select_exact(n, budget, kind):
                 np.testing.assert_array_equal(got[s, b, h], want)
 
 
+@pytest.mark.parametrize("rows,n,budget,kind", [
+    (200, 32768, 2048, "normal"),    # 512-thread CTAs (149..296 rows)
+    (320, 32768, 2048, "normal"),    # 256-thread CTAs (> 296 rows)
+    (320, 20000, 1500, "ties"),
+    (200, 9000, 700, "allequal"),
+    (320, 65536, 2048, "planted"),
+    (2, 262144, 16384, "normal"),    # longest supported row (bitmap 32 KB)
+    (300, 262144, 4096, "planted"),
+])
+def test_topk_select_exact_all_cta_widths(rows, n, budget, kind):
+    """The SELECT CTA width follows the row count (1024 / 512 / 256 threads): every width
+    returns the reference's exact sets, including at the maximum row length."""
+    rng = np.random.default_rng(rows * 7 + n)
+    if kind == "normal":
+        x = rng.standard_normal((rows, n)).astype(np.float32)
+    elif kind == "ties":
+        x = rng.integers(-20, 20, size=(rows, n)).astype(np.float32)
+    elif kind == "allequal":
+        x = np.full((rows, n), -0.25, dtype=np.float32)
+    else:
+        x = rng.standard_normal((rows, n)).astype(np.float32)
+        for r in range(rows):
+            x[r, rng.choice(n, 512, replace=False)] += 8.0
+    rs = (n + 7) & ~7
+    buf = np.zeros((1, rows, 1, rs), dtype=np.float32)
+    buf[0, :, 0, :n] = x
+    got = topk_select(torch.from_numpy(buf).to(DEV), budget, n).cpu().numpy()
+    for r in range(rows):
+        want = orc.topk_of_logits(x[r].astype(np.float64), budget)
+        np.testing.assert_array_equal(got[0, r, 0], want)
+
+
 def test_topk_select_group_sum_matches_layer_wide_rule():
     # sel_group = Hkv: one set per layer from the head-order sum (engine.py:177-183)
     rng = np.random.default_rng(3)
