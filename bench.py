@@ -458,13 +458,13 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                     "h2d_bytes_per_step": int(loop.h2d_bytes),
                     "d2h_bytes_per_step": int(loop.d2h_bytes),
                     "ms_per_step": t_e2e * 1e3,
-                    "path": "DecodeLoop.run() per step: pinned host q (H2D copies; REUSE "
-                            "layers' on a side stream behind the FULL kernel) + new K/V rows "
-                            "(appended by hylra_append_kv reading pinned host memory in place)"
-                            " -> hybrid step -> fp32 outputs stored by the kernels straight "
-                            "into pinned host memory; one graph launch + host sync per step, "
-                            "wall clock, max over ranks (each rank's host receives its shard)"
-                            + ("" if loop.overlap else " (serialised copies)")}
+                    "path": "DecodeLoop.run() per step, one graph launch + host sync: "
+                            "hylra_append_kv reads the new K/V rows from pinned host memory "
+                            "in place, the FULL/SELECT/REUSE kernels read the queries from "
+                            "pinned host memory and store the fp32 outputs straight into "
+                            "pinned host memory (no copy operations); wall clock, max over "
+                            "ranks (each rank's host receives its shard)"
+                            + ("" if loop.zero_copy else " [serialised copies]")}
     clk = clocks.stop()
 
     peaks = _peaks()

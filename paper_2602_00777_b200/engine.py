@@ -431,16 +431,14 @@ class DecodeLoop:
     outputs land in the pinned `out_host`. Fill the host buffers, call `run()`; it returns
     `out_host` after the step completed.
 
-    overlap=True (token-mode HybridDecoder): the FULL layers' queries are copied and their
-    new rows appended first (hylra_append_kv reads the pinned rows across the link in
-    place); the REUSE layers' queries and rows follow on a side stream behind the FULL
-    kernel (the REUSE launch waits on them: hylra_decode_step_events); the kernels store
-    the outputs straight into the pinned `out_host` as each (layer, KV head) completes,
-    so no device-to-host copy follows the step. overlap=False: plain H2D copies, append,
-    step, D2H copy, serialised.
+    zero_copy=True (token-mode HybridDecoder): no copy operations at all — hylra_append_kv
+    reads the new rows from pinned host memory in place, the attention kernels read each
+    (layer, KV head)'s queries across the link when their CTAs start and store the outputs
+    straight into `out_host`: a 4-kernel graph. zero_copy=False: H2D copies, append, step,
+    D2H copy, serialised (the reference point).
     """
 
-    def __init__(self, decoder: HybridDecoder, pos: int, *, overlap: bool = True):
+    def __init__(self, decoder: HybridDecoder, pos: int, *, zero_copy: bool = True):
         k = decoder.k
         L, B, Hkv, cap, d = k.shape
         if not 0 <= pos < cap:
@@ -452,48 +450,27 @@ class DecodeLoop:
         self.k_host = torch.zeros((L, B, Hkv, d), dtype=dt).pin_memory()
         self.v_host = torch.zeros((L, B, Hkv, d), dtype=dt).pin_memory()
         self.out_host = torch.zeros((L, B, Hq, d), dtype=torch.float32).pin_memory()
-        self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
         self.graph = None
         self.h2d_bytes = (self.q_host.numel() + 2 * self.k_host.numel()) * self.q_host.element_size()
         self.d2h_bytes = self.out_host.numel() * 4
-        self.overlap = bool(overlap) and type(decoder) is HybridDecoder \
+        self.zero_copy = bool(zero_copy) and type(decoder) is HybridDecoder \
             and decoder.block_size == 1
-        acts = decoder.actions
-        self.full_layers = [l for l in range(L) if acts[l] is Action.FULL]
-        self.reuse_layers = [l for l in range(L) if acts[l] is Action.REUSE]
-        if self.overlap:
-            self.side = torch.cuda.Stream(device=k.device)
-            # torch creates events lazily: record once so the handle exists for the ABI
-            self.ev_side = torch.cuda.Event()
-            self.ev_side.record()
-        else:
+        if not self.zero_copy:
+            self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
             self.kv_dev = torch.zeros((2, L, B, Hkv, d), dtype=dt, device=k.device)
 
     def _body(self):
         dec, pos = self.dec, self.pos
-        if not self.overlap:
-            self.q_dev.copy_(self.q_host, non_blocking=True)
-            self.kv_dev[0].copy_(self.k_host, non_blocking=True)
-            self.kv_dev[1].copy_(self.v_host, non_blocking=True)
-            dec.append(self.kv_dev[0], self.kv_dev[1], pos)
-            dec.step(self.q_dev, pos + 1)
-            self.out_host.copy_(dec.out, non_blocking=True)
+        if self.zero_copy:
+            dec.append(self.k_host, self.v_host, pos)
+            dec.step(self.q_host, pos + 1, out=self.out_host)
             return
-        main = torch.cuda.current_stream(dec.k.device)
-        if self.reuse_layers:
-            self.side.wait_stream(main)
-            with torch.cuda.stream(self.side):
-                for a, b in _runs(self.reuse_layers):
-                    self.q_dev[a:b].copy_(self.q_host[a:b], non_blocking=True)
-                dec.append(self.k_host, self.v_host, pos, self.reuse_layers)
-                self.ev_side.record(self.side)
-        for a, b in _runs(self.full_layers):
-            self.q_dev[a:b].copy_(self.q_host[a:b], non_blocking=True)
-        dec.append(self.k_host, self.v_host, pos, self.full_layers)
-        dec.step(self.q_dev, pos + 1, out=self.out_host,
-                 reuse_wait=self.ev_side if self.reuse_layers else None)
-        if self.reuse_layers:
-            main.wait_stream(self.side)
+        self.q_dev.copy_(self.q_host, non_blocking=True)
+        self.kv_dev[0].copy_(self.k_host, non_blocking=True)
+        self.kv_dev[1].copy_(self.v_host, non_blocking=True)
+        dec.append(self.kv_dev[0], self.kv_dev[1], pos)
+        dec.step(self.q_dev, pos + 1)
+        self.out_host.copy_(dec.out, non_blocking=True)
 
     def capture(self):
         """Warm up and capture the step (host copies included) into a CUDA graph."""

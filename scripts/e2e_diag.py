@@ -48,7 +48,7 @@ with torch.cuda.graph(gr):
     dec.step(q, cfg.context)
 res = {"step": ev_time(gr.replay, a.steps)}
 for ov in (False, True):
-    loop = DecodeLoop(dec, cfg.context - 1, overlap=ov)
+    loop = DecodeLoop(dec, cfg.context - 1, zero_copy=ov)
     pos = cfg.context - 1
     loop.q_host.copy_(q.cpu())  # real inputs: all-zero queries would make every score tie
     loop.k_host.copy_(k[:, :, :, pos].cpu())
@@ -61,6 +61,15 @@ for ov in (False, True):
     for _ in range(a.steps):
         loop.run()
     res[f"loop_wc_overlap{int(ov)}"] = (time.perf_counter() - t0) / a.steps * 1e3
+    # the same with a spin on an event instead of the blocking stream sync
+    ev = torch.cuda.Event()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        loop.graph.replay()
+        ev.record()
+        while not ev.query():
+            pass
+    res[f"loop_wc_spin_overlap{int(ov)}"] = (time.perf_counter() - t0) / a.steps * 1e3
     # host-side cost of one replay call alone
     torch.cuda.synchronize()
     t0 = time.perf_counter()

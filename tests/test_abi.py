@@ -87,3 +87,29 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_abi, "_lib", None)
     with pytest.raises(CudaError, match="not been built"):
         _abi.lib()
+
+
+def test_step_ex_and_append_validate_on_the_host():
+    lib = _abi.lib()
+    g = _geom()
+    acts = _abi.uint8_array([1, 0, 1, 0])
+    need = lib.hylra_decode_step_workspace_bytes(g, acts, 2048, 128, 1, 0, 0)
+    opt = _abi.StepOptions()
+    opt.side_stream = 1  # a side stream without its four events
+    with pytest.raises(ConfigurationError, match="four events"):
+        _abi.check(lib.hylra_decode_step_ex(g, 1, 1, 1, 2048, acts, 128, 1, 1, 0, 0, 1, 1, 128,
+                                            1, need, None, ctypes.byref(opt)))
+    with pytest.raises(InvalidInputError, match="first layer"):
+        _abi.check(lib.hylra_decode_step_ex(g, 1, 1, 1, 2048, _abi.uint8_array([0, 1, 1, 0]),
+                                            128, 1, 1, 0, 0, 1, 1, 128, 1, need, None, None))
+    with pytest.raises(InvalidInputError, match="pos"):
+        _abi.check(lib.hylra_append_kv(g, 1, 1, 1, 1, 2048, 0, None, None))
+    with pytest.raises(ConfigurationError, match="NULL"):
+        _abi.check(lib.hylra_append_kv(g, None, 1, 1, 1, 5, 0, None, None))
+
+
+def test_layer_runs():
+    from paper_2602_00777_b200.engine import _runs
+    assert _runs([]) == []
+    assert _runs([0, 1, 2, 8, 15, 16, 24, 31]) == [(0, 3), (8, 9), (15, 17), (24, 25), (31, 32)]
+    assert _runs(range(3, 8)) == [(3, 8)]

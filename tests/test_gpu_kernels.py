@@ -285,18 +285,18 @@ def test_pipelined_schedules_match_fused(schedule):
     assert max_head_err(dec.out.double().cpu().numpy(), r) < 4e-3
 
 
-@pytest.mark.parametrize("overlap", [False, True])
-def test_decode_loop_host_io_graph(overlap):
+@pytest.mark.parametrize("zero_copy", [False, True])
+def test_decode_loop_host_io_graph(zero_copy):
     """DecodeLoop: H2D (q + new K/V row) -> append -> step -> D2H in one graph launch;
-    overlap=True: REUSE inputs on a side stream, rows appended from pinned host memory in
-    place, outputs stored by the kernels straight into pinned host memory."""
+    zero_copy=True: rows appended and queries read from pinned host memory in place,
+    outputs stored by the kernels straight into pinned host memory."""
     from paper_2602_00777_b200.engine import DecodeLoop
     L, B, Hq, Hkv, d, cap, budget = 9, 2, 8, 2, 128, 2048, 128
     q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=13, planted=16)
     actions = ("full", "reuse", "full", "reuse", "reuse", "full", "reuse", "reuse", "reuse")
     dec = HybridDecoder(actions, k.clone(), v.clone(), budget, q_heads=Hq)
     pos = 1500
-    loop = DecodeLoop(dec, pos, overlap=overlap)
+    loop = DecodeLoop(dec, pos, zero_copy=zero_copy)
     g = torch.Generator().manual_seed(3)
     for step in range(3):
         qh = torch.randn((L, B, Hq, d), generator=g).to(torch.bfloat16)
