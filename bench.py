@@ -510,9 +510,14 @@ def run_ours(a):
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
+    n_dev = torch.cuda.device_count()
+    torch.cuda.set_device(local % n_dev)
+    shared_gpu = world > n_dev  # functional check only: ranks share GPUs, gloo collectives
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[a.config]
     batch = a.batch or cfg.batch
     main = measure_config(a, cfg, batch, rank, world, torch, dist)
@@ -577,6 +582,8 @@ def run_ours(a):
             "roofline": main["roofline"], "kernels": main["kernels"],
             "cpu_baseline": cpu, "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
             "clocks": main["clocks"], "schedules": main["schedules"], "check": main["check"],
+            **({"functional_only": f"{world} ranks on {n_dev} GPU(s), gloo collectives: "
+                                   "not a scaling measurement"} if shared_gpu else {}),
             "extra": extra,
         }
         print(json.dumps(line), flush=True)

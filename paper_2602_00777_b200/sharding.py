@@ -75,13 +75,14 @@ def gather_outputs(out_local, plan: ShardPlan, group=None):
     if plan.world == 1:
         return out_local
     src = out_local.contiguous()
-    if src.is_cuda:
+    if src.is_cuda and dist.get_backend(group) == "nccl":
         buf = torch.empty((plan.world,) + tuple(src.shape), dtype=src.dtype, device=src.device)
         dist.all_gather_into_tensor(buf, src, group=group)
-    else:  # gloo (CPU tests)
-        parts = [torch.empty_like(src) for _ in range(plan.world)]
-        dist.all_gather(parts, src, group=group)
-        buf = torch.stack(parts)
+    else:  # gloo (CPU tests; ranks sharing a GPU in a functional check)
+        host = src.cpu()
+        parts = [torch.empty_like(host) for _ in range(plan.world)]
+        dist.all_gather(parts, host, group=group)
+        buf = torch.stack(parts).to(src.device)
     if plan.mode == "kvhead":
         # [P, L, B, Hq/P, d] -> [L, B, P*Hq/P, d]
         return buf.permute(1, 2, 0, 3, 4).reshape(
