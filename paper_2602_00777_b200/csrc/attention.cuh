@@ -195,6 +195,141 @@ __device__ __forceinline__ uint32_t swz_addr(uint32_t tile_base, int r, int chun
   return tile_base + (chunk >> 3) * (kTileRows * 128) + r * 128 + (((chunk & 7) ^ (r & 7)) << 4);
 }
 
+// One 64-row stage for one consumer warp (its 16 rows): S = Q K^T on tensor cores, the
+// tail mask, the selection-score emission (FULL), the online softmax and O += P V.
+template <int D, bool GATHER, bool GBIG>
+__device__ __forceinline__ void mma_consume_tile(const AttnParams& p, uint32_t kt, uint32_t vt,
+                                                 const uint32_t (&qa)[D / 16][4],
+                                                 float (&o)[D / 8][4], float& m0, float& m1,
+                                                 float& l0, float& l1, int row0, int n_rows,
+                                                 float* score_row, int lane) {
+  const int g = lane >> 2;
+  const int t = lane & 3;
+  const float c = p.scale_log2;
+  const int rbase = ((threadIdx.x >> 5) & 3) * 16;
+  const int lk_row = rbase + (lane & 7) + ((lane >> 4) << 3);   // K: matrices (n0,k0)(n0,k1)(n1,k0)(n1,k1)
+  const int lk_chk = (lane >> 3) & 1;
+  const int lv_row = rbase + (lane & 7) + (((lane >> 3) & 1) << 3);  // V: (k0,n)(k1,n)(k0,n+1)(k1,n+1)
+  const int lv_chk = lane >> 4;
+  // ---- S = Q K^T (16 x 16 per warp)
+  float sacc[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < D / 16; ++ks) {
+    uint32_t b0, b1, b2, b3;
+    ldsm_x4(swz_addr(kt, lk_row, 2 * ks + lk_chk), b0, b1, b2, b3);
+    mma_bf16_16816(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+    mma_bf16_16816(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+  }
+
+  // ---- mask rows past the end of the range
+  const bool tail = row0 + 16 > n_rows;
+  if (tail) {
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (row0 + nt * 8 + 2 * t + e >= n_rows) {
+          sacc[nt][e] = -INFINITY;
+          sacc[nt][2 + e] = -INFINITY;
+        }
+      }
+  }
+
+  // ---- selection score: sum over the group's heads (rows) of q.k, times 1/sqrt(d)
+  if (!GATHER && score_row != nullptr) {
+    float v00 = sacc[0][0], v01 = sacc[0][1], v10 = sacc[1][0], v11 = sacc[1][1];
+    if (GBIG) {
+      v00 += sacc[0][2];
+      v01 += sacc[0][3];
+      v10 += sacc[1][2];
+      v11 += sacc[1][3];
+    }
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      v00 += __shfl_xor_sync(0xffffffffu, v00, off);
+      v01 += __shfl_xor_sync(0xffffffffu, v01, off);
+      v10 += __shfl_xor_sync(0xffffffffu, v10, off);
+      v11 += __shfl_xor_sync(0xffffffffu, v11, off);
+    }
+    if (g == 0) {
+      const int n0 = row0 + 2 * t;
+      const int n1 = row0 + 8 + 2 * t;
+      if (!tail) {
+        *reinterpret_cast<float2*>(score_row + n0) =
+            make_float2(v00 * p.inv_sqrt_d, v01 * p.inv_sqrt_d);
+        *reinterpret_cast<float2*>(score_row + n1) =
+            make_float2(v10 * p.inv_sqrt_d, v11 * p.inv_sqrt_d);
+      } else {
+        if (n0 < n_rows) score_row[n0] = v00 * p.inv_sqrt_d;
+        if (n0 + 1 < n_rows) score_row[n0 + 1] = v01 * p.inv_sqrt_d;
+        if (n1 < n_rows) score_row[n1] = v10 * p.inv_sqrt_d;
+        if (n1 + 1 < n_rows) score_row[n1 + 1] = v11 * p.inv_sqrt_d;
+      }
+    }
+  }
+
+  // ---- online softmax (row g, and row g+8 when G > 8)
+  uint32_t pa0, pa1, pa2, pa3;
+  {
+    float mx = fmaxf(fmaxf(sacc[0][0], sacc[0][1]), fmaxf(sacc[1][0], sacc[1][1]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m0, mx);
+    const float mu = (mn == -INFINITY) ? 0.f : mn;
+    const float alpha = fast_exp2((m0 - mu) * c);
+    const float mc = mu * c;
+    const float p00 = fast_exp2(fmaf(sacc[0][0], c, -mc));
+    const float p01 = fast_exp2(fmaf(sacc[0][1], c, -mc));
+    const float p10 = fast_exp2(fmaf(sacc[1][0], c, -mc));
+    const float p11 = fast_exp2(fmaf(sacc[1][1], c, -mc));
+    l0 = fmaf(l0, alpha, (p00 + p01) + (p10 + p11));
+    m0 = mn;
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      o[j][0] *= alpha;
+      o[j][1] *= alpha;
+    }
+    pa0 = pack_bf16(p00, p01);
+    pa2 = pack_bf16(p10, p11);
+  }
+  if (GBIG) {
+    float mx = fmaxf(fmaxf(sacc[0][2], sacc[0][3]), fmaxf(sacc[1][2], sacc[1][3]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m1, mx);
+    const float mu = (mn == -INFINITY) ? 0.f : mn;
+    const float alpha = fast_exp2((m1 - mu) * c);
+    const float mc = mu * c;
+    const float p00 = fast_exp2(fmaf(sacc[0][2], c, -mc));
+    const float p01 = fast_exp2(fmaf(sacc[0][3], c, -mc));
+    const float p10 = fast_exp2(fmaf(sacc[1][2], c, -mc));
+    const float p11 = fast_exp2(fmaf(sacc[1][3], c, -mc));
+    l1 = fmaf(l1, alpha, (p00 + p01) + (p10 + p11));
+    m1 = mn;
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      o[j][2] *= alpha;
+      o[j][3] *= alpha;
+    }
+    pa1 = pack_bf16(p00, p01);
+    pa3 = pack_bf16(p10, p11);
+  } else {
+    pa1 = 0u;
+    pa3 = 0u;
+  }
+
+  // ---- O += P V
+#pragma unroll
+  for (int j = 0; j < D / 8; j += 2) {
+    uint32_t b0, b1, b2, b3;
+    ldsm_x4_t(swz_addr(vt, lv_row, j + lv_chk), b0, b1, b2, b3);
+    mma_bf16_16816(o[j], pa0, pa1, pa2, pa3, b0, b1);
+    mma_bf16_16816(o[j + 1], pa0, pa1, pa2, pa3, b2, b3);
+  }
+}
+
 template <int D, bool GATHER, bool GBIG, int STAGES>
 __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     attn_mma_kernel(const __grid_constant__ CUtensorMap tmk,
@@ -361,7 +496,6 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
   const int g = lane >> 2;  // row of the m16n8 fragments (query head within the group)
   const int t = lane & 3;
   const int G = p.G;
-  const float c = p.scale_log2;
 
   // Q A-fragments for all D/16 k-steps.
   uint32_t qa[D / 16][4];
@@ -390,11 +524,6 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     score_row = p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + kh) * p.cap;
 
   const int rbase = warp * 16;
-  // ldmatrix lane roles
-  const int lk_row = rbase + (lane & 7) + ((lane >> 4) << 3);   // K: matrices (n0,k0)(n0,k1)(n1,k0)(n1,k1)
-  const int lk_chk = (lane >> 3) & 1;
-  const int lv_row = rbase + (lane & 7) + (((lane >> 3) & 1) << 3);  // V: (k0,n)(k1,n)(k0,n+1)(k1,n+1)
-  const int lv_chk = lane >> 4;
 
   for (int i = 0; i < n_my; ++i) {
     const int s = i % STAGES;
@@ -403,123 +532,8 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     const uint32_t vt = kt + SM::kTileBytes;
     const int row0 = (t_begin + i) * kTileRows + rbase;  // first row of this warp's slice
 
-    // ---- S = Q K^T (16 x 16 per warp)
-    float sacc[2][4];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(swz_addr(kt, lk_row, 2 * ks + lk_chk), b0, b1, b2, b3);
-      mma_bf16_16816(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-      mma_bf16_16816(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
-    }
-
-    // ---- mask rows past the end of the range
-    const bool tail = row0 + 16 > n_rows;
-    if (tail) {
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (row0 + nt * 8 + 2 * t + e >= n_rows) {
-            sacc[nt][e] = -INFINITY;
-            sacc[nt][2 + e] = -INFINITY;
-          }
-        }
-    }
-
-    // ---- selection score: sum over the group's heads (rows) of q.k, times 1/sqrt(d)
-    if (!GATHER && score_row != nullptr) {
-      float v00 = sacc[0][0], v01 = sacc[0][1], v10 = sacc[1][0], v11 = sacc[1][1];
-      if (GBIG) {
-        v00 += sacc[0][2];
-        v01 += sacc[0][3];
-        v10 += sacc[1][2];
-        v11 += sacc[1][3];
-      }
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        v00 += __shfl_xor_sync(0xffffffffu, v00, off);
-        v01 += __shfl_xor_sync(0xffffffffu, v01, off);
-        v10 += __shfl_xor_sync(0xffffffffu, v10, off);
-        v11 += __shfl_xor_sync(0xffffffffu, v11, off);
-      }
-      if (g == 0) {
-        const int n0 = row0 + 2 * t;
-        const int n1 = row0 + 8 + 2 * t;
-        if (!tail) {
-          *reinterpret_cast<float2*>(score_row + n0) =
-              make_float2(v00 * p.inv_sqrt_d, v01 * p.inv_sqrt_d);
-          *reinterpret_cast<float2*>(score_row + n1) =
-              make_float2(v10 * p.inv_sqrt_d, v11 * p.inv_sqrt_d);
-        } else {
-          if (n0 < n_rows) score_row[n0] = v00 * p.inv_sqrt_d;
-          if (n0 + 1 < n_rows) score_row[n0 + 1] = v01 * p.inv_sqrt_d;
-          if (n1 < n_rows) score_row[n1] = v10 * p.inv_sqrt_d;
-          if (n1 + 1 < n_rows) score_row[n1 + 1] = v11 * p.inv_sqrt_d;
-        }
-      }
-    }
-
-    // ---- online softmax (row g, and row g+8 when G > 8)
-    uint32_t pa0, pa1, pa2, pa3;
-    {
-      float mx = fmaxf(fmaxf(sacc[0][0], sacc[0][1]), fmaxf(sacc[1][0], sacc[1][1]));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float mn = fmaxf(m0, mx);
-      const float mu = (mn == -INFINITY) ? 0.f : mn;
-      const float alpha = fast_exp2((m0 - mu) * c);
-      const float mc = mu * c;
-      const float p00 = fast_exp2(fmaf(sacc[0][0], c, -mc));
-      const float p01 = fast_exp2(fmaf(sacc[0][1], c, -mc));
-      const float p10 = fast_exp2(fmaf(sacc[1][0], c, -mc));
-      const float p11 = fast_exp2(fmaf(sacc[1][1], c, -mc));
-      l0 = fmaf(l0, alpha, (p00 + p01) + (p10 + p11));
-      m0 = mn;
-#pragma unroll
-      for (int j = 0; j < D / 8; ++j) {
-        o[j][0] *= alpha;
-        o[j][1] *= alpha;
-      }
-      pa0 = pack_bf16(p00, p01);
-      pa2 = pack_bf16(p10, p11);
-    }
-    if (GBIG) {
-      float mx = fmaxf(fmaxf(sacc[0][2], sacc[0][3]), fmaxf(sacc[1][2], sacc[1][3]));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float mn = fmaxf(m1, mx);
-      const float mu = (mn == -INFINITY) ? 0.f : mn;
-      const float alpha = fast_exp2((m1 - mu) * c);
-      const float mc = mu * c;
-      const float p00 = fast_exp2(fmaf(sacc[0][2], c, -mc));
-      const float p01 = fast_exp2(fmaf(sacc[0][3], c, -mc));
-      const float p10 = fast_exp2(fmaf(sacc[1][2], c, -mc));
-      const float p11 = fast_exp2(fmaf(sacc[1][3], c, -mc));
-      l1 = fmaf(l1, alpha, (p00 + p01) + (p10 + p11));
-      m1 = mn;
-#pragma unroll
-      for (int j = 0; j < D / 8; ++j) {
-        o[j][2] *= alpha;
-        o[j][3] *= alpha;
-      }
-      pa1 = pack_bf16(p00, p01);
-      pa3 = pack_bf16(p10, p11);
-    } else {
-      pa1 = 0u;
-      pa3 = 0u;
-    }
-
-    // ---- O += P V
-#pragma unroll
-    for (int j = 0; j < D / 8; j += 2) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(swz_addr(vt, lv_row, j + lv_chk), b0, b1, b2, b3);
-      mma_bf16_16816(o[j], pa0, pa1, pa2, pa3, b0, b1);
-      mma_bf16_16816(o[j + 1], pa0, pa1, pa2, pa3, b2, b3);
-    }
+    mma_consume_tile<D, GATHER, GBIG>(p, kt, vt, qa, o, m0, m1, l0, l1, row0, n_rows,
+                                      score_row, lane);
 
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_bar + s);
