@@ -232,6 +232,72 @@ def _block_mode_line(a, cfg, torch):
             "step_gbs": by / (ms * 1e-3) / 1e9, "kernels_per_step": 5}
 
 
+def _offload_line(a, cfg, torch, batch=1):
+    """Index-guided offload (row f2): cfg2 at B=1 with the 24 REUSE layers' K/V in pinned
+    host memory (3.2 GB); the REUSE kernel reads only the selected rows across the link.
+    link_gbs = selected K/V bytes / REUSE launch time, against a pinned H2D copy measured
+    in the same run."""
+    from paper_2602_00777_b200 import _abi
+    from paper_2602_00777_b200.engine import OffloadDecoder
+    from paper_2602_00777_b200.synthetic import generate_torch
+
+    c = cfg.with_(batch=batch)
+    q, k, v = generate_torch(c, "cuda")
+    kf, vf, kr, vr = OffloadDecoder.split_cache(c.actions, k, v)
+    del k, v
+    torch.cuda.empty_cache()
+    dec = OffloadDecoder(c.actions, kf, vf, kr, vr, c.budget, q_heads=c.q_heads)
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    reps = max(3, min(a.steps, 10))
+    ms = timed(lambda: dec.step(q, c.context), reps)
+    dec.check_flags()
+    # the REUSE launch alone, reading the pinned host cache
+    g = dec._geometry(q)
+    rl = list(dec.reuse_layers)
+    k_eff = min(c.budget, c.context)
+    lib = _abi.lib()
+    ws = torch.zeros(lib.hylra_attention_workspace_bytes(g, len(rl), k_eff), dtype=torch.uint8,
+                     device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    # the primitive addresses K/V by layer id: compact ids 0..n_reuse-1 index the offloaded
+    # buffer (their q / out rows are other layers' - irrelevant for the timing)
+    compact = _abi.int32_array(range(len(rl)))
+    srcs = _abi.int32_array(dec.slot_of_layer[l] for l in rl)
+
+    def reuse():
+        _abi.check(lib.hylra_reuse_decode(
+            g, q.data_ptr(), kr.data_ptr(), vr.data_ptr(), c.context, len(rl), compact, srcs,
+            dec.idx.data_ptr(), None, dec.k_stride, k_eff, 1, dec.out.data_ptr(),
+            ws.data_ptr(), ws.numel(), st))
+    reuse_bytes = len(rl) * c.batch * c.kv_heads * 2 * k_eff * c.head_dim * 2
+    t_reuse = timed(reuse, reps)
+    h = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    dd = torch.empty_like(h, device="cuda")
+    t_copy = timed(lambda: dd.copy_(h, non_blocking=True), 5)
+    copy_gbs = h.numel() / (t_copy * 1e-3) / 1e9
+    res = {"batch": c.batch, "value": c.batch / (ms * 1e-3), "ms_per_step": ms,
+           "offloaded_bytes": 2 * kr.numel() * kr.element_size(),
+           "reuse_link_bytes_per_step": reuse_bytes,
+           "pinned_h2d_copy_gbs": copy_gbs}
+    res.update({"reuse_ms": t_reuse, "link_gbs": reuse_bytes / (t_reuse * 1e-3) / 1e9,
+                "link_frac_of_h2d_copy": reuse_bytes / (t_reuse * 1e-3) / 1e9 / copy_gbs})
+    del dec, kf, vf, kr, vr, q, h, dd, ws
+    torch.cuda.empty_cache()
+    return res
+
+
 def _read_stream_gbs(torch):
     """Context for the roofline: a read-only stream (torch.sum over 8 GiB of int64), the
     ceiling a pure-read kernel can approach; the reported frac uses MEASURED_PEAKS.json."""
@@ -560,6 +626,10 @@ def run_ours(a):
             extra["cfg2_blocks_b8"] = _block_mode_line(a, cfg, torch)
         except Exception as exc:  # noqa: BLE001
             extra["cfg2_blocks_b8"] = {"error": str(exc)}
+        try:
+            extra["cfg2_offload_b1"] = _offload_line(a, cfg, torch)
+        except Exception as exc:  # noqa: BLE001
+            extra["cfg2_offload_b1"] = {"error": str(exc)}
         for b_small in (1, 4):
             try:
                 rb = measure_config(a, cfg, b_small, rank, world, torch, dist, e2e=False)
