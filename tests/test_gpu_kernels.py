@@ -409,3 +409,63 @@ def test_non_finite_inputs_raise_numeric_error(where):
     torch.cuda.synchronize()
     with pytest.raises(NumericInputError):
         dec.check_flags()
+
+
+def _embed(rows, d=32):
+    """2-D reference fixtures embedded in d dims (zero padding keeps every dot product)."""
+    x = torch.zeros((len(rows), d), dtype=torch.float32)
+    x[:, :2] = torch.tensor(rows, dtype=torch.float64).float()
+    return x
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_known_answers_on_gpu(dtype):
+    """The reference's known-answer tests through the kernels (tests/test_attention.py:33-59,
+    100-105, 192-200). The 2-D fixtures are zero-padded to d = 32 (f32) / 64 (bf16) and the
+    query is scaled by sqrt(d / 2), so logits equal the reference's q.k / sqrt(2) (in bf16 up
+    to the rounding of that scaled query, inside the 2e-3 tolerance)."""
+    import math
+    d = 32 if dtype == "f32" else 64
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    tol = 1e-6 if dtype == "f32" else 2e-3
+    s = math.sqrt(d / 2)
+
+    def attend(q2, keys, values):
+        q = (_embed([q2], d) * s).to(dt).view(1, 1, 1, d).to(DEV)
+        k = _embed(keys, d).to(dt).view(1, 1, 1, len(keys), d).to(DEV)
+        v = _embed(values, d).to(dt).view(1, 1, 1, len(values), d).to(DEV)
+        return q, k, v
+
+    # single token: the output is its value row
+    q, k, v = attend([0.5, 0.5], [[1.0, 2.0]], [[5.0, -3.0]])
+    out, _ = full_attention(q, k, v)
+    assert torch.allclose(out[0, 0, 0, :2].cpu(), torch.tensor([5.0, -3.0]), rtol=tol, atol=tol)
+    # orthogonal query: uniform weights
+    q, k, v = attend([0.0, 1.0], [[1.0, 0.0], [2.0, 0.0], [-1.0, 0.0]],
+                     [[3.0, 0.0], [0.0, 3.0], [0.0, 0.0]])
+    out, _ = full_attention(q, k, v)
+    assert torch.allclose(out[0, 0, 0, :2].cpu(), torch.tensor([1.0, 1.0]), rtol=tol, atol=tol)
+    # two-token fixture [[10, 0], [0, 0]]: logit 10 / sqrt(2), weight 1 / (1 + e^-l)
+    q, k, v = attend([1.0, 0.0], [[10.0, 0.0], [0.0, 0.0]], [[1.0, 0.0], [0.0, 1.0]])
+    out, sc = full_attention(q, k, v)
+    w1 = 1.0 / (1.0 + math.exp(-10 / math.sqrt(2)))
+    assert abs(float(sc[0, 0, 0, 0]) - 10 / math.sqrt(2)) < 10 * tol
+    assert torch.allclose(out[0, 0, 0, :2].cpu().double(), torch.tensor([w1, 1 - w1],
+                          dtype=torch.float64), rtol=tol, atol=tol)
+    # subset fixture: selection {0, 2}, softmax renormalised over the subset
+    keys = [[10.0, 0.0], [0.0, 0.0], [1.0, 1.0], [-2.0, 0.5]]
+    values = [[1.0, 0.0], [0.0, 1.0], [2.0, 2.0], [3.0, -1.0]]
+    q, k, v = attend([1.0, 0.0], keys, values)
+    idx = torch.tensor([[[[0, 2]]]], dtype=torch.int32, device=DEV)
+    got = sparse_attention(q, k, v, idx)
+    l0, l2 = 10 / math.sqrt(2), 1 / math.sqrt(2)
+    w0 = 1 / (1 + math.exp(l2 - l0))
+    want = torch.tensor([w0 * 1 + (1 - w0) * 2, (1 - w0) * 2], dtype=torch.float64)
+    assert torch.allclose(got[0, 0, 0, :2].cpu().double(), want, rtol=tol, atol=tol)
+    # top-k ties and saturation
+    for row, budget, want in (([3.0, 1.0, 2.0], 2, [0, 2]), ([5.0, 5.0, 5.0], 2, [0, 1]),
+                              ([1.0, 2.0], 10, [0, 1])):
+        buf = torch.zeros((1, 1, 1, 8), dtype=torch.float32)
+        buf[0, 0, 0, :len(row)] = torch.tensor(row)
+        got = topk_select(buf.to(DEV), budget, len(row))
+        assert got[0, 0, 0].cpu().tolist() == want
