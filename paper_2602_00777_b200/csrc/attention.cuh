@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();
 
   if (warp >= kConsumerWarps) {
     // ------------------------------------------------------------- producer warp
@@ -538,6 +539,7 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_bar + s);
   }
+  pdl_launch_dependents();
 
   // ---- merge the 4 warps through shared memory (pipeline buffers are drained)
   asm volatile("bar.sync 1, 128;" ::: "memory");

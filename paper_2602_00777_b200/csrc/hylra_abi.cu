@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "../../include/hylra.h"
@@ -206,6 +207,36 @@ int encode_kv_map(CUtensorMap* map, const hylra_geometry* g, const void* base, i
   return HYLRA_OK;
 }
 
+// ------------------------------------------------------------------ launches
+// Programmatic dependent launch for the step's kernels (FULL, SELECT, REUSE): each may be
+// scheduled while its predecessor drains (the kernels wait on griddepcontrol before
+// touching memory). HYLRA_PDL=0 turns it off.
+bool pdl_enabled() {
+  static int v = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_PDL");
+    v = (e && *e) ? (atoi(e) != 0) : 1;
+  });
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ------------------------------------------------------------------ kernel tables
 template <int D, bool GATHER, bool GBIG>
 constexpr int mma_stages() {
@@ -229,8 +260,7 @@ cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const 
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  kern<<<grid, attn_threads<GATHER>(), smem, st>>>(tk, tv, p);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(attn_threads<GATHER>()), smem, st, tk, tv, p);
 }
 
 template <typename T, int D, int GM, bool GATHER>
@@ -361,8 +391,7 @@ cudaError_t launch_select_nt(dim3 grid, size_t smem, cudaStream_t st, const Sele
                                     (int)sel_smem_bytes(kSelMaxTokens, NT));
   });
   if (attr_err != cudaSuccess) return attr_err;
-  topk_select_kernel<NT><<<grid, NT, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(topk_select_kernel<NT>, grid, dim3(NT), smem, st, p);
 }
 
 struct BlockRows {  // block mode: rows are pooled block scores

@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
   int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
   const SelSmem sm = carve<NT>(sraw, n);
+  pdl_wait();
   const long long t0 = clock64();
 
   RowReader rd;
@@ -935,6 +936,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
   }
   __syncthreads();
 
+  pdl_launch_dependents();
   // ---- E. index-ordered compaction of the bitmap
   int run = 0;
   for (int c = 0; c < nch; ++c) {
