@@ -193,6 +193,12 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
  *     side_stream under FULL(B) and SELECT(B) under the REUSE launch; `stream` finally
  *     waits for side_stream. Ignored without REUSE layers, when every FULL layer feeds a
  *     REUSE layer, or with sinks / recent.
+ *   fuse_select (with side_stream + fork_event and join_event): the selections of the FULL
+ *     layers some REUSE layer inherits from are made inside the FULL kernel (the last CTA
+ *     of each (layer, b, kv-head) pair selects that pair's row while other CTAs keep
+ *     streaming); those layers' pairs come first in the grid. The other FULL layers'
+ *     SELECT runs on side_stream under the REUSE launch. Tensor-core path, sel_group 1,
+ *     no sinks / recent; otherwise the plain or side-stream schedule applies.
  *   reuse_wait_event: the REUSE launches wait on it (e.g. REUSE layers' queries arriving).
  *   layer_events: L entries (NULL allowed); layer_events[l] is recorded as soon as out[l] is
  *     final — FULL layers right after their FULL launch, REUSE layers after the REUSE
@@ -202,6 +208,7 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
  * Workspace: as hylra_decode_step.
  */
 typedef struct hylra_step_options {
+  int32_t fuse_select; /* !=0 (with side_stream, fork_event, join_event): see below */
   void* side_stream;
   void* fork_event;   /* stream -> side: FULL(A) done   */
   void* select_event; /* side -> stream: SELECT(A) done */

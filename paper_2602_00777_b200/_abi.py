@@ -81,6 +81,7 @@ class StepOptions(ctypes.Structure):
     """Mirror of `hylra_step_options` (include/hylra.h)."""
 
     _fields_ = [
+        ("fuse_select", ctypes.c_int32),
         ("side_stream", ctypes.c_void_p),
         ("fork_event", ctypes.c_void_p),
         ("select_event", ctypes.c_void_p),

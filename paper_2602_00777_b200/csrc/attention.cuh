@@ -15,10 +15,10 @@
 #pragma once
 
 #include "common.cuh"
+#include "select.cuh"
 
 namespace hylra {
 
-constexpr int kMaxSlots = 64;   // layer slots per launch
 constexpr int kTileRows = 64;   // rows per pipeline stage
 constexpr int kConsumerWarps = 4;
 // REUSE producer warps: the gather's cp.async rows of a stage are split between them
@@ -59,6 +59,9 @@ struct AttnParams {
   int layers[kMaxSlots];     // q / out layer of each slot
   int kv_layers[kMaxSlots];  // K / V layer of each slot (differs for split caches)
   int src_slot[kMaxSlots];
+  // FULL: launch-local slots [0, fuse_select) select their rows inside the kernel (the last
+  // CTA of a pair, once the pair's score row is complete); SelectParams come alongside
+  int fuse_select;
 };
 
 // Stage n selection indices from global into shared memory, validated (out-of-range ->
@@ -94,7 +97,7 @@ __device__ __forceinline__ void stage_indices(const int32_t* __restrict__ src, i
 // sm_m/sm_l: [4][16], sm_o: [4][16][D] partial states of the 4 consumer warps, with
 // m in raw dot units (scaled by scale_log2 inside exp2).
 template <int D>
-__device__ __forceinline__ void merge_and_store(const AttnParams& p, int slot, int b, int kh,
+__device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, int b, int kh,
                                                 int split, const float* sm_m,
                                                 const float* sm_l, const float* sm_o,
                                                 int tid, int nthreads, int bar_id) {
@@ -121,7 +124,7 @@ __device__ __forceinline__ void merge_and_store(const AttnParams& p, int slot, i
       if (!isfinite(val)) atomicOr(p.flags, 2);  // NaN/inf in q, K or V
       out_base[g * D + d] = val;
     }
-    return;
+    return true;
   }
   const int part = pair * p.splits + split;
   float* wo = p.ws_o + (int64_t)part * G * D;
@@ -153,7 +156,7 @@ __device__ __forceinline__ void merge_and_store(const AttnParams& p, int slot, i
     s_last = (prev == p.splits - 1);
   }
   asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
-  if (!s_last) return;
+  if (!s_last) return false;
   __threadfence();
   const float* po = p.ws_o + (int64_t)pair * p.splits * G * D;
   const float* pml = p.ws_ml + (int64_t)pair * p.splits * G * 2;
@@ -173,6 +176,7 @@ __device__ __forceinline__ void merge_and_store(const AttnParams& p, int slot, i
     out_base[g * D + d] = val;
   }
   if (tid == 0) p.counters[pair] = 0;  // leave the workspace zeroed for the next call
+  return true;
 }
 
 // ---------------------------------------------------------------------------------
@@ -333,7 +337,8 @@ __device__ __forceinline__ void mma_consume_tile(const AttnParams& p, uint32_t k
 template <int D, bool GATHER, bool GBIG, int STAGES>
 __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     attn_mma_kernel(const __grid_constant__ CUtensorMap tmk,
-                    const __grid_constant__ CUtensorMap tmv, const AttnParams p) {
+                    const __grid_constant__ CUtensorMap tmv, const AttnParams p,
+                    const __grid_constant__ SelectParams sp) {
   using SM = MmaSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -567,7 +572,19 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
           make_float2(o[j][2], o[j][3]);
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
-  merge_and_store<D>(p, slot, b, kh, split, sm_m, sm_l, sm_o, threadIdx.x, 128, 1);
+  const bool final_cta = merge_and_store<D>(p, slot, b, kh, split, sm_m, sm_l, sm_o,
+                                            threadIdx.x, 128, 1);
+  if constexpr (!GATHER) {
+    // fused selection: the pair's score row is complete (every split wrote its part before
+    // the counter), so its top-k is taken right here while other CTAs keep streaming;
+    // the drained pipeline buffers hold the select's shared memory
+    if (final_cta && slot < p.fuse_select) {
+      __shared__ Red sel_red;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // merge reads of smem are done
+      __threadfence();
+      select_row<kConsumerWarps * 32>(sp, kh, b, slot, smem, sel_red, false);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------

@@ -10,6 +10,7 @@
 
 namespace hylra {
 
+constexpr int kMaxSlots = 64;   // layer slots per launch
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

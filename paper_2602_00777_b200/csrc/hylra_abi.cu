@@ -250,7 +250,7 @@ size_t mma_smem_bytes() {
 
 template <int D, bool GATHER, bool GBIG>
 cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const AttnParams& p) {
+                       const AttnParams& p, const SelectParams& sp) {
   constexpr int S = mma_stages<D, GATHER, GBIG>();
   auto kern = attn_mma_kernel<D, GATHER, GBIG, S>;
   const size_t smem = mma_smem_bytes<D, GATHER, GBIG>();
@@ -260,7 +260,7 @@ cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const 
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  return launch_pdl(kern, grid, dim3(attn_threads<GATHER>()), smem, st, tk, tv, p);
+  return launch_pdl(kern, grid, dim3(attn_threads<GATHER>()), smem, st, tk, tv, p, sp);
 }
 
 template <typename T, int D, int GM, bool GATHER>
@@ -290,7 +290,8 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
                      const int32_t* layer_ids, const int32_t* src_slots, const int32_t* idx,
                      const int32_t* counts, int k_stride, int sel_group, float* out,
                      float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st,
-                     const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0) {
+                     const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0,
+                     const SelectParams* fused = nullptr, int fuse_nslots = 0) {
   if (int e = check_geometry(g)) return e;
   if (n_layers < 1 || n_layers > kMaxSlots)
     return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", n_layers, kMaxSlots);
@@ -335,6 +336,9 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   }
   dim3 grid(lay.splits, g->kv_heads, g->batch * n_layers);
   cudaError_t ce;
+  static const SelectParams no_select{};
+  const SelectParams& sp = fused ? *fused : no_select;
+  p.fuse_select = (fused && !gather && use_mma_path(g)) ? fuse_nslots : 0;
   if (use_mma_path(g)) {
     CUtensorMap tk{}, tv{};
     if (!gather) {
@@ -343,15 +347,15 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
     }
     const bool big = G > 8;
     if (g->head_dim == 128) {
-      if (gather) ce = big ? launch_mma<128, true, true>(grid, st, tk, tv, p)
-                           : launch_mma<128, true, false>(grid, st, tk, tv, p);
-      else ce = big ? launch_mma<128, false, true>(grid, st, tk, tv, p)
-                    : launch_mma<128, false, false>(grid, st, tk, tv, p);
+      if (gather) ce = big ? launch_mma<128, true, true>(grid, st, tk, tv, p, sp)
+                           : launch_mma<128, true, false>(grid, st, tk, tv, p, sp);
+      else ce = big ? launch_mma<128, false, true>(grid, st, tk, tv, p, sp)
+                    : launch_mma<128, false, false>(grid, st, tk, tv, p, sp);
     } else {
-      if (gather) ce = big ? launch_mma<64, true, true>(grid, st, tk, tv, p)
-                           : launch_mma<64, true, false>(grid, st, tk, tv, p);
-      else ce = big ? launch_mma<64, false, true>(grid, st, tk, tv, p)
-                    : launch_mma<64, false, false>(grid, st, tk, tv, p);
+      if (gather) ce = big ? launch_mma<64, true, true>(grid, st, tk, tv, p, sp)
+                           : launch_mma<64, true, false>(grid, st, tk, tv, p, sp);
+      else ce = big ? launch_mma<64, false, true>(grid, st, tk, tv, p, sp)
+                    : launch_mma<64, false, false>(grid, st, tk, tv, p, sp);
     }
   } else if (g->dtype == HYLRA_F32) {
     ce = gather ? dispatch_simt<float, true>(g->head_dim, G, grid, st, p)
@@ -399,11 +403,13 @@ struct BlockRows {  // block mode: rows are pooled block scores
   const float* tok_scores = nullptr;  // the token scores they were pooled from
 };
 
-int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
-                  int budget, int sel_group, const void* q, const void* k,
-                  const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
-                  int* flags, cudaStream_t st, const BlockRows& br = BlockRows(),
-                  const int32_t* kv_layer_ids = nullptr, const int32_t* out_slots = nullptr) {
+// Validated SelectParams for n_slots score slots (shared by the SELECT kernel and the
+// selection fused into the FULL kernel).
+int build_select_params(SelectParams* out, const hylra_geometry* g, const float* scores,
+                        int n_slots, int n_valid, int budget, int sel_group, const void* q,
+                        const void* k, const int32_t* layer_ids, int32_t* idx, int k_stride,
+                        int32_t* info, int* flags, const BlockRows& br,
+                        const int32_t* kv_layer_ids, const int32_t* out_slots) {
   if (int e = check_geometry(g)) return e;
   if (budget < 1) return fail(HYLRA_ERR_INVALID_INPUT, "budget must be >= 1, got %d", budget);
   if (n_slots < 1 || n_slots > kMaxSlots)
@@ -446,8 +452,23 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
     p.kv_layers[i] = kv_layer_ids ? kv_layer_ids[i] : l;
     p.out_slot[i] = out_slots ? out_slots[i] : i;
   }
+  *out = p;
+  return HYLRA_OK;
+}
+
+int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int n_valid,
+                  int budget, int sel_group, const void* q, const void* k,
+                  const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
+                  int* flags, cudaStream_t st, const BlockRows& br = BlockRows(),
+                  const int32_t* kv_layer_ids = nullptr, const int32_t* out_slots = nullptr,
+                  int force_nt = 0) {
+  SelectParams p{};
+  if (int e = build_select_params(&p, g, scores, n_slots, n_valid, budget, sel_group, q, k,
+                                  layer_ids, idx, k_stride, info, flags, br, kv_layer_ids,
+                                  out_slots))
+    return e;
   dim3 grid(p.n_groups, g->batch, n_slots);
-  const int nt = select_threads(p.n_groups * g->batch * n_slots);
+  const int nt = force_nt ? force_nt : select_threads(p.n_groups * g->batch * n_slots);
   cudaError_t ce;
   if (nt == 1024) ce = launch_select_nt<1024>(grid, sel_smem_bytes(n_valid, 1024), st, p);
   else if (nt == 512) ce = launch_select_nt<512>(grid, sel_smem_bytes(n_valid, 512), st, p);
@@ -621,8 +642,18 @@ struct SplitKv {
   const void *kf, *vf, *kr, *vr;
 };
 
+// The fused select of the FULL kernel uses the drained pipeline buffers as its shared
+// memory (128 threads).
+bool fused_select_fits(const hylra_geometry* g, int n_valid) {
+  const size_t ring = g->head_dim == 128
+                          ? (size_t)mma_stages<128, false, false>() * MmaSmem<128>::kStageBytes
+                          : (size_t)mma_stages<64, false, false>() * MmaSmem<64>::kStageBytes;
+  return n_valid <= kSelMaxTokens && sel_smem_bytes(n_valid, kConsumerWarps * 32) <= ring;
+}
+
 // Options of hylra_decode_step_ex (all optional; see include/hylra.h).
 struct StepOpts {
+  bool fuse = false;  // selects of the FULL layers feeding REUSE fused into the FULL kernel
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, select = nullptr, full = nullptr, join = nullptr;
   cudaEvent_t reuse_wait = nullptr;
@@ -671,7 +702,11 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     (feeds ? a_kv : b_kv).push_back(i);  // compact KV index (split caches) = FULL slot
   }
   const bool dual = o.side && !a_ids.empty() && !b_ids.empty() && !s.aug_stride;
-  if (o.side && !(o.fork && o.select && o.full && o.join))
+  // fused selects (StepOpts::fuse): tensor-core FULL path, per-KV-head rows, A non-empty;
+  // the select's shared memory must fit in the FULL kernel's pipeline buffers
+  const bool fused_sel = o.fuse && o.side && !a_ids.empty() && !s.aug_stride && sel_group == 1 &&
+                         use_mma_path(g) && fused_select_fits(g, n_valid);
+  if (o.side && !(o.fork && o.join && (o.fuse || (o.select && o.full))))
     return fail(HYLRA_ERR_CONFIGURATION, "a side stream needs its four events");
   // groups of FULL layers: one launch (all FULL layers) or two (A then B)
   struct Group {
@@ -685,22 +720,23 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   const Group g_all{&s.full_ids, &all_slot, &all_kv, 0};
   const Group g_a{&a_ids, &a_slot, &a_kv, 0};
   const Group g_b{&b_ids, &b_slot, &b_kv, (int)a_ids.size()};
-  auto full = [&](const Group& gr, cudaStream_t sx) -> int {
+  auto full = [&](const Group& gr, cudaStream_t sx, const SelectParams* fused = nullptr,
+                  int n_fused = 0) -> int {
     const int n = (int)gr.ids->size();
     if (int e = launch_attention(g, false, q, kf, vf, n_valid, n_valid, n, gr.ids->data(),
                                  nullptr, nullptr, nullptr, 0, 1, out,
                                  scores + gr.score_base * score_slot, aws, s.attn_bytes, flags, sx,
-                                 split ? gr.kv->data() : nullptr, nf))
+                                 split ? gr.kv->data() : nullptr, nf, fused, n_fused))
       return e;
     for (int l : *gr.ids)
       if (int e = record(o.layer_events, l, sx)) return e;
     return HYLRA_OK;
   };
-  auto select = [&](const Group& gr, cudaStream_t sx) -> int {
+  auto select = [&](const Group& gr, cudaStream_t sx, int force_nt = 0) -> int {
     return launch_select(g, scores + gr.score_base * score_slot, (int)gr.ids->size(), n_valid,
                          budget, sel_group, refine ? q : nullptr, refine ? kf : nullptr,
                          gr.ids->data(), idx, k_stride, nullptr, flags, sx, BlockRows(),
-                         split ? gr.kv->data() : nullptr, gr.slots->data());
+                         split ? gr.kv->data() : nullptr, gr.slots->data(), force_nt);
   };
   auto reuse = [&](cudaStream_t sx) -> int {
     if (s.reuse_ids.empty()) return HYLRA_OK;
@@ -743,7 +779,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     return HYLRA_OK;
   };
 
-  if (!dual) {
+  if (!dual && !fused_sel) {
     if (int e = full(g_all, st)) return e;
     if (int e = select(g_all, st)) return e;
     return reuse(st);
@@ -754,6 +790,31 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   auto wait = [](cudaStream_t sx, cudaEvent_t ev) {
     return cuda_check(cudaStreamWaitEvent(sx, ev, 0), "stream wait event");
   };
+  if (fused_sel) {
+    // one FULL launch over A then B; A's selections are taken inside it by the last CTA of
+    // each pair (A's pairs come first in the grid, so those selects run under B's
+    // streaming); SELECT(B) runs on the side stream under the REUSE launch
+    std::vector<int32_t> ab_ids(a_ids), ab_slot(a_slot), ab_kv(a_kv);
+    ab_ids.insert(ab_ids.end(), b_ids.begin(), b_ids.end());
+    ab_slot.insert(ab_slot.end(), b_slot.begin(), b_slot.end());
+    ab_kv.insert(ab_kv.end(), b_kv.begin(), b_kv.end());
+    const Group g_ab{&ab_ids, &ab_slot, &ab_kv, 0};
+    SelectParams sp{};
+    if (int e = build_select_params(&sp, g, scores, (int)ab_ids.size(), n_valid, budget,
+                                    sel_group, refine ? q : nullptr, refine ? kf : nullptr,
+                                    ab_ids.data(), idx, k_stride, nullptr, flags, BlockRows(),
+                                    split ? ab_kv.data() : nullptr, ab_slot.data()))
+      return e;
+    if (int e = full(g_ab, st, &sp, (int)a_ids.size())) return e;
+    if (!b_ids.empty()) {
+      if (int e = rec(o.fork, st)) return e;
+      if (int e = wait(o.side, o.fork)) return e;
+      if (int e = select(g_b, o.side)) return e;
+      if (int e = rec(o.join, o.side)) return e;
+    }
+    if (int e = reuse(st)) return e;
+    return b_ids.empty() ? HYLRA_OK : wait(st, o.join);
+  }
   // side: SELECT(A) once FULL(A) is done, SELECT(B) once FULL(B) is done
   if (int e = full(g_a, st)) return e;
   if (int e = rec(o.fork, st)) return e;
@@ -862,6 +923,7 @@ int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, 
                          const hylra_step_options* opt) {
   StepOpts o;
   if (opt) {
+    o.fuse = opt->fuse_select != 0;
     o.side = static_cast<cudaStream_t>(opt->side_stream);
     o.fork = static_cast<cudaEvent_t>(opt->fork_event);
     o.select = static_cast<cudaEvent_t>(opt->select_event);

@@ -69,7 +69,7 @@ __host__ __device__ constexpr size_t sel_bitmap_bytes(int n, int nt) {
 // Band list: indices of the scores inside the bracket [lo, hi], collected by pass B so the
 // second pass reads only them (4096 entries per 256 threads; it shares the small-row keys
 // region, which the large-row path does not otherwise use before the window step).
-__host__ __device__ constexpr int sel_band_cap(int nt) { return 16 * nt; }
+__host__ __device__ constexpr int sel_band_cap(int nt) { return 16 * nt > 4096 ? 16 * nt : 4096; }
 __host__ __device__ constexpr size_t sel_keys_bytes(int nt) {
   return (size_t)(kSmallN * 8 > sel_band_cap(nt) * 4 ? kSmallN * 8 : sel_band_cap(nt) * 4);
 }
@@ -115,6 +115,14 @@ struct Red {
   unsigned hist256[256];
 };
 
+// The CTA-wide barrier of the select code: barrier 0 over the NT threads running it — the
+// whole CTA of topk_select_kernel, or the 4 consumer warps of the FULL kernel when the
+// selection is fused into it (its producer warp has exited by then).
+template <int NT>
+__device__ __forceinline__ void sel_sync() {
+  asm volatile("bar.sync 0, %0;" ::"n"(NT) : "memory");
+}
+
 // Block reductions: warps reduce with shuffles, the NT/32 warp partials go through shared
 // memory and every warp reduces them again with shuffles (one shared load per lane instead
 // of NT/32 per thread — the 1024-thread CTAs spent ~20% of their instructions there).
@@ -128,18 +136,18 @@ template <int NT>
 __device__ __forceinline__ int block_sum_int(int v, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_sum_int(v);
-  __syncthreads();
+  sel_sync<NT>();
   if (lane == 0) r.i[warp] = v;
-  __syncthreads();
+  sel_sync<NT>();
   return warp_sum_int(lane < NT / 32 ? r.i[lane] : 0);
 }
 template <int NT>
 __device__ __forceinline__ float block_max_float(float v, Red& r) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_max(v);
-  __syncthreads();
+  sel_sync<NT>();
   if (lane == 0) r.f[warp] = v;
-  __syncthreads();
+  sel_sync<NT>();
   return warp_max(lane < NT / 32 ? r.f[lane] : -INFINITY);
 }
 
@@ -153,7 +161,7 @@ __device__ __forceinline__ void block_reduce_pass_b(float& a, float& b, int& c, 
   c = warp_sum_int(c);
   d = warp_sum_int(d);
   e = warp_sum_int(e);
-  __syncthreads();
+  sel_sync<NT>();
   if (lane == 0) {
     r.f[warp] = a;
     r.pf[warp] = b;
@@ -161,7 +169,7 @@ __device__ __forceinline__ void block_reduce_pass_b(float& a, float& b, int& c, 
     r.wt[warp] = d;
     r.pi[warp] = e;
   }
-  __syncthreads();
+  sel_sync<NT>();
   const bool in = lane < NT / 32;
   a = warp_max(in ? r.f[lane] : -INFINITY);
   b = warp_max(in ? r.pf[lane] : -INFINITY);
@@ -180,9 +188,9 @@ __device__ __forceinline__ int block_scan(int v, int* total, Red& r) {
     const int y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  __syncthreads();
+  sel_sync<NT>();
   if (lane == 31) r.wt[warp] = x;
-  __syncthreads();
+  sel_sync<NT>();
   // lane l scans the warp totals 0..l
   int t = lane < NT / 32 ? r.wt[lane] : 0;
 #pragma unroll
@@ -215,14 +223,14 @@ struct RowReader {
   int64_t hstride;    // elements between the group's kv-head rows
   int sg;
   __device__ __forceinline__ float at(int i) const {
-    float s = __ldg(base + i);
-    for (int h = 1; h < sg; ++h) s += __ldg(base + h * hstride + i);
+    float s = __ldcg(base + i);
+    for (int h = 1; h < sg; ++h) s += __ldcg(base + h * hstride + i);
     return s;
   }
   __device__ __forceinline__ float4 at4(int i4) const {
-    float4 s = __ldg(reinterpret_cast<const float4*>(base) + i4);
+    float4 s = __ldcg(reinterpret_cast<const float4*>(base) + i4);
     for (int h = 1; h < sg; ++h) {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(base + h * hstride) + i4);
+      const float4 t = __ldcg(reinterpret_cast<const float4*>(base + h * hstride) + i4);
       s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
     }
     return s;
@@ -316,7 +324,7 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
   const int bs = p.block_size;
   const int total = n * bs;
   if (threadIdx.x == 0) s_cnt = p.tok_scores ? 0 : kSmallN + 1;
-  __syncthreads();
+  sel_sync<NT>();
   if (p.tok_scores) {
     const float* trow = p.tok_scores +
                         ((int64_t)(slot * p.B + b) * p.Hkv + grp * p.sel_group) * p.tok_row_stride;
@@ -332,12 +340,12 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
       }
     }
   }
-  __syncthreads();
+  sel_sync<NT>();
   const bool listed = s_cnt <= kSmallN;
   const int items = listed ? s_cnt : total;
   unsigned long long* vk = reinterpret_cast<unsigned long long*>(vals);
   for (int c = threadIdx.x; c < n; c += NT) vk[c] = 0ull;
-  __syncthreads();
+  sel_sync<NT>();
   for (int e0 = warp * kTpw; e0 < items; e0 += (NT / 32) * kTpw) {  // warp-uniform trips
     const int e = min(e0 + slot_in_warp, items - 1);
     int c, tok;
@@ -353,7 +361,7 @@ __device__ void rescore_f64_blocks(const SelectParams& p, int slot, int b, int g
                                        ok ? tok : blocks[c] * bs);
     if (ok && sub == 0) atomicMax(vk + c, f64_key(agg));
   }
-  __syncthreads();
+  sel_sync<NT>();
   for (int c = threadIdx.x; c < n; c += NT) vals[c] = key_f64(vk[c]);
 }
 
@@ -367,7 +375,7 @@ __device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, f
   int krem = rank;
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int j = tid; j < 256; j += NT) r.hist256[j] = 0;
-    __syncthreads();
+    sel_sync<NT>();
     for (int base = 0; base < n; base += NT) {
       const int j = base + tid;
       bool act = false;
@@ -383,7 +391,7 @@ __device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, f
         if (lane == __ffs(peers) - 1) atomicAdd(r.hist256 + dig, (unsigned)__popc(peers));
       }
     }
-    __syncthreads();
+    sel_sync<NT>();
     if (tid == 0) {
       int acc = 0, d = 255;
       for (; d > 0; --d) {
@@ -393,11 +401,11 @@ __device__ void radix_select_row(const RowReader& rd, int n, int rank, Red& r, f
       r.misc[8] = d;
       r.misc[9] = acc;
     }
-    __syncthreads();
+    sel_sync<NT>();
     krem -= r.misc[9];
     prefix |= (uint32_t)r.misc[8] << shift;
     mask |= 255u << shift;
-    __syncthreads();
+    sel_sync<NT>();
   }
   *T_out = key_float(prefix);
   *gt_out = rank - krem;
@@ -417,7 +425,7 @@ __device__ void bitonic_sort_desc(uint64_t* a, int np) {
           a[j] = x;
         }
       }
-      __syncthreads();
+      sel_sync<NT>();
     }
   }
 }
@@ -449,7 +457,7 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
   const int bad = block_sum_int<NT>(nanacc != nanacc ? 1 : 0, red);
   mx = block_max_float<NT>(mx, red);
   if (bad && tid == 0) atomicOr(p.flags, 2);
-  __syncthreads();
+  sel_sync<NT>();
   bitonic_sort_desc<NT>(keys, np);
   auto val = [&](int pos) { return key_float((uint32_t)(keys[pos] >> 32)); };
   auto tok = [&](int pos) { return (int)(~(uint32_t)keys[pos]); };
@@ -485,13 +493,15 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
 }
 
 // ----------------------------------------------------------------------------- kernel
+// One selection row (slot, b, grp) by the NT threads 0..NT-1 of the calling CTA, with
+// sel_smem_bytes(n_valid, NT) bytes of shared memory at sraw. Called by
+// topk_select_kernel (one CTA per row) and, fused, by the FULL kernel's last CTA of a
+// pair (NT = 128 consumer threads). release: let dependent launches start before the
+// compaction (standalone kernel only).
 template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const SelectParams p) {
+__device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint8_t* sraw,
+                           Red& red, bool release) {
   constexpr int kChunk = sel_chunk<NT>();
-  extern __shared__ __align__(16) uint8_t sraw[];
-  __shared__ Red red;
-
-  const int grp = blockIdx.x, b = blockIdx.y, slot = blockIdx.z;
   const int tid = threadIdx.x;
   const int n = p.n_valid;
   const int k = p.k_eff;
@@ -500,7 +510,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
   int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
   const SelSmem sm = carve<NT>(sraw, n);
-  pdl_wait();
   const long long t0 = clock64();
 
   RowReader rd;
@@ -569,7 +578,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
 #pragma unroll
       for (int j = 0; j < SPT; ++j)
         if (isfinite(smp[j])) atomicAdd(sm.hist + sbin(smp[j]), 1u);
-      __syncthreads();
+      sel_sync<NT>();
       // thread t scans sample bins 1023 - BPT t .. 1024 - BPT (t + 1) (descending)
       int hb[BPT], s4 = 0;
 #pragma unroll
@@ -589,14 +598,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
         acc += hb[j];
       }
       if (tid == 0) red.misc[3] = red.misc[5] = 0;
-      __syncthreads();
+      sel_sync<NT>();
       const int bh = red.misc[12], bl = red.misc[13];
       // hi: upper edge of the hi_i-th sample's bin (the top sample's bin: the sample max);
       // lo: lower edge of the lo_i-th sample's bin
       hi = (bh >= 1023) ? smax : smin + (float)(bh + 1) / sscale;
       lo = smin + (float)bl / sscale;
       for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
-      __syncthreads();
+      sel_sync<NT>();
     }
     t1 = clock64();
 
@@ -619,7 +628,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
       float nanacc = 0.f;
       int cg = 0, ci = 0;
       if (tid == 0) red.misc[10] = 0;  // band list length
-      __syncthreads();
+      sel_sync<NT>();
       auto pass_b = [&](int c, bool full) {
         const int w4 = (c * kChunk + tid * 32) >> 2;
         float4 vv[8];
@@ -679,7 +688,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
         lo = vmin;
       }
       for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
-      __syncthreads();
+      sel_sync<NT>();
     }
     if (bad && tid == 0) atomicOr(p.flags, 2);
     auto bin_of = [&](float v) { return min(kBins - 1, (int)((v - lo) * scale)); };
@@ -713,7 +722,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
           acc += hb[j];
         }
       }
-      __syncthreads();
+      sel_sync<NT>();
       const int bstar = red.misc[1], cum_above = red.misc[2];
       // candidate bins [b_lo, b_hi]: b* widened by the refinement tolerance
       const int wb = refine ? (int)ceilf(tau * scale) + 1 : 0;
@@ -742,7 +751,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
           red.misc[6 + tid] = __float_as_int(key_float(z));
         }
       }
-      __syncthreads();
+      sel_sync<NT>();
       const float v_hi = __int_as_float(red.misc[6]);  // v >= v_hi  <=>  bin > b_hi
       const float v_lo = __int_as_float(red.misc[7]);  // v >= v_lo  <=>  bin >= b_lo
       auto pass_d = [&](int c, bool full) {
@@ -802,7 +811,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
         for (int c = 0; c < nfull; ++c) pass_d(c, true);
         if (nfull < nch) pass_d(nfull, false);
       }
-      __syncthreads();
+      sel_sync<NT>();
       const int nc = red.misc[3];
       fast = nc >= 1 && nc <= kCandCap;
       if (!fast) why = 64;
@@ -821,7 +830,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
           }
           if (gt < r2 && r2 <= ge) red.misc[4] = __float_as_int(vj);
         }
-        __syncthreads();
+        sel_sync<NT>();
         T = __int_as_float(red.misc[4]);
         lo_w = refine ? T - tau : T;
         hi_w = refine ? T + tau : T;
@@ -847,7 +856,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
               ++abv;
             }
           }
-          __syncthreads();
+          sel_sync<NT>();
           const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
           if (in) {
             sm.cv[pos] = v;
@@ -868,7 +877,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
       hi_w = refine ? T + tau : T;
       for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
       if (tid == 0) red.misc[5] = 0;
-      __syncthreads();
+      sel_sync<NT>();
       int abv = 0;
       for (int base = 0; base < n; base += NT) {
         const int i = base + tid;
@@ -891,7 +900,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
         if (refine && tid == 0) atomicOr(p.flags, 4);
         if (refine) {
           for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
-          __syncthreads();
+          sel_sync<NT>();
           for (int base = 0; base < n; base += NT) {
             const int i = base + tid;
             if (i < n && rd.at(i) > T) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
@@ -915,12 +924,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
 
   // ---- window: re-score (refine) and keep the top k - above_w by (score desc, index asc)
   if (nw > 0) {
-    __syncthreads();
+    sel_sync<NT>();
     if (refine) {
       if (p.block_size > 1)
         rescore_f64_blocks<NT>(p, slot, b, grp, sm.ci, sm.cv, nw, tau_w, sm.keys);
       else rescore_f64<NT>(p, slot, b, grp, sm.ci, sm.cv, nw);
-      __syncthreads();
+      sel_sync<NT>();
     }
     const int take = k - above_w;
     for (int j = tid; j < nw; j += NT) {
@@ -934,9 +943,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
       if (rank < take) atomicOr(sm.bitmap + (ij >> 5), 1u << (ij & 31));
     }
   }
-  __syncthreads();
+  sel_sync<NT>();
 
-  pdl_launch_dependents();
+  if (release) pdl_launch_dependents();
   // ---- E. index-ordered compaction of the bitmap
   int run = 0;
   for (int c = 0; c < nch; ++c) {
@@ -964,6 +973,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
     info[6] = (int32_t)(t3 - t2);
     info[7] = (int32_t)(clock64() - t3);
   }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const SelectParams p) {
+  extern __shared__ __align__(16) uint8_t sraw[];
+  __shared__ Red red;
+  pdl_wait();
+  select_row<NT>(p, blockIdx.x, blockIdx.y, blockIdx.z, sraw, red, true);
 }
 
 }  // namespace hylra

@@ -73,7 +73,8 @@ class HybridDecoder:
 
     def __init__(self, policy, k_cache: torch.Tensor, v_cache: torch.Tensor, budget: int, *,
                  q_heads: int, sel_group: int = 1, refine: bool = True, block_size: int = 1,
-                 include_sinks: int = 0, include_recent: int = 0, dual_stream: bool = False):
+                 include_sinks: int = 0, include_recent: int = 0, dual_stream: bool = False,
+                 fuse_select: bool = True):
         self.actions = _actions_of(policy)
         if len(self.actions) != k_cache.shape[0]:
             raise ConfigurationError(
@@ -119,9 +120,18 @@ class HybridDecoder:
         feeds = [l for l in self.full_layers if l + 1 < L and self.actions[l + 1] is Action.REUSE]
         self.dual = (bool(dual_stream) and block_size == 1 and not (include_sinks or include_recent)
                      and 0 < len(feeds) < len(self.full_layers))
+        # fused selects (token mode): the FULL kernel selects the rows of the FULL layers that
+        # feed REUSE layers itself; the other FULL layers' SELECT runs on the side stream
+        # under the REUSE launch (hylra_decode_step_ex fuse_select; tensor-core path only)
+        self.fused = (bool(fuse_select) and block_size == 1 and not (include_sinks or include_recent)
+                      and len(feeds) > 0 and sel_group == 1 and k_cache.dtype == torch.bfloat16
+                      and d in (64, 128))
+        if self.fused:
+            self.dual = False
         self.kernels_per_step = ((2 + has_reuse + (has_reuse and bool(include_sinks or include_recent)))
-                                 if block_size == 1 else (3 + 2 * has_reuse)) + 2 * self.dual
-        if self.dual:
+                                 if block_size == 1 else (3 + 2 * has_reuse)) + 2 * self.dual \
+            - (self.fused and len(feeds) == len(self.full_layers))
+        if self.dual or self.fused:
             # high priority: select CTAs are dispatched ahead of the queued FULL / REUSE CTAs
             self._side = torch.cuda.Stream(device=k_cache.device, priority=-8)
             self._events = [torch.cuda.Event() for _ in range(4)]
@@ -168,7 +178,8 @@ class HybridDecoder:
             if self.ws.numel() < need:
                 self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
             opt = _abi.StepOptions()
-            if self.dual:
+            if self.dual or self.fused:
+                opt.fuse_select = int(self.fused)
                 opt.side_stream = self._side.cuda_stream
                 (opt.fork_event, opt.select_event, opt.full_event,
                  opt.join_event) = (e.cuda_event for e in self._events)
@@ -274,7 +285,7 @@ class OffloadDecoder(HybridDecoder):
         full_view = k_full[:1].expand((len(actions),) + tuple(k_full.shape[1:]))
         super().__init__(actions, full_view, full_view, budget, q_heads=q_heads,
                          sel_group=sel_group, refine=refine, include_sinks=include_sinks,
-                         include_recent=include_recent, dual_stream=False)
+                         include_recent=include_recent, dual_stream=False, fuse_select=False)
         self.k_full, self.v_full, self.k_reuse, self.v_reuse = k_full, v_full, k_reuse, v_reuse
         self.reuse_layers = tuple(l for l, a in enumerate(actions) if a is Action.REUSE)
 
@@ -335,7 +346,8 @@ class PipelinedDecoder(HybridDecoder):
     def __init__(self, policy, k_cache, v_cache, budget, *, q_heads, sel_group=1,
                  refine=True, schedule="pipelined"):
         super().__init__(policy, k_cache, v_cache, budget, q_heads=q_heads,
-                         sel_group=sel_group, refine=refine, dual_stream=False)
+                         sel_group=sel_group, refine=refine, dual_stream=False,
+                         fuse_select=False)
         if schedule not in ("pipelined", "sequential"):
             raise ConfigurationError(f"unknown schedule {schedule!r}")
         self.schedule = schedule

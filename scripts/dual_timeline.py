@@ -19,8 +19,9 @@ cfg = CONFIGS["cfg2"].with_(batch=a.batch)
 q, k, v = generate_torch(cfg, "cuda")
 L = cfg.layers
 acts = cfg.actions
-for dual in (False, True):
-    dec = HybridDecoder(acts, k, v, cfg.budget, q_heads=cfg.q_heads, dual_stream=dual)
+for dual in (False, True, "fused"):
+    dec = HybridDecoder(acts, k, v, cfg.budget, q_heads=cfg.q_heads, dual_stream=dual is True,
+                        fuse_select=dual == "fused")
     feeds = [l for l in range(L) if acts[l] == "full" and l + 1 < L and acts[l + 1] == "reuse"]
     others = [l for l in range(L) if acts[l] == "full" and l not in feeds]
     last_reuse = max(l for l in range(L) if acts[l] == "reuse")

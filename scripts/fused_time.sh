@@ -1,0 +1,6 @@
+for b in 8 1 4; do
+  timeout 600 python bench.py --no-extra --no-cpu --batch $b --steps 40 --schedule fusedsel > gpurun_out/b.json 2>gpurun_out/b.err
+  python -c "
+import json; d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1])
+print('B=$b', round(d['ms_per_step'],4), {k: round(v['ms_per_step'],4) for k,v in d['schedules'].items()}, 'e2e', round(d['e2e']['ms_per_step'],4))" || tail -5 gpurun_out/b.err
+done

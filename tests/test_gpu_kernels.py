@@ -322,15 +322,15 @@ def test_decode_loop_host_io_graph(zero_copy):
     ("full", "full", "reuse", "reuse"),
 ])
 def test_dual_stream_step_matches_single_stream(actions):
-    """hylra_decode_step_ex with a side stream: FULL layers feeding REUSE layers first, their
-    SELECT + REUSE on the side stream under the other FULL layers. Same selections; outputs
+    """hylra_decode_step_ex with a side stream (no fusion): FULL(A) -> FULL(B) -> REUSE on the
+    caller's stream, SELECT(A) / SELECT(B) on the side stream. Same selections; outputs
     within split-K rounding of the one-stream step; also under CUDA-graph capture."""
     L = len(actions)
     B, Hq, Hkv, d, cap, budget = 2, 16, 4, 128, 4096, 256
     q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=31, planted=64)
     ref = HybridDecoder(actions, k, v, budget, q_heads=Hq).step(q, cap)
     ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
-    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, dual_stream=True)
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, dual_stream=True, fuse_select=False)
     assert dec.dual
     res = dec.step(q, cap)
     torch.cuda.synchronize()
@@ -352,6 +352,47 @@ def test_dual_stream_step_matches_single_stream(actions):
     torch.cuda.synchronize()
     assert torch.equal(dec.idx[..., :budget], ref_idx)
     assert max_head_err(dec.out.double().cpu().numpy(), r) < 4e-3
+
+
+@pytest.mark.parametrize("actions,d,refine,n", [
+    (("full", "reuse", "full", "full", "reuse", "reuse", "full", "reuse", "full", "full"), 128, True, 4096),
+    (("full", "full", "reuse", "reuse"), 64, True, 3001),
+    (("full", "reuse", "full", "reuse"), 128, False, 4096),   # every FULL layer feeds REUSE
+    (("full", "full", "reuse", "full", "reuse"), 128, True, 70000),  # 3 bitmap chunks/row
+])
+def test_fused_select_step_equals_unfused(actions, d, refine, n):
+    """hylra_decode_step_ex fuse_select: the FULL kernel selects the rows of the layers that
+    feed REUSE layers itself (last CTA of each pair), the other selections run on the side
+    stream under REUSE. Same launches and split-K partitions as the plain step, so outputs
+    and selections are bit-identical — eager and under CUDA-graph capture."""
+    L = len(actions)
+    B, Hq, Hkv, budget = 2, 16, 4, 256
+    cap = n
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=41, planted=64)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine,
+                        fuse_select=False).step(q, n)
+    ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine, fuse_select=True)
+    assert dec.fused
+    res = dec.step(q, n)
+    torch.cuda.synchronize()
+    dec.check_flags()
+    assert torch.equal(res.selections, ref_idx)
+    assert torch.equal(res.outputs, ref_out)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dec.step(q, n)
+    torch.cuda.current_stream().wait_stream(s)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        dec.step(q, n)
+    dec.out.zero_()
+    dec.idx.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(dec.idx[..., :budget], ref_idx)
+    assert torch.equal(dec.out, ref_out)
 
 
 def test_step_layer_events_chunks_reuse():
