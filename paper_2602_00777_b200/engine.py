@@ -444,9 +444,10 @@ class DecodeLoop:
     `out_host` after the step completed.
 
     zero_copy=True (token-mode HybridDecoder): no copy operations at all — hylra_append_kv
-    reads the new rows from pinned host memory in place, the attention kernels read each
-    (layer, KV head)'s queries across the link when their CTAs start and store the outputs
-    straight into `out_host`: a 4-kernel graph. zero_copy=False: H2D copies, append, step,
+    reads the new rows from pinned host memory in place (the FULL layers' rows before the
+    FULL kernel, the REUSE layers' on a side stream under it, waited on by the REUSE
+    launch), the attention kernels read each (layer, KV head)'s queries across the link
+    when their CTAs start and store the outputs straight into `out_host`. zero_copy=False: H2D copies, append, step,
     D2H copy, serialised (the reference point).
     """
 
@@ -470,12 +471,31 @@ class DecodeLoop:
         if not self.zero_copy:
             self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
             self.kv_dev = torch.zeros((2, L, B, Hkv, d), dtype=dt, device=k.device)
+        acts = decoder.actions
+        self.full_layers = [l for l in range(L) if acts[l] is Action.FULL]
+        self.reuse_layers = [l for l in range(L) if acts[l] is Action.REUSE]
+        if self.zero_copy and self.reuse_layers:
+            # the REUSE layers' new rows are appended on a side stream under the FULL kernel;
+            # the REUSE launch waits on them (hylra_decode_step_ex reuse_wait_event)
+            self.side = torch.cuda.Stream(device=k.device)
+            self.ev_rows = torch.cuda.Event()
+            self.ev_rows.record()  # torch creates events lazily
 
     def _body(self):
         dec, pos = self.dec, self.pos
         if self.zero_copy:
-            dec.append(self.k_host, self.v_host, pos)
-            dec.step(self.q_host, pos + 1, out=self.out_host)
+            if not self.reuse_layers:
+                dec.append(self.k_host, self.v_host, pos)
+                dec.step(self.q_host, pos + 1, out=self.out_host)
+                return
+            main = torch.cuda.current_stream(dec.k.device)
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                dec.append(self.k_host, self.v_host, pos, self.reuse_layers)
+                self.ev_rows.record(self.side)
+            dec.append(self.k_host, self.v_host, pos, self.full_layers)
+            dec.step(self.q_host, pos + 1, out=self.out_host, reuse_wait=self.ev_rows)
+            main.wait_stream(self.side)
             return
         self.q_dev.copy_(self.q_host, non_blocking=True)
         self.kv_dev[0].copy_(self.k_host, non_blocking=True)

@@ -359,6 +359,8 @@ def test_dual_stream_step_matches_single_stream(actions):
     (("full", "full", "reuse", "reuse"), 64, True, 3001),
     (("full", "reuse", "full", "reuse"), 128, False, 4096),   # every FULL layer feeds REUSE
     (("full", "full", "reuse", "full", "reuse"), 128, True, 70000),  # 3 bitmap chunks/row
+    (("full", "reuse", "full", "reuse"), 128, True, 1500),    # small-row (sorting) path
+    (("full", "reuse", "reuse"), 64, True, 200),              # budget >= rows: every index
 ])
 def test_fused_select_step_equals_unfused(actions, d, refine, n):
     """hylra_decode_step_ex fuse_select: the FULL kernel selects the rows of the layers that
