@@ -75,6 +75,11 @@ def run_reference(a):
     rank = _env_int("RANK", 0)
     if rank != 0:
         return
+    # all host threads for OpenBLAS (torchrun exports OMP_NUM_THREADS=1, which OpenBLAS
+    # would otherwise follow); numpy is first imported below
+    n_threads = os.cpu_count() or 1
+    if "OPENBLAS_NUM_THREADS" not in os.environ:
+        os.environ["OPENBLAS_NUM_THREADS"] = str(n_threads)
     import numpy as np
 
     from oracle.cpu_baseline import full_layer, group_data, reuse_layer
