@@ -60,11 +60,13 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--schedule", default="fusedsel",
-                    choices=["fusedsel", "fused3", "dual", "pipelined", "sequential"],
+                    choices=["fusedsel", "single", "fused3", "dual", "pipelined", "sequential"],
                     help="fusedsel (default): FULL (selecting the rows of the layers that feed "
                          "REUSE inside the kernel) -> REUSE, the other selections on a side "
                          "stream; fused3: FULL -> SELECT -> REUSE on one stream; dual: "
-                         "selects on a side stream under split FULL launches")
+                         "selects on a side stream under split FULL launches; single: one "
+                         "launch per step (FULL items with every select fused, then REUSE items "
+                         "gated by per-row ready flags)")
     return ap.parse_args()
 
 
@@ -364,9 +366,10 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     n_valid = cfg.context
 
     def make(kind):
-        if kind in ("dual", "fused3", "fusedsel"):
+        if kind in ("dual", "fused3", "fusedsel", "single"):
             return HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1,
-                                 dual_stream=kind == "dual", fuse_select=kind == "fusedsel")
+                                 dual_stream=kind == "dual", fuse_select=kind == "fusedsel",
+                                 single_launch=kind == "single")
         return PipelinedDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1,
                                 schedule=kind)
 
@@ -419,7 +422,8 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     dec = make(a.schedule)
     graph = capture(dec)
     schedules = {}
-    for kind in [x for x in ("fused3", "fusedsel", "dual", "sequential") if x != a.schedule]:
+    for kind in [x for x in ("fused3", "fusedsel", "single", "dual", "sequential")
+                 if x != a.schedule]:
         d2 = make(kind)
         g2 = capture(d2)
         schedules[kind] = {"ms_per_step": time_replays(g2, d2, max(10, a.steps // 2)),

@@ -74,7 +74,7 @@ __device__ __forceinline__ void stage_indices(const int32_t* __restrict__ src, i
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * 32 + lane;
-      r[u] = (j < n) ? __ldg(src + j) : 0;
+      r[u] = (j < n) ? __ldcg(src + j) : 0;  // coherent: written earlier in a single-launch step
     }
     bool bad = false;
 #pragma unroll
@@ -201,8 +201,11 @@ __device__ __forceinline__ uint32_t swz_addr(uint32_t tile_base, int r, int chun
 
 // One 64-row stage for one consumer warp (its 16 rows): S = Q K^T on tensor cores, the
 // tail mask, the selection-score emission (FULL), the online softmax and O += P V.
+// Returns a word that depends on every V fragment loaded from the stage: the caller stores
+// it to shared memory before releasing the stage, so the release cannot overtake the last
+// ldmatrix reads (see the empty-barrier arrive below).
 template <int D, bool GATHER, bool GBIG>
-__device__ __forceinline__ void mma_consume_tile(const AttnParams& p, uint32_t kt, uint32_t vt,
+__device__ __forceinline__ uint32_t mma_consume_tile(const AttnParams& p, uint32_t kt, uint32_t vt,
                                                  const uint32_t (&qa)[D / 16][4],
                                                  float (&o)[D / 8][4], float& m0, float& m1,
                                                  float& l0, float& l1, int row0, int n_rows,
@@ -325,31 +328,70 @@ __device__ __forceinline__ void mma_consume_tile(const AttnParams& p, uint32_t k
   }
 
   // ---- O += P V
+  uint32_t dep = 0u;
 #pragma unroll
   for (int j = 0; j < D / 8; j += 2) {
     uint32_t b0, b1, b2, b3;
     ldsm_x4_t(swz_addr(vt, lv_row, j + lv_chk), b0, b1, b2, b3);
     mma_bf16_16816(o[j], pa0, pa1, pa2, pa3, b0, b1);
     mma_bf16_16816(o[j + 1], pa0, pa1, pa2, pa3, b2, b3);
+    dep ^= b0 ^ b1 ^ b2 ^ b3;
+  }
+  return dep;
+}
+
+// Consumer release of a pipeline stage. mbarrier.arrive does not wait for the warp's
+// outstanding ldmatrix reads: ptxas scheduled the arrive right after the last two V
+// ldmatrix of the stage (their HMMAs after it), so the producer could refill the stage
+// (TMA / cp.async) before those reads happened — V columns 96..127 of a tile then came
+// from the next tile, rarely, when a co-resident CTA loaded the shared-memory pipe
+// (scripts/determinism.py). The shared store of a word computed from every fragment
+// cannot issue before the ldmatrix results are back, and the arrive (release) is ordered
+// after the store.
+__device__ __forceinline__ void release_stage(uint64_t* empty, uint32_t* scratch, uint32_t dep,
+                                              int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(scratch)), "r"(dep) : "memory");
+    mbar_arrive(empty);
   }
 }
 
+// The 1024-B aligned start of the dynamic shared memory, as POINTER ARITHMETIC on the
+// __shared__ array: the compiler keeps the shared state space and emits LDS/STS/ATOMS for
+// every access through it (incl. the fused select's). Aligning through an integer cast loses
+// it: the select's histogram / bitmap atomics then compiled to generic ATOM.E.*.STRONG.GPU,
+// and with those, FULL pairs streaming on the same SM came out non-deterministic (a few
+// per launch, ~1e-3 off; scripts/determinism.py).
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
+// ready flag of a selection row: 0 until the fused select of its FULL pair has written the
+// row's indices (single-launch step); release by one thread after a CTA-scope barrier,
+// acquire by every reader lane
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+
+// One work item of the tensor-core kernels: the rows [split range] of one (layer slot, b,
+// kv-head) pair. `smem` is the 1024-B aligned dynamic shared memory. REUSE items with
+// `ready_wait` first wait for their selection row's ready flag (single-launch step); FULL
+// items with `ready_set` publish each fused selection's ready flag.
 template <int D, bool GATHER, bool GBIG, int STAGES>
-__global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
-    attn_mma_kernel(const __grid_constant__ CUtensorMap tmk,
-                    const __grid_constant__ CUtensorMap tmv, const AttnParams p,
-                    const __grid_constant__ SelectParams sp) {
+__device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUtensorMap& tmv,
+                                              const AttnParams& p, const SelectParams& sp,
+                                              uint8_t* smem, int split, int kh, int slot, int b,
+                                              const int* ready_wait, int* ready_set) {
   using SM = MmaSmem<D>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * SM::kStageBytes);
   uint64_t* empty_bar = full_bar + STAGES;
 
-  const int split = blockIdx.x;
-  const int kh = blockIdx.y;
-  const int slot = blockIdx.z / p.B;
-  const int b = blockIdx.z % p.B;
   const int layer = p.layers[slot];
   const int kvl = p.kv_layers[slot];
   const int warp = threadIdx.x >> 5;
@@ -378,7 +420,7 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
   if (warp >= kConsumerWarps) {
     // ------------------------------------------------------------- producer warp
     if constexpr (!GATHER) {
-      if (lane == 0) {
+      if (warp == kConsumerWarps && lane == 0) {
         tma_prefetch_desc(&tmk);
         tma_prefetch_desc(&tmv);
         const uint64_t pol = l2_policy_evict_first();
@@ -418,13 +460,20 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
       const int pos_begin = t_begin * kTileRows;
       const int n_pos = min(n_rows, t_end * kTileRows) - pos_begin;
       const bool staged = n_pos <= kIdxStage;
+      if (ready_wait != nullptr) {
+        // single-launch step: the selection row is written by a FULL item of the same grid
+        if (lane == 0)
+          while (ld_acquire_gpu(ready_wait) == 0) __nanosleep(64);
+        __syncwarp();
+        (void)ld_acquire_gpu(ready_wait);
+      }
       if (staged) {
         stage_indices(ib + pos_begin, n_pos, p.n_valid, sidx, p.flags, lane);
         __syncwarp();
       }
       auto row_at = [&](int pos) -> int {  // pos < n_rows
         if (staged) return sidx[pos - pos_begin];
-        int row = __ldg(ib + pos);
+        int row = __ldcg(ib + pos);
         if (row < 0 || row >= p.n_valid) {
           atomicOr(p.flags, 1);
           row = 0;
@@ -530,6 +579,8 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     score_row = p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + kh) * p.cap;
 
   const int rbase = warp * 16;
+  // one word per consumer warp between the barriers and the REUSE index staging area
+  uint32_t* release_word = reinterpret_cast<uint32_t*>(smem + STAGES * SM::kStageBytes + 128);
 
   for (int i = 0; i < n_my; ++i) {
     const int s = i % STAGES;
@@ -538,11 +589,9 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
     const uint32_t vt = kt + SM::kTileBytes;
     const int row0 = (t_begin + i) * kTileRows + rbase;  // first row of this warp's slice
 
-    mma_consume_tile<D, GATHER, GBIG>(p, kt, vt, qa, o, m0, m1, l0, l1, row0, n_rows,
-                                      score_row, lane);
-
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_bar + s);
+    const uint32_t dep = mma_consume_tile<D, GATHER, GBIG>(p, kt, vt, qa, o, m0, m1, l0, l1,
+                                                           row0, n_rows, score_row, lane);
+    release_stage(empty_bar + s, release_word + warp, dep, lane);
   }
   pdl_launch_dependents();
 
@@ -583,6 +632,83 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
       asm volatile("bar.sync 1, 128;" ::: "memory");  // merge reads of smem are done
       __threadfence();
       select_row<kConsumerWarps * 32>(sp, kh, b, slot, smem, sel_red, false);
+      if (ready_set != nullptr) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the row's indices are written
+        if (threadIdx.x == 0) {
+          __threadfence();
+          st_release_gpu(ready_set + (sp.out_slot[slot] * p.B + b) * p.n_groups + kh, 1);
+        }
+      }
+    }
+  }
+}
+
+template <int D, bool GATHER, bool GBIG, int STAGES>
+__global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
+    attn_mma_kernel(const __grid_constant__ CUtensorMap tmk,
+                    const __grid_constant__ CUtensorMap tmv, const AttnParams p,
+                    const __grid_constant__ SelectParams sp) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  attn_mma_item<D, GATHER, GBIG, STAGES>(tmk, tmv, p, sp, smem, blockIdx.x, blockIdx.y,
+                                         blockIdx.z / p.B, blockIdx.z % p.B, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------------------------------
+// Single-launch step: every FULL item (pairs of the layers some REUSE layer inherits from
+// first, selections fused), then every REUSE item, in ONE grid. Items are claimed in
+// ticket order (atomic counter) rather than by blockIdx, so a REUSE item waiting on its
+// selection's ready flag only ever waits on FULL items already claimed by resident CTAs:
+// no deadlock whatever the CTA dispatch order. The FULL tail (last splits, fused selects)
+// overlaps the REUSE gathers instead of ending a launch. The last CTA to finish resets the
+// ticket, the done counter and the ready flags (the workspace stays zeroed between steps).
+struct StepSync {
+  int* ctr;     // [0] ticket, [1] done
+  int* ready;   // [n_full][B][n_groups]
+  int n_ready;
+  int n_full_items, n_items;
+};
+
+template <int D, bool GBIG, int STAGES>
+__global__ void __launch_bounds__(attn_threads<true>(), 2)
+    step_mma_kernel(const __grid_constant__ CUtensorMap tmk,
+                    const __grid_constant__ CUtensorMap tmv, const AttnParams pf,
+                    const AttnParams pr, const __grid_constant__ SelectParams sp,
+                    const StepSync ss) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ int s_ticket;
+  pdl_wait();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(ss.ctr, 1);
+  __syncthreads();
+  int t = s_ticket;
+  if (t < ss.n_full_items) {
+    const int split = t % pf.splits;
+    t /= pf.splits;
+    const int kh = t % pf.Hkv;
+    t /= pf.Hkv;
+    attn_mma_item<D, false, GBIG, STAGES>(tmk, tmv, pf, sp, smem, split, kh, t / pf.B, t % pf.B,
+                                          nullptr, ss.ready);
+  } else {
+    t -= ss.n_full_items;
+    const int split = t % pr.splits;
+    t /= pr.splits;
+    const int kh = t % pr.Hkv;
+    t /= pr.Hkv;
+    const int slot = t / pr.B, b = t % pr.B;
+    const int* rw = ss.ready + (pr.src_slot[slot] * pr.B + b) * pr.n_groups + kh / pr.sel_group;
+    attn_mma_item<D, true, GBIG, STAGES>(tmk, tmv, pr, sp, smem, split, kh, slot, b, rw, nullptr);
+  }
+  // every warp is done with the item (barrier 2: barrier 0 belongs to the fused select's 128
+  // threads while the producer warps wait here)
+  asm volatile("bar.sync 2, %0;" ::"n"(32 * (kConsumerWarps + kGatherProducers)) : "memory");
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ss.ctr + 1, 1) == ss.n_items - 1) {
+      for (int i = 0; i < ss.n_ready; ++i) ss.ready[i] = 0;
+      ss.ctr[0] = 0;
+      ss.ctr[1] = 0;
+      __threadfence();
     }
   }
 }

@@ -263,6 +263,24 @@ cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const 
   return launch_pdl(kern, grid, dim3(attn_threads<GATHER>()), smem, st, tk, tv, p, sp);
 }
 
+// Single-launch step (FULL items with fused selects, then REUSE items; attention.cuh).
+template <int D, bool GBIG>
+cudaError_t launch_step_mma(int n_items, cudaStream_t st, const CUtensorMap& tk,
+                            const CUtensorMap& tv, const AttnParams& pf, const AttnParams& pr,
+                            const SelectParams& sp, const StepSync& ss) {
+  constexpr int S = mma_stages<D, true, GBIG>();
+  auto kern = step_mma_kernel<D, GBIG, S>;
+  const size_t smem = mma_smem_bytes<D, true, GBIG>();
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  return launch_pdl(kern, dim3(n_items), dim3(attn_threads<true>()), smem, st, tk, tv, pf, pr, sp,
+                    ss);
+}
+
 template <typename T, int D, int GM, bool GATHER>
 cudaError_t launch_simt(dim3 grid, cudaStream_t st, const AttnParams& p) {
   attn_simt_kernel<T, D, GM, GATHER><<<grid, 128, 0, st>>>(p);
@@ -285,13 +303,13 @@ cudaError_t dispatch_simt(int D, int G, dim3 grid, cudaStream_t st, const AttnPa
   return cudaErrorInvalidValue;
 }
 
-int launch_attention(const hylra_geometry* g, bool gather, const void* q, const void* k,
-                     const void* v, int n_valid, int n_rows, int n_layers,
-                     const int32_t* layer_ids, const int32_t* src_slots, const int32_t* idx,
-                     const int32_t* counts, int k_stride, int sel_group, float* out,
-                     float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st,
-                     const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0,
-                     const SelectParams* fused = nullptr, int fuse_nslots = 0) {
+// Validated AttnParams of one FULL or REUSE launch (or of one half of a single-launch step).
+int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* g, bool gather,
+                     const void* q, const void* k, const void* v, int n_valid, int n_rows,
+                     int n_layers, const int32_t* layer_ids, const int32_t* src_slots,
+                     const int32_t* idx, const int32_t* counts, int k_stride, int sel_group,
+                     float* out, float* scores, void* ws, size_t ws_bytes, int* flags,
+                     const int32_t* kv_layer_ids, int kv_layer_count) {
   if (int e = check_geometry(g)) return e;
   if (n_layers < 1 || n_layers > kMaxSlots)
     return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", n_layers, kMaxSlots);
@@ -334,6 +352,26 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
       return fail(HYLRA_ERR_CONFIGURATION, "KV layer %d out of range", p.kv_layers[i]);
     p.src_slot[i] = src_slots ? src_slots[i] : 0;
   }
+  *pp = p;
+  *lay_out = lay;
+  return HYLRA_OK;
+}
+
+int launch_attention(const hylra_geometry* g, bool gather, const void* q, const void* k,
+                     const void* v, int n_valid, int n_rows, int n_layers,
+                     const int32_t* layer_ids, const int32_t* src_slots, const int32_t* idx,
+                     const int32_t* counts, int k_stride, int sel_group, float* out,
+                     float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st,
+                     const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0,
+                     const SelectParams* fused = nullptr, int fuse_nslots = 0) {
+  AttnParams p{};
+  AttnLayout lay{};
+  if (int e = make_attn_params(&p, &lay, g, gather, q, k, v, n_valid, n_rows, n_layers, layer_ids,
+                               src_slots, idx, counts, k_stride, sel_group, out, scores, ws,
+                               ws_bytes, flags, kv_layer_ids, kv_layer_count))
+    return e;
+  const int G = g->q_heads / g->kv_heads;
+  const int n_kv = kv_layer_ids ? kv_layer_count : g->num_layers;
   dim3 grid(lay.splits, g->kv_heads, g->batch * n_layers);
   cudaError_t ce;
   static const SelectParams no_select{};
@@ -542,6 +580,8 @@ struct StepLayout {
   int aug_stride = 0;                           // sink / recent augmentation
   size_t off_aug = 0, off_aug_counts = 0;
   size_t off_scores, off_attn, attn_bytes, off_attn_r, attn_bytes_r, total;
+  size_t off_sync = 0;  // single-launch step: ticket / done counters + selection ready flags
+  int n_ready = 0;
 };
 
 int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, int budget,
@@ -614,7 +654,9 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   for (int n = 1; n <= (int)s->reuse_ids.size(); ++n)
     s->attn_bytes_r = std::max(
         s->attn_bytes_r, attn_layout(g, n, s->aug_stride ? s->aug_stride : s->k_eff, true).total);
-  s->total = s->off_attn_r + s->attn_bytes_r;
+  s->off_sync = align_up(s->off_attn_r + s->attn_bytes_r, 256);
+  s->n_ready = (int)(nf * g->batch * s->n_groups);
+  s->total = align_up(s->off_sync + 256 + sizeof(int) * (size_t)s->n_ready, 256);
   return HYLRA_OK;
 }
 
@@ -654,6 +696,7 @@ bool fused_select_fits(const hylra_geometry* g, int n_valid) {
 // Options of hylra_decode_step_ex (all optional; see include/hylra.h).
 struct StepOpts {
   bool fuse = false;  // selects of the FULL layers feeding REUSE fused into the FULL kernel
+  bool unified = false;  // single-launch step (fuse_select == 2)
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, select = nullptr, full = nullptr, join = nullptr;
   cudaEvent_t reuse_wait = nullptr;
@@ -706,6 +749,64 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   // the select's shared memory must fit in the FULL kernel's pipeline buffers
   const bool fused_sel = o.fuse && o.side && !a_ids.empty() && !s.aug_stride && sel_group == 1 &&
                          use_mma_path(g) && fused_select_fits(g, n_valid);
+  // single-launch step: every select fused into the FULL items, REUSE items in the same grid
+  const bool unified = o.unified && !s.aug_stride && sel_group == 1 && use_mma_path(g) &&
+                       fused_select_fits(g, n_valid) && !o.layer_events;
+  if (unified) {
+    std::vector<int32_t> ab_ids(a_ids), ab_slot(a_slot), ab_kv(a_kv);
+    ab_ids.insert(ab_ids.end(), b_ids.begin(), b_ids.end());
+    ab_slot.insert(ab_slot.end(), b_slot.begin(), b_slot.end());
+    ab_kv.insert(ab_kv.end(), b_kv.begin(), b_kv.end());
+    SelectParams sp{};
+    if (int e = build_select_params(&sp, g, scores, nf, n_valid, budget, sel_group,
+                                    refine ? q : nullptr, refine ? kf : nullptr, ab_ids.data(),
+                                    idx, k_stride, nullptr, flags, BlockRows(),
+                                    split ? ab_kv.data() : nullptr, ab_slot.data()))
+      return e;
+    AttnParams pf{}, pr{};
+    AttnLayout lf{}, lr{};
+    if (int e = make_attn_params(&pf, &lf, g, false, q, kf, vf, n_valid, n_valid, nf,
+                                 ab_ids.data(), nullptr, nullptr, nullptr, 0, 1, out, scores, aws,
+                                 s.attn_bytes, flags, split ? ab_kv.data() : nullptr, nf))
+      return e;
+    pf.fuse_select = nf;
+    const long items_f = (long)lf.splits * g->kv_heads * g->batch * nf;
+    long items_r = 0;
+    std::vector<int32_t> rkv(nr);
+    for (int i = 0; i < nr; ++i) rkv[i] = i;
+    if (nr > 0) {
+      if (int e = make_attn_params(&pr, &lr, g, true, q, split ? split->kr : k,
+                                   split ? split->vr : v, n_valid, s.k_eff, nr,
+                                   s.reuse_ids.data(), s.reuse_src.data(), idx, nullptr, k_stride,
+                                   sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r,
+                                   flags, split ? rkv.data() : nullptr, nr))
+        return e;
+      items_r = (long)lr.splits * g->kv_heads * g->batch * nr;
+    }
+    if (items_f + items_r > INT32_MAX) return fail(HYLRA_ERR_CONFIGURATION, "grid too large");
+    CUtensorMap tk{}, tv{};
+    if (int e = encode_kv_map(&tk, g, kf, split ? nf : g->num_layers)) return e;
+    if (int e = encode_kv_map(&tv, g, vf, split ? nf : g->num_layers)) return e;
+    StepSync ss{};
+    ss.ctr = reinterpret_cast<int*>(w + s.off_sync);
+    ss.ready = ss.ctr + 64;
+    ss.n_ready = s.n_ready;
+    ss.n_full_items = (int)items_f;
+    ss.n_items = (int)(items_f + items_r);
+    if (o.reuse_wait)
+      if (int e = cuda_check(cudaStreamWaitEvent(st, o.reuse_wait, 0), "stream wait event"))
+        return e;
+    const int G = g->q_heads / g->kv_heads;
+    cudaError_t ce;
+    if (g->head_dim == 128)
+      ce = G > 8 ? launch_step_mma<128, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
+                 : launch_step_mma<128, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
+    else
+      ce = G > 8 ? launch_step_mma<64, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
+                 : launch_step_mma<64, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_check(ce, "single-launch step");
+  }
   if (o.side && !(o.fork && o.join && (o.fuse || (o.select && o.full))))
     return fail(HYLRA_ERR_CONFIGURATION, "a side stream needs its four events");
   // groups of FULL layers: one launch (all FULL layers) or two (A then B)
@@ -924,6 +1025,7 @@ int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, 
   StepOpts o;
   if (opt) {
     o.fuse = opt->fuse_select != 0;
+    o.unified = opt->fuse_select == 2;
     o.side = static_cast<cudaStream_t>(opt->side_stream);
     o.fork = static_cast<cudaEvent_t>(opt->fork_event);
     o.select = static_cast<cudaEvent_t>(opt->select_event);

@@ -74,7 +74,7 @@ class HybridDecoder:
     def __init__(self, policy, k_cache: torch.Tensor, v_cache: torch.Tensor, budget: int, *,
                  q_heads: int, sel_group: int = 1, refine: bool = True, block_size: int = 1,
                  include_sinks: int = 0, include_recent: int = 0, dual_stream: bool = False,
-                 fuse_select: bool = True):
+                 fuse_select: bool = True, single_launch: bool = False):
         self.actions = _actions_of(policy)
         if len(self.actions) != k_cache.shape[0]:
             raise ConfigurationError(
@@ -128,9 +128,19 @@ class HybridDecoder:
                       and d in (64, 128))
         if self.fused:
             self.dual = False
+        # single-launch step (hylra_decode_step_ex fuse_select=2): FULL items with every
+        # select fused, then the REUSE items, in one grid; REUSE items wait on per-row ready
+        # flags. Same eligibility as the fused selects, any policy.
+        self.single = (bool(single_launch) and block_size == 1
+                       and not (include_sinks or include_recent) and sel_group == 1
+                       and k_cache.dtype == torch.bfloat16 and d in (64, 128))
+        if self.single:
+            self.dual = self.fused = False
         self.kernels_per_step = ((2 + has_reuse + (has_reuse and bool(include_sinks or include_recent)))
                                  if block_size == 1 else (3 + 2 * has_reuse)) + 2 * self.dual \
             - (self.fused and len(feeds) == len(self.full_layers))
+        if self.single:
+            self.kernels_per_step = 1
         if self.dual or self.fused:
             # high priority: select CTAs are dispatched ahead of the queued FULL / REUSE CTAs
             self._side = torch.cuda.Stream(device=k_cache.device, priority=-8)
@@ -178,6 +188,8 @@ class HybridDecoder:
             if self.ws.numel() < need:
                 self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
             opt = _abi.StepOptions()
+            if self.single:
+                opt.fuse_select = 2
             if self.dual or self.fused:
                 opt.fuse_select = int(self.fused)
                 opt.side_stream = self._side.cuda_stream

@@ -20,7 +20,8 @@ a = ap.parse_args()
 cfg = CONFIGS[a.config].with_(batch=a.batch)
 q, k, v = generate_torch(cfg, "cuda")
 kinds = {"fused3": {"fuse_select": False}, "fusedsel": {"fuse_select": True},
-         "dual": {"dual_stream": True, "fuse_select": False}}
+         "dual": {"dual_stream": True, "fuse_select": False},
+         "single": {"single_launch": True}}
 graphs = {}
 for name, kw in kinds.items():
     dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads, **kw)
@@ -36,6 +37,15 @@ for name, kw in kinds.items():
     with torch.cuda.graph(g):
         dec.step(q, cfg.context)
     graphs[name] = (g, dec)
+torch.cuda.synchronize()
+ref = graphs["fused3"][1]
+for name, (g, dec) in graphs.items():
+    # dual splits the FULL launch (other split-K partitions): same sets, outputs to rounding
+    assert torch.equal(dec.idx, ref.idx), name
+    if name != "dual" and not torch.equal(dec.out, ref.out):
+        bad = [(l, float((dec.out[l] - ref.out[l]).abs().max()))
+               for l in range(dec.out.shape[0]) if not torch.equal(dec.out[l], ref.out[l])]
+        print(f"{name}: outputs differ from fused3 at layers {bad}", flush=True)
 res = {n: [] for n in kinds}
 for _ in range(a.reps):
     for name, (g, _) in graphs.items():

@@ -397,6 +397,84 @@ def test_fused_select_step_equals_unfused(actions, d, refine, n):
     assert torch.equal(dec.out, ref_out)
 
 
+@pytest.mark.parametrize("actions,d,refine,n,B", [
+    (("full", "reuse", "full", "full", "reuse", "reuse", "full", "reuse", "full", "full"), 128, True, 4096, 2),
+    (("full", "full", "reuse", "reuse"), 64, True, 3001, 2),
+    (("full", "reuse", "full", "reuse"), 128, False, 4096, 1),
+    (("full", "full", "reuse", "full", "reuse"), 128, True, 70000, 1),
+    (("full", "reuse", "full", "reuse"), 128, True, 1500, 3),
+    (("full", "reuse", "reuse"), 64, True, 200, 2),
+    (("full", "full", "full"), 128, True, 2048, 2),            # no REUSE layer
+    (("full",) + ("reuse",) * 15, 128, True, 8192, 4),         # one source, many waiters
+])
+def test_single_launch_step_equals_unfused(actions, d, refine, n, B):
+    """hylra_decode_step_ex fuse_select=2: FULL items (every select fused) and REUSE items
+    (waiting on per-row ready flags) in one grid. Same split-K partitions as the plain
+    3-launch step, so outputs and selections are bit-identical; repeated eager steps and
+    CUDA-graph replays check that the ticket / ready flags reset themselves."""
+    L = len(actions)
+    Hq, Hkv, budget = 16, 4, 256
+    cap = n
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=43, planted=64)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine,
+                        fuse_select=False).step(q, n)
+    ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine, single_launch=True)
+    assert dec.single and dec.kernels_per_step == 1
+    for _ in range(3):
+        dec.out.zero_()
+        dec.idx.zero_()
+        res = dec.step(q, n)
+        torch.cuda.synchronize()
+        dec.check_flags()
+        assert torch.equal(res.selections, ref_idx)
+        assert torch.equal(res.outputs, ref_out)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dec.step(q, n)
+    torch.cuda.current_stream().wait_stream(s)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        dec.step(q, n)
+    for _ in range(5):
+        dec.out.zero_()
+        dec.idx.zero_()
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(dec.idx[..., :budget], ref_idx)
+        assert torch.equal(dec.out, ref_out)
+    # the synchronisation words are back at zero after every step
+    sync = dec.ws[-(256 + 4 * len(dec.full_layers) * B * Hkv):].view(torch.int32)
+    assert int(sync.abs().sum()) == 0
+
+
+def test_schedules_bit_identical_at_config2_scale():
+    """Regression test for a pipeline-stage release race. The consumer warps released a
+    stage (mbarrier arrive) before their last V ldmatrix reads had completed, so the
+    producer could refill it early. It showed only at config-2 scale, when a CTA running a
+    fused select shared the SM with streaming CTAs: V columns 96..127 of a tile were then
+    read from the next tile. Every schedule must reproduce the plain 3-launch step bit for
+    bit, on repeated steps."""
+    from paper_2602_00777_b200.synthetic import CONFIGS, generate_torch
+    cfg = CONFIGS["cfg2"].with_(batch=8, layers=17, full_layers=(0, 1, 2, 8, 15, 16))
+    q, k, v = generate_torch(cfg, DEV)
+    ref = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads, fuse_select=False)
+    ref.step(q, cfg.context)
+    torch.cuda.synchronize()
+    R, I = ref.out.clone(), ref.idx.clone()
+    for kw in ({"fuse_select": True}, {"single_launch": True}, {"fuse_select": False}):
+        dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads, **kw)
+        for _ in range(3):
+            dec.step(q, cfg.context)
+            torch.cuda.synchronize()
+            assert torch.equal(dec.idx, I), kw
+            bad = [l for l in range(cfg.layers) if not torch.equal(dec.out[l], R[l])]
+            assert not bad, (kw, bad)
+    del q, k, v, ref, dec
+    torch.cuda.empty_cache()
+
+
 def test_step_layer_events_chunks_reuse():
     """hylra_decode_step_events: per-layer completion events split the REUSE launch into
     chunks; selections identical, outputs within split-K rounding; events fire."""
