@@ -199,6 +199,15 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
  *     streaming); those layers' pairs come first in the grid. The other FULL layers'
  *     SELECT runs on side_stream under the REUSE launch. Tensor-core path, sel_group 1,
  *     no sinks / recent; otherwise the plain or side-stream schedule applies.
+ *   fuse_select = 2 (no side stream needed): single-launch step. ONE kernel runs every
+ *     FULL (layer, b, kv-head) split with every selection fused into the last CTA of its
+ *     pair, then every REUSE split; a REUSE CTA first waits for its selection row's ready
+ *     flag. CTAs claim work by an atomic ticket, so a waiting REUSE CTA only ever waits on
+ *     FULL work already running (no deadlock for any dispatch order). Same split-K
+ *     partitions as the plain step: outputs and selections are bit-identical to it.
+ *     Tensor-core path, sel_group 1, no sinks / recent, no layer_events (otherwise the
+ *     schedules above apply); reuse_wait_event is waited on before the launch. The
+ *     workspace carries the ticket / ready words and the kernel leaves them zeroed.
  *   reuse_wait_event: the REUSE launches wait on it (e.g. REUSE layers' queries arriving).
  *   layer_events: L entries (NULL allowed); layer_events[l] is recorded as soon as out[l] is
  *     final — FULL layers right after their FULL launch, REUSE layers after the REUSE
@@ -208,7 +217,7 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
  * Workspace: as hylra_decode_step.
  */
 typedef struct hylra_step_options {
-  int32_t fuse_select; /* !=0 (with side_stream, fork_event, join_event): see below */
+  int32_t fuse_select; /* 1 (with side_stream, fork_event, join_event) or 2: see above */
   void* side_stream;
   void* fork_event;   /* stream -> side: FULL(A) done   */
   void* select_event; /* side -> stream: SELECT(A) done */

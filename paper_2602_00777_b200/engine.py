@@ -74,7 +74,7 @@ class HybridDecoder:
     def __init__(self, policy, k_cache: torch.Tensor, v_cache: torch.Tensor, budget: int, *,
                  q_heads: int, sel_group: int = 1, refine: bool = True, block_size: int = 1,
                  include_sinks: int = 0, include_recent: int = 0, dual_stream: bool = False,
-                 fuse_select: bool = True, single_launch: bool = False):
+                 fuse_select: bool = True, single_launch="auto"):
         self.actions = _actions_of(policy)
         if len(self.actions) != k_cache.shape[0]:
             raise ConfigurationError(
@@ -131,6 +131,14 @@ class HybridDecoder:
         # single-launch step (hylra_decode_step_ex fuse_select=2): FULL items with every
         # select fused, then the REUSE items, in one grid; REUSE items wait on per-row ready
         # flags. Same eligibility as the fused selects, any policy.
+        # "auto": where it measured faster on B200 (scripts/ab_schedules.py,
+        # profiles/r01_schedule_matrix.txt): enough FULL pairs that the fused selects of the
+        # last FULL wave overlap REUSE items instead of delaying them, rows short enough that
+        # a 128-thread select stays short (cfg2 B>=4, cfg4 B=16; not cfg2 B<=2, cfg3, cfg4 B<=8)
+        if single_launch == "auto":
+            pairs = len(self.full_layers) * B * Hkv
+            single_launch = bool(fuse_select) and not dual_stream and len(feeds) > 0 and (
+                (pairs >= 256 and cap <= 32768) or (pairs >= 384 and cap <= 65536))
         self.single = (bool(single_launch) and block_size == 1
                        and not (include_sinks or include_recent) and sel_group == 1
                        and k_cache.dtype == torch.bfloat16 and d in (64, 128))
@@ -496,7 +504,8 @@ class DecodeLoop:
     def _body(self):
         dec, pos = self.dec, self.pos
         if self.zero_copy:
-            if not self.reuse_layers:
+            if not self.reuse_layers or dec.single:
+                # single-launch step: one kernel after the append, nothing to overlap
                 dec.append(self.k_host, self.v_host, pos)
                 dec.step(self.q_host, pos + 1, out=self.out_host)
                 return

@@ -19,7 +19,8 @@ ap.add_argument("--norefine", action="store_true")
 a = ap.parse_args()
 cfg = CONFIGS[a.config].with_(batch=a.batch)
 q, k, v = generate_torch(cfg, "cuda")
-kinds = {"fused3": {"fuse_select": False}, "fusedsel": {"fuse_select": True},
+kinds = {"fused3": {"fuse_select": False},
+         "fusedsel": {"fuse_select": True, "single_launch": False},
          "single": {"single_launch": True},
          "dual": {"dual_stream": True, "fuse_select": False}}
 for name, kw in kinds.items():

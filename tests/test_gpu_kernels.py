@@ -374,7 +374,8 @@ def test_fused_select_step_equals_unfused(actions, d, refine, n):
     ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine,
                         fuse_select=False).step(q, n)
     ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
-    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine, fuse_select=True)
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine, fuse_select=True,
+                        single_launch=False)
     assert dec.fused
     res = dec.step(q, n)
     torch.cuda.synchronize()
@@ -463,7 +464,8 @@ def test_schedules_bit_identical_at_config2_scale():
     ref.step(q, cfg.context)
     torch.cuda.synchronize()
     R, I = ref.out.clone(), ref.idx.clone()
-    for kw in ({"fuse_select": True}, {"single_launch": True}, {"fuse_select": False}):
+    for kw in ({"fuse_select": True, "single_launch": False}, {"single_launch": True},
+               {"fuse_select": False}):
         dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads, **kw)
         for _ in range(3):
             dec.step(q, cfg.context)
