@@ -285,8 +285,8 @@ def test_pipelined_schedules_match_fused(schedule):
     assert max_head_err(dec.out.double().cpu().numpy(), r) < 4e-3
 
 
-@pytest.mark.parametrize("zero_copy", [False, True])
-def test_decode_loop_host_io_graph(zero_copy):
+@pytest.mark.parametrize("zero_copy,single", [(False, "auto"), (True, "auto"), (True, True)])
+def test_decode_loop_host_io_graph(zero_copy, single):
     """DecodeLoop: H2D (q + new K/V row) -> append -> step -> D2H in one graph launch;
     zero_copy=True: rows appended and queries read from pinned host memory in place,
     outputs stored by the kernels straight into pinned host memory."""
@@ -294,7 +294,8 @@ def test_decode_loop_host_io_graph(zero_copy):
     L, B, Hq, Hkv, d, cap, budget = 9, 2, 8, 2, 128, 2048, 128
     q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=13, planted=16)
     actions = ("full", "reuse", "full", "reuse", "reuse", "full", "reuse", "reuse", "reuse")
-    dec = HybridDecoder(actions, k.clone(), v.clone(), budget, q_heads=Hq)
+    dec = HybridDecoder(actions, k.clone(), v.clone(), budget, q_heads=Hq, single_launch=single)
+    assert dec.single == (single is True)
     pos = 1500
     loop = DecodeLoop(dec, pos, zero_copy=zero_copy)
     g = torch.Generator().manual_seed(3)
