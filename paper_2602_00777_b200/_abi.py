@@ -11,7 +11,8 @@ from pathlib import Path
 
 from .errors import STATUS_TO_ERROR, CudaError, LayerReuseError
 
-LIB_PATH = Path(__file__).resolve().parent / "libhylra.so"
+# HYLRA_LIB: another build of the same ABI (A/B experiments between library versions)
+LIB_PATH = Path(os.environ.get("HYLRA_LIB") or Path(__file__).resolve().parent / "libhylra.so")
 
 HYLRA_BF16 = 0
 HYLRA_F32 = 1

@@ -631,7 +631,7 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
       __shared__ Red sel_red;
       asm volatile("bar.sync 1, 128;" ::: "memory");  // merge reads of smem are done
       __threadfence();
-      select_row<kConsumerWarps * 32>(sp, kh, b, slot, smem, sel_red, false);
+      select_row<kConsumerWarps * 32, true>(sp, kh, b, slot, smem, sel_red, false);
       if (ready_set != nullptr) {
         asm volatile("bar.sync 1, 128;" ::: "memory");  // the row's indices are written
         if (threadIdx.x == 0) {

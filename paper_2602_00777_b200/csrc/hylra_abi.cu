@@ -415,7 +415,8 @@ int select_threads(int rows) {
   std::call_once(once, [] {
     const char* v = std::getenv("HYLRA_SELECT_THREADS");
     const int t = (v && *v) ? atoi(v) : 0;
-    forced = (t == 256 || t == 512 || t == 1024) ? t : 0;
+    // 128 = the fused select's width (diagnostics: scripts/select_diag.py)
+    forced = (t == 128 || t == 256 || t == 512 || t == 1024) ? t : 0;
   });
   if (forced) return forced;
   if (rows <= kNumSMs) return 1024;
@@ -510,6 +511,7 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
   cudaError_t ce;
   if (nt == 1024) ce = launch_select_nt<1024>(grid, sel_smem_bytes(n_valid, 1024), st, p);
   else if (nt == 512) ce = launch_select_nt<512>(grid, sel_smem_bytes(n_valid, 512), st, p);
+  else if (nt == 128) ce = launch_select_nt<128>(grid, sel_smem_bytes(n_valid, 128), st, p);
   else ce = launch_select_nt<256>(grid, sel_smem_bytes(n_valid, 256), st, p);
   if (ce != cudaSuccess) return cuda_check(ce, "topk_select launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -690,7 +692,7 @@ bool fused_select_fits(const hylra_geometry* g, int n_valid) {
   const size_t ring = g->head_dim == 128
                           ? (size_t)mma_stages<128, false, false>() * MmaSmem<128>::kStageBytes
                           : (size_t)mma_stages<64, false, false>() * MmaSmem<64>::kStageBytes;
-  return n_valid <= kSelMaxTokens && sel_smem_bytes(n_valid, kConsumerWarps * 32) <= ring;
+  return n_valid <= kSelMaxTokens && sel_smem_bytes(n_valid, kConsumerWarps * 32, true) <= ring;
 }
 
 // Options of hylra_decode_step_ex (all optional; see include/hylra.h).

@@ -24,6 +24,8 @@
 // full-row MSB radix select, then the same window logic, or an index-ordered tie pass.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace hylra {
@@ -69,15 +71,20 @@ __host__ __device__ constexpr size_t sel_bitmap_bytes(int n, int nt) {
 // Band list: indices of the scores inside the bracket [lo, hi], collected by pass B so the
 // second pass reads only them (4096 entries per 256 threads; it shares the small-row keys
 // region, which the large-row path does not otherwise use before the window step).
-__host__ __device__ constexpr int sel_band_cap(int nt) { return 16 * nt > 4096 ? 16 * nt : 4096; }
-__host__ __device__ constexpr size_t sel_keys_bytes(int nt) {
-  return (size_t)(kSmallN * 8 > sel_band_cap(nt) * 4 ? kSmallN * 8 : sel_band_cap(nt) * 4);
+// `big`: the fused select of the FULL kernel, whose shared memory (the drained pipeline
+// ring) has room for 8192 band entries.
+__host__ __device__ constexpr int sel_band_cap(int nt, bool big = false) {
+  return big ? 8192 : (16 * nt > 4096 ? 16 * nt : 4096);
 }
-__host__ __device__ constexpr size_t sel_fixed_bytes(int nt) {
-  return kBins * 4 + kCandCap * (8 + 4) + nt * 4 + sel_keys_bytes(nt);
+__host__ __device__ constexpr size_t sel_keys_bytes(int nt, bool big = false) {
+  return (size_t)(kSmallN * 8 > sel_band_cap(nt, big) * 4 ? kSmallN * 8
+                                                           : sel_band_cap(nt, big) * 4);
 }
-__host__ __device__ constexpr size_t sel_smem_bytes(int n, int nt) {
-  return sel_bitmap_bytes(n, nt) + sel_fixed_bytes(nt);
+__host__ __device__ constexpr size_t sel_fixed_bytes(int nt, bool big = false) {
+  return kBins * 4 + kCandCap * (8 + 4) + nt * 4 + sel_keys_bytes(nt, big);
+}
+__host__ __device__ constexpr size_t sel_smem_bytes(int n, int nt, bool big = false) {
+  return sel_bitmap_bytes(n, nt) + sel_fixed_bytes(nt, big);
 }
 
 struct SelSmem {
@@ -87,7 +94,7 @@ struct SelSmem {
   int* ci;           // [kCandCap] window token indices
   float* xchg;       // [NT]
   uint64_t* keys;    // [kSmallN] small-row sort keys
-  int* band;         // [sel_band_cap(NT)] pass-B band list (aliases keys)
+  int* band;         // [sel_band_cap(NT, big)] pass-B band list (aliases keys)
 };
 
 template <int NT>
@@ -201,6 +208,45 @@ __device__ __forceinline__ int block_scan(int v, int* total, Red& r) {
   *total = __shfl_sync(0xffffffffu, t, 31);
   const int pre = __shfl_sync(0xffffffffu, t, (warp + 31) & 31);  // inclusive of warp-1
   return (warp > 0 ? pre : 0) + x - v;
+}
+
+// Block exclusive scan of 4 words at once (for packed 16-bit counts: every partial sum of
+// a half stays below 2^16, so halves never carry into each other); tot = block sums.
+template <int NT>
+__device__ __forceinline__ void block_scan4(const uint32_t (&v)[4], uint32_t (&ex)[4],
+                                            uint32_t (&tot)[4], Red& r) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) x[q] = v[q];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x[q], o);
+      if (lane >= o) x[q] += y;
+    }
+  }
+  uint32_t* arr[4] = {reinterpret_cast<uint32_t*>(r.i), reinterpret_cast<uint32_t*>(r.wt),
+                      reinterpret_cast<uint32_t*>(r.pi), reinterpret_cast<uint32_t*>(r.f)};
+  sel_sync<NT>();
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) arr[q][warp] = x[q];
+  }
+  sel_sync<NT>();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t t = lane < NT / 32 ? arr[q][lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    const uint32_t pre = __shfl_sync(0xffffffffu, t, (warp + 31) & 31);  // through warp-1
+    tot[q] = __shfl_sync(0xffffffffu, t, 31);
+    ex[q] = (warp > 0 ? pre : 0u) + x[q] - v[q];
+  }
 }
 
 // Warp-aggregated append: each thread adds `cnt` items; returns its first slot.
@@ -498,7 +544,9 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
 // topk_select_kernel (one CTA per row) and, fused, by the FULL kernel's last CTA of a
 // pair (NT = 128 consumer threads). release: let dependent launches start before the
 // compaction (standalone kernel only).
-template <int NT>
+// PIPE: pass B keeps the next chunk's loads in flight while it processes the current one
+// (twice the registers: the fused select of the FULL kernel, which has them to spare).
+template <int NT, bool PIPE = false>
 __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint8_t* sraw,
                            Red& red, bool release) {
   constexpr int kChunk = sel_chunk<NT>();
@@ -510,6 +558,7 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
   int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
   const SelSmem sm = carve<NT>(sraw, n);
+  constexpr int kBandCap = sel_band_cap(NT, PIPE);
   const long long t0 = clock64();
 
   RowReader rd;
@@ -552,27 +601,34 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
     mode = 3;
     t1 = t2 = t3 = clock64();
   } else {
-    // ---- A. brackets [lo, hi] around the k-th rank from 4 NT strided samples: their
-    //         quantiles are read off a 1024-bin histogram over [sample min, sample max]
-    //         (no sort); edges are widened outward so the bracket stays conservative.
-    //         Wider CTAs take more samples: a narrower band for pass D.
-    constexpr int SPT = 4, kS = SPT * NT, BPT = 1024 / NT;
-    float smp[SPT];
-    float smin = INFINITY, smax = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < SPT; ++j) {
-      smp[j] = rd.at((int)(((int64_t)(tid + j * NT) * n) / kS));
-      smin = fminf(smin, smp[j]);
-      smax = fmaxf(smax, smp[j]);
-    }
-    smax = block_max_float<NT>(smax, red);
-    smin = -block_max_float<NT>(-smin, red);
+    // ---- A. brackets [lo, hi] around the k-th rank from strided samples: their quantiles
+    //         are read off a 1024-bin histogram over [sample min, sample max] (no sort);
+    //         edges are widened outward so the bracket stays conservative. 4 NT samples;
+    //         rows over 64K tokens take at least 2048 (a narrower band for passes H and D;
+    //         shorter rows measured faster with fewer: the extra scattered reads cost more
+    //         than they save once the score rows no longer sit in L2, e.g. cfg2 B=16).
     float hi, lo;
-    {
+    // band expected to overflow the band list: build the histogram inside pass B instead
+    bool inline_hist;
+    auto pass_a = [&](auto spt_c) {
+      constexpr int SPT = decltype(spt_c)::value, kS = SPT * NT, BPT = 1024 / NT;
+      float smp[SPT];
+      float smin = INFINITY, smax = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < SPT; ++j) {
+        smp[j] = rd.at((int)(((int64_t)(tid + j * NT) * n) / kS));
+        smin = fminf(smin, smp[j]);
+        smax = fmaxf(smax, smp[j]);
+      }
+      smax = block_max_float<NT>(smax, red);
+      smin = -block_max_float<NT>(-smin, red);
       const float pr = (float)k / (float)n;
       const float delta = 3.0f * sqrtf(kS * pr * (1.0f - pr)) + 2.0f;
       const int hi_i = max(0, (int)floorf(pr * kS - delta));        // ranks from the top
       const int lo_i = min(kS - 1, (int)ceilf(pr * kS + delta));
+      // (wide CTAs keep it inline: enough warps per scheduler to hide the atomics)
+      inline_hist = NT >= 512 ||
+                    (int64_t)(lo_i - hi_i + 3) * n > (int64_t)kBandCap * kS * 3 / 4;
       const float sscale = (smax > smin) ? 1024.f / (smax - smin) : 0.f;
       auto sbin = [&](float v) { return min(1023, max(0, (int)((v - smin) * sscale))); };
 #pragma unroll
@@ -606,7 +662,10 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       lo = smin + (float)bl / sscale;
       for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
       sel_sync<NT>();
-    }
+    };
+    constexpr int kSptLong = NT >= 512 ? 4 : 2048 / NT;
+    if (n > 65536) pass_a(std::integral_constant<int, kSptLong>{});
+    else pass_a(std::integral_constant<int, 4>{});
     t1 = clock64();
 
     // ---- B. above-bits -> bitmap, [lo, hi] -> histogram, max|s|, non-finite check.
@@ -629,12 +688,11 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       int cg = 0, ci = 0;
       if (tid == 0) red.misc[10] = 0;  // band list length
       sel_sync<NT>();
-      auto pass_b = [&](int c, bool full) {
+      // per chunk: above-bits -> bitmap, band bits -> band list, max / min / NaN
+      auto pass_b = [&](auto full_c, auto inl_c, int c, const float4 (&vv)[8]) {
+        constexpr bool full = decltype(full_c)::value;
+        constexpr bool inl = decltype(inl_c)::value;
         const int w4 = (c * kChunk + tid * 32) >> 2;
-        float4 vv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
         uint32_t word = 0u, band = 0u;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -646,28 +704,59 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
               vmax = fmaxf(vmax, v);
               vmin = fminf(vmin, v);
               word |= (v > bhi) ? (1u << (u * 4 + cc)) : 0u;
-              if (brackets && v >= blo && v <= bhi) {
-                atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
-                band |= 1u << (u * 4 + cc);
-              }
+              const bool in_band = brackets && v >= blo && v <= bhi;
+              band |= in_band ? (1u << (u * 4 + cc)) : 0u;
+              if (inl && in_band) atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
             }
           }
         }
         sm.bitmap[c * NT + tid] = word;
         cg += __popc(word);
         ci += __popc(band);
-        // band members' indices -> the band list (dropped past its capacity: pass D then
-        // falls back to re-reading the row)
+        // band members' indices -> the band list (dropped past its capacity: pass H and
+        // pass D then fall back to re-reading the row)
         int pos = warp_append(__popc(band), &red.misc[10]);
         while (band) {
           const int bit = __ffs(band) - 1;
           band &= band - 1;
-          if (pos < sel_band_cap(NT)) sm.band[pos] = 4 * w4 + bit;
+          if (pos < kBandCap) sm.band[pos] = 4 * w4 + bit;
           ++pos;
         }
       };
-      for (int c = 0; c < nfull; ++c) pass_b(c, true);
-      if (nfull < nch) pass_b(nfull, false);
+      auto load_chunk = [&](int c, float4 (&vv)[8]) {
+        const int w4 = (c * kChunk + tid * 32) >> 2;
+        const bool full = c < nfull;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+      };
+      auto run_b = [&](int c, const float4 (&vv)[8]) {
+        if (NT >= 512 || inline_hist) {
+          if (c < nfull) pass_b(std::true_type{}, std::true_type{}, c, vv);
+          else pass_b(std::false_type{}, std::true_type{}, c, vv);
+        } else {
+          if (c < nfull) pass_b(std::true_type{}, std::false_type{}, c, vv);
+          else pass_b(std::false_type{}, std::false_type{}, c, vv);
+        }
+      };
+      if constexpr (PIPE) {
+        float4 va[8], vb[8];
+        if (nch > 0) load_chunk(0, va);
+        for (int c = 0; c < nch; c += 2) {
+          if (c + 1 < nch) load_chunk(c + 1, vb);
+          run_b(c, va);
+          if (c + 1 < nch) {
+            if (c + 2 < nch) load_chunk(c + 2, va);
+            run_b(c + 1, vb);
+          }
+        }
+      } else {
+        for (int c = 0; c < nch; ++c) {
+          float4 vv[8];
+          load_chunk(c, vv);
+          run_b(c, vv);
+        }
+      }
       {
         float nmin = -vmin;
         int nb = nanacc != nanacc ? 1 : 0;
@@ -679,7 +768,9 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       }
       mabs = fmaxf(fabsf(vmax), fabsf(vmin));
       if (bad || !brackets || (cgt < k && k <= cgt + cin) || attempt == 1) break;
-      // retry once: the k-th value lies above hi (too many above) or below lo
+      // retry once: the k-th value lies above hi (too many above) or below lo; the new
+      // band's size is unknown, its histogram is built in the pass
+      inline_hist = true;
       if (cgt >= k) {
         lo = hi;
         hi = vmax;
@@ -692,6 +783,36 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
     }
     if (bad && tid == 0) atomicOr(p.flags, 2);
     auto bin_of = [&](float v) { return min(kBins - 1, (int)((v - lo) * scale)); };
+    // ---- H. histogram of the band [lo, hi] around rank k, built from the band list: only
+    //         those scores are re-read (L2), 4 loads in flight per thread. Only the final
+    //         bracket's histogram is needed, and only on the fast path.
+    if (!inline_hist && brackets && cgt < k && k <= cgt + cin) {
+      const int nband = red.misc[10];
+      if (nband <= kBandCap) {
+        constexpr int U = 4;
+        for (int base = 0; base < nband; base += NT * U) {
+          float v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = base + u * NT + tid;
+            v[u] = j < nband ? rd.at(sm.band[j]) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (base + u * NT + tid < nband) atomicAdd(sm.hist + bin_of(v[u]), 1u);
+        }
+      } else {
+        for (int i4 = tid; i4 < n4; i4 += NT) {
+          const float4 v4 = rd.at4(i4);
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const float v = lane4(v4, cc);
+            if (4 * i4 + cc < n && v >= lo && v <= hi) atomicAdd(sm.hist + bin_of(v), 1u);
+          }
+        }
+      }
+      sel_sync<NT>();
+    }
     t2 = clock64();
 
     const float tau = tau_w = fmaxf(p.tau_rel * mabs, 1e-30f);
@@ -792,19 +913,30 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
         }
       };
       const int nband = red.misc[10];
-      if (nband <= sel_band_cap(NT)) {
+      if (nband <= kBandCap) {
         // the band list holds every score in [lo, hi]: only those are re-read
-        for (int base = 0; base < nband; base += NT) {
-          const int j = base + tid;
-          const int i = j < nband ? sm.band[j] : 0;
-          const float v = j < nband ? rd.at(i) : -INFINITY;
-          const bool in = j < nband;
-          if (in && v >= v_hi) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
-          const bool cand = in && v >= v_lo && v < v_hi;
-          int pos = warp_append(cand ? 1 : 0, &red.misc[3]);
-          if (cand && pos < kCandCap) {
-            sm.cv[pos] = (double)v;
-            sm.ci[pos] = i;
+        constexpr int U = NT >= 512 ? 1 : 4;  // loads in flight per thread
+        for (int base = 0; base < nband; base += NT * U) {
+          int iu[U];
+          float vu[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = base + u * NT + tid;
+            iu[u] = j < nband ? sm.band[j] : 0;
+            vu[u] = j < nband ? rd.at(iu[u]) : -INFINITY;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = iu[u];
+            const float v = vu[u];
+            const bool in = base + u * NT + tid < nband;
+            if (in && v >= v_hi) atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+            const bool cand = in && v >= v_lo && v < v_hi;
+            int pos = warp_append(cand ? 1 : 0, &red.misc[3]);
+            if (cand && pos < kCandCap) {
+              sm.cv[pos] = (double)v;
+              sm.ci[pos] = i;
+            }
           }
         }
       } else {
@@ -946,20 +1078,44 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
   sel_sync<NT>();
 
   if (release) pdl_launch_dependents();
-  // ---- E. index-ordered compaction of the bitmap
+  // ---- E. index-ordered compaction of the bitmap: 8 chunks per block scan (their
+  //         per-thread counts packed 2 x 16 bits per word), 2 barriers per 8 chunks
   int run = 0;
-  for (int c = 0; c < nch; ++c) {
-    const uint32_t w = sm.bitmap[c * NT + tid];
+  if (nch == 1) {  // one chunk (wide CTAs, short rows): a single-word scan
+    const uint32_t w = sm.bitmap[tid];
     int tot;
-    int pos = run + block_scan<NT>(__popc(w), &tot, red);
+    int pos = block_scan<NT>(__popc(w), &tot, red);
     uint32_t m = w;
     while (m) {
       const int bit = __ffs(m) - 1;
       m &= m - 1;
-      if (pos < k) out[pos] = c * kChunk + tid * 32 + bit;
+      if (pos < k) out[pos] = tid * 32 + bit;
       ++pos;
     }
-    run += tot;
+    run = tot;
+  }
+  for (int c0 = 0; nch > 1 && c0 < nch; c0 += 8) {
+    uint32_t w[8], pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      w[j] = (c0 + j < nch) ? sm.bitmap[(c0 + j) * NT + tid] : 0u;
+      pk[j >> 1] |= (uint32_t)__popc(w[j]) << (16 * (j & 1));
+    }
+    uint32_t ex[4], tot[4];
+    block_scan4<NT>(pk, ex, tot, red);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (c0 + j >= nch) break;
+      int pos = run + (int)((ex[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+      uint32_t m = w[j];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (pos < k) out[pos] = (c0 + j) * kChunk + tid * 32 + bit;
+        ++pos;
+      }
+      run += (int)((tot[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+    }
   }
   // invariant: exactly k indices were emitted
   if (tid == 0 && run != k) atomicOr(p.flags, 8);

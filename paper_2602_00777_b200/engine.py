@@ -132,13 +132,13 @@ class HybridDecoder:
         # select fused, then the REUSE items, in one grid; REUSE items wait on per-row ready
         # flags. Same eligibility as the fused selects, any policy.
         # "auto": where it measured faster on B200 (scripts/ab_schedules.py,
-        # profiles/r01_schedule_matrix.txt): enough FULL pairs that the fused selects of the
-        # last FULL wave overlap REUSE items instead of delaying them, rows short enough that
-        # a 128-thread select stays short (cfg2 B>=4, cfg4 B=16; not cfg2 B<=2, cfg3, cfg4 B<=8)
+        # profiles/r01_schedule_matrix.txt): enough FULL (layer, b, kv-head) pairs that the
+        # fused selects of the last FULL pairs overlap REUSE items instead of delaying them
+        # (cfg2 B>=4, cfg3 B=4, cfg4 B>=8; not B=1, cfg2 B=2, cfg4 B=4)
         if single_launch == "auto":
             pairs = len(self.full_layers) * B * Hkv
-            single_launch = bool(fuse_select) and not dual_stream and len(feeds) > 0 and (
-                (pairs >= 256 and cap <= 32768) or (pairs >= 384 and cap <= 65536))
+            single_launch = (bool(fuse_select) and not dual_stream and len(feeds) > 0
+                             and pairs >= 192)
         self.single = (bool(single_launch) and block_size == 1
                        and not (include_sinks or include_recent) and sel_group == 1
                        and k_cache.dtype == torch.bfloat16 and d in (64, 128))

@@ -25,6 +25,14 @@ for refine in (True, False):
                            k=kk if refine else None, layers=fl, info=True)
     torch.cuda.synchronize()
     i = inf.view(-1, 8).cpu().numpy()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        topk_select(sc, cfg.budget, cfg.context, q=q if refine else None,
+                    k=kk if refine else None, layers=fl)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"  launch time {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
     print(f"{cfg.name} N={cfg.context} k={cfg.budget} B={cfg.batch} refine={refine} rows={len(i)}")
     print("  mode counts", dict(zip(*[x.tolist() for x in np.unique(i[:, 2], return_counts=True)])))
     print("  band size min/med/max", i[:, 3].min(), np.median(i[:, 3]), i[:, 3].max())
