@@ -65,31 +65,59 @@ struct AttnParams {
 };
 
 // Stage n selection indices from global into shared memory, validated (out-of-range ->
-// row 0 + HYLRA_FLAG_INDEX_OUT_OF_RANGE). One warp; 8 independent loads in flight per lane.
+// row 0 + HYLRA_FLAG_INDEX_OUT_OF_RANGE). The `parts` producer warps share the work (warp
+// `part` takes every parts-th 32-group slice) with 16-byte loads when the source is 16-byte
+// aligned: a 2048-row range is one round trip (8 x 16 B in flight per lane), not the 8
+// dependent rounds of one warp's 4-byte loads (~1 us each before the first gather). The
+// caller synchronises the producer warps afterwards.
 __device__ __forceinline__ void stage_indices(const int32_t* __restrict__ src, int n, int n_valid,
-                                              int32_t* dst, int* flags, int lane) {
+                                              int32_t* dst, int* flags, int lane, int part,
+                                              int parts) {
   constexpr int U = 8;
-  for (int j0 = 0; j0 < n; j0 += 32 * U) {
-    int r[U];
+  bool bad = false;
+  auto fix = [&](int v) {
+    const bool ok = v >= 0 && v < n_valid;
+    bad |= !ok;
+    return ok ? v : 0;
+  };
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const int n4 = n >> 2;
+    const int4* s4 = reinterpret_cast<const int4*>(src);
+    int4* d4 = reinterpret_cast<int4*>(dst);
+    for (int g0 = 0; g0 < n4; g0 += 32 * parts * U) {
+      int4 r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * 32 + lane;
-      r[u] = (j < n) ? __ldcg(src + j) : 0;  // coherent: written earlier in a single-launch step
-    }
-    bool bad = false;
+      for (int u = 0; u < U; ++u) {
+        const int g = g0 + (u * parts + part) * 32 + lane;
+        // coherent loads: the indices may have been written earlier in a single-launch step
+        r[u] = g < n4 ? __ldcg(s4 + g) : make_int4(0, 0, 0, 0);
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * 32 + lane;
-      if (j < n) {
-        if (r[u] < 0 || r[u] >= n_valid) {
-          bad = true;
-          r[u] = 0;
-        }
-        dst[j] = r[u];
+      for (int u = 0; u < U; ++u) {
+        const int g = g0 + (u * parts + part) * 32 + lane;
+        if (g < n4) d4[g] = make_int4(fix(r[u].x), fix(r[u].y), fix(r[u].z), fix(r[u].w));
       }
     }
-    if (bad) atomicOr(flags, 1);
+    if (part == 0 && lane < (n & 3)) {
+      const int j = (n4 << 2) + lane;
+      dst[j] = fix(__ldcg(src + j));
+    }
+  } else {
+    for (int j0 = 0; j0 < n; j0 += 32 * parts * U) {
+      int r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + (u * parts + part) * 32 + lane;
+        r[u] = (j < n) ? __ldcg(src + j) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + (u * parts + part) * 32 + lane;
+        if (j < n) dst[j] = fix(r[u]);
+      }
+    }
   }
+  if (bad) atomicOr(flags, 1);
 }
 
 // ---------------------------------------------------------------------------------
@@ -468,8 +496,12 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
         (void)ld_acquire_gpu(ready_wait);
       }
       if (staged) {
-        stage_indices(ib + pos_begin, n_pos, p.n_valid, sidx, p.flags, lane);
-        __syncwarp();
+        stage_indices(ib + pos_begin, n_pos, p.n_valid, sidx, p.flags, lane,
+                      warp - kConsumerWarps, kGatherProducers);
+        if (kGatherProducers > 1)
+          asm volatile("bar.sync 3, %0;" ::"n"(32 * kGatherProducers) : "memory");
+        else
+          __syncwarp();
       }
       auto row_at = [&](int pos) -> int {  // pos < n_rows
         if (staged) return sidx[pos - pos_begin];
