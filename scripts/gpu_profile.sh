@@ -5,14 +5,16 @@
 # capture travels back as an .ncu-rep.
 set -x
 mkdir -p gpurun_out
+if [ "$1" != "--captures-only" ]; then
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-extra --no-cpu \
   > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+fi
 cap() {  # name, kernel regex, count, prof_step args...
   local name=$1 kre=$2 cnt=$3; shift 3
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$kre" -c $cnt \
+  timeout 900 ncu -f --set full --import-source on --clock-control none -k regex:"$kre" -c $cnt \
     -o /tmp/$name python scripts/prof_step.py "$@" > gpurun_out/ncu_$name.log 2>&1
   echo "ncu $name rc=$?"
   python scripts/ncu_summary.py /tmp/$name.ncu-rep --json gpurun_out/ncu_$name.json > gpurun_out/ncu_$name.txt 2>&1
