@@ -604,9 +604,10 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
     // ---- A. brackets [lo, hi] around the k-th rank from strided samples: their quantiles
     //         are read off a 1024-bin histogram over [sample min, sample max] (no sort);
     //         edges are widened outward so the bracket stays conservative. 4 NT samples;
-    //         rows over 64K tokens take at least 2048 (a narrower band for passes H and D;
-    //         shorter rows measured faster with fewer: the extra scattered reads cost more
-    //         than they save once the score rows no longer sit in L2, e.g. cfg2 B=16).
+    //         the fused select takes 2048 on rows over 64K tokens (a narrower band for
+    //         passes H and D). Elsewhere the extra scattered reads measured slower, as the
+    //         rows of a standalone launch at large batch no longer sit in L2 (cfg2 B=16,
+    //         128K B=32).
     float hi, lo;
     // band expected to overflow the band list: build the histogram inside pass B instead
     bool inline_hist;
@@ -664,7 +665,7 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       sel_sync<NT>();
     };
     constexpr int kSptLong = NT >= 512 ? 4 : 2048 / NT;
-    if (n > 65536) pass_a(std::integral_constant<int, kSptLong>{});
+    if (PIPE && n > 65536) pass_a(std::integral_constant<int, kSptLong>{});
     else pass_a(std::integral_constant<int, 4>{});
     t1 = clock64();
 
@@ -1004,27 +1005,52 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       // ---------------------------------------------------------------- generic path
       mode = 1 + why;
       int c_gt = 0;
-      radix_select_row<NT>(rd, n, k, red, &T, &c_gt);
+      // why 80: the fast path found the exact k-th value T, only its refinement window
+      // reaches past the band's bins: T stands, one pass over the row collects the window
+      const bool t_known = why == 80;
+      if (!t_known) radix_select_row<NT>(rd, n, k, red, &T, &c_gt);
       lo_w = refine ? T - tau : T;
       hi_w = refine ? T + tau : T;
       for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
       if (tid == 0) red.misc[5] = 0;
       sel_sync<NT>();
-      int abv = 0;
-      for (int base = 0; base < n; base += NT) {
-        const int i = base + tid;
-        const float v = (i < n) ? rd.at(i) : -INFINITY;
-        const bool in = i < n && v >= lo_w && v <= hi_w;
-        if (i < n && v > hi_w) {
-          atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
-          ++abv;
+      int abv = 0, gt = 0;
+      for (int b4 = 0; b4 < n4; b4 += 2 * NT) {  // 2 x 16-byte loads in flight per thread
+        float4 va[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i4 = b4 + u * NT + tid;
+          va[u] = i4 < n4 ? rd.at4(i4) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
-        if (in && pos < kCandCap) {
-          sm.cv[pos] = (double)v;
-          sm.ci[pos] = i;
+        uint32_t win = 0u;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int i = 4 * (b4 + u * NT + tid) + cc;
+            const float v = lane4(va[u], cc);
+            const bool ok = i < n;
+            if (ok && v > hi_w) {
+              atomicOr(sm.bitmap + (i >> 5), 1u << (i & 31));
+              ++abv;
+            }
+            gt += (ok && v > T) ? 1 : 0;
+            win |= (ok && v >= lo_w && v <= hi_w) ? (1u << (u * 4 + cc)) : 0u;
+          }
+        }
+        int pos = warp_append(__popc(win), &red.misc[5]);
+        while (win) {
+          const int bit = __ffs(win) - 1;
+          win &= win - 1;
+          const int i = 4 * (b4 + (bit >> 2) * NT + tid) + (bit & 3);
+          if (pos < kCandCap) {
+            sm.cv[pos] = (double)lane4((bit >> 2) ? va[1] : va[0], bit & 3);
+            sm.ci[pos] = i;
+          }
+          ++pos;
         }
       }
+      if (t_known) c_gt = block_sum_int<NT>(gt, red);
       above_w = block_sum_int<NT>(abv, red);
       nw = red.misc[5];
       if (nw > kCandCap) {

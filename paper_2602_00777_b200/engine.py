@@ -144,17 +144,74 @@ class HybridDecoder:
                        and k_cache.dtype == torch.bfloat16 and d in (64, 128))
         if self.single:
             self.dual = self.fused = False
-        self.kernels_per_step = ((2 + has_reuse + (has_reuse and bool(include_sinks or include_recent)))
-                                 if block_size == 1 else (3 + 2 * has_reuse)) + 2 * self.dual \
-            - (self.fused and len(feeds) == len(self.full_layers))
-        if self.single:
-            self.kernels_per_step = 1
-        if self.dual or self.fused:
+        self._feeds_all = len(feeds) == len(self.full_layers)
+        self._has_reuse = has_reuse
+        # schedules this decoder can switch between (autotune): the fused-select and
+        # single-launch variants need the tensor-core path, token mode, sel_group 1
+        self._fused_ok = (block_size == 1 and not (include_sinks or include_recent)
+                          and len(feeds) > 0 and sel_group == 1
+                          and k_cache.dtype == torch.bfloat16 and d in (64, 128))
+        self._count_kernels()
+        if self.dual or self._fused_ok:
             # high priority: select CTAs are dispatched ahead of the queued FULL / REUSE CTAs
             self._side = torch.cuda.Stream(device=k_cache.device, priority=-8)
             self._events = [torch.cuda.Event() for _ in range(4)]
             for e in self._events:  # torch creates events lazily
                 e.record(torch.cuda.current_stream(k_cache.device))
+
+    def _count_kernels(self):
+        aug = self._has_reuse and bool(self.sinks or self.recent)
+        self.kernels_per_step = ((2 + self._has_reuse + aug) if self.block_size == 1
+                                 else (3 + 2 * self._has_reuse)) + 2 * self.dual \
+            - (self.fused and self._feeds_all)
+        if self.single:
+            self.kernels_per_step = 1
+
+    @property
+    def schedule(self) -> str:
+        return ("single" if self.single else "fusedsel" if self.fused else
+                "dual" if self.dual else "fused3")
+
+    def set_schedule(self, name: str) -> None:
+        """Switch between the step schedules ("single", "fusedsel", "fused3"); every one
+        gives bit-identical outputs and selections, only the launch structure differs."""
+        if name not in ("single", "fusedsel", "fused3"):
+            raise ConfigurationError(f"unknown schedule {name!r}")
+        if name != "fused3" and not self._fused_ok:
+            raise ConfigurationError(f"schedule {name!r} needs token mode, sel_group 1, "
+                                     "bf16 and head_dim 64/128 with a FULL layer feeding REUSE")
+        self.single, self.fused, self.dual = name == "single", name == "fusedsel", False
+        self._count_kernels()
+
+    def autotune(self, q: torch.Tensor, n_valid: int | None = None, reps: int = 10) -> dict:
+        """Time the schedules this decoder can run on these inputs (CUDA-graph replays, CUDA
+        events on the current stream) and keep the fastest. Returns {schedule: ms}. The
+        measured steps overwrite `out` / the selections (the next step rewrites them)."""
+        names = ["single", "fusedsel", "fused3"] if self._fused_ok else ["fused3"]
+        times = {}
+        cur = torch.cuda.current_stream(self.k.device)
+        for name in names:
+            self.set_schedule(name)
+            side = torch.cuda.Stream(device=self.k.device)
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    self.step(q, n_valid)
+            cur.wait_stream(side)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                self.step(q, n_valid)
+            gr.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                gr.replay()
+            e1.record()
+            e1.synchronize()
+            times[name] = e0.elapsed_time(e1) / reps
+            del gr
+        self.set_schedule(min(times, key=times.get))
+        return times
 
     def _geometry(self, q):
         return geometry(q, self.k, self.v, self.out)
@@ -370,7 +427,7 @@ class PipelinedDecoder(HybridDecoder):
                          fuse_select=False)
         if schedule not in ("pipelined", "sequential"):
             raise ConfigurationError(f"unknown schedule {schedule!r}")
-        self.schedule = schedule
+        self.pipe_schedule = schedule
         L, B, Hkv, cap, d = k_cache.shape
         from .attention import scores_row_stride
         self.scores = torch.empty((len(self.full_layers), B, Hkv, scores_row_stride(cap)),
@@ -385,6 +442,10 @@ class PipelinedDecoder(HybridDecoder):
         n_reuse_launch = (sum(1 for g in self.reuse_groups if g) if schedule == "pipelined"
                           else sum(len(g) for g in self.reuse_groups))
         self.kernels_per_step = len(self.full_layers) * 2 + n_reuse_launch
+
+    @property
+    def schedule(self) -> str:
+        return self.pipe_schedule
 
     def _buf(self, key, nbytes):
         t = self._ws.get(key)
@@ -403,9 +464,9 @@ class PipelinedDecoder(HybridDecoder):
         sc_slot = self.scores[0].numel()
         idx_slot = self.idx[0].numel()
         main = torch.cuda.current_stream(self.k.device)
-        side = self.side if self.schedule == "pipelined" else main
+        side = self.side if self.pipe_schedule == "pipelined" else main
         ws_f = self._buf("full", lib.hylra_attention_workspace_bytes(g, 1, n_valid))
-        sizes = {len(x) if self.schedule == "pipelined" else 1 for x in self.reuse_groups if x}
+        sizes = {len(x) if self.pipe_schedule == "pipelined" else 1 for x in self.reuse_groups if x}
         ws_r = self._buf("reuse", max([lib.hylra_attention_workspace_bytes(g, n, k_eff)
                                        for n in sizes] or [256]))
         flags = self.ws if self.ws.numel() >= 256 else self._buf("flags", 256)
@@ -431,7 +492,7 @@ class PipelinedDecoder(HybridDecoder):
                 self.k_stride, None, flags.data_ptr(), flags.numel(), side.cuda_stream))
             rg = self.reuse_groups[s]
             # pipelined: one launch for the whole chain; sequential: one launch per layer
-            launches = [rg] if (rg and self.schedule == "pipelined") else [[l] for l in rg]
+            launches = [rg] if (rg and self.pipe_schedule == "pipelined") else [[l] for l in rg]
             for grp in launches:
                 _abi.check(lib.hylra_reuse_decode(
                     g, qp, kp, vp, n_valid, len(grp), _abi.int32_array(grp),

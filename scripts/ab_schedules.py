@@ -16,8 +16,17 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--steps", type=int, default=50)
+ap.add_argument("--context", type=int, default=None)
+ap.add_argument("--budget", type=int, default=None)
+ap.add_argument("--layers", type=int, default=None)
 a = ap.parse_args()
 cfg = CONFIGS[a.config].with_(batch=a.batch)
+if a.context:
+    cfg = cfg.with_(context=a.context)
+if a.budget:
+    cfg = cfg.with_(budget=a.budget)
+if a.layers:
+    cfg = cfg.with_(layers=a.layers, full_layers=tuple(f for f in cfg.full_layers if f < a.layers))
 q, k, v = generate_torch(cfg, "cuda")
 kinds = {"fused3": {"fuse_select": False},
          "fusedsel": {"fuse_select": True, "single_launch": False},
@@ -59,5 +68,5 @@ for _ in range(a.reps):
         e1.record()
         torch.cuda.synchronize()
         res[name].append(e0.elapsed_time(e1) / a.steps * 1e3)
-print(f"{a.config} B={a.batch}", {n: (round(statistics.median(v), 1), round(min(v), 1))
+print(f"{a.config} N={cfg.context} k={cfg.budget} L={cfg.layers} B={a.batch}", {n: (round(statistics.median(v), 1), round(min(v), 1))
                                   for n, v in res.items()})

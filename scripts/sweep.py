@@ -53,6 +53,7 @@ def point(N, ratio, B):
     cfg = base.with_(layers=L, context=N, budget=k, batch=B, full_layers=full)
     q, kk, vv = generate_torch(cfg, "cuda")
     dec = HybridDecoder(cfg.actions, kk, vv, k, q_heads=cfg.q_heads)
+    tuned = dec.autotune(q, N)
     dec.step(q, N)
     torch.cuda.synchronize()
     dec.check_flags()
@@ -84,6 +85,7 @@ def point(N, ratio, B):
     fb = len(fl) * B * cfg.kv_heads * 2 * N * cfg.head_dim * 2
     rb = len(rl) * B * cfg.kv_heads * 2 * min(k, N) * cfg.head_dim * 2
     res = {"context": N, "top_k": k, "ratio": ratio, "batch": B, "layers": L,
+           "schedule": dec.schedule, "autotune_ms": tuned,
            "full_layers": len(fl), "reuse_layers": len(rl),
            "full_ms": t_full, "select_ms": t_sel, "reuse_ms": t_reuse, "step_ms": t_step,
            "full_frac": fb / (t_full * 1e-3) / 1e9 / PEAK,

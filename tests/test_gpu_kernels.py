@@ -478,6 +478,30 @@ def test_schedules_bit_identical_at_config2_scale():
     torch.cuda.empty_cache()
 
 
+def test_autotune_keeps_results_bit_identical():
+    """HybridDecoder.autotune times single / fusedsel / fused3 as graph replays and keeps
+    the fastest; whichever it keeps, the step's outputs and selections are unchanged."""
+    L, B, Hq, Hkv, d, cap, budget = 6, 2, 16, 4, 128, 4096, 256
+    actions = ("full", "reuse", "full", "full", "reuse", "reuse")
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=47, planted=32)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, fuse_select=False).step(q, cap)
+    R, I = ref.outputs.clone(), ref.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq)
+    times = dec.autotune(q, cap, reps=3)
+    assert set(times) == {"single", "fusedsel", "fused3"} and all(t > 0 for t in times.values())
+    assert dec.schedule == min(times, key=times.get)
+    res = dec.step(q, cap)
+    torch.cuda.synchronize()
+    assert torch.equal(res.selections, I) and torch.equal(res.outputs, R)
+    for name in ("single", "fusedsel", "fused3"):
+        dec.set_schedule(name)
+        res = dec.step(q, cap)
+        torch.cuda.synchronize()
+        assert torch.equal(res.selections, I) and torch.equal(res.outputs, R), name
+    f32 = HybridDecoder(actions, k.float(), v.float(), budget, q_heads=Hq)
+    assert f32.autotune(q.float(), cap, reps=2).keys() == {"fused3"}
+
+
 def test_step_layer_events_chunks_reuse():
     """hylra_decode_step_events: per-layer completion events split the REUSE launch into
     chunks; selections identical, outputs within split-K rounding; events fire."""
