@@ -705,9 +705,14 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
               vmax = fmaxf(vmax, v);
               vmin = fminf(vmin, v);
               word |= (v > bhi) ? (1u << (u * 4 + cc)) : 0u;
-              const bool in_band = brackets && v >= blo && v <= bhi;
-              band |= in_band ? (1u << (u * 4 + cc)) : 0u;
-              if (inl && in_band) atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
+              if (inl) {
+                if (brackets && v >= blo && v <= bhi) {
+                  atomicAdd(sm.hist + min(kBins - 1, (int)((v - blo) * bsc)), 1u);
+                  band |= 1u << (u * 4 + cc);
+                }
+              } else {
+                band |= (brackets && v >= blo && v <= bhi) ? (1u << (u * 4 + cc)) : 0u;
+              }
             }
           }
         }
@@ -726,10 +731,14 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       };
       auto load_chunk = [&](int c, float4 (&vv)[8]) {
         const int w4 = (c * kChunk + tid * 32) >> 2;
-        const bool full = c < nfull;
+        if (c < nfull) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          vv[u] = (full || w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+          for (int u = 0; u < 8; ++u) vv[u] = rd.at4(w4 + u);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            vv[u] = (w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+        }
       };
       auto run_b = [&](int c, const float4 (&vv)[8]) {
         if (NT >= 512 || inline_hist) {
