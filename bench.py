@@ -549,10 +549,12 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                     "ms_per_step": t_e2e * 1e3,
                     "path": "DecodeLoop.run() per step, one graph launch + host sync: "
                             "hylra_append_kv reads the new K/V rows from pinned host memory "
-                            "in place, the FULL/SELECT/REUSE kernels read the queries from "
-                            "pinned host memory and store the fp32 outputs straight into "
-                            "pinned host memory (no copy operations); wall clock, max over "
-                            "ranks (each rank's host receives its shard)"
+                            "in place, the kernels store the fp32 outputs straight into "
+                            "pinned host memory; queries "
+                            + ("copied H2D on a side stream under the append"
+                               if loop.q_copy else "read in place from pinned host memory")
+                            + " (DecodeLoop timed both, kept the faster); wall clock, max "
+                            "over ranks (each rank's host receives its shard)"
                             + ("" if loop.zero_copy else " [serialised copies]")}
     clk = clocks.stop()
 
@@ -667,10 +669,12 @@ def run_ours(a):
             extra["cfg2_offload_b1"] = {"error": str(exc)}
         for b_small in (1, 4):
             try:
-                rb = measure_config(a, cfg, b_small, rank, world, torch, dist, e2e=False)
+                rb = measure_config(a, cfg, b_small, rank, world, torch, dist,
+                                    e2e=b_small == 1)
                 extra[f"{cfg.name}_b{b_small}"] = {k: rb[k] for k in ("value", "ms_per_step",
                                                                      "step_gbs", "kernels",
-                                                                     "schedule", "schedules")}
+                                                                     "schedule", "schedules",
+                                                                     "e2e")}
             except Exception as exc:  # noqa: BLE001
                 extra[f"{cfg.name}_b{b_small}"] = {"error": str(exc)}
 

@@ -19,6 +19,7 @@ recent FULL layer's selection of the same step (engine.py:173,176,185-194).
 from __future__ import annotations
 
 import ctypes
+import time
 
 from dataclasses import dataclass
 
@@ -532,7 +533,8 @@ class DecodeLoop:
     D2H copy, serialised (the reference point).
     """
 
-    def __init__(self, decoder: HybridDecoder, pos: int, *, zero_copy: bool = True):
+    def __init__(self, decoder: HybridDecoder, pos: int, *, zero_copy: bool = True,
+                 q_copy="auto"):
         k = decoder.k
         L, B, Hkv, cap, d = k.shape
         if not 0 <= pos < cap:
@@ -555,28 +557,45 @@ class DecodeLoop:
         acts = decoder.actions
         self.full_layers = [l for l in range(L) if acts[l] is Action.FULL]
         self.reuse_layers = [l for l in range(L) if acts[l] is Action.REUSE]
-        if self.zero_copy and self.reuse_layers:
+        # zero_copy q_copy: the queries come over in one H2D copy on a side stream, under the
+        # append, instead of being read across the link by every CTA as it starts (costly
+        # when the whole step is one wave: +20 us at cfg2 B=1, +14 us at B=8 where the copy
+        # itself takes longer). "auto": capture() times both and keeps the faster.
+        if q_copy not in ("auto", True, False):
+            raise ConfigurationError(f"q_copy must be 'auto', True or False, got {q_copy!r}")
+        self.q_copy = q_copy if self.zero_copy else False
+        if self.zero_copy:
+            self.side = torch.cuda.Stream(device=k.device)
+            self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
             # the REUSE layers' new rows are appended on a side stream under the FULL kernel;
             # the REUSE launch waits on them (hylra_decode_step_ex reuse_wait_event)
-            self.side = torch.cuda.Stream(device=k.device)
             self.ev_rows = torch.cuda.Event()
             self.ev_rows.record()  # torch creates events lazily
 
-    def _body(self):
+    def _body(self, q_copy: bool = False):
         dec, pos = self.dec, self.pos
         if self.zero_copy:
+            main = torch.cuda.current_stream(dec.k.device)
+            q = self.q_host
+            if q_copy:
+                self.side.wait_stream(main)
+                with torch.cuda.stream(self.side):
+                    self.q_dev.copy_(self.q_host, non_blocking=True)
+                q = self.q_dev
             if not self.reuse_layers or dec.single:
                 # single-launch step: one kernel after the append, nothing to overlap
                 dec.append(self.k_host, self.v_host, pos)
-                dec.step(self.q_host, pos + 1, out=self.out_host)
+                if q_copy:
+                    main.wait_stream(self.side)
+                dec.step(q, pos + 1, out=self.out_host)
                 return
-            main = torch.cuda.current_stream(dec.k.device)
-            self.side.wait_stream(main)
+            if not q_copy:
+                self.side.wait_stream(main)
             with torch.cuda.stream(self.side):
                 dec.append(self.k_host, self.v_host, pos, self.reuse_layers)
                 self.ev_rows.record(self.side)
             dec.append(self.k_host, self.v_host, pos, self.full_layers)
-            dec.step(self.q_host, pos + 1, out=self.out_host, reuse_wait=self.ev_rows)
+            dec.step(q, pos + 1, out=self.out_host, reuse_wait=self.ev_rows)
             main.wait_stream(self.side)
             return
         self.q_dev.copy_(self.q_host, non_blocking=True)
@@ -586,18 +605,38 @@ class DecodeLoop:
         dec.step(self.q_dev, pos + 1)
         self.out_host.copy_(dec.out, non_blocking=True)
 
-    def capture(self):
-        """Warm up and capture the step (host copies included) into a CUDA graph."""
+    def _graph(self, q_copy: bool):
         s = torch.cuda.Stream(device=self.dec.k.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(2):
-                self._body()
+                self._body(q_copy)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self._body()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._body(q_copy)
+        return g
+
+    def capture(self, reps: int = 10):
+        """Warm up and capture the step (host copies included) into a CUDA graph; with
+        q_copy="auto" both query paths are captured and timed, the faster is kept."""
+        if self.q_copy != "auto":
+            self.graph = self._graph(bool(self.q_copy))
+            return self
+        times = {}
+        for qc in (False, True):
+            g = self._graph(qc)
+            g.replay()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                g.replay()
+                torch.cuda.current_stream().synchronize()
+            times[qc] = (time.perf_counter() - t0) / reps
+            del g
+        self.q_copy = min(times, key=times.get)
+        self.graph = self._graph(self.q_copy)
         return self
 
     def run(self) -> torch.Tensor:

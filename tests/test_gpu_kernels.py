@@ -285,8 +285,10 @@ def test_pipelined_schedules_match_fused(schedule):
     assert max_head_err(dec.out.double().cpu().numpy(), r) < 4e-3
 
 
-@pytest.mark.parametrize("zero_copy,single", [(False, "auto"), (True, "auto"), (True, True)])
-def test_decode_loop_host_io_graph(zero_copy, single):
+@pytest.mark.parametrize("zero_copy,single,q_copy", [
+    (False, "auto", "auto"), (True, "auto", False), (True, "auto", True), (True, True, False),
+    (True, True, True), (True, True, "auto")])
+def test_decode_loop_host_io_graph(zero_copy, single, q_copy):
     """DecodeLoop: H2D (q + new K/V row) -> append -> step -> D2H in one graph launch;
     zero_copy=True: rows appended and queries read from pinned host memory in place,
     outputs stored by the kernels straight into pinned host memory."""
@@ -297,7 +299,7 @@ def test_decode_loop_host_io_graph(zero_copy, single):
     dec = HybridDecoder(actions, k.clone(), v.clone(), budget, q_heads=Hq, single_launch=single)
     assert dec.single == (single is True)
     pos = 1500
-    loop = DecodeLoop(dec, pos, zero_copy=zero_copy)
+    loop = DecodeLoop(dec, pos, zero_copy=zero_copy, q_copy=q_copy)
     g = torch.Generator().manual_seed(3)
     for step in range(3):
         qh = torch.randn((L, B, Hq, d), generator=g).to(torch.bfloat16)
