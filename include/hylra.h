@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define HYLRA_ABI_VERSION 4
+#define HYLRA_ABI_VERSION 5
 
 enum hylra_status {
   HYLRA_OK = 0,
@@ -225,6 +225,15 @@ typedef struct hylra_step_options {
   void* join_event;   /* side -> stream: SELECT(B) done */
   void* reuse_wait_event;
   void* const* layer_events;
+  /* the step's new K/V rows, [L][B][Hkv][d] in the cache dtype, device or pinned host memory
+     (NULL: none), written at cache row append_pos (< n_valid) before they are read. With
+     fuse_select = 2 the single-launch kernel writes them itself (no extra launch: each FULL
+     pair's own row by the split that streams it, the REUSE layers' rows by the FULL pair
+     whose selection they inherit); otherwise hylra_append_kv runs first. Not with
+     hylra_decode_step_offload. (ABI 5) */
+  const void* append_k_rows;
+  const void* append_v_rows;
+  int32_t append_pos;
 } hylra_step_options;
 
 int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, const void* v,

@@ -90,6 +90,9 @@ class StepOptions(ctypes.Structure):
         ("join_event", ctypes.c_void_p),
         ("reuse_wait_event", ctypes.c_void_p),
         ("layer_events", ctypes.c_void_p),
+        ("append_k_rows", ctypes.c_void_p),
+        ("append_v_rows", ctypes.c_void_p),
+        ("append_pos", ctypes.c_int32),
     ]
 
 

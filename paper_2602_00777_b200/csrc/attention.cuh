@@ -50,6 +50,7 @@ struct AttnParams {
   int B, Hkv, G, cap;
   int n_valid;          // valid cache rows
   int n_rows;           // rows this op attends over: n_valid (FULL) or k_eff (REUSE)
+  int n_slots;          // layer slots of the launch
   int splits;
   int tiles_per_split;
   int k_stride, sel_group, n_groups;
@@ -694,12 +695,42 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
 // no deadlock whatever the CTA dispatch order. The FULL tail (last splits, fused selects)
 // overlaps the REUSE gathers instead of ending a launch. The last CTA to finish resets the
 // ticket, the done counter and the ready flags (the workspace stays zeroed between steps).
+// The step's new K/V rows (hylra_step_options append_*), written by the FULL items
+// themselves: the split whose tile range holds row `pos` writes its own pair's FULL-layer
+// row before its TMA loads (generic writes, then a proxy fence, then the TMA), and the
+// splits of every FULL pair share out the rows of the REUSE layers that inherit its
+// selection (visible to those REUSE items through the same ready flag they wait on).
+struct StepAppend {
+  const uint4* k_rows;  // [L][B][Hkv][d] in 16-byte chunks (device or pinned host), or null
+  const uint4* v_rows;
+  uint8_t* k;           // cache bases (bytes)
+  uint8_t* v;
+  int64_t kv_sl, kv_sb, kv_sh, pos_bytes;  // bytes
+  int pos, chunks;                          // chunks = 16-byte chunks per row
+};
+
 struct StepSync {
   int* ctr;     // [0] ticket, [1] done
   int* ready;   // [n_full][B][n_groups]
   int n_ready;
   int n_full_items, n_items;
+  StepAppend app;
 };
+
+// One (layer, b, kv-head) row pair of the step's new K/V rows into the cache: threads
+// [0, 2 chunks) copy one 16-byte chunk each (K then V).
+__device__ __forceinline__ void append_row(const StepAppend& a, int B, int Hkv, int row_layer,
+                                           int cache_layer, int b, int kh) {
+  const int t = threadIdx.x;
+  if (t >= 2 * a.chunks) return;
+  const bool is_v = t >= a.chunks;
+  const int c = is_v ? t - a.chunks : t;
+  const int64_t src = (((int64_t)row_layer * B + b) * Hkv + kh) * a.chunks + c;
+  const uint4 val = is_v ? a.v_rows[src] : a.k_rows[src];
+  uint8_t* dst = (is_v ? a.v : a.k) + cache_layer * a.kv_sl + b * a.kv_sb + kh * a.kv_sh +
+                 a.pos_bytes;
+  reinterpret_cast<uint4*>(dst)[c] = val;
+}
 
 template <int D, bool GBIG, int STAGES>
 __global__ void __launch_bounds__(attn_threads<true>(), 2)
@@ -719,8 +750,22 @@ __global__ void __launch_bounds__(attn_threads<true>(), 2)
     t /= pf.splits;
     const int kh = t % pf.Hkv;
     t /= pf.Hkv;
-    attn_mma_item<D, false, GBIG, STAGES>(tmk, tmv, pf, sp, smem, split, kh, t / pf.B, t % pf.B,
-                                          nullptr, ss.ready);
+    const int slot = t / pf.B, b = t % pf.B;
+    if (ss.app.k_rows != nullptr) {
+      if (split == (ss.app.pos / kTileRows) / pf.tiles_per_split)
+        append_row(ss.app, pf.B, pf.Hkv, pf.layers[slot], pf.kv_layers[slot], b, kh);
+      int j = 0;
+      for (int r = 0; r < pr.n_slots; ++r) {
+        if (pr.src_slot[r] != sp.out_slot[slot]) continue;
+        if (j % pf.splits == split)
+          append_row(ss.app, pf.B, pf.Hkv, pr.layers[r], pr.kv_layers[r], b, kh);
+        ++j;
+      }
+      // the writes are read by this CTA's TMA (async proxy) and by other CTAs' cp.async
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    attn_mma_item<D, false, GBIG, STAGES>(tmk, tmv, pf, sp, smem, split, kh, slot, b, nullptr,
+                                          ss.ready);
   } else {
     t -= ss.n_full_items;
     const int split = t % pr.splits;

@@ -335,7 +335,7 @@ int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* 
   p.o_sl = g->out_stride_layer; p.o_sb = g->out_stride_batch;
   p.B = g->batch; p.Hkv = g->kv_heads; p.G = G;
   p.cap = scores_row_stride(g);
-  p.n_valid = n_valid; p.n_rows = n_rows;
+  p.n_valid = n_valid; p.n_rows = n_rows; p.n_slots = n_layers;
   p.splits = lay.splits; p.tiles_per_split = lay.tps;
   p.k_stride = k_stride; p.sel_group = sel_group > 0 ? sel_group : 1;
   p.n_groups = g->kv_heads / p.sel_group;
@@ -699,6 +699,9 @@ bool fused_select_fits(const hylra_geometry* g, int n_valid) {
 struct StepOpts {
   bool fuse = false;  // selects of the FULL layers feeding REUSE fused into the FULL kernel
   bool unified = false;  // single-launch step (fuse_select == 2)
+  const void* app_k = nullptr;  // the step's new K/V rows [L][B][Hkv][d] (append_* options)
+  const void* app_v = nullptr;
+  int app_pos = -1;
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, select = nullptr, full = nullptr, join = nullptr;
   cudaEvent_t reuse_wait = nullptr;
@@ -754,6 +757,21 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   // single-launch step: every select fused into the FULL items, REUSE items in the same grid
   const bool unified = o.unified && !s.aug_stride && sel_group == 1 && use_mma_path(g) &&
                        fused_select_fits(g, n_valid) && !o.layer_events;
+  // the step's new K/V rows: written inside the single-launch kernel, else by the append
+  // kernel ahead of the step
+  const bool appending = o.app_k != nullptr || o.app_v != nullptr;
+  if (appending) {
+    if (!o.app_k || !o.app_v)
+      return fail(HYLRA_ERR_CONFIGURATION, "append needs both append_k_rows and append_v_rows");
+    if (split) return fail(HYLRA_ERR_CONFIGURATION, "append is not supported with split caches");
+    if (o.app_pos < 0 || o.app_pos >= n_valid)
+      return fail(HYLRA_ERR_INVALID_INPUT, "append_pos %d not in [0, n_valid=%d)", o.app_pos,
+                  n_valid);
+    if (!unified)
+      if (int e = hylra_append_kv(g, const_cast<void*>(k), const_cast<void*>(v), o.app_k, o.app_v,
+                                  o.app_pos, 0, nullptr, st))
+        return e;
+  }
   if (unified) {
     std::vector<int32_t> ab_ids(a_ids), ab_slot(a_slot), ab_kv(a_kv);
     ab_ids.insert(ab_ids.end(), b_ids.begin(), b_ids.end());
@@ -795,6 +813,27 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     ss.n_ready = s.n_ready;
     ss.n_full_items = (int)items_f;
     ss.n_items = (int)(items_f + items_r);
+    if (appending) {
+      StepAppend& ap = ss.app;
+      if (int e = device_view(o.app_k, reinterpret_cast<const void**>(&ap.k_rows), "append_k_rows"))
+        return e;
+      if (int e = device_view(o.app_v, reinterpret_cast<const void**>(&ap.v_rows), "append_v_rows"))
+        return e;
+      const int64_t es = 2, row_bytes = (int64_t)g->head_dim * es;  // tensor-core path: bf16
+      if ((g->kv_stride_layer * es) % 16 || (g->kv_stride_batch * es) % 16 ||
+          (g->kv_stride_head * es) % 16 || reinterpret_cast<uintptr_t>(k) % 16 ||
+          reinterpret_cast<uintptr_t>(v) % 16 || reinterpret_cast<uintptr_t>(ap.k_rows) % 16 ||
+          reinterpret_cast<uintptr_t>(ap.v_rows) % 16)
+        return fail(HYLRA_ERR_CONFIGURATION, "append needs 16-byte aligned rows and strides");
+      ap.k = static_cast<uint8_t*>(const_cast<void*>(k));
+      ap.v = static_cast<uint8_t*>(const_cast<void*>(v));
+      ap.kv_sl = g->kv_stride_layer * es;
+      ap.kv_sb = g->kv_stride_batch * es;
+      ap.kv_sh = g->kv_stride_head * es;
+      ap.pos = o.app_pos;
+      ap.pos_bytes = (int64_t)o.app_pos * row_bytes;
+      ap.chunks = (int)(row_bytes / 16);
+    }
     if (o.reuse_wait)
       if (int e = cuda_check(cudaStreamWaitEvent(st, o.reuse_wait, 0), "stream wait event"))
         return e;
@@ -1028,6 +1067,9 @@ int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, 
   if (opt) {
     o.fuse = opt->fuse_select != 0;
     o.unified = opt->fuse_select == 2;
+    o.app_k = opt->append_k_rows;
+    o.app_v = opt->append_v_rows;
+    o.app_pos = opt->append_pos;
     o.side = static_cast<cudaStream_t>(opt->side_stream);
     o.fork = static_cast<cudaEvent_t>(opt->fork_event);
     o.select = static_cast<cudaEvent_t>(opt->select_event);

@@ -223,13 +223,17 @@ class HybridDecoder:
             g, self._acts, int(n_valid), self.budget, self.sel_group, self.sinks, self.recent))
 
     def step(self, q: torch.Tensor, n_valid: int | None = None, *, layer_events=None,
-             reuse_wait=None, out: torch.Tensor | None = None) -> StepResult:
+             reuse_wait=None, out: torch.Tensor | None = None, append=None) -> StepResult:
         """Enqueue one decode step. layer_events (optional, L torch.cuda.Event or None):
         event l is recorded once out[l] is final, REUSE layers being launched in chunks
         that end at the evented layers; reuse_wait (optional event): the REUSE launches
         wait on it (hylra_decode_step_ex). Token mode only. out (optional): fp32
         [L, B, Hq, d] destination instead of the decoder's own buffer — device memory or
-        pinned host memory, which the kernels then write across the link directly."""
+        pinned host memory, which the kernels then write across the link directly.
+        append (optional, token mode): (k_rows, v_rows, pos) — this step's new K/V rows
+        [L, B, Hkv, d] (device or pinned host, cache dtype), written at cache row pos
+        (< n_valid) before they are read; the single-launch step writes them inside its one
+        kernel (hylra_step_options append_*)."""
         if out is not None:
             if out.shape != self.out.shape or out.dtype != torch.float32 \
                     or not out.is_contiguous() or not (out.is_cuda or out.is_pinned()):
@@ -238,7 +242,8 @@ class HybridDecoder:
             own = self.out
             self.out = out
             try:
-                return self.step(q, n_valid, layer_events=layer_events, reuse_wait=reuse_wait)
+                return self.step(q, n_valid, layer_events=layer_events, reuse_wait=reuse_wait,
+                                 append=append)
             finally:
                 self.out = own
         g = self._geometry(q)
@@ -263,6 +268,17 @@ class HybridDecoder:
                  opt.join_event) = (e.cuda_event for e in self._events)
             if reuse_wait is not None:
                 opt.reuse_wait_event = reuse_wait.cuda_event
+            if append is not None:
+                k_rows, v_rows, pos = append
+                L, B, Hkv, cap, d = self.k.shape
+                for t in (k_rows, v_rows):
+                    if t.shape != (L, B, Hkv, d) or t.dtype != self.k.dtype \
+                            or not t.is_contiguous() or not (t.is_cuda or t.is_pinned()):
+                        raise ConfigurationError("new rows must be contiguous [L, B, Hkv, d] "
+                                                 "device or pinned host tensors of the cache "
+                                                 "dtype")
+                opt.append_k_rows, opt.append_v_rows = k_rows.data_ptr(), v_rows.data_ptr()
+                opt.append_pos = int(pos)
             evs = None
             if layer_events is not None:
                 evs = _abi.pointer_array(e.cuda_event if e is not None else None
@@ -276,8 +292,8 @@ class HybridDecoder:
             k_eff = min(self.budget, n_valid)
             return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer,
                               self.full_layers)
-        if layer_events is not None or reuse_wait is not None:
-            raise ConfigurationError("per-layer events apply to token selection only")
+        if layer_events is not None or reuse_wait is not None or append is not None:
+            raise ConfigurationError("per-layer events and append apply to token selection only")
         if self.block_size > 1:
             need = int(lib.hylra_decode_step_blocks_workspace_bytes(
                 g, self._acts, n_valid, self.budget, self.block_size, self.sel_group))
@@ -582,8 +598,14 @@ class DecodeLoop:
                 with torch.cuda.stream(self.side):
                     self.q_dev.copy_(self.q_host, non_blocking=True)
                 q = self.q_dev
-            if not self.reuse_layers or dec.single:
-                # single-launch step: one kernel after the append, nothing to overlap
+            if dec.single:
+                # single-launch step: the kernel writes the new rows itself (one launch)
+                if q_copy:
+                    main.wait_stream(self.side)
+                dec.step(q, pos + 1, out=self.out_host,
+                         append=(self.k_host, self.v_host, pos))
+                return
+            if not self.reuse_layers:
                 dec.append(self.k_host, self.v_host, pos)
                 if q_copy:
                     main.wait_stream(self.side)

@@ -68,6 +68,9 @@ parts = {
     "h2d": lambda: (q_dev.copy_(q_host, non_blocking=True), kv_dev.copy_(kv_host, non_blocking=True)),
     "append": lambda: (dec.k[:, :, :, pos].copy_(kv_dev[0]), dec.v[:, :, :, pos].copy_(kv_dev[1])),
     "d2h": lambda: out_host.copy_(dec.out, non_blocking=True),
+    # the new rows written by the step itself (single-launch kernel: no append launch)
+    "zc_step_append": lambda: dec.step(q_host, pos + 1, out=out_host,
+                                       append=(k_rows, v_rows, pos)),
 }
 res = {}
 for name, fn in parts.items():

@@ -504,6 +504,40 @@ def test_autotune_keeps_results_bit_identical():
     assert f32.autotune(q.float(), cap, reps=2).keys() == {"fused3"}
 
 
+@pytest.mark.parametrize("schedule", ["single", "fusedsel", "fused3"])
+def test_step_append_option_equals_separate_append(schedule):
+    """hylra_step_options append_*: the step's new K/V rows written inside the step (by the
+    single-launch kernel itself: each FULL pair's own row by the split that streams it, the
+    REUSE layers' rows by the FULL pair they inherit from; by the append kernel otherwise)
+    give the same cache, selections and outputs as hylra_append_kv followed by the step. The
+    new row's key is aligned with the queries so every selection contains it."""
+    L, B, Hq, Hkv, d, cap, budget = 7, 2, 16, 4, 128, 3000, 192
+    actions = ("full", "reuse", "reuse", "full", "full", "reuse", "reuse")
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=53, planted=32)
+    pos = 2500
+    g = torch.Generator().manual_seed(9)
+    qm = q.float().view(L, B, Hkv, Hq // Hkv, d).mean(3)
+    k_new = (4.0 * qm / qm.norm(dim=-1, keepdim=True)
+             + 0.1 * torch.randn((L, B, Hkv, d), generator=g).cuda()).to(torch.bfloat16)
+    v_new = torch.randn((L, B, Hkv, d), generator=g).to(torch.bfloat16)
+    k_pinned, v_pinned = k_new.cpu().pin_memory(), v_new.pin_memory()
+    k1, v1 = k.clone(), v.clone()
+    ref = HybridDecoder(actions, k1, v1, budget, q_heads=Hq, fuse_select=False)
+    ref.append(k_pinned, v_pinned, pos)
+    r = ref.step(q, pos + 1)
+    torch.cuda.synchronize()
+    R, I = r.outputs.clone(), r.selections.clone()
+    assert bool((I == pos).any(-1).all()), "the new row must be selected everywhere"
+    k2, v2 = k.clone(), v.clone()
+    dec = HybridDecoder(actions, k2, v2, budget, q_heads=Hq)
+    dec.set_schedule(schedule)
+    res = dec.step(q, pos + 1, append=(k_pinned, v_pinned, pos))
+    torch.cuda.synchronize()
+    dec.check_flags()
+    assert torch.equal(k2, k1) and torch.equal(v2, v1)
+    assert torch.equal(res.selections, I) and torch.equal(res.outputs, R)
+
+
 def test_step_layer_events_chunks_reuse():
     """hylra_decode_step_events: per-layer completion events split the REUSE launch into
     chunks; selections identical, outputs within split-K rounding; events fire."""
