@@ -264,6 +264,10 @@ cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const 
 }
 
 // Single-launch step (FULL items with fused selects, then REUSE items; attention.cuh).
+// Its parameters stay within the classic 4 KB kernel-parameter space.
+static_assert(2 * sizeof(CUtensorMap) + 2 * sizeof(AttnParams) + sizeof(SelectParams) +
+                      sizeof(StepSync) <= 4096,
+              "step_mma_kernel parameters exceed 4 KB");
 template <int D, bool GBIG>
 cudaError_t launch_step_mma(int n_items, cudaStream_t st, const CUtensorMap& tk,
                             const CUtensorMap& tv, const AttnParams& pf, const AttnParams& pr,
