@@ -40,6 +40,11 @@ struct AttnParams {
   float* scores;        // FULL: [slot][b][kh][cap] or null
   const int32_t* idx;   // REUSE: [src_slot][b][group][k_stride]
   const int32_t* counts;  // REUSE: optional rows per selection row (block coverage)
+  // block-mode REUSE by TMA tiles (blk != null; tensor-core path, blk_size % 64 == 0): the
+  // selection row's ascending block ids [src_slot][b][grp][blk_stride]; tile t of the pair
+  // covers cache rows blk[t / (blk_size/64)] * blk_size + (t % (blk_size/64)) * 64 + [0, 64)
+  const int32_t* blk;
+  int blk_stride, blk_size;
   float* ws_o;          // [pair][split][G][D]
   float* ws_ml;         // [pair][split][G][2]
   int* counters;        // [pair]
@@ -431,7 +436,7 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
   const int t_end = min(n_tiles, t_begin + p.tiles_per_split);
   const int n_my = t_end - t_begin;
   // rows of this pair: uniform, or the selection row's own length (block coverage)
-  const int n_rows = (GATHER && p.counts != nullptr)
+  const int n_rows = ((GATHER || p.blk != nullptr) && p.counts != nullptr)
                          ? min(p.n_rows, __ldg(p.counts + (int64_t)(p.src_slot[slot] * p.B + b) *
                                                               p.n_groups + kh / p.sel_group))
                          : p.n_rows;
@@ -453,13 +458,31 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
         tma_prefetch_desc(&tmk);
         tma_prefetch_desc(&tmv);
         const uint64_t pol = l2_policy_evict_first();
+        // block-mode REUSE: tile t covers rows blk[t / tpb] * blk_size + (t % tpb) * 64; the
+        // block ids are loaded kAhead tiles ahead so no TMA issue waits on a global load
+        constexpr int kAhead = 4;
+        const int tpb = p.blk != nullptr ? p.blk_size / kTileRows : 1;
+        const int32_t* bl =
+            p.blk == nullptr ? nullptr
+                             : p.blk + ((int64_t)(p.src_slot[slot] * p.B + b) * p.n_groups +
+                                        kh / p.sel_group) * p.blk_stride;
+        int ahead[kAhead];
+#pragma unroll
+        for (int j = 0; j < kAhead; ++j)
+          ahead[j] = (bl != nullptr && j < n_my) ? __ldcg(bl + (t_begin + j) / tpb) : 0;
         for (int i = 0; i < n_my; ++i) {
           const int s = i % STAGES;
+          int row = (t_begin + i) * kTileRows;
+          if (bl != nullptr) {
+            row = ahead[0] * p.blk_size + ((t_begin + i) % tpb) * kTileRows;
+#pragma unroll
+            for (int j = 0; j + 1 < kAhead; ++j) ahead[j] = ahead[j + 1];
+            ahead[kAhead - 1] = (i + kAhead < n_my) ? __ldcg(bl + (t_begin + i + kAhead) / tpb) : 0;
+          }
           mbar_wait(empty_bar + s, ((i / STAGES) & 1) ^ 1);
           uint8_t* kt = smem + s * SM::kStageBytes;
           uint8_t* vt = kt + SM::kTileBytes;
           mbar_arrive_expect_tx(full_bar + s, SM::kStageBytes);
-          const int row = (t_begin + i) * kTileRows;
 #pragma unroll
           for (int bx = 0; bx < SM::kBoxes; ++bx) {
             tma_load_5d(kt + bx * kTileRows * 128, &tmk, full_bar + s, bx * 64, row, kh, b, kvl,

@@ -367,13 +367,24 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
                      const int32_t* counts, int k_stride, int sel_group, float* out,
                      float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st,
                      const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0,
-                     const SelectParams* fused = nullptr, int fuse_nslots = 0) {
+                     const SelectParams* fused = nullptr, int fuse_nslots = 0,
+                     const int32_t* blk = nullptr, int blk_stride = 0, int blk_size = 0) {
   AttnParams p{};
   AttnLayout lay{};
   if (int e = make_attn_params(&p, &lay, g, gather, q, k, v, n_valid, n_rows, n_layers, layer_ids,
                                src_slots, idx, counts, k_stride, sel_group, out, scores, ws,
                                ws_bytes, flags, kv_layer_ids, kv_layer_count))
     return e;
+  // block-mode REUSE by TMA tiles of the selected blocks: REUSE split rules, the streaming
+  // (TMA) kernel
+  if (blk != nullptr) {
+    if (!gather || !use_mma_path(g) || blk_size % kTileRows != 0 || scores != nullptr)
+      return fail(HYLRA_ERR_CONFIGURATION, "block tiles need a tensor-core REUSE launch");
+    p.blk = blk;
+    p.blk_stride = blk_stride;
+    p.blk_size = blk_size;
+    gather = false;
+  }
   const int G = g->q_heads / g->kv_heads;
   const int n_kv = kv_layer_ids ? kv_layer_count : g->num_layers;
   dim3 grid(lay.splits, g->kv_heads, g->batch * n_layers);
@@ -978,6 +989,15 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   return wait(st, o.join);
 }
 
+// HYLRA_BLOCK_TILES=1: block-mode REUSE streams the selected blocks as TMA tiles instead of
+// gathering the coverage row by row. Bit-identical; measured at cfg2 B=8 (block_size 128,
+// 16 blocks): REUSE alone 248 vs 254 us, but the graph-replayed step 1.56 vs 1.52-1.55 ms,
+// so the gather stays the default (scripts/block_ab.py).
+bool block_tiles_off() {
+  const char* e = std::getenv("HYLRA_BLOCK_TILES");
+  return !(e && *e && atoi(e) == 1);
+}
+
 }  // namespace
 
 // ======================================================================== extern "C"
@@ -1231,10 +1251,14 @@ int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void*
                                   nullptr, flags, st))
     return e;
   if (!s.reuse_ids.empty()) {
+    // whole blocks of 64-row multiples can stream as TMA tiles (the coverage rows are
+    // contiguous within a block; HYLRA_BLOCK_TILES=1), else the coverage is gathered
+    const bool tiles = use_mma_path(g) && block_size % kTileRows == 0 && !block_tiles_off();
     if (int e = launch_attention(g, true, q, k, v, n_valid, s.k_eff, (int)s.reuse_ids.size(),
                                  s.reuse_ids.data(), s.reuse_src.data(), toks, cnts, s.tok_stride,
                                  sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags,
-                                 st))
+                                 st, nullptr, 0, nullptr, 0, tiles ? blocks : nullptr, bk_stride,
+                                 block_size))
       return e;
   }
   return HYLRA_OK;

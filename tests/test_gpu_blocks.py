@@ -140,3 +140,29 @@ def test_block_refinement_all_tied(n, bs, bb):
     assert np.array_equal(sel[res.slot_of_layer[0]], ref_blocks[0])
     assert list(ref_blocks[0][0, 0]) == list(range(bb))
     assert max_head_err(res.outputs.double().cpu().numpy(), ref_out) < 2e-2
+
+
+@pytest.mark.parametrize("bs,bb,n_valid", [(128, 8, 4100), (64, 12, 4096), (192, 6, 3900)])
+def test_block_reuse_tiles_equal_row_gather(bs, bb, n_valid, monkeypatch):
+    """Block-mode REUSE by TMA tiles of the selected blocks (block_size a multiple of 64)
+    reads the same rows in the same order as the row-by-row coverage gather: identical
+    outputs and selections (HYLRA_BLOCK_TILES=0 forces the gather). A ragged last block
+    (n_valid not a multiple of block_size) is masked by the coverage count."""
+    L, B, Hq, Hkv, d, cap = 5, 2, 16, 4, 128, 4200
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=23, planted=48)
+    # plant the final token so the ragged last block is selected
+    k[:, :, :, n_valid - 1, :] = 4.0 * q.float().view(L, B, Hkv, Hq // Hkv, d).mean(3).to(k.dtype)
+    actions = ("full", "reuse", "full", "reuse", "reuse")
+    monkeypatch.setenv("HYLRA_BLOCK_TILES", "0")
+    ref = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs).step(q, n_valid)
+    torch.cuda.synchronize()
+    R, S = ref.outputs.clone(), ref.selections.clone()
+    nb = -(-n_valid // bs)
+    assert bool((S == nb - 1).any(-1).all()), "the ragged last block must be selected"
+    monkeypatch.setenv("HYLRA_BLOCK_TILES", "1")
+    dec = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs)
+    res = dec.step(q, n_valid)
+    torch.cuda.synchronize()
+    dec.check_flags()
+    assert torch.equal(res.selections, S)
+    assert torch.equal(res.outputs, R)
