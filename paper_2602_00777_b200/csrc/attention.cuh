@@ -401,6 +401,20 @@ __device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
   return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
 }
 
+#ifdef HYLRA_TRACE
+// Diagnostics build only (-DHYLRA_TRACE, scripts/trace_single.py): per single-launch CTA,
+// globaltimer marks [0 ticket, 1 select start, 2 REUSE ready, 3 select end, 4 done, 5 smid]
+__device__ long long* g_trace;
+__shared__ int g_trace_row;
+__device__ __forceinline__ long long* hylra_trace_rec() { return g_trace + g_trace_row * 8; }
+__device__ __forceinline__ void hylra_trace_mark(int k) {
+  if (g_trace == nullptr) return;
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  hylra_trace_rec()[k] = t;
+}
+#endif
+
 // ready flag of a selection row: 0 until the fused select of its FULL pair has written the
 // row's indices (single-launch step); release by one thread after a CTA-scope barrier,
 // acquire by every reader lane
@@ -518,6 +532,9 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
           while (ld_acquire_gpu(ready_wait) == 0) __nanosleep(64);
         __syncwarp();
         (void)ld_acquire_gpu(ready_wait);
+#ifdef HYLRA_TRACE
+        if (lane == 0 && warp == kConsumerWarps) hylra_trace_mark(2);
+#endif
       }
       if (staged) {
         stage_indices(ib + pos_begin, n_pos, p.n_valid, sidx, p.flags, lane,
@@ -687,7 +704,13 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
       __shared__ Red sel_red;
       asm volatile("bar.sync 1, 128;" ::: "memory");  // merge reads of smem are done
       __threadfence();
+#ifdef HYLRA_TRACE
+      if (threadIdx.x == 0) hylra_trace_mark(1);
+#endif
       select_row<kConsumerWarps * 32, true>(sp, kh, b, slot, smem, sel_red, false);
+#ifdef HYLRA_TRACE
+      if (threadIdx.x == 0) hylra_trace_mark(3);
+#endif
       if (ready_set != nullptr) {
         asm volatile("bar.sync 1, 128;" ::: "memory");  // the row's indices are written
         if (threadIdx.x == 0) {
@@ -768,6 +791,15 @@ __global__ void __launch_bounds__(attn_threads<true>(), 2)
   if (threadIdx.x == 0) s_ticket = atomicAdd(ss.ctr, 1);
   __syncthreads();
   int t = s_ticket;
+#ifdef HYLRA_TRACE
+  if (threadIdx.x == 0) {
+    g_trace_row = t;
+    hylra_trace_mark(0);
+    unsigned sm;
+    asm("mov.u32 %0, %%smid;" : "=r"(sm));
+    if (g_trace != nullptr) hylra_trace_rec()[5] = sm;
+  }
+#endif
   if (t < ss.n_full_items) {
     const int split = t % pf.splits;
     t /= pf.splits;
@@ -802,6 +834,9 @@ __global__ void __launch_bounds__(attn_threads<true>(), 2)
   // every warp is done with the item (barrier 2: barrier 0 belongs to the fused select's 128
   // threads while the producer warps wait here)
   asm volatile("bar.sync 2, %0;" ::"n"(32 * (kConsumerWarps + kGatherProducers)) : "memory");
+#ifdef HYLRA_TRACE
+  if (threadIdx.x == 0) hylra_trace_mark(4);
+#endif
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(ss.ctr + 1, 1) == ss.n_items - 1) {

@@ -1003,6 +1003,14 @@ bool block_tiles_off() {
 // ======================================================================== extern "C"
 extern "C" {
 
+#ifdef HYLRA_TRACE
+// diagnostics build only: the per-CTA trace buffer of the single-launch kernel (8 x int64
+// per ticket) or NULL
+int hylra_trace_set(void* buf) {
+  return cuda_check(cudaMemcpyToSymbol(hylra::g_trace, &buf, sizeof(buf)), "trace set");
+}
+#endif
+
 int hylra_abi_version(void) { return HYLRA_ABI_VERSION; }
 
 const char* hylra_status_string(int status) {
