@@ -1009,6 +1009,9 @@ extern "C" {
 int hylra_trace_set(void* buf) {
   return cuda_check(cudaMemcpyToSymbol(hylra::g_trace, &buf, sizeof(buf)), "trace set");
 }
+int hylra_trace_set_select_info(void* buf) {
+  return cuda_check(cudaMemcpyToSymbol(hylra::g_sel_info, &buf, sizeof(buf)), "trace set");
+}
 #endif
 
 int hylra_abi_version(void) { return HYLRA_ABI_VERSION; }

@@ -87,6 +87,12 @@ __host__ __device__ constexpr size_t sel_smem_bytes(int n, int nt, bool big = fa
   return sel_bitmap_bytes(n, nt) + sel_fixed_bytes(nt, big);
 }
 
+#ifdef HYLRA_TRACE
+// diagnostics build only: per-row phase cycles of selections that have no info buffer
+// (the fused ones), [row][8] as SelectParams::info
+__device__ int32_t* g_sel_info;
+#endif
+
 struct SelSmem {
   uint32_t* bitmap;  // [chunks * NT]
   unsigned* hist;    // [kBins]
@@ -557,6 +563,9 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
   const int row_id = (p.out_slot[slot] * p.B + b) * p.n_groups + grp;
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
   int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
+#ifdef HYLRA_TRACE
+  if (info == nullptr && g_sel_info != nullptr) info = g_sel_info + row_id * 8;
+#endif
   const SelSmem sm = carve<NT>(sraw, n);
   constexpr int kBandCap = sel_band_cap(NT, PIPE);
   const long long t0 = clock64();

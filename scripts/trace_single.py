@@ -29,9 +29,21 @@ buf = torch.zeros(200000 * 8, dtype=torch.int64, device="cuda")
 lib = _abi.lib()
 lib.hylra_trace_set.argtypes = [ctypes.c_void_p]
 lib.hylra_trace_set(buf.data_ptr())
+info = torch.zeros(100000 * 8, dtype=torch.int32, device="cuda")
+lib.hylra_trace_set_select_info.argtypes = [ctypes.c_void_p]
+lib.hylra_trace_set_select_info(info.data_ptr())
 dec.step(q, cfg.context)
 torch.cuda.synchronize()
 lib.hylra_trace_set(None)
+lib.hylra_trace_set_select_info(None)
+inf = info.view(-1, 8).cpu().numpy()
+inf = inf[inf[:, 0] != 0]
+if len(inf):
+    names = ["A sample", "B pass(+H)", "C+D", "E window+compact"]
+    print("  fused select phases (median cycles):",
+          {nm: int(np.median(inf[:, 4 + j])) for j, nm in enumerate(names)},
+          "modes", dict(zip(*[x.tolist() for x in np.unique(inf[:, 2], return_counts=True)])),
+          "band median", int(np.median(inf[:, 3])))
 tr = buf.view(-1, 8).cpu().numpy()
 n = int((tr[:, 0] != 0).sum())
 tr = tr[:n]
