@@ -528,8 +528,17 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
       const bool staged = n_pos <= kIdxStage;
       if (ready_wait != nullptr) {
         // single-launch step: the selection row is written by a FULL item of the same grid
-        if (lane == 0)
-          while (ld_acquire_gpu(ready_wait) == 0) __nanosleep(64);
+        // bounded: a flag that never comes (it cannot, short of a corrupted workspace) turns
+        // into HYLRA_FLAG_INTERNAL after ~2 s instead of a hung GPU
+        if (lane == 0) {
+          for (long long spins = 0; ld_acquire_gpu(ready_wait) == 0; ++spins) {
+            if (spins > (1ll << 25)) {
+              atomicOr(p.flags, 8);
+              break;
+            }
+            __nanosleep(64);
+          }
+        }
         __syncwarp();
         (void)ld_acquire_gpu(ready_wait);
 #ifdef HYLRA_TRACE
@@ -790,7 +799,9 @@ __global__ void __launch_bounds__(attn_threads<true>(), 2)
   pdl_wait();
   if (threadIdx.x == 0) s_ticket = atomicAdd(ss.ctr, 1);
   __syncthreads();
-  int t = s_ticket;
+  // modulo: even a counter left non-zero (a workspace that was not zeroed) hands out every
+  // item exactly once, so no REUSE item can wait on a FULL item that never runs
+  int t = s_ticket % ss.n_items;
 #ifdef HYLRA_TRACE
   if (threadIdx.x == 0) {
     g_trace_row = t;
