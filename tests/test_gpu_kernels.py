@@ -401,23 +401,25 @@ def test_fused_select_step_equals_unfused(actions, d, refine, n):
     assert torch.equal(dec.out, ref_out)
 
 
-@pytest.mark.parametrize("actions,d,refine,n,B", [
-    (("full", "reuse", "full", "full", "reuse", "reuse", "full", "reuse", "full", "full"), 128, True, 4096, 2),
-    (("full", "full", "reuse", "reuse"), 64, True, 3001, 2),
-    (("full", "reuse", "full", "reuse"), 128, False, 4096, 1),
-    (("full", "full", "reuse", "full", "reuse"), 128, True, 70000, 1),
-    (("full", "reuse", "full", "reuse"), 128, True, 1500, 3),
-    (("full", "reuse", "reuse"), 64, True, 200, 2),
-    (("full", "full", "full"), 128, True, 2048, 2),            # no REUSE layer
-    (("full",) + ("reuse",) * 15, 128, True, 8192, 4),         # one source, many waiters
+@pytest.mark.parametrize("actions,d,refine,n,B,Hq,Hkv", [
+    (("full", "reuse", "full", "full", "reuse", "reuse", "full", "reuse", "full", "full"), 128, True, 4096, 2, 16, 4),
+    (("full", "full", "reuse", "reuse"), 64, True, 3001, 2, 16, 4),
+    (("full", "reuse", "full", "reuse"), 128, False, 4096, 1, 16, 4),
+    (("full", "full", "reuse", "full", "reuse"), 128, True, 70000, 1, 16, 4),
+    (("full", "reuse", "full", "reuse"), 128, True, 1500, 3, 16, 4),
+    (("full", "reuse", "reuse"), 64, True, 200, 2, 16, 4),
+    (("full", "full", "full"), 128, True, 2048, 2, 16, 4),            # no REUSE layer
+    (("full",) + ("reuse",) * 15, 128, True, 8192, 4, 16, 4),         # one source, many waiters
+    (("full", "reuse", "full", "reuse"), 128, True, 3000, 2, 16, 1),   # G = 16 (both halves)
+    (("full", "reuse", "reuse"), 64, True, 2500, 3, 12, 1),            # G = 12, d = 64
 ])
-def test_single_launch_step_equals_unfused(actions, d, refine, n, B):
+def test_single_launch_step_equals_unfused(actions, d, refine, n, B, Hq, Hkv):
     """hylra_decode_step_ex fuse_select=2: FULL items (every select fused) and REUSE items
     (waiting on per-row ready flags) in one grid. Same split-K partitions as the plain
     3-launch step, so outputs and selections are bit-identical; repeated eager steps and
     CUDA-graph replays check that the ticket / ready flags reset themselves."""
     L = len(actions)
-    Hq, Hkv, budget = 16, 4, 256
+    budget = 256
     cap = n
     q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=43, planted=64)
     ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=refine,
