@@ -170,8 +170,30 @@ int main(void) {
         }
       }
   }
-  printf("decode_step.c: launches %llu, worst relative L2 %.2e, set mismatches %d\n",
-         (unsigned long long)hylra_launch_count(), worst, bad_sets);
+  /* the same step as ONE kernel (hylra_decode_step_ex, fuse_select = 2): same split-K
+     partitions, so outputs and selections must match the 3-launch step bit for bit */
+  hylra_step_options opt;
+  memset(&opt, 0, sizeof(opt));
+  opt.fuse_select = 2;
+  const unsigned long long before = hylra_launch_count();
+  CK(cudaMemset(dout, 0, nq * 4));
+  CK(cudaMemset(didx, 0, sizeof(int32_t) * n_full * B * HKV * k_eff));
+  HY(hylra_decode_step_ex(&g, dq, dk, dv, N, actions, BUDGET, 1, 1, 0, 0, dout, didx, k_eff, dws,
+                          ws_bytes, st, &opt));
+  CK(cudaStreamSynchronize(st));
+  const unsigned long long single_launches = hylra_launch_count() - before;
+  float* hout1 = malloc(nq * 4);
+  int32_t* hidx1 = malloc(sizeof(int32_t) * n_full * B * HKV * k_eff);
+  CK(cudaMemcpy(hout1, dout, nq * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hidx1, didx, sizeof(int32_t) * n_full * B * HKV * k_eff, cudaMemcpyDeviceToHost));
+  const int single_same = memcmp(hout1, hout, nq * 4) == 0 &&
+                          memcmp(hidx1, hidx, sizeof(int32_t) * n_full * B * HKV * k_eff) == 0;
+  printf("decode_step.c: launches %llu, worst relative L2 %.2e, set mismatches %d, "
+         "single-launch step: %llu launch, bit-identical %d\n",
+         (unsigned long long)hylra_launch_count(), worst, bad_sets, single_launches, single_same);
+  free(hout1);
+  free(hidx1);
+  if (!single_same || single_launches != 1) return 5;
   cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(didx); cudaFree(dws);
   cudaStreamDestroy(st);
   return (worst < 2e-2 && bad_sets == 0) ? 0 : 1;

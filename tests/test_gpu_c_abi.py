@@ -26,3 +26,4 @@ def test_c_host_decode_step(tmp_path):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "set mismatches 0" in r.stdout
+    assert "single-launch step: 1 launch, bit-identical 1" in r.stdout
