@@ -359,9 +359,15 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
 
     dev = torch.device("cuda", torch.cuda.current_device())
     global_batch = batch * world
-    plan = plan_shards(cfg.kv_heads, cfg.q_heads, global_batch, world, mode="kvhead")[rank]
-    local = cfg.with_(batch=global_batch, kv_heads=cfg.kv_heads // world,
-                      q_heads=cfg.q_heads // world, seed=cfg.seed + rank)
+    # Llama shapes (8 KV heads) shard by KV head; Qwen's 4 KV heads shard by batch (BASELINE
+    # configs 3 and 4). Weak scaling either way: per-GPU work stays that of `batch` at N=1.
+    mode = "kvhead" if cfg.kv_heads >= 8 and cfg.kv_heads % world == 0 else "batch"
+    plan = plan_shards(cfg.kv_heads, cfg.q_heads, global_batch, world, mode=mode)[rank]
+    if mode == "kvhead":
+        local = cfg.with_(batch=global_batch, kv_heads=cfg.kv_heads // world,
+                          q_heads=cfg.q_heads // world, seed=cfg.seed + rank)
+    else:
+        local = cfg.with_(batch=batch, seed=cfg.seed + rank)
     cap = cfg.context  # the e2e step writes the new token at row context-1
     q, k, v = generate_torch(local, dev, capacity=cap)
     L, B, Hq, d = q.shape
@@ -592,7 +598,7 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                                 "per launch)",
                       "bytes_per_launch": full_bytes, "launch_ms": t_full,
                       "traffic": ncu.get("full_traffic_bytes_per_launch")}),
-        "schedule": kind_used,
+        "schedule": kind_used, "parallelism": f"{mode}-shard{world}",
         "gpu_launches": dec.kernels_per_step * a.steps,
         "schedules": schedules, "check": check,
         "e2e": e2e_line, "clocks": clk,
@@ -641,13 +647,15 @@ def run_ours(a):
                    "sample": f"failed: {exc}"}
 
     extra = {}
-    if not a.no_extra and world == 1:
+    # configs 3 (128K, KV-head shards) and 4 (Qwen, batch shards) at every N; the block,
+    # offload and small-batch lines at N = 1 only
+    if not a.no_extra:
         c3 = CONFIGS["cfg3"]
         try:
             r3 = measure_config(a, c3, c3.batch, rank, world, torch, dist, e2e=False)
             extra["cfg3_128k_b4"] = {k: r3[k] for k in ("value", "ms_per_step", "step_gbs",
                                                         "kernels", "roofline", "schedule",
-                                                        "schedules")}
+                                                        "schedules", "parallelism")}
         except Exception as exc:  # noqa: BLE001
             extra["cfg3_128k_b4"] = {"error": str(exc)}
         c4 = CONFIGS["cfg4"]
@@ -655,9 +663,10 @@ def run_ours(a):
             r4 = measure_config(a, c4, c4.batch, rank, world, torch, dist, e2e=False)
             extra["cfg4_qwen_64k_b16"] = {k: r4[k] for k in ("value", "ms_per_step", "step_gbs",
                                                              "kernels", "roofline", "schedule",
-                                                        "schedules")}
+                                                             "schedules", "parallelism")}
         except Exception as exc:  # noqa: BLE001
             extra["cfg4_qwen_64k_b16"] = {"error": str(exc)}
+    if not a.no_extra and world == 1:
         # block mode (paper §3.5): 16 blocks of 128 tokens = the same 2048-token coverage
         try:
             extra["cfg2_blocks_b8"] = _block_mode_line(a, cfg, torch)
