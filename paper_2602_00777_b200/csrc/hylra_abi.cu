@@ -78,9 +78,9 @@ int check_geometry(const hylra_geometry* g) {
 //  * REUSE, 1-4 waves of pairs: unsplit unless that leaves a nearly empty last wave
 //    (B=4 24 layers: 145 us unsplit vs 155 at 4; B=8 5 layers, 1.08 waves: 83 us
 //    unsplit -> 76 at 4 splits);
-//  * REUSE, >= 4 waves of pairs: ~8 waves of >= 8-tile splits (B=8 24 layers: 283 vs
-//    295 us unsplit — the tail of a many-wave grid is short); "pairs" above count
-//    32-tile units of a pair (longer selections start out split);
+//  * REUSE, >= 4 waves of pairs: unsplit 32-tile units (B=8 24 layers: 259 vs 265-270 us
+//    at 2 splits); "pairs" above count 32-tile units of a pair (longer selections start
+//    out split);
 //  * FULL: ~4 waves of >= 32-tile splits, or up to one wave of shorter splits when
 //    rows are few (B=1: 186.5 -> 168.8 us).
 // HYLRA_{FULL,REUSE}_{WAVES,MIN_TILES} replace a rule by "waves x S CTAs, >= min tiles
@@ -121,8 +121,10 @@ int choose_splits(int pairs, int tiles, bool gather) {
     const int s0 = std::max(1, (tiles + 31) / 32);
     const long units = (long)pairs * s0;
     if (units >= 4l * kSlots) {
-      // >= 8-tile splits: N=8K k=512 B=8 (8 tiles/pair) took 117 us at 4-tile splits, 87 unsplit
-      s = std::max(s0, splits_by_waves(pairs, tiles, 8, 8));
+      // many waves of 32-tile units: unsplit. cfg2 B=8 (5.2 waves): REUSE 259 vs 265-270 us
+      // at 2 splits, single-launch step 1453 vs 1474 us (once the producer warps staged the
+      // indices together, the per-CTA start cost no longer favoured shorter units)
+      s = s0;
     } else if (units <= kSlots) {
       s = std::max(s0, std::min(kSlots / pairs, tiles / 8));
     } else {
