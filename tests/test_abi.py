@@ -108,6 +108,26 @@ def test_step_ex_and_append_validate_on_the_host():
         _abi.check(lib.hylra_append_kv(g, None, 1, 1, 1, 5, 0, None, None))
 
 
+def test_step_append_options_validate_on_the_host():
+    """hylra_step_options append_* (ABI 5): both row buffers or neither, and a position
+    inside the attended rows; rejected before anything is launched."""
+    lib = _abi.lib()
+    g = _geom()
+    acts = _abi.uint8_array([1, 0, 1, 0])
+    need = lib.hylra_decode_step_workspace_bytes(g, acts, 2048, 128, 1, 0, 0)
+    opt = _abi.StepOptions()
+    opt.fuse_select = 2
+    opt.append_k_rows = 1
+    with pytest.raises(ConfigurationError, match="both"):
+        _abi.check(lib.hylra_decode_step_ex(g, 1, 1, 1, 2048, acts, 128, 1, 1, 0, 0, 1, 1, 128,
+                                            1, need, None, ctypes.byref(opt)))
+    opt.append_v_rows = 1
+    opt.append_pos = 2048
+    with pytest.raises(InvalidInputError, match="append_pos"):
+        _abi.check(lib.hylra_decode_step_ex(g, 1, 1, 1, 2048, acts, 128, 1, 1, 0, 0, 1, 1, 128,
+                                            1, need, None, ctypes.byref(opt)))
+
+
 def test_layer_runs():
     from paper_2602_00777_b200.engine import _runs
     assert _runs([]) == []
