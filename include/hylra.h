@@ -287,6 +287,18 @@ int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void*
                              float* out, int32_t* blocks, int bk_stride, void* ws,
                              size_t ws_bytes, void* stream);
 
+/* hylra_decode_step_blocks with options (ABI 5): opt->fuse_select = 2 runs the block step as
+ * ONE kernel. The final CTA of every FULL (layer, b, kv-head) pair pools that pair's scores
+ * into blocks, selects them (block_budget, float64 refinement as above) and writes the
+ * token coverage; the REUSE items gather it once their row's ready flag is set. Same
+ * results as the multi-launch block step (tensor-core path, sel_group 1; otherwise the
+ * multi-launch step runs). Other option fields are ignored. Workspace: as above. */
+int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const void* k,
+                                const void* v, int n_valid, const uint8_t* actions,
+                                int block_budget, int block_size, int sel_group, int refine,
+                                float* out, int32_t* blocks, int bk_stride, void* ws,
+                                size_t ws_bytes, void* stream, const hylra_step_options* opt);
+
 /*
  * Pairwise selection overlaps: counts[t][r][j][i] = |S(t,i,r) & S(t,j,r)| where
  * S(t,l,r) = idx[t][l][r][0..k) (ascending, distinct, each < n_tokens).

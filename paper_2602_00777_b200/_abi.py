@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "hylra_block_select",
     "hylra_decode_step_blocks_workspace_bytes",
     "hylra_decode_step_blocks",
+    "hylra_decode_step_blocks_ex",
     "hylra_read_flags",
     "hylra_clear_flags",
 )
@@ -136,6 +137,10 @@ def lib() -> ctypes.CDLL:
         l.hylra_decode_step_blocks.restype = i32
         l.hylra_decode_step_blocks.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32, vp,
                                                vp, i32, vp, sz, vp]
+        l.hylra_decode_step_blocks_ex.restype = i32
+        l.hylra_decode_step_blocks_ex.argtypes = [gp, vp, vp, vp, i32, vp, i32, i32, i32, i32,
+                                                  vp, vp, i32, vp, sz, vp,
+                                                  ctypes.POINTER(StepOptions)]
         l.hylra_decode_step_workspace_bytes.restype = sz
         l.hylra_decode_step_workspace_bytes.argtypes = [gp, vp, i32, i32, i32, i32, i32]
         l.hylra_decode_step.restype = i32

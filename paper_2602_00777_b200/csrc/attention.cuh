@@ -427,6 +427,49 @@ __device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
 }
 
+// Block mode, fused (single-launch step, sel_group 1): the final CTA of a FULL pair pools its
+// token score row into the block row the select reads (block max, as block_pool_kernel;
+// one thread per block, 16-byte loads) ...
+__device__ __forceinline__ void fused_block_pool(const SelectParams& sp, int Hkv, int kh, int b,
+                                                 int slot) {
+  const int tid = threadIdx.x, bs = sp.block_size, n = sp.n_tokens, nb = sp.n_valid;
+  const float* trow = sp.tok_scores + ((int64_t)(slot * sp.B + b) * Hkv + kh) * sp.tok_row_stride;
+  float* brow = const_cast<float*>(sp.scores) +
+                ((int64_t)(slot * sp.B + b) * sp.n_groups + kh) * sp.row_stride;
+  for (int blk = tid; blk < nb; blk += kConsumerWarps * 32) {
+    const int t0 = blk * bs, t1 = min(n, t0 + bs);
+    float m = -INFINITY;
+    if (bs % 4 == 0 && t1 - t0 == bs) {
+      const float4* r4 = reinterpret_cast<const float4*>(trow + t0);
+#pragma unroll 8
+      for (int j = 0; j < bs / 4; ++j) {
+        const float4 x = __ldcg(r4 + j);
+        m = fmaxf(m, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+      }
+    } else {
+      for (int t = t0; t < t1; ++t) m = fmaxf(m, __ldcg(trow + t));
+    }
+    brow[blk] = m;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // the block row is written
+}
+
+// ... and after the select writes the selected blocks' token coverage for the REUSE items
+// (block_expand_kernel's layout: ascending tokens, -1 past the cache, count per row).
+__device__ __forceinline__ void fused_block_expand(const SelectParams& sp, int kh, int b,
+                                                   int slot) {
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // the selected blocks are written
+  const int tid = threadIdx.x, bs = sp.block_size, n = sp.n_tokens, bb = sp.k_eff;
+  const int64_t row = (int64_t)(sp.out_slot[slot] * sp.B + b) * sp.n_groups + kh;
+  const int32_t* br = sp.idx + row * sp.k_stride;
+  int32_t* tr = sp.cov_tokens + row * sp.cov_stride;
+  for (int e = tid; e < bb * bs; e += kConsumerWarps * 32) {
+    const int tok = br[e / bs] * bs + e % bs;
+    tr[e] = tok < n ? tok : -1;
+  }
+  if (tid == 0) sp.cov_counts[row] = (bb - 1) * bs + min(bs, n - br[bb - 1] * bs);
+}
+
 // One work item of the tensor-core kernels: the rows [split range] of one (layer slot, b,
 // kv-head) pair. `smem` is the 1024-B aligned dynamic shared memory. REUSE items with
 // `ready_wait` first wait for their selection row's ready flag (single-launch step); FULL
@@ -449,12 +492,6 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
   const int t_begin = split * p.tiles_per_split;
   const int t_end = min(n_tiles, t_begin + p.tiles_per_split);
   const int n_my = t_end - t_begin;
-  // rows of this pair: uniform, or the selection row's own length (block coverage)
-  const int n_rows = ((GATHER || p.blk != nullptr) && p.counts != nullptr)
-                         ? min(p.n_rows, __ldg(p.counts + (int64_t)(p.src_slot[slot] * p.B + b) *
-                                                              p.n_groups + kh / p.sel_group))
-                         : p.n_rows;
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar + s, GATHER ? 32 * kGatherProducers : 1);
@@ -462,8 +499,30 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
     }
     mbar_fence_init();
   }
+  pdl_wait();  // before any global read: the previous launch may still be writing
+  if (ready_wait != nullptr && threadIdx.x == 0) {
+    // single-launch step: this item's selection row (and its coverage count) is written by
+    // a FULL item of the same grid. Bounded: a flag that never comes (it cannot, short of a
+    // corrupted workspace) turns into HYLRA_FLAG_INTERNAL after ~2 s instead of a hung GPU.
+    for (long long spins = 0; ld_acquire_gpu(ready_wait) == 0; ++spins) {
+      if (spins > (1ll << 25)) {
+        atomicOr(p.flags, 8);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
   __syncthreads();
-  pdl_wait();
+  if (ready_wait != nullptr) (void)ld_acquire_gpu(ready_wait);  // every thread: acquire
+#ifdef HYLRA_TRACE
+  if (ready_wait != nullptr && threadIdx.x == 0) hylra_trace_mark(2);
+#endif
+  // rows of this pair: uniform, or the selection row's own length (block coverage); read
+  // coherently (written earlier in the step)
+  const int n_rows = ((GATHER || p.blk != nullptr) && p.counts != nullptr)
+                         ? min(p.n_rows, __ldcg(p.counts + (int64_t)(p.src_slot[slot] * p.B + b) *
+                                                               p.n_groups + kh / p.sel_group))
+                         : p.n_rows;
 
   if (warp >= kConsumerWarps) {
     // ------------------------------------------------------------- producer warp
@@ -526,25 +585,6 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
       const int pos_begin = t_begin * kTileRows;
       const int n_pos = min(n_rows, t_end * kTileRows) - pos_begin;
       const bool staged = n_pos <= kIdxStage;
-      if (ready_wait != nullptr) {
-        // single-launch step: the selection row is written by a FULL item of the same grid
-        // bounded: a flag that never comes (it cannot, short of a corrupted workspace) turns
-        // into HYLRA_FLAG_INTERNAL after ~2 s instead of a hung GPU
-        if (lane == 0) {
-          for (long long spins = 0; ld_acquire_gpu(ready_wait) == 0; ++spins) {
-            if (spins > (1ll << 25)) {
-              atomicOr(p.flags, 8);
-              break;
-            }
-            __nanosleep(64);
-          }
-        }
-        __syncwarp();
-        (void)ld_acquire_gpu(ready_wait);
-#ifdef HYLRA_TRACE
-        if (lane == 0 && warp == kConsumerWarps) hylra_trace_mark(2);
-#endif
-      }
       if (staged) {
         stage_indices(ib + pos_begin, n_pos, p.n_valid, sidx, p.flags, lane,
                       warp - kConsumerWarps, kGatherProducers);
@@ -716,7 +756,9 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
 #ifdef HYLRA_TRACE
       if (threadIdx.x == 0) hylra_trace_mark(1);
 #endif
+      if (sp.block_size > 1) fused_block_pool(sp, p.Hkv, kh, b, slot);
       select_row<kConsumerWarps * 32, true>(sp, kh, b, slot, smem, sel_red, false);
+      if (sp.block_size > 1) fused_block_expand(sp, kh, b, slot);
 #ifdef HYLRA_TRACE
       if (threadIdx.x == 0) hylra_trace_mark(3);
 #endif

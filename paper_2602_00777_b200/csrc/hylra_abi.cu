@@ -703,6 +703,22 @@ struct SplitKv {
   const void *kf, *vf, *kr, *vr;
 };
 
+// The single-launch kernel for this geometry (tensor-core path).
+int dispatch_step(const hylra_geometry* g, cudaStream_t st, const CUtensorMap& tk,
+                  const CUtensorMap& tv, const AttnParams& pf, const AttnParams& pr,
+                  const SelectParams& sp, const StepSync& ss) {
+  const int G = g->q_heads / g->kv_heads;
+  cudaError_t ce;
+  if (g->head_dim == 128)
+    ce = G > 8 ? launch_step_mma<128, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
+               : launch_step_mma<128, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
+  else
+    ce = G > 8 ? launch_step_mma<64, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
+               : launch_step_mma<64, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_check(ce, "single-launch step");
+}
+
 // The fused select of the FULL kernel uses the drained pipeline buffers as its shared
 // memory (128 threads).
 bool fused_select_fits(const hylra_geometry* g, int n_valid) {
@@ -854,16 +870,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     if (o.reuse_wait)
       if (int e = cuda_check(cudaStreamWaitEvent(st, o.reuse_wait, 0), "stream wait event"))
         return e;
-    const int G = g->q_heads / g->kv_heads;
-    cudaError_t ce;
-    if (g->head_dim == 128)
-      ce = G > 8 ? launch_step_mma<128, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
-                 : launch_step_mma<128, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
-    else
-      ce = G > 8 ? launch_step_mma<64, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
-                 : launch_step_mma<64, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return cuda_check(ce, "single-launch step");
+    return dispatch_step(g, st, tk, tv, pf, pr, sp, ss);
   }
   if (o.side && !(o.fork && o.join && (o.fuse || (o.select && o.full))))
     return fail(HYLRA_ERR_CONFIGURATION, "a side stream needs its four events");
@@ -1234,11 +1241,11 @@ size_t hylra_decode_step_blocks_workspace_bytes(const hylra_geometry* g, const u
   return s.total;
 }
 
-int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void* k,
-                             const void* v, int n_valid, const uint8_t* actions,
-                             int block_budget, int block_size, int sel_group, int refine,
-                             float* out, int32_t* blocks, int bk_stride, void* ws,
-                             size_t ws_bytes, void* stream) {
+int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const void* k,
+                                const void* v, int n_valid, const uint8_t* actions,
+                                int block_budget, int block_size, int sel_group, int refine,
+                                float* out, int32_t* blocks, int bk_stride, void* ws,
+                                size_t ws_bytes, void* stream, const hylra_step_options* opt) {
   if (block_size < 1) return fail(HYLRA_ERR_INVALID_INPUT, "block_size must be >= 1");
   StepLayout s;
   if (int e = step_layout(g, actions, n_valid, block_budget, sel_group, &s, block_size)) return e;
@@ -1253,6 +1260,64 @@ int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void*
   int32_t* toks = reinterpret_cast<int32_t*>(w + s.off_tokens);
   int32_t* cnts = reinterpret_cast<int32_t*>(w + s.off_counts);
   const int nf = (int)s.full_ids.size();
+  const int nr = (int)s.reuse_ids.size();
+  const int nb = (n_valid + block_size - 1) / block_size;
+  // single-launch block step (fuse_select = 2): the final CTA of every FULL pair pools its
+  // row into blocks, selects them and writes the token coverage the REUSE items gather
+  if (opt && opt->fuse_select == 2 && sel_group == 1 && use_mma_path(g) &&
+      fused_select_fits(g, nb)) {
+    std::vector<int32_t> ab_ids, ab_slot, b_ids, b_slot;
+    for (int i = 0; i < nf; ++i) {
+      const int l = s.full_ids[i];
+      const bool feeds = l + 1 < g->num_layers && actions[l + 1] == 0;
+      (feeds ? ab_ids : b_ids).push_back(l);
+      (feeds ? ab_slot : b_slot).push_back(i);
+    }
+    ab_ids.insert(ab_ids.end(), b_ids.begin(), b_ids.end());
+    ab_slot.insert(ab_slot.end(), b_slot.begin(), b_slot.end());
+    BlockRows br;
+    br.block_size = block_size;
+    br.n_tokens = n_valid;
+    br.row_stride = nb_stride_of(nb);
+    br.tok_scores = scores;
+    SelectParams sp{};
+    if (int e = build_select_params(&sp, g, reinterpret_cast<float*>(w + s.off_bscores), nf, nb,
+                                    block_budget, 1, refine ? q : nullptr, refine ? k : nullptr,
+                                    ab_ids.data(), blocks, bk_stride, nullptr, flags, br, nullptr,
+                                    ab_slot.data()))
+      return e;
+    sp.cov_tokens = toks;
+    sp.cov_counts = cnts;
+    sp.cov_stride = s.tok_stride;
+    AttnParams pf{}, pr{};
+    AttnLayout lf{}, lr{};
+    if (int e = make_attn_params(&pf, &lf, g, false, q, k, v, n_valid, n_valid, nf, ab_ids.data(),
+                                 nullptr, nullptr, nullptr, 0, 1, out, scores, w + s.off_attn,
+                                 s.attn_bytes, flags, nullptr, 0))
+      return e;
+    pf.fuse_select = nf;
+    const long items_f = (long)lf.splits * g->kv_heads * g->batch * nf;
+    long items_r = 0;
+    if (nr > 0) {
+      if (int e = make_attn_params(&pr, &lr, g, true, q, k, v, n_valid, s.k_eff, nr,
+                                   s.reuse_ids.data(), s.reuse_src.data(), toks, cnts,
+                                   s.tok_stride, 1, out, nullptr, w + s.off_attn_r,
+                                   s.attn_bytes_r, flags, nullptr, 0))
+        return e;
+      items_r = (long)lr.splits * g->kv_heads * g->batch * nr;
+    }
+    if (items_f + items_r > INT32_MAX) return fail(HYLRA_ERR_CONFIGURATION, "grid too large");
+    CUtensorMap tk{}, tv{};
+    if (int e = encode_kv_map(&tk, g, k, g->num_layers)) return e;
+    if (int e = encode_kv_map(&tv, g, v, g->num_layers)) return e;
+    StepSync ss{};
+    ss.ctr = reinterpret_cast<int*>(w + s.off_sync);
+    ss.ready = ss.ctr + 64;
+    ss.n_ready = s.n_ready;
+    ss.n_full_items = (int)items_f;
+    ss.n_items = (int)(items_f + items_r);
+    return dispatch_step(g, st, tk, tv, pf, pr, sp, ss);
+  }
   if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, nf, s.full_ids.data(), nullptr,
                                nullptr, nullptr, 0, 1, out, scores, w + s.off_attn, s.attn_bytes,
                                flags, st))
@@ -1275,6 +1340,16 @@ int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void*
       return e;
   }
   return HYLRA_OK;
+}
+
+int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void* k,
+                             const void* v, int n_valid, const uint8_t* actions,
+                             int block_budget, int block_size, int sel_group, int refine,
+                             float* out, int32_t* blocks, int bk_stride, void* ws,
+                             size_t ws_bytes, void* stream) {
+  return hylra_decode_step_blocks_ex(g, q, k, v, n_valid, actions, block_budget, block_size,
+                                     sel_group, refine, out, blocks, bk_stride, ws, ws_bytes,
+                                     stream, nullptr);
 }
 
 int hylra_overlap_counts(const int32_t* idx, int steps, int layers, int rows, int k,

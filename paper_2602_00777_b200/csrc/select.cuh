@@ -62,6 +62,12 @@ struct SelectParams {
   int layers[kMaxSlots];     // q layer of each slot
   int kv_layers[kMaxSlots];  // K layer of each slot (refinement)
   int out_slot[kMaxSlots];   // idx / info slot each score slot's selection is written to
+  // block mode fused into the FULL kernel (single-launch step): the final CTA of a pair pools
+  // its token scores into the block row (`scores`), selects, then writes the token coverage
+  // [row][cov_stride] and its length cov_counts[row] for the REUSE items
+  int32_t* cov_tokens;
+  int32_t* cov_counts;
+  int cov_stride;
 };
 
 // Dynamic shared memory: the bitmap sized for the row, then fixed arrays.

@@ -140,9 +140,11 @@ class HybridDecoder:
             pairs = len(self.full_layers) * B * Hkv
             single_launch = (bool(fuse_select) and not dual_stream and len(feeds) > 0
                              and pairs >= 192)
-        self.single = (bool(single_launch) and block_size == 1
-                       and not (include_sinks or include_recent) and sel_group == 1
-                       and k_cache.dtype == torch.bfloat16 and d in (64, 128))
+        # token or block mode (hylra_decode_step_blocks_ex: the FULL pairs' final CTAs pool,
+        # select blocks and write the coverage)
+        self._single_ok = (not (include_sinks or include_recent) and sel_group == 1
+                           and k_cache.dtype == torch.bfloat16 and d in (64, 128))
+        self.single = bool(single_launch) and self._single_ok
         if self.single:
             self.dual = self.fused = False
         self._feeds_all = len(feeds) == len(self.full_layers)
@@ -174,13 +176,15 @@ class HybridDecoder:
                 "dual" if self.dual else "fused3")
 
     def set_schedule(self, name: str) -> None:
-        """Switch between the step schedules ("single", "fusedsel", "fused3"); every one
-        gives bit-identical outputs and selections, only the launch structure differs."""
+        """Switch between the step schedules ("single", "fusedsel", "fused3"; block mode:
+        "single", "fused3"); every one gives bit-identical outputs and selections, only the
+        launch structure differs."""
         if name not in ("single", "fusedsel", "fused3"):
             raise ConfigurationError(f"unknown schedule {name!r}")
-        if name != "fused3" and not self._fused_ok:
-            raise ConfigurationError(f"schedule {name!r} needs token mode, sel_group 1, "
-                                     "bf16 and head_dim 64/128 with a FULL layer feeding REUSE")
+        if (name == "fusedsel" and not self._fused_ok) or (name == "single" and not self._single_ok):
+            raise ConfigurationError(f"schedule {name!r} needs the tensor-core path (bf16, "
+                                     "head_dim 64/128), sel_group 1, no sinks / recent"
+                                     + (" and token mode" if name == "fusedsel" else ""))
         self.single, self.fused, self.dual = name == "single", name == "fusedsel", False
         self._count_kernels()
 
@@ -188,7 +192,8 @@ class HybridDecoder:
         """Time the schedules this decoder can run on these inputs (CUDA-graph replays, CUDA
         events on the current stream) and keep the fastest. Returns {schedule: ms}. The
         measured steps overwrite `out` / the selections (the next step rewrites them)."""
-        names = ["single", "fusedsel", "fused3"] if self._fused_ok else ["fused3"]
+        names = ([n for n, ok in (("single", self._single_ok), ("fusedsel", self._fused_ok))
+                  if ok] + ["fused3"])
         times = {}
         cur = torch.cuda.current_stream(self.k.device)
         for name in names:
@@ -299,11 +304,13 @@ class HybridDecoder:
                 g, self._acts, n_valid, self.budget, self.block_size, self.sel_group))
             if self.ws.numel() < need:
                 self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
-            _abi.check(lib.hylra_decode_step_blocks(
+            opt = _abi.StepOptions()
+            opt.fuse_select = 2 if self.single else 0
+            _abi.check(lib.hylra_decode_step_blocks_ex(
                 g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
                 self.budget, self.block_size, self.sel_group, int(self.refine),
                 self.out.data_ptr(), self.idx.data_ptr(), self.k_stride, self.ws.data_ptr(),
-                self.ws.numel(), st))
+                self.ws.numel(), st, ctypes.byref(opt)))
             bb = min(self.budget, -(-n_valid // self.block_size))
             return StepResult(self.out, self.idx[..., :bb], self.slot_of_layer,
                               self.full_layers)

@@ -166,3 +166,41 @@ def test_block_reuse_tiles_equal_row_gather(bs, bb, n_valid, monkeypatch):
     dec.check_flags()
     assert torch.equal(res.selections, S)
     assert torch.equal(res.outputs, R)
+
+
+@pytest.mark.parametrize("bs,bb,n_valid,B", [(128, 8, 4100, 2), (64, 12, 4096, 1), (16, 40, 3001, 2),
+                                             (12, 30, 2000, 3)])
+def test_block_single_launch_equals_multi_launch(bs, bb, n_valid, B):
+    """hylra_decode_step_blocks_ex fuse_select=2: the final CTA of each FULL pair pools the
+    token scores into blocks, selects them and writes the coverage, REUSE items gather it
+    after their row's ready flag: bit-identical to the multi-launch block step (pool kernel,
+    block SELECT, expansion, REUSE), over repeated steps and graph replays. Ragged last
+    blocks and block sizes that are not multiples of 4 included."""
+    L, Hq, Hkv, d, cap = 6, 16, 4, 128, 4200
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=29, planted=48)
+    actions = ("full", "reuse", "full", "reuse", "reuse", "full")
+    ref = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs, single_launch=False)
+    r = ref.step(q, n_valid)
+    torch.cuda.synchronize()
+    R, S = r.outputs.clone(), r.selections.clone()
+    dec = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs, single_launch=True)
+    assert dec.single and dec.kernels_per_step == 1
+    for _ in range(2):
+        res = dec.step(q, n_valid)
+        torch.cuda.synchronize()
+        dec.check_flags()
+        assert torch.equal(res.selections, S)
+        assert torch.equal(res.outputs, R)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dec.step(q, n_valid)
+    torch.cuda.current_stream().wait_stream(s)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        dec.step(q, n_valid)
+    for _ in range(3):
+        dec.out.zero_()
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(dec.out, R)
