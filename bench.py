@@ -236,10 +236,11 @@ def _block_mode_line(a, cfg, torch):
     L, B = q.shape[0], q.shape[1]
     nf = len(cfg.full_layers)
     by = (nf * cfg.context + (L - nf) * bb * bs) * B * k.shape[2] * 2 * cfg.head_dim * 2
+    sched, kps = dec.schedule, dec.kernels_per_step
     del gr, dec, q, k, v
     torch.cuda.empty_cache()
     return {"value": B / (ms * 1e-3), "ms_per_step": ms, "block_size": bs, "block_budget": bb,
-            "step_gbs": by / (ms * 1e-3) / 1e9, "kernels_per_step": 5}
+            "step_gbs": by / (ms * 1e-3) / 1e9, "schedule": sched, "kernels_per_step": kps}
 
 
 def _offload_line(a, cfg, torch, batch=1):
