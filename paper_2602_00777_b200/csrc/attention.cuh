@@ -470,6 +470,42 @@ __device__ __forceinline__ void fused_block_expand(const SelectParams& sp, int k
   if (tid == 0) sp.cov_counts[row] = (bb - 1) * bs + min(bs, n - br[bb - 1] * bs);
 }
 
+// Token mode with sinks / recent, fused: after the select the final CTA writes the
+// augmented row sorted(sel | [0, sinks) | [n - recent, n)) and its length (augment_kernel,
+// engine.py:122-126 _augment_selection) for the REUSE items.
+__device__ __forceinline__ void fused_augment(const SelectParams& sp, int kh, int b, int slot) {
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // the selection is written
+  constexpr int NT = kConsumerWarps * 32;
+  const int tid = threadIdx.x, n = sp.n_valid, k = sp.k_eff;
+  const int64_t row = (int64_t)(sp.out_slot[slot] * sp.B + b) * sp.n_groups + kh;
+  const int32_t* src = sp.idx + row * sp.k_stride;
+  int32_t* dst = sp.cov_tokens + row * sp.cov_stride;
+  const int s = min(sp.sinks, n), u0 = max(n - sp.recent, 0);
+  if (u0 <= s) {  // the two ranges already cover every token
+    for (int i = tid; i < n; i += NT) dst[i] = i;
+    if (tid == 0) sp.cov_counts[row] = n;
+    return;
+  }
+  // selected tokens strictly between the ranges: [lower_bound(s), lower_bound(u0))
+  __shared__ int s_lb[2];
+  if (tid < 2) {
+    const int key = tid == 0 ? s : u0;
+    int a = 0, z = k;
+    while (a < z) {
+      const int m = (a + z) >> 1;
+      if (src[m] < key) a = m + 1;
+      else z = m;
+    }
+    s_lb[tid] = a;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int mid0 = s_lb[0], mid = s_lb[1] - s_lb[0];
+  for (int i = tid; i < s; i += NT) dst[i] = i;
+  for (int i = tid; i < mid; i += NT) dst[s + i] = src[mid0 + i];
+  for (int i = tid; i < n - u0; i += NT) dst[s + mid + i] = u0 + i;
+  if (tid == 0) sp.cov_counts[row] = s + mid + (n - u0);
+}
+
 // One work item of the tensor-core kernels: the rows [split range] of one (layer slot, b,
 // kv-head) pair. `smem` is the 1024-B aligned dynamic shared memory. REUSE items with
 // `ready_wait` first wait for their selection row's ready flag (single-launch step); FULL
@@ -759,6 +795,7 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
       if (sp.block_size > 1) fused_block_pool(sp, p.Hkv, kh, b, slot);
       select_row<kConsumerWarps * 32, true>(sp, kh, b, slot, smem, sel_red, false);
       if (sp.block_size > 1) fused_block_expand(sp, kh, b, slot);
+      else if (sp.cov_tokens != nullptr) fused_augment(sp, kh, b, slot);
 #ifdef HYLRA_TRACE
       if (threadIdx.x == 0) hylra_trace_mark(3);
 #endif

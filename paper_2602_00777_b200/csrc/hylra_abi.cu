@@ -788,7 +788,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   const bool fused_sel = o.fuse && o.side && !a_ids.empty() && !s.aug_stride && sel_group == 1 &&
                          use_mma_path(g) && fused_select_fits(g, n_valid);
   // single-launch step: every select fused into the FULL items, REUSE items in the same grid
-  const bool unified = o.unified && !s.aug_stride && sel_group == 1 && use_mma_path(g) &&
+  const bool unified = o.unified && sel_group == 1 && use_mma_path(g) &&
                        fused_select_fits(g, n_valid) && !o.layer_events;
   // the step's new K/V rows: written inside the single-launch kernel, else by the append
   // kernel ahead of the step
@@ -816,6 +816,20 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                     idx, k_stride, nullptr, flags, BlockRows(),
                                     split ? ab_kv.data() : nullptr, ab_slot.data()))
       return e;
+    // sinks / recent: the final CTA of each pair also writes the augmented row
+    const int32_t* ridx = idx;
+    const int32_t* rcnt = nullptr;
+    int rstride = k_stride, rk = s.k_eff;
+    if (s.aug_stride) {
+      sp.cov_tokens = reinterpret_cast<int32_t*>(w + s.off_aug);
+      sp.cov_counts = reinterpret_cast<int32_t*>(w + s.off_aug_counts);
+      sp.cov_stride = s.aug_stride;
+      sp.sinks = sinks;
+      sp.recent = recent;
+      ridx = sp.cov_tokens;
+      rcnt = sp.cov_counts;
+      rstride = rk = s.aug_stride;
+    }
     AttnParams pf{}, pr{};
     AttnLayout lf{}, lr{};
     if (int e = make_attn_params(&pf, &lf, g, false, q, kf, vf, n_valid, n_valid, nf,
@@ -829,8 +843,8 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     for (int i = 0; i < nr; ++i) rkv[i] = i;
     if (nr > 0) {
       if (int e = make_attn_params(&pr, &lr, g, true, q, split ? split->kr : k,
-                                   split ? split->vr : v, n_valid, s.k_eff, nr,
-                                   s.reuse_ids.data(), s.reuse_src.data(), idx, nullptr, k_stride,
+                                   split ? split->vr : v, n_valid, rk, nr,
+                                   s.reuse_ids.data(), s.reuse_src.data(), ridx, rcnt, rstride,
                                    sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r,
                                    flags, split ? rkv.data() : nullptr, nr))
         return e;

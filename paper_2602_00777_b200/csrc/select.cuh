@@ -65,9 +65,12 @@ struct SelectParams {
   // block mode fused into the FULL kernel (single-launch step): the final CTA of a pair pools
   // its token scores into the block row (`scores`), selects, then writes the token coverage
   // [row][cov_stride] and its length cov_counts[row] for the REUSE items
+  // Token mode with sinks / recent (cov_tokens set, block_size 1): the augmented selection
+  // sorted(sel | [0, sinks) | [n - recent, n)) and its length, as augment_kernel
   int32_t* cov_tokens;
   int32_t* cov_counts;
   int cov_stride;
+  int sinks, recent;
 };
 
 // Dynamic shared memory: the bitmap sized for the row, then fixed arrays.

@@ -142,7 +142,8 @@ class HybridDecoder:
                              and pairs >= 192)
         # token or block mode (hylra_decode_step_blocks_ex: the FULL pairs' final CTAs pool,
         # select blocks and write the coverage)
-        self._single_ok = (not (include_sinks or include_recent) and sel_group == 1
+        self._single_ok = (not (block_size > 1 and (include_sinks or include_recent))
+                           and sel_group == 1
                            and k_cache.dtype == torch.bfloat16 and d in (64, 128))
         self.single = bool(single_launch) and self._single_ok
         if self.single:
@@ -183,8 +184,9 @@ class HybridDecoder:
             raise ConfigurationError(f"unknown schedule {name!r}")
         if (name == "fusedsel" and not self._fused_ok) or (name == "single" and not self._single_ok):
             raise ConfigurationError(f"schedule {name!r} needs the tensor-core path (bf16, "
-                                     "head_dim 64/128), sel_group 1, no sinks / recent"
-                                     + (" and token mode" if name == "fusedsel" else ""))
+                                     "head_dim 64/128) and sel_group 1"
+                                     + (", token mode and no sinks / recent"
+                                        if name == "fusedsel" else ""))
         self.single, self.fused, self.dual = name == "single", name == "fusedsel", False
         self._count_kernels()
 

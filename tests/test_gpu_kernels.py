@@ -655,3 +655,28 @@ def test_known_answers_on_gpu(dtype):
         buf[0, 0, 0, :len(row)] = torch.tensor(row)
         got = topk_select(buf.to(DEV), budget, len(row))
         assert got[0, 0, 0].cpu().tolist() == want
+
+
+@pytest.mark.parametrize("sinks,recent,n", [(4, 16, 4096), (0, 64, 3000), (8, 0, 2048),
+                                            (3000, 3000, 2500)])
+def test_single_launch_with_sinks_recent(sinks, recent, n):
+    """Sink / recent augmentation (engine.py:122-126) inside the single-launch step: the
+    final CTA of each FULL pair writes the augmented row after its select; identical to the
+    multi-launch step with the augment kernel (including ranges that cover every token)."""
+    L, B, Hq, Hkv, d, budget = 6, 2, 16, 4, 128, 256
+    actions = ("full", "reuse", "full", "reuse", "reuse", "full")
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, n, "bf16", seed=61, planted=32)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, include_sinks=sinks,
+                        include_recent=recent, fuse_select=False, single_launch=False)
+    r = ref.step(q, n)
+    torch.cuda.synchronize()
+    R, S = r.outputs.clone(), r.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, include_sinks=sinks,
+                        include_recent=recent, single_launch=True)
+    assert dec.single and dec.kernels_per_step == 1
+    for _ in range(2):
+        res = dec.step(q, n)
+        torch.cuda.synchronize()
+        dec.check_flags()
+        assert torch.equal(res.selections, S)
+        assert torch.equal(res.outputs, R)
