@@ -680,3 +680,21 @@ def test_single_launch_with_sinks_recent(sinks, recent, n):
         dec.check_flags()
         assert torch.equal(res.selections, S)
         assert torch.equal(res.outputs, R)
+
+
+def test_single_launch_at_the_longest_row():
+    """The single-launch step at the longest supported row (262144 tokens: the fused select's
+    bitmap, band list and candidates in the FULL kernel's drained ring) is bit-identical to
+    the 3-launch step."""
+    L, B, Hq, Hkv, d, n, budget = 3, 1, 8, 2, 128, 262144, 4096
+    actions = ("full", "reuse", "reuse")
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, n, "bf16", seed=71, planted=256)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, fuse_select=False,
+                        single_launch=False).step(q, n)
+    torch.cuda.synchronize()
+    R, S = ref.outputs.clone(), ref.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, single_launch=True)
+    res = dec.step(q, n)
+    torch.cuda.synchronize()
+    dec.check_flags()
+    assert torch.equal(res.selections, S) and torch.equal(res.outputs, R)
