@@ -205,8 +205,9 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
  *     flag. CTAs claim work by an atomic ticket, so a waiting REUSE CTA only ever waits on
  *     FULL work already running (no deadlock for any dispatch order). Same split-K
  *     partitions as the plain step: outputs and selections are bit-identical to it.
- *     With sinks / recent the final CTA also writes the augmented row. Tensor-core path,
- *     sel_group 1, no layer_events (otherwise the schedules above apply);
+ *     With sinks / recent the final CTA also writes the augmented row; with sel_group > 1
+ *     the last pair of each selection group to finish selects. Tensor-core path, no
+ *     layer_events (otherwise the schedules above apply);
  *     reuse_wait_event is waited on before the launch. The
  *     workspace carries the ticket / ready words and the kernel leaves them zeroed.
  *   reuse_wait_event: the REUSE launches wait on it (e.g. REUSE layers' queries arriving).

@@ -514,7 +514,8 @@ template <int D, bool GATHER, bool GBIG, int STAGES>
 __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUtensorMap& tmv,
                                               const AttnParams& p, const SelectParams& sp,
                                               uint8_t* smem, int split, int kh, int slot, int b,
-                                              const int* ready_wait, int* ready_set) {
+                                              const int* ready_wait, int* ready_set,
+                                              int* group_ctr = nullptr) {
   using SM = MmaSmem<D>;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * SM::kStageBytes);
   uint64_t* empty_bar = full_bar + STAGES;
@@ -787,23 +788,40 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
     // the drained pipeline buffers hold the select's shared memory
     if (final_cta && slot < p.fuse_select) {
       __shared__ Red sel_red;
+      __shared__ int s_group_last;
       asm volatile("bar.sync 1, 128;" ::: "memory");  // merge reads of smem are done
       __threadfence();
-#ifdef HYLRA_TRACE
-      if (threadIdx.x == 0) hylra_trace_mark(1);
-#endif
-      if (sp.block_size > 1) fused_block_pool(sp, p.Hkv, kh, b, slot);
-      select_row<kConsumerWarps * 32, true>(sp, kh, b, slot, smem, sel_red, false);
-      if (sp.block_size > 1) fused_block_expand(sp, kh, b, slot);
-      else if (sp.cov_tokens != nullptr) fused_augment(sp, kh, b, slot);
-#ifdef HYLRA_TRACE
-      if (threadIdx.x == 0) hylra_trace_mark(3);
-#endif
-      if (ready_set != nullptr) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the row's indices are written
+      const int grp = kh / p.sel_group;
+      bool run = true;
+      if (p.sel_group > 1) {
+        // the selection row sums the scores of sel_group KV heads (single-launch step): the
+        // last of those pairs to finish selects; its counter resets itself
         if (threadIdx.x == 0) {
-          __threadfence();
-          st_release_gpu(ready_set + (sp.out_slot[slot] * p.B + b) * p.n_groups + kh, 1);
+          const int row = (sp.out_slot[slot] * p.B + b) * p.n_groups + grp;
+          s_group_last = atomicAdd(group_ctr + row, 1) == p.sel_group - 1;
+          if (s_group_last) group_ctr[row] = 0;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        run = s_group_last != 0;
+        if (run) __threadfence();
+      }
+      if (run) {
+#ifdef HYLRA_TRACE
+        if (threadIdx.x == 0) hylra_trace_mark(1);
+#endif
+        if (sp.block_size > 1) fused_block_pool(sp, p.Hkv, kh, b, slot);
+        select_row<kConsumerWarps * 32, true>(sp, grp, b, slot, smem, sel_red, false);
+        if (sp.block_size > 1) fused_block_expand(sp, kh, b, slot);
+        else if (sp.cov_tokens != nullptr) fused_augment(sp, grp, b, slot);
+#ifdef HYLRA_TRACE
+        if (threadIdx.x == 0) hylra_trace_mark(3);
+#endif
+        if (ready_set != nullptr) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // the row's indices are written
+          if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_gpu(ready_set + (sp.out_slot[slot] * p.B + b) * p.n_groups + grp, 1);
+          }
         }
       }
     }
@@ -846,6 +864,7 @@ struct StepAppend {
 struct StepSync {
   int* ctr;     // [0] ticket, [1] done
   int* ready;   // [n_full][B][n_groups]
+  int* group;   // [n_full][B][n_groups] pairs of a selection group done (sel_group > 1)
   int n_ready;
   int n_full_items, n_items;
   StepAppend app;
@@ -910,7 +929,7 @@ __global__ void __launch_bounds__(attn_threads<true>(), 2)
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     attn_mma_item<D, false, GBIG, STAGES>(tmk, tmv, pf, sp, smem, split, kh, slot, b, nullptr,
-                                          ss.ready);
+                                          ss.ready, ss.group);
   } else {
     t -= ss.n_full_items;
     const int split = t % pr.splits;

@@ -675,7 +675,8 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
         s->attn_bytes_r, attn_layout(g, n, s->aug_stride ? s->aug_stride : s->k_eff, true).total);
   s->off_sync = align_up(s->off_attn_r + s->attn_bytes_r, 256);
   s->n_ready = (int)(nf * g->batch * s->n_groups);
-  s->total = align_up(s->off_sync + 256 + sizeof(int) * (size_t)s->n_ready, 256);
+  // ticket / done, then ready flags and selection-group counters [n_ready] each
+  s->total = align_up(s->off_sync + 256 + 2 * sizeof(int) * (size_t)s->n_ready, 256);
   return HYLRA_OK;
 }
 
@@ -788,8 +789,8 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   const bool fused_sel = o.fuse && o.side && !a_ids.empty() && !s.aug_stride && sel_group == 1 &&
                          use_mma_path(g) && fused_select_fits(g, n_valid);
   // single-launch step: every select fused into the FULL items, REUSE items in the same grid
-  const bool unified = o.unified && sel_group == 1 && use_mma_path(g) &&
-                       fused_select_fits(g, n_valid) && !o.layer_events;
+  const bool unified = o.unified && use_mma_path(g) && fused_select_fits(g, n_valid) &&
+                       !o.layer_events;
   // the step's new K/V rows: written inside the single-launch kernel, else by the append
   // kernel ahead of the step
   const bool appending = o.app_k != nullptr || o.app_v != nullptr;
@@ -832,9 +833,11 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     }
     AttnParams pf{}, pr{};
     AttnLayout lf{}, lr{};
+    // sel_group: the fused select of a pair's final CTA covers its selection group
     if (int e = make_attn_params(&pf, &lf, g, false, q, kf, vf, n_valid, n_valid, nf,
-                                 ab_ids.data(), nullptr, nullptr, nullptr, 0, 1, out, scores, aws,
-                                 s.attn_bytes, flags, split ? ab_kv.data() : nullptr, nf))
+                                 ab_ids.data(), nullptr, nullptr, nullptr, 0, sel_group, out,
+                                 scores, aws, s.attn_bytes, flags,
+                                 split ? ab_kv.data() : nullptr, nf))
       return e;
     pf.fuse_select = nf;
     const long items_f = (long)lf.splits * g->kv_heads * g->batch * nf;
@@ -857,6 +860,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     StepSync ss{};
     ss.ctr = reinterpret_cast<int*>(w + s.off_sync);
     ss.ready = ss.ctr + 64;
+    ss.group = ss.ready + s.n_ready;
     ss.n_ready = s.n_ready;
     ss.n_full_items = (int)items_f;
     ss.n_items = (int)(items_f + items_r);
@@ -1327,6 +1331,7 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
     StepSync ss{};
     ss.ctr = reinterpret_cast<int*>(w + s.off_sync);
     ss.ready = ss.ctr + 64;
+    ss.group = ss.ready + s.n_ready;
     ss.n_ready = s.n_ready;
     ss.n_full_items = (int)items_f;
     ss.n_items = (int)(items_f + items_r);

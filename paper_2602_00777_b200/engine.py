@@ -142,8 +142,8 @@ class HybridDecoder:
                              and pairs >= 192)
         # token or block mode (hylra_decode_step_blocks_ex: the FULL pairs' final CTAs pool,
         # select blocks and write the coverage)
-        self._single_ok = (not (block_size > 1 and (include_sinks or include_recent))
-                           and sel_group == 1
+        self._single_ok = (not (block_size > 1 and (include_sinks or include_recent
+                                                     or sel_group > 1))
                            and k_cache.dtype == torch.bfloat16 and d in (64, 128))
         self.single = bool(single_launch) and self._single_ok
         if self.single:

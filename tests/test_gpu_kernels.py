@@ -451,7 +451,7 @@ def test_single_launch_step_equals_unfused(actions, d, refine, n, B, Hq, Hkv):
         assert torch.equal(dec.idx[..., :budget], ref_idx)
         assert torch.equal(dec.out, ref_out)
     # the synchronisation words are back at zero after every step
-    sync = dec.ws[-(256 + 4 * len(dec.full_layers) * B * Hkv):].view(torch.int32)
+    sync = dec.ws[-(256 + 8 * len(dec.full_layers) * B * Hkv):].view(torch.int32)
     assert int(sync.abs().sum()) == 0
 
 
@@ -698,3 +698,28 @@ def test_single_launch_at_the_longest_row():
     torch.cuda.synchronize()
     dec.check_flags()
     assert torch.equal(res.selections, S) and torch.equal(res.outputs, R)
+
+
+@pytest.mark.parametrize("sel_group,Hkv,Hq,B", [(2, 4, 16, 2), (4, 4, 16, 1), (8, 8, 8, 1)])
+def test_single_launch_with_selection_groups(sel_group, Hkv, Hq, B):
+    """Selection rows that sum several KV heads (sel_group > 1; sel_group = Hkv is the
+    reference's layer-wide set): in the single-launch step the last FULL pair of each group
+    to finish selects (a self-resetting per-group counter); identical to the multi-launch
+    step, over repeated steps."""
+    L, d, n, budget = 5, 128, 3000, 192
+    actions = ("full", "reuse", "full", "reuse", "reuse")
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, n, "bf16", seed=67, planted=32)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, sel_group=sel_group,
+                        fuse_select=False, single_launch=False)
+    r = ref.step(q, n)
+    torch.cuda.synchronize()
+    R, S = r.outputs.clone(), r.selections.clone()
+    dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, sel_group=sel_group,
+                        single_launch=True)
+    assert dec.single and dec.kernels_per_step == 1
+    for _ in range(3):
+        res = dec.step(q, n)
+        torch.cuda.synchronize()
+        dec.check_flags()
+        assert torch.equal(res.selections, S)
+        assert torch.equal(res.outputs, R)
