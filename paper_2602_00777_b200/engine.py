@@ -136,10 +136,12 @@ class HybridDecoder:
         # profiles/r01_schedule_matrix.txt): enough FULL (layer, b, kv-head) pairs that the
         # fused selects of the last FULL pairs overlap REUSE items instead of delaying them
         # (cfg2 B>=4, cfg3 B=4, cfg4 B>=8; not B=1, cfg2 B=2, cfg4 B=4)
+        # Block mode: always (its fused block selects are short; cfg2 B=1 229 vs 232 us,
+        # B=8 1.44 vs 1.52 ms, scripts/block_single_ab.py).
         if single_launch == "auto":
             pairs = len(self.full_layers) * B * Hkv
             single_launch = (bool(fuse_select) and not dual_stream and len(feeds) > 0
-                             and pairs >= 192)
+                             and (pairs >= 192 or block_size > 1))
         # token or block mode (hylra_decode_step_blocks_ex: the FULL pairs' final CTAs pool,
         # select blocks and write the coverage)
         self._single_ok = (not (block_size > 1 and (include_sinks or include_recent

@@ -154,13 +154,14 @@ def test_block_reuse_tiles_equal_row_gather(bs, bb, n_valid, monkeypatch):
     k[:, :, :, n_valid - 1, :] = 4.0 * q.float().view(L, B, Hkv, Hq // Hkv, d).mean(3).to(k.dtype)
     actions = ("full", "reuse", "full", "reuse", "reuse")
     monkeypatch.setenv("HYLRA_BLOCK_TILES", "0")
-    ref = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs).step(q, n_valid)
+    ref = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs,
+                        single_launch=False).step(q, n_valid)
     torch.cuda.synchronize()
     R, S = ref.outputs.clone(), ref.selections.clone()
     nb = -(-n_valid // bs)
     assert bool((S == nb - 1).any(-1).all()), "the ragged last block must be selected"
     monkeypatch.setenv("HYLRA_BLOCK_TILES", "1")
-    dec = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs)
+    dec = HybridDecoder(actions, k, v, bb, q_heads=Hq, block_size=bs, single_launch=False)
     res = dec.step(q, n_valid)
     torch.cuda.synchronize()
     dec.check_flags()
