@@ -294,7 +294,9 @@ int hylra_decode_step_blocks(const hylra_geometry* g, const void* q, const void*
  * into blocks, selects them (block_budget, float64 refinement as above) and writes the
  * token coverage; the REUSE items gather it once their row's ready flag is set. Same
  * results as the multi-launch block step (tensor-core path, sel_group 1; otherwise the
- * multi-launch step runs). Other option fields are ignored. Workspace: as above. */
+ * multi-launch step runs). append_k_rows / append_v_rows / append_pos as for
+ * hylra_decode_step_ex (written inside the single-launch kernel, else appended first).
+ * Other option fields are ignored. Workspace: as above. */
 int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const void* k,
                                 const void* v, int n_valid, const uint8_t* actions,
                                 int block_budget, int block_size, int sel_group, int refine,

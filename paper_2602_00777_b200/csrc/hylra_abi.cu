@@ -747,6 +747,40 @@ int record(void* const* evs, int l, cudaStream_t st) {
   return cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(evs[l]), st), "event record");
 }
 
+// The step's append option (hylra_step_options append_*): validated here; in_kernel fills
+// *ap for the single-launch kernel (its FULL items write the rows), else hylra_append_kv
+// runs ahead of the step on the same stream.
+int step_append(const hylra_geometry* g, const void* k, const void* v, const void* rows_k,
+                const void* rows_v, int pos, int n_valid, bool in_kernel, StepAppend* ap,
+                cudaStream_t st) {
+  if (!rows_k || !rows_v)
+    return fail(HYLRA_ERR_CONFIGURATION, "append needs both append_k_rows and append_v_rows");
+  if (pos < 0 || pos >= n_valid)
+    return fail(HYLRA_ERR_INVALID_INPUT, "append_pos %d not in [0, n_valid=%d)", pos, n_valid);
+  if (!in_kernel)
+    return hylra_append_kv(g, const_cast<void*>(k), const_cast<void*>(v), rows_k, rows_v, pos, 0,
+                           nullptr, st);
+  if (int e = device_view(rows_k, reinterpret_cast<const void**>(&ap->k_rows), "append_k_rows"))
+    return e;
+  if (int e = device_view(rows_v, reinterpret_cast<const void**>(&ap->v_rows), "append_v_rows"))
+    return e;
+  const int64_t es = 2, row_bytes = (int64_t)g->head_dim * es;  // tensor-core path: bf16
+  if ((g->kv_stride_layer * es) % 16 || (g->kv_stride_batch * es) % 16 ||
+      (g->kv_stride_head * es) % 16 || reinterpret_cast<uintptr_t>(k) % 16 ||
+      reinterpret_cast<uintptr_t>(v) % 16 || reinterpret_cast<uintptr_t>(ap->k_rows) % 16 ||
+      reinterpret_cast<uintptr_t>(ap->v_rows) % 16)
+    return fail(HYLRA_ERR_CONFIGURATION, "append needs 16-byte aligned rows and strides");
+  ap->k = static_cast<uint8_t*>(const_cast<void*>(k));
+  ap->v = static_cast<uint8_t*>(const_cast<void*>(v));
+  ap->kv_sl = g->kv_stride_layer * es;
+  ap->kv_sb = g->kv_stride_batch * es;
+  ap->kv_sh = g->kv_stride_head * es;
+  ap->pos = pos;
+  ap->pos_bytes = (int64_t)pos * row_bytes;
+  ap->chunks = (int)(row_bytes / 16);
+  return HYLRA_OK;
+}
+
 int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, const void* v,
                      int n_valid, const uint8_t* actions, int budget, int sel_group, int refine,
                      int sinks, int recent, float* out, int32_t* idx, int k_stride, void* ws,
@@ -794,18 +828,12 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   // the step's new K/V rows: written inside the single-launch kernel, else by the append
   // kernel ahead of the step
   const bool appending = o.app_k != nullptr || o.app_v != nullptr;
-  if (appending) {
-    if (!o.app_k || !o.app_v)
-      return fail(HYLRA_ERR_CONFIGURATION, "append needs both append_k_rows and append_v_rows");
-    if (split) return fail(HYLRA_ERR_CONFIGURATION, "append is not supported with split caches");
-    if (o.app_pos < 0 || o.app_pos >= n_valid)
-      return fail(HYLRA_ERR_INVALID_INPUT, "append_pos %d not in [0, n_valid=%d)", o.app_pos,
-                  n_valid);
-    if (!unified)
-      if (int e = hylra_append_kv(g, const_cast<void*>(k), const_cast<void*>(v), o.app_k, o.app_v,
-                                  o.app_pos, 0, nullptr, st))
-        return e;
-  }
+  if (appending && split)
+    return fail(HYLRA_ERR_CONFIGURATION, "append is not supported with split caches");
+  StepAppend app{};
+  if (appending)
+    if (int e = step_append(g, k, v, o.app_k, o.app_v, o.app_pos, n_valid, unified, &app, st))
+      return e;
   if (unified) {
     std::vector<int32_t> ab_ids(a_ids), ab_slot(a_slot), ab_kv(a_kv);
     ab_ids.insert(ab_ids.end(), b_ids.begin(), b_ids.end());
@@ -864,27 +892,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     ss.n_ready = s.n_ready;
     ss.n_full_items = (int)items_f;
     ss.n_items = (int)(items_f + items_r);
-    if (appending) {
-      StepAppend& ap = ss.app;
-      if (int e = device_view(o.app_k, reinterpret_cast<const void**>(&ap.k_rows), "append_k_rows"))
-        return e;
-      if (int e = device_view(o.app_v, reinterpret_cast<const void**>(&ap.v_rows), "append_v_rows"))
-        return e;
-      const int64_t es = 2, row_bytes = (int64_t)g->head_dim * es;  // tensor-core path: bf16
-      if ((g->kv_stride_layer * es) % 16 || (g->kv_stride_batch * es) % 16 ||
-          (g->kv_stride_head * es) % 16 || reinterpret_cast<uintptr_t>(k) % 16 ||
-          reinterpret_cast<uintptr_t>(v) % 16 || reinterpret_cast<uintptr_t>(ap.k_rows) % 16 ||
-          reinterpret_cast<uintptr_t>(ap.v_rows) % 16)
-        return fail(HYLRA_ERR_CONFIGURATION, "append needs 16-byte aligned rows and strides");
-      ap.k = static_cast<uint8_t*>(const_cast<void*>(k));
-      ap.v = static_cast<uint8_t*>(const_cast<void*>(v));
-      ap.kv_sl = g->kv_stride_layer * es;
-      ap.kv_sb = g->kv_stride_batch * es;
-      ap.kv_sh = g->kv_stride_head * es;
-      ap.pos = o.app_pos;
-      ap.pos_bytes = (int64_t)o.app_pos * row_bytes;
-      ap.chunks = (int)(row_bytes / 16);
-    }
+    ss.app = app;
     if (o.reuse_wait)
       if (int e = cuda_check(cudaStreamWaitEvent(st, o.reuse_wait, 0), "stream wait event"))
         return e;
@@ -1280,10 +1288,17 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
   const int nf = (int)s.full_ids.size();
   const int nr = (int)s.reuse_ids.size();
   const int nb = (n_valid + block_size - 1) / block_size;
+  const bool single = opt && opt->fuse_select == 2 && sel_group == 1 && use_mma_path(g) &&
+                      fused_select_fits(g, nb);
+  // the step's new K/V rows: written by the single-launch kernel, else appended ahead
+  StepAppend app{};
+  if (opt && (opt->append_k_rows || opt->append_v_rows))
+    if (int e = step_append(g, k, v, opt->append_k_rows, opt->append_v_rows, opt->append_pos,
+                            n_valid, single, &app, st))
+      return e;
   // single-launch block step (fuse_select = 2): the final CTA of every FULL pair pools its
   // row into blocks, selects them and writes the token coverage the REUSE items gather
-  if (opt && opt->fuse_select == 2 && sel_group == 1 && use_mma_path(g) &&
-      fused_select_fits(g, nb)) {
+  if (single) {
     std::vector<int32_t> ab_ids, ab_slot, b_ids, b_slot;
     for (int i = 0; i < nf; ++i) {
       const int l = s.full_ids[i];
@@ -1335,6 +1350,7 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
     ss.n_ready = s.n_ready;
     ss.n_full_items = (int)items_f;
     ss.n_items = (int)(items_f + items_r);
+    ss.app = app;
     return dispatch_step(g, st, tk, tv, pf, pr, sp, ss);
   }
   if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, nf, s.full_ids.data(), nullptr,

@@ -239,7 +239,7 @@ class HybridDecoder:
         wait on it (hylra_decode_step_ex). Token mode only. out (optional): fp32
         [L, B, Hq, d] destination instead of the decoder's own buffer — device memory or
         pinned host memory, which the kernels then write across the link directly.
-        append (optional, token mode): (k_rows, v_rows, pos) — this step's new K/V rows
+        append (optional): (k_rows, v_rows, pos) — this step's new K/V rows
         [L, B, Hkv, d] (device or pinned host, cache dtype), written at cache row pos
         (< n_valid) before they are read; the single-launch step writes them inside its one
         kernel (hylra_step_options append_*)."""
@@ -277,17 +277,7 @@ class HybridDecoder:
                  opt.join_event) = (e.cuda_event for e in self._events)
             if reuse_wait is not None:
                 opt.reuse_wait_event = reuse_wait.cuda_event
-            if append is not None:
-                k_rows, v_rows, pos = append
-                L, B, Hkv, cap, d = self.k.shape
-                for t in (k_rows, v_rows):
-                    if t.shape != (L, B, Hkv, d) or t.dtype != self.k.dtype \
-                            or not t.is_contiguous() or not (t.is_cuda or t.is_pinned()):
-                        raise ConfigurationError("new rows must be contiguous [L, B, Hkv, d] "
-                                                 "device or pinned host tensors of the cache "
-                                                 "dtype")
-                opt.append_k_rows, opt.append_v_rows = k_rows.data_ptr(), v_rows.data_ptr()
-                opt.append_pos = int(pos)
+            self._append_option(opt, append)
             evs = None
             if layer_events is not None:
                 evs = _abi.pointer_array(e.cuda_event if e is not None else None
@@ -301,8 +291,8 @@ class HybridDecoder:
             k_eff = min(self.budget, n_valid)
             return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer,
                               self.full_layers)
-        if layer_events is not None or reuse_wait is not None or append is not None:
-            raise ConfigurationError("per-layer events and append apply to token selection only")
+        if layer_events is not None or reuse_wait is not None:
+            raise ConfigurationError("per-layer events apply to token selection only")
         if self.block_size > 1:
             need = int(lib.hylra_decode_step_blocks_workspace_bytes(
                 g, self._acts, n_valid, self.budget, self.block_size, self.sel_group))
@@ -310,6 +300,7 @@ class HybridDecoder:
                 self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
             opt = _abi.StepOptions()
             opt.fuse_select = 2 if self.single else 0
+            self._append_option(opt, append)
             _abi.check(lib.hylra_decode_step_blocks_ex(
                 g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
                 self.budget, self.block_size, self.sel_group, int(self.refine),
@@ -318,6 +309,20 @@ class HybridDecoder:
             bb = min(self.budget, -(-n_valid // self.block_size))
             return StepResult(self.out, self.idx[..., :bb], self.slot_of_layer,
                               self.full_layers)
+
+    def _append_option(self, opt, append) -> None:
+        """hylra_step_options append_* from step(append=(k_rows, v_rows, pos))."""
+        if append is None:
+            return
+        k_rows, v_rows, pos = append
+        L, B, Hkv, cap, d = self.k.shape
+        for t in (k_rows, v_rows):
+            if t.shape != (L, B, Hkv, d) or t.dtype != self.k.dtype or not t.is_contiguous() \
+                    or not (t.is_cuda or t.is_pinned()):
+                raise ConfigurationError("new rows must be contiguous [L, B, Hkv, d] device or "
+                                         "pinned host tensors of the cache dtype")
+        opt.append_k_rows, opt.append_v_rows = k_rows.data_ptr(), v_rows.data_ptr()
+        opt.append_pos = int(pos)
 
     def append(self, k_rows: torch.Tensor, v_rows: torch.Tensor, pos: int, layers=None) -> None:
         """Write one step's new K/V rows [L, B, Hkv, d] (device or pinned host tensors, the
@@ -552,7 +557,7 @@ class DecodeLoop:
     outputs land in the pinned `out_host`. Fill the host buffers, call `run()`; it returns
     `out_host` after the step completed.
 
-    zero_copy=True (token-mode HybridDecoder): no copy operations at all — hylra_append_kv
+    zero_copy=True (HybridDecoder): no copy operations at all — hylra_append_kv
     reads the new rows from pinned host memory in place (the FULL layers' rows before the
     FULL kernel, the REUSE layers' on a side stream under it, waited on by the REUSE
     launch), the attention kernels read each (layer, KV head)'s queries across the link
@@ -576,8 +581,7 @@ class DecodeLoop:
         self.graph = None
         self.h2d_bytes = (self.q_host.numel() + 2 * self.k_host.numel()) * self.q_host.element_size()
         self.d2h_bytes = self.out_host.numel() * 4
-        self.zero_copy = bool(zero_copy) and type(decoder) is HybridDecoder \
-            and decoder.block_size == 1
+        self.zero_copy = bool(zero_copy) and type(decoder) is HybridDecoder
         if not self.zero_copy:
             self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
             self.kv_dev = torch.zeros((2, L, B, Hkv, d), dtype=dt, device=k.device)
@@ -609,8 +613,9 @@ class DecodeLoop:
                 with torch.cuda.stream(self.side):
                     self.q_dev.copy_(self.q_host, non_blocking=True)
                 q = self.q_dev
-            if dec.single:
-                # single-launch step: the kernel writes the new rows itself (one launch)
+            if dec.single or dec.block_size > 1:
+                # the step's append option: the single-launch kernel writes the new rows
+                # itself (one launch); the block-mode multi-launch step appends them first
                 if q_copy:
                     main.wait_stream(self.side)
                 dec.step(q, pos + 1, out=self.out_host,

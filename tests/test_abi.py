@@ -133,3 +133,24 @@ def test_layer_runs():
     assert _runs([]) == []
     assert _runs([0, 1, 2, 8, 15, 16, 24, 31]) == [(0, 3), (8, 9), (15, 17), (24, 25), (31, 32)]
     assert _runs(range(3, 8)) == [(3, 8)]
+
+
+def test_block_step_append_options_validate_on_the_host():
+    """hylra_decode_step_blocks_ex takes the same append_* options (written by the
+    single-launch block kernel or appended ahead): validated before any launch."""
+    lib = _abi.lib()
+    g = _geom()
+    acts = _abi.uint8_array([1, 0, 1, 0])
+    need = lib.hylra_decode_step_blocks_workspace_bytes(g, acts, 2048, 16, 64, 1)
+    assert need > 0
+    opt = _abi.StepOptions()
+    opt.fuse_select = 2
+    opt.append_v_rows = 1
+    with pytest.raises(ConfigurationError, match="both"):
+        _abi.check(lib.hylra_decode_step_blocks_ex(g, 1, 1, 1, 2048, acts, 16, 64, 1, 1, 1, 1,
+                                                   16, 1, need, None, ctypes.byref(opt)))
+    opt.append_k_rows = 1
+    opt.append_pos = -1
+    with pytest.raises(InvalidInputError, match="append_pos"):
+        _abi.check(lib.hylra_decode_step_blocks_ex(g, 1, 1, 1, 2048, acts, 16, 64, 1, 1, 1, 1,
+                                                   16, 1, need, None, ctypes.byref(opt)))

@@ -205,3 +205,40 @@ def test_block_single_launch_equals_multi_launch(bs, bb, n_valid, B):
         gr.replay()
         torch.cuda.synchronize()
         assert torch.equal(dec.out, R)
+
+
+@pytest.mark.parametrize("single", [True, False])
+def test_block_decode_loop_appends_in_step(single):
+    """DecodeLoop over a block-mode decoder (zero copy): the step's new K/V rows ride the
+    step's append option (hylra_decode_step_blocks_ex append_*) — written inside the
+    single-launch kernel, or appended ahead of the multi-launch step — queries and outputs
+    in pinned host memory. Equal to an eager step over a cache holding the same rows."""
+    from paper_2602_00777_b200.engine import DecodeLoop
+    L, B, Hq, Hkv, d, cap, bs, bb = 6, 2, 16, 4, 128, 4200, 64, 12
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=37, planted=48)
+    actions = ("full", "reuse", "full", "reuse", "reuse", "full")
+    dec = HybridDecoder(actions, k.clone(), v.clone(), bb, q_heads=Hq, block_size=bs,
+                        single_launch=single)
+    assert dec.single == single
+    pos = 3999
+    loop = DecodeLoop(dec, pos, q_copy=False)
+    assert loop.zero_copy
+    g = torch.Generator().manual_seed(5)
+    for _ in range(3):
+        qh = torch.randn((L, B, Hq, d), generator=g).to(torch.bfloat16)
+        kh = torch.randn((L, B, Hkv, d), generator=g).to(torch.bfloat16)
+        vh = torch.randn((L, B, Hkv, d), generator=g).to(torch.bfloat16)
+        loop.q_host.copy_(qh)
+        loop.k_host.copy_(kh)
+        loop.v_host.copy_(vh)
+        out = loop.run().clone()
+        dec.check_flags()
+        k2, v2 = k.clone(), v.clone()
+        k2[:, :, :, pos] = kh.cuda()
+        v2[:, :, :, pos] = vh.cuda()
+        assert torch.equal(dec.k, k2) and torch.equal(dec.v, v2)
+        ref = HybridDecoder(actions, k2, v2, bb, q_heads=Hq, block_size=bs,
+                            single_launch=False).step(qh.cuda(), pos + 1)
+        torch.cuda.synchronize()
+        assert torch.equal(dec.idx[..., :ref.selections.shape[-1]], ref.selections)
+        assert torch.equal(out, ref.outputs.cpu())
