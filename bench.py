@@ -237,10 +237,31 @@ def _block_mode_line(a, cfg, torch):
     nf = len(cfg.full_layers)
     by = (nf * cfg.context + (L - nf) * bb * bs) * B * k.shape[2] * 2 * cfg.head_dim * 2
     sched, kps = dec.schedule, dec.kernels_per_step
-    del gr, dec, q, k, v
+    del gr
+    # e2e: DecodeLoop with host I/O (zero copy: queries and new K/V rows read from pinned
+    # host memory in place, the rows written by the step itself, outputs stored to host)
+    from paper_2602_00777_b200.engine import DecodeLoop
+    pos = cfg.context - 1
+    loop = DecodeLoop(dec, pos)
+    loop.q_host.copy_(q.cpu())
+    loop.k_host.copy_(k[:, :, :, pos].cpu())
+    loop.v_host.copy_(v[:, :, :, pos].cpu())
+    loop.capture()
+    for _ in range(3):
+        loop.run()
+    n_e2e = max(10, a.steps)
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        loop.run()
+    t_e2e = (time.perf_counter() - t0) / n_e2e
+    e2e = {"value": B / t_e2e, "unit": "tok/s", "ms_per_step": t_e2e * 1e3,
+           "h2d_bytes_per_step": int(loop.h2d_bytes), "d2h_bytes_per_step": int(loop.d2h_bytes),
+           "q_copy": bool(loop.q_copy)}
+    del loop, dec, q, k, v
     torch.cuda.empty_cache()
     return {"value": B / (ms * 1e-3), "ms_per_step": ms, "block_size": bs, "block_budget": bb,
-            "step_gbs": by / (ms * 1e-3) / 1e9, "schedule": sched, "kernels_per_step": kps}
+            "step_gbs": by / (ms * 1e-3) / 1e9, "schedule": sched, "kernels_per_step": kps,
+            "e2e": e2e}
 
 
 def _offload_line(a, cfg, torch, batch=1):
@@ -555,8 +576,9 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
                     "d2h_bytes_per_step": int(loop.d2h_bytes),
                     "ms_per_step": t_e2e * 1e3,
                     "path": "DecodeLoop.run() per step, one graph launch + host sync: "
-                            "hylra_append_kv reads the new K/V rows from pinned host memory "
-                            "in place, the kernels store the fp32 outputs straight into "
+                            "the new K/V rows are read from pinned host memory in place (by "
+                            "the single-launch step itself, else by hylra_append_kv), the "
+                            "kernels store the fp32 outputs straight into "
                             "pinned host memory; queries "
                             + ("copied H2D on a side stream under the append"
                                if loop.q_copy else "read in place from pinned host memory")

@@ -89,6 +89,10 @@ for key, name in (("cfg3_128k_b4", "cfg3 128K B=4"), ("cfg4_qwen_64k_b16", "cfg4
                    "", "", ""))
 tbl.append(row("cfg2 blocks (16 × 128) B=8", "block", f"{e['cfg2_blocks_b8']['ms_per_step']:.3f} ms",
                f"{e['cfg2_blocks_b8']['value']:.0f}", "", "", ""))
+be = e["cfg2_blocks_b8"].get("e2e")
+if be:
+    tbl.append(row("cfg2 blocks B=8 e2e (host I/O)", "block", f"{be['ms_per_step']:.3f} ms",
+                   f"{be['value']:.0f}", "", "", ""))
 tbl.append(row("cfg2 offload B=1 (REUSE K/V in pinned host memory)", "offload",
                f"{o['ms_per_step']:.3f} ms", f"{o['value']:.0f}", "", "",
                f"link {o['link_gbs']:.1f} GB/s = {o['link_frac_of_h2d_copy']:.2f} of a pinned H2D copy"))
