@@ -53,7 +53,17 @@ def _make(seed=0):
 ACTIONS = ("full", "reuse", "full")
 
 
-def _worker(rank, world, port, mode, q):
+def _step(q, k, v, blocks):
+    """The oracle step standing in for the kernels: token mode (budget 10) or block mode
+    (block budget 3 of 8-token blocks)."""
+    if blocks:
+        out, sets = orc.hybrid_step_blocks(q, k, v, k.shape[3], ACTIONS, 3, 8)
+        return out, sets
+    out, sets, _ = orc.hybrid_step(q, k, v, k.shape[3], ACTIONS, 10)
+    return out, sets
+
+
+def _worker(rank, world, port, mode, q, blocks=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -62,20 +72,22 @@ def _worker(rank, world, port, mode, q):
         plan = plan_shards(kn.shape[2], Hq, B, world, mode=mode)[rank]
         qs, ks, vs = shard_slices(plan, torch.from_numpy(qn), torch.from_numpy(kn),
                                   torch.from_numpy(vn))
-        out, sets, _ = orc.hybrid_step(qs.numpy(), ks.numpy(), vs.numpy(), kn.shape[3],
-                                       ACTIONS, 10)
+        out, sets = _step(qs.numpy(), ks.numpy(), vs.numpy(), blocks)
         full = gather_outputs(torch.from_numpy(out), plan)
         q.put((rank, full.numpy(), {l: sets[l] for l in sets}))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["kvhead", "batch"])
-def test_gloo_two_rank_step_equals_unsharded(mode):
+@pytest.mark.parametrize("mode,blocks", [("kvhead", False), ("batch", False),
+                                         ("kvhead", True)])
+def test_gloo_two_rank_step_equals_unsharded(mode, blocks):
+    """Token mode, and block mode (its block sets are per (b, kv-head) row too)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q, blocks))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = dict((r, (o, s)) for r, o, s in (q.get(timeout=120) for _ in procs))
@@ -83,7 +95,7 @@ def test_gloo_two_rank_step_equals_unsharded(mode):
         p.join(timeout=60)
         assert p.exitcode == 0
     qn, kn, vn = _make()
-    ref, ref_sets, _ = orc.hybrid_step(qn, kn, vn, kn.shape[3], ACTIONS, 10)
+    ref, ref_sets = _step(qn, kn, vn, blocks)
     for r in range(2):
         assert np.array_equal(res[r][0], ref)  # replicated, identical on both ranks
     # shard-local index sets equal the corresponding slices of the unsharded sets
