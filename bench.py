@@ -656,18 +656,27 @@ def run_ours(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        env = dict(os.environ)
-        n = os.cpu_count() or 1
-        env.update(OPENBLAS_NUM_THREADS=str(n), OMP_NUM_THREADS=str(n), MKL_NUM_THREADS=str(n))
-        try:
-            r = subprocess.run([sys.executable, "-m", "oracle.cpu_baseline", "--config", cfg.name,
-                                "--batch", str(batch), "--seconds", str(a.cpu_seconds)],
-                               cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
-            cpu = json.loads(r.stdout.strip().splitlines()[-1])
-            cpu.pop("step_seconds", None)
-        except Exception as exc:  # noqa: BLE001
-            cpu = {"value": None, "unit": "tok/s", "cores": n, "kind": "port",
-                   "sample": f"failed: {exc}"}
+        def cpu_run(n, seconds):
+            env = dict(os.environ)
+            env.update(OPENBLAS_NUM_THREADS=str(n), OMP_NUM_THREADS=str(n),
+                       MKL_NUM_THREADS=str(n))
+            try:
+                r = subprocess.run([sys.executable, "-m", "oracle.cpu_baseline", "--config",
+                                    cfg.name, "--batch", str(batch), "--seconds", str(seconds)],
+                                   cwd=ROOT, env=env, capture_output=True, text=True,
+                                   timeout=600)
+                res = json.loads(r.stdout.strip().splitlines()[-1])
+                res.pop("step_seconds", None)
+                return res
+            except Exception as exc:  # noqa: BLE001
+                return {"value": None, "unit": "tok/s", "cores": n, "kind": "port",
+                        "sample": f"failed: {exc}"}
+
+        # all host threads (the baseline), and one thread (SURVEY §8d's second setting)
+        cpu = cpu_run(os.cpu_count() or 1, a.cpu_seconds)
+        one = cpu_run(1, max(1.0, a.cpu_seconds / 2))
+        cpu["single_thread"] = {"value": one.get("value"), "cores": 1,
+                                "sample": one.get("sample")}
 
     extra = {}
     # configs 3 (128K, KV-head shards) and 4 (Qwen, batch shards) at every N; the block,
