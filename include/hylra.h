@@ -34,9 +34,16 @@
  *     (a cudaStream_t passed as void*) and is asynchronous.
  *   - Workspaces must be zero-filled once before first use; the kernels leave them
  *     in the zero state they found them in, so a workspace can be reused by any
- *     number of calls and CUDA-graph replays on one stream.
+ *     number of calls and CUDA-graph replays on one stream. The words kernels expect
+ *     zeroed (split-K counters, single-launch sync words) sit at offsets that depend
+ *     only on the geometry's batch and kv_heads (and, for the decode step, the policy),
+ *     never on n_valid, budget or the layer count of a call: one workspace serves every
+ *     call on one (batch, kv_heads) geometry, e.g. a decoder whose cache grows each step.
+ *     Re-zero it before using it with another geometry.
  *   - Stateless and re-entrant: concurrent calls are safe on distinct streams with
- *     non-aliasing outputs and workspaces.
+ *     non-aliasing outputs and workspaces, from any host thread and on any device
+ *     (function attributes are set per device; grids are sized from the current
+ *     device's SM count).
  *   - Status codes map 1:1 onto the reference's exception taxonomy
  *     (pkg/src/layerreuse/errors.py:4-21).
  */
@@ -50,7 +57,7 @@
 extern "C" {
 #endif
 
-#define HYLRA_ABI_VERSION 5
+#define HYLRA_ABI_VERSION 6
 
 enum hylra_status {
   HYLRA_OK = 0,
@@ -68,8 +75,11 @@ enum hylra_dtype { HYLRA_BF16 = 0, HYLRA_F32 = 1 };
 enum hylra_flag {
   HYLRA_FLAG_INDEX_OUT_OF_RANGE = 1, /* a REUSE index >= n_valid  (attention.py:256-259) */
   HYLRA_FLAG_NON_FINITE_SCORE = 2,   /* a NaN/inf score or output (attention.py:43-44)   */
-  HYLRA_FLAG_REFINE_SKIPPED = 4,     /* boundary band exceeded the f64 refinement cap    */
-  HYLRA_FLAG_INTERNAL = 8            /* a kernel invariant failed (selection size != k)  */
+  HYLRA_FLAG_REFINE_SKIPPED = 4,     /* a row's f64 refinement window exceeded 1024
+                                        scores: its k-th boundary follows fp32 order     */
+  HYLRA_FLAG_INTERNAL = 8,           /* a kernel invariant failed (selection size != k)  */
+  HYLRA_FLAG_NON_FINITE_CACHE = 16   /* a NaN/inf K/V entry (hylra_check_cache, appended
+                                        rows; attention.py:38-46,61-71)                 */
 };
 
 /*
@@ -236,6 +246,11 @@ typedef struct hylra_step_options {
   const void* append_k_rows;
   const void* append_v_rows;
   int32_t append_pos;
+  /* a second copy of the selections (idx / blocks, same layout and stride), in device or
+     page-locked host memory (NULL: none). Written by the selecting CTAs as they write idx,
+     so a caller that wants the per-layer index sets on the host needs no copy after the
+     step (ABI 6). */
+  void* idx_mirror;
 } hylra_step_options;
 
 int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, const void* v,
@@ -271,6 +286,20 @@ int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void
 int hylra_append_kv(const hylra_geometry* g, void* k, void* v, const void* k_rows,
                     const void* v_rows, int pos, int n_layers, const int32_t* layer_ids,
                     void* stream);
+
+/* hylra_append_kv that also validates the new rows: a NaN / inf entry sets
+ * HYLRA_FLAG_NON_FINITE_CACHE in the workspace flag word ws[0] (ABI 6). The decode steps'
+ * append_* options validate the same way. */
+int hylra_append_kv_checked(const hylra_geometry* g, void* k, void* v, const void* k_rows,
+                            const void* v_rows, int pos, int n_layers, const int32_t* layer_ids,
+                            void* ws, void* stream);
+
+/* Whole-cache validation (attention.py:38-46,61-71: the reference rejects any non-finite
+ * K/V entry of every layer when it builds its float64 caches): one streaming pass over rows
+ * [0, n_valid) of layers layer_ids[0..n_layers) (host array; NULL = all g->num_layers) sets
+ * HYLRA_FLAG_NON_FINITE_CACHE in ws[0] if any entry is NaN or inf (ABI 6). */
+int hylra_check_cache(const hylra_geometry* g, const void* k, const void* v, int n_valid,
+                      int n_layers, const int32_t* layer_ids, void* ws, void* stream);
 
 /* Sink / recent augmentation (engine.py:122-126): out[r] = sorted(idx[r][0..k_eff) |
  * [0, sinks) | [n_valid - recent, n_valid)), counts[r] its length. */
@@ -310,7 +339,10 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
 int hylra_overlap_counts(const int32_t* idx, int steps, int layers, int rows, int k,
                          int k_stride, int n_tokens, int32_t* counts, void* stream);
 
-/* Flag word helpers (the flag word lives in the attention / select workspaces). */
+/* Flag word helpers. The flag word is the first int32 of the attention / select / step
+ * workspaces; the second int32 counts the selection rows that raised
+ * HYLRA_FLAG_REFINE_SKIPPED. hylra_read_flags returns the flag word, hylra_clear_flags zeroes
+ * both words. */
 int hylra_read_flags(const void* ws, int32_t* flags_host, void* stream);
 int hylra_clear_flags(void* ws, void* stream);
 

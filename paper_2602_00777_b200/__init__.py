@@ -8,9 +8,9 @@ kernel feeds the host-side DP planner. All device work goes through libhylra.so 
 include/hylra.h); there is no CPU fallback.
 """
 from .errors import (ConfigurationError, CudaError, InvalidInputError, InvalidSelectionError,
-                     LayerReuseError, NumericInputError)
-from .policy import (Action, LayerPolicy, dp_optimize, policy_from_actions, static_jump_policy,
-                     validate_policy)
+                     LayerReuseError, NumericInputError, SelectionPrecisionWarning)
+from .policy import (BRUTE_FORCE_MAX_LAYERS, Action, LayerPolicy, brute_force_policy,
+                     dp_optimize, policy_from_actions, static_jump_policy, validate_policy)
 from .profiling import (LayerSensitivity, SensitivityReport, SimilarityMatrix, kl_extended,
                         merge_similarity_matrices, overlap_counts, relative_l2_error,
                         sensitivity_profile, similarity_from_counts)
@@ -21,7 +21,8 @@ from .sets import BlockSet, TopKSet
 __version__ = "0.1.0"
 
 __all__ = [
-    "Action", "LayerPolicy", "dp_optimize", "policy_from_actions", "static_jump_policy",
+    "Action", "LayerPolicy", "dp_optimize", "brute_force_policy", "BRUTE_FORCE_MAX_LAYERS",
+    "SelectionPrecisionWarning", "policy_from_actions", "static_jump_policy",
     "validate_policy", "SimilarityMatrix", "merge_similarity_matrices", "overlap_counts",
     "relative_l2_error", "similarity_from_counts", "LayerReuseError", "ConfigurationError",
     "NumericInputError", "InvalidSelectionError", "InvalidInputError", "CudaError",

@@ -14,6 +14,9 @@ from .errors import STATUS_TO_ERROR, CudaError, LayerReuseError
 # HYLRA_LIB: another build of the same ABI (A/B experiments between library versions)
 LIB_PATH = Path(os.environ.get("HYLRA_LIB") or Path(__file__).resolve().parent / "libhylra.so")
 
+# include/hylra.h HYLRA_ABI_VERSION this binding is written against (checked at load)
+ABI_VERSION = 6
+
 HYLRA_BF16 = 0
 HYLRA_F32 = 1
 
@@ -29,6 +32,39 @@ FLAG_INDEX_OUT_OF_RANGE = 1
 FLAG_NON_FINITE_SCORE = 2
 FLAG_REFINE_SKIPPED = 4
 FLAG_INTERNAL = 8
+FLAG_NON_FINITE_CACHE = 16
+
+
+def raise_for_flags(words, strict: bool = False) -> None:
+    """Map the workspace flag words (include/hylra.h: flag word, refine-skipped row count) to
+    the reference's exceptions. HYLRA_FLAG_REFINE_SKIPPED means some selection row's k-th
+    boundary could not be re-resolved in float64 (more than 1024 scores inside the
+    refinement window): that row follows fp32 order with ties to the lower index, which can
+    differ from the reference's float64 order (attention.py:264-275). It warns
+    (SelectionPrecisionWarning), or raises InvalidSelectionError when `strict`."""
+    flags, skipped = int(words[0]), int(words[1]) if len(words) > 1 else 0
+    if flags & FLAG_INDEX_OUT_OF_RANGE:
+        from .errors import InvalidSelectionError
+        raise InvalidSelectionError("a selection index is out of range for the cache")
+    if flags & FLAG_NON_FINITE_SCORE:
+        from .errors import NumericInputError
+        raise NumericInputError("selection scores contain non-finite entries")
+    if flags & FLAG_NON_FINITE_CACHE:
+        from .errors import NumericInputError
+        raise NumericInputError("the KV cache contains non-finite entries")
+    if flags & FLAG_INTERNAL:
+        raise CudaError("a selection kernel invariant failed (internal error)")
+    if flags & FLAG_REFINE_SKIPPED:
+        msg = (f"{max(skipped, 1)} selection row(s) had more than 1024 scores within the "
+               "float64 refinement window of the k-th value; their boundary follows fp32 "
+               "order (ties to the lower index), not the reference's float64 order")
+        if strict:
+            from .errors import InvalidSelectionError
+            raise InvalidSelectionError(msg)
+        import warnings
+
+        from .errors import SelectionPrecisionWarning
+        warnings.warn(msg, SelectionPrecisionWarning, stacklevel=3)
 
 # Every symbol include/hylra.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
@@ -46,6 +82,8 @@ EXPORTED_SYMBOLS = (
     "hylra_decode_step_offload",
     "hylra_decode_step_ex",
     "hylra_append_kv",
+    "hylra_append_kv_checked",
+    "hylra_check_cache",
     "hylra_overlap_counts",
     "hylra_augment_selection",
     "hylra_block_select",
@@ -94,6 +132,7 @@ class StepOptions(ctypes.Structure):
         ("append_k_rows", ctypes.c_void_p),
         ("append_v_rows", ctypes.c_void_p),
         ("append_pos", ctypes.c_int32),
+        ("idx_mirror", ctypes.c_void_p),
     ]
 
 
@@ -113,6 +152,9 @@ def lib() -> ctypes.CDLL:
         vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
         gp = ctypes.POINTER(Geometry)
         l.hylra_abi_version.restype = i32
+        if l.hylra_abi_version() != ABI_VERSION:
+            raise CudaError(f"{LIB_PATH} implements ABI {l.hylra_abi_version()}, this binding "
+                            f"needs {ABI_VERSION}: rebuild it (__graft_entry__.build())")
         l.hylra_status_string.restype = ctypes.c_char_p
         l.hylra_status_string.argtypes = [i32]
         l.hylra_last_error.restype = ctypes.c_char_p
@@ -154,6 +196,10 @@ def lib() -> ctypes.CDLL:
                                            vp, vp, i32, vp, sz, vp, ctypes.POINTER(StepOptions)]
         l.hylra_append_kv.restype = i32
         l.hylra_append_kv.argtypes = [gp, vp, vp, vp, vp, i32, i32, vp, vp]
+        l.hylra_append_kv_checked.restype = i32
+        l.hylra_append_kv_checked.argtypes = [gp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
+        l.hylra_check_cache.restype = i32
+        l.hylra_check_cache.argtypes = [gp, vp, vp, i32, i32, vp, vp, vp]
         l.hylra_augment_selection.restype = i32
         l.hylra_augment_selection.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp]
         l.hylra_overlap_counts.restype = i32

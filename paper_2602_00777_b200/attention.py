@@ -230,14 +230,6 @@ def sparse_attention(q, k, v, idx, n_valid: int | None = None, *, sel_group: int
     return out[0] if single else out
 
 
-def _raise_flags(ws: torch.Tensor) -> None:
-    """Synchronising check of the device flag word (eager API only; graphs skip it)."""
-    flags = int(ws[:4].view(torch.int32).item())
-    if flags & _abi.FLAG_INDEX_OUT_OF_RANGE:
-        raise InvalidSelectionError("a selection index is out of range for the cache")
-    if flags & _abi.FLAG_NON_FINITE_SCORE:
-        from .errors import NumericInputError
-        raise NumericInputError("selection scores contain non-finite entries")
-    if flags & _abi.FLAG_INTERNAL:
-        from .errors import CudaError
-        raise CudaError("a selection kernel invariant failed (internal error)")
+def _raise_flags(ws: torch.Tensor, strict: bool = False) -> None:
+    """Synchronising check of the device flag words (eager API only; graphs skip it)."""
+    _abi.raise_for_flags(ws[:8].view(torch.int32).tolist(), strict)

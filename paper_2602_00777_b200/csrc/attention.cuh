@@ -404,7 +404,7 @@ __device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
 #ifdef HYLRA_TRACE
 // Diagnostics build only (-DHYLRA_TRACE, scripts/trace_single.py): per single-launch CTA,
 // globaltimer marks [0 ticket, 1 select start, 2 REUSE ready, 3 select end, 4 done, 5 smid]
-__device__ long long* g_trace;
+static __device__ long long* g_trace;
 __shared__ int g_trace_row;
 __device__ __forceinline__ long long* hylra_trace_rec() { return g_trace + g_trace_row * 8; }
 __device__ __forceinline__ void hylra_trace_mark(int k) {
@@ -857,6 +857,7 @@ struct StepAppend {
   const uint4* v_rows;
   uint8_t* k;           // cache bases (bytes)
   uint8_t* v;
+  int* flags;           // a non-finite new row sets HYLRA_FLAG_NON_FINITE_CACHE
   int64_t kv_sl, kv_sb, kv_sh, pos_bytes;  // bytes
   int pos, chunks;                          // chunks = 16-byte chunks per row
 };
@@ -883,6 +884,13 @@ __device__ __forceinline__ void append_row(const StepAppend& a, int B, int Hkv, 
   uint8_t* dst = (is_v ? a.v : a.k) + cache_layer * a.kv_sl + b * a.kv_sb + kh * a.kv_sh +
                  a.pos_bytes;
   reinterpret_cast<uint4*>(dst)[c] = val;
+  // bf16 (the tensor-core path): any all-ones exponent among the 8 values
+  const uint32_t w[4] = {val.x, val.y, val.z, val.w};
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    bad |= ((w[i] & 0x7f80u) == 0x7f80u) || ((w[i] & 0x7f800000u) == 0x7f800000u);
+  if (bad) atomicOr(a.flags, 16);
 }
 
 template <int D, bool GBIG, int STAGES>

@@ -2,7 +2,7 @@
 //
 // Host side of the drop-in boundary: validates shapes (ConfigurationError /
 // InvalidInputError, reference errors.py:4-21), picks the kernel family, sizes the
-// split-K grid for 148 SMs, encodes the TMA tensor maps and enqueues on the caller's
+// split-K grid for the device's SM count, encodes the TMA tensor maps and enqueues on the caller's
 // stream. No allocation, no synchronisation, no retained state besides cached
 // function attributes.
 #include <atomic>
@@ -11,22 +11,22 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <utility>
 #include <vector>
 
 #include "../../include/hylra.h"
 #include "append.cuh"
-#include "attention.cuh"
 #include "blocks.cuh"
+#include "launch.cuh"
 #include "overlap.cuh"
-#include "select.cuh"
 
 using namespace hylra;
+using namespace hylra::host;
 
 namespace {
 
-constexpr int kNumSMs = 148;
 constexpr size_t kHeader = 256;
 // REUSE L2 prefetch distance in 64-row tiles. Swept on B200 at cfg2 B=8 once the CTA's
 // indices are staged in shared memory: 0/1/2/3/4/6/8/12/16 tiles -> 305.6/307.0/311.1/
@@ -50,6 +50,7 @@ int cuda_check(cudaError_t e, const char* what) {
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
 int scores_row_stride(const hylra_geometry* g) { return (g->capacity + 7) & ~7; }
 
 int check_geometry(const hylra_geometry* g) {
@@ -85,9 +86,8 @@ int check_geometry(const hylra_geometry* g) {
 //    rows are few (B=1: 186.5 -> 168.8 us).
 // HYLRA_{FULL,REUSE}_{WAVES,MIN_TILES} replace a rule by "waves x S CTAs, >= min tiles
 // per split" for tuning experiments.
-constexpr int kSlots = kNumSMs * 2;
-
 int splits_by_waves(int pairs, int tiles, int waves, int min_tiles) {
+  const int kSlots = 2 * num_sms();
   int s = (kSlots * waves + pairs - 1) / pairs;
   return std::min(s, std::max(1, tiles / min_tiles));
 }
@@ -106,6 +106,7 @@ int choose_splits(int pairs, int tiles, bool gather) {
     env[1][1] = get("HYLRA_REUSE_MIN_TILES");
   });
   const int* e = env[gather ? 1 : 0];
+  const int kSlots = 2 * num_sms();  // 2 attention CTAs resident per SM
   int s;
   if (e[0] || e[1]) {
     s = splits_by_waves(pairs, tiles, e[0] ? e[0] : 8, e[1] ? e[1] : 4);
@@ -147,7 +148,20 @@ struct AttnLayout {
   size_t off_counters, off_ml, off_o, total;
 };
 
-AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows, bool gather) {
+// Split-K counters of one launch: one int per (layer slot, b, kv-head) pair, always sized for
+// kMaxSlots slots so their place and extent depend on the geometry's B and Hkv only — never
+// on n_valid, the row count or the layer count of a call. Counters are left zeroed by the
+// merging CTA, but the float partials that follow them are not: were the counter region
+// to move or grow between calls on one workspace, a counter could start on a stale partial
+// and the merge would never fire.
+size_t counter_region_bytes(const hylra_geometry* g) {
+  return align_up(sizeof(int) * (size_t)kMaxSlots * g->batch * g->kv_heads, 256);
+}
+
+// ext_ctr: the counters live elsewhere (the decode step's fixed counter regions) and the
+// layout holds only the partials
+AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows, bool gather,
+                       bool ext_ctr = false) {
   AttnLayout a{};
   const int G = g->q_heads / g->kv_heads;
   a.pairs = n_layers * g->batch * g->kv_heads;
@@ -155,11 +169,12 @@ AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows, bool gat
   a.splits = choose_splits(a.pairs, a.tiles, gather);
   a.tps = (a.tiles + a.splits - 1) / a.splits;
   const size_t parts = a.splits;  // partial slots per pair
-  a.off_counters = kHeader;
-  a.off_ml = align_up(a.off_counters + sizeof(int) * a.pairs, 256);
+  a.off_counters = ext_ctr ? 0 : kHeader;
+  const size_t ctr_end = ext_ctr ? 0 : kHeader + counter_region_bytes(g);
+  a.off_ml = align_up(ctr_end, 256);
   a.off_o = align_up(a.off_ml + sizeof(float) * 2 * (size_t)a.pairs * parts * G, 256);
   a.total = align_up(a.off_o + sizeof(float) * (size_t)a.pairs * parts * G * g->head_dim, 256);
-  if (parts == 1) a.total = align_up(a.off_counters + sizeof(int) * a.pairs, 256);
+  if (parts == 1) a.total = std::max<size_t>(ctr_end, 256);
   return a;
 }
 
@@ -209,113 +224,13 @@ int encode_kv_map(CUtensorMap* map, const hylra_geometry* g, const void* base, i
   return HYLRA_OK;
 }
 
-// ------------------------------------------------------------------ launches
-// Programmatic dependent launch for the step's kernels (FULL, SELECT, REUSE): each may be
-// scheduled while its predecessor drains (the kernels wait on griddepcontrol before
-// touching memory). HYLRA_PDL=0 turns it off.
-bool pdl_enabled() {
-  static int v = -1;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    const char* e = std::getenv("HYLRA_PDL");
-    v = (e && *e) ? (atoi(e) != 0) : 1;
-  });
-  return v == 1;
-}
-
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                       cudaStream_t st, Args&&... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-
-// ------------------------------------------------------------------ kernel tables
-template <int D, bool GATHER, bool GBIG>
-constexpr int mma_stages() {
-  return D == 128 ? 3 : 5;
-}
-template <int D, bool GATHER, bool GBIG>
-size_t mma_smem_bytes() {
-  return (size_t)mma_stages<D, GATHER, GBIG>() * MmaSmem<D>::kStageBytes + 1024 + 256 +
-         (GATHER ? kIdxStage * sizeof(int32_t) : 0);
-}
-
-template <int D, bool GATHER, bool GBIG>
-cudaError_t launch_mma(dim3 grid, cudaStream_t st, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const AttnParams& p, const SelectParams& sp) {
-  constexpr int S = mma_stages<D, GATHER, GBIG>();
-  auto kern = attn_mma_kernel<D, GATHER, GBIG, S>;
-  const size_t smem = mma_smem_bytes<D, GATHER, GBIG>();
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
-  return launch_pdl(kern, grid, dim3(attn_threads<GATHER>()), smem, st, tk, tv, p, sp);
-}
-
-// Single-launch step (FULL items with fused selects, then REUSE items; attention.cuh).
-// Its parameters stay within the classic 4 KB kernel-parameter space.
-static_assert(2 * sizeof(CUtensorMap) + 2 * sizeof(AttnParams) + sizeof(SelectParams) +
-                      sizeof(StepSync) <= 4096,
-              "step_mma_kernel parameters exceed 4 KB");
-template <int D, bool GBIG>
-cudaError_t launch_step_mma(int n_items, cudaStream_t st, const CUtensorMap& tk,
-                            const CUtensorMap& tv, const AttnParams& pf, const AttnParams& pr,
-                            const SelectParams& sp, const StepSync& ss) {
-  constexpr int S = mma_stages<D, true, GBIG>();
-  auto kern = step_mma_kernel<D, GBIG, S>;
-  const size_t smem = mma_smem_bytes<D, true, GBIG>();
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
-  return launch_pdl(kern, dim3(n_items), dim3(attn_threads<true>()), smem, st, tk, tv, pf, pr, sp,
-                    ss);
-}
-
-template <typename T, int D, int GM, bool GATHER>
-cudaError_t launch_simt(dim3 grid, cudaStream_t st, const AttnParams& p) {
-  attn_simt_kernel<T, D, GM, GATHER><<<grid, 128, 0, st>>>(p);
-  return cudaGetLastError();
-}
-
-template <typename T, bool GATHER>
-cudaError_t dispatch_simt(int D, int G, dim3 grid, cudaStream_t st, const AttnParams& p) {
-#define HY_SIMT_D(DD)                                                  \
-  if (D == DD) {                                                       \
-    if (G <= 1) return launch_simt<T, DD, 1, GATHER>(grid, st, p);     \
-    if (G <= 4) return launch_simt<T, DD, 4, GATHER>(grid, st, p);     \
-    if (G <= 8) return launch_simt<T, DD, 8, GATHER>(grid, st, p);     \
-    return launch_simt<T, DD, 16, GATHER>(grid, st, p);                \
-  }
-  HY_SIMT_D(32)
-  HY_SIMT_D(64)
-  HY_SIMT_D(128)
-#undef HY_SIMT_D
-  return cudaErrorInvalidValue;
-}
-
 // Validated AttnParams of one FULL or REUSE launch (or of one half of a single-launch step).
 int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* g, bool gather,
                      const void* q, const void* k, const void* v, int n_valid, int n_rows,
                      int n_layers, const int32_t* layer_ids, const int32_t* src_slots,
                      const int32_t* idx, const int32_t* counts, int k_stride, int sel_group,
                      float* out, float* scores, void* ws, size_t ws_bytes, int* flags,
-                     const int32_t* kv_layer_ids, int kv_layer_count) {
+                     const int32_t* kv_layer_ids, int kv_layer_count, int* counters = nullptr) {
   if (int e = check_geometry(g)) return e;
   if (n_layers < 1 || n_layers > kMaxSlots)
     return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", n_layers, kMaxSlots);
@@ -325,14 +240,14 @@ int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* 
   if (n_rows < 1) return fail(HYLRA_ERR_INVALID_INPUT, "no rows to attend over");
   if (!q || !k || !v || !out || !ws || !layer_ids)
     return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
-  const AttnLayout lay = attn_layout(g, n_layers, n_rows, gather);
+  const AttnLayout lay = attn_layout(g, n_layers, n_rows, gather, counters != nullptr);
   if (ws_bytes < lay.total)
     return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, lay.total);
   const int G = g->q_heads / g->kv_heads;
   AttnParams p{};
   p.q = q; p.k = k; p.v = v; p.out = out; p.scores = scores; p.idx = idx; p.counts = counts;
   uint8_t* w = static_cast<uint8_t*>(ws);
-  p.counters = reinterpret_cast<int*>(w + lay.off_counters);
+  p.counters = counters ? counters : reinterpret_cast<int*>(w + lay.off_counters);
   p.ws_ml = reinterpret_cast<float*>(w + lay.off_ml);
   p.ws_o = reinterpret_cast<float*>(w + lay.off_o);
   p.flags = flags;
@@ -370,12 +285,13 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
                      float* scores, void* ws, size_t ws_bytes, int* flags, cudaStream_t st,
                      const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0,
                      const SelectParams* fused = nullptr, int fuse_nslots = 0,
-                     const int32_t* blk = nullptr, int blk_stride = 0, int blk_size = 0) {
+                     const int32_t* blk = nullptr, int blk_stride = 0, int blk_size = 0,
+                     int* counters = nullptr) {
   AttnParams p{};
   AttnLayout lay{};
   if (int e = make_attn_params(&p, &lay, g, gather, q, k, v, n_valid, n_rows, n_layers, layer_ids,
                                src_slots, idx, counts, k_stride, sel_group, out, scores, ws,
-                               ws_bytes, flags, kv_layer_ids, kv_layer_count))
+                               ws_bytes, flags, kv_layer_ids, kv_layer_count, counters))
     return e;
   // block-mode REUSE by TMA tiles of the selected blocks: REUSE split rules, the streaming
   // (TMA) kernel
@@ -400,24 +316,9 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
       if (int e = encode_kv_map(&tk, g, k, n_kv)) return e;
       if (int e = encode_kv_map(&tv, g, v, n_kv)) return e;
     }
-    const bool big = G > 8;
-    if (g->head_dim == 128) {
-      if (gather) ce = big ? launch_mma<128, true, true>(grid, st, tk, tv, p, sp)
-                           : launch_mma<128, true, false>(grid, st, tk, tv, p, sp);
-      else ce = big ? launch_mma<128, false, true>(grid, st, tk, tv, p, sp)
-                    : launch_mma<128, false, false>(grid, st, tk, tv, p, sp);
-    } else {
-      if (gather) ce = big ? launch_mma<64, true, true>(grid, st, tk, tv, p, sp)
-                           : launch_mma<64, true, false>(grid, st, tk, tv, p, sp);
-      else ce = big ? launch_mma<64, false, true>(grid, st, tk, tv, p, sp)
-                    : launch_mma<64, false, false>(grid, st, tk, tv, p, sp);
-    }
-  } else if (g->dtype == HYLRA_F32) {
-    ce = gather ? dispatch_simt<float, true>(g->head_dim, G, grid, st, p)
-                : dispatch_simt<float, false>(g->head_dim, G, grid, st, p);
+    ce = run_attn_mma(g->head_dim, gather, G > 8, grid, st, tk, tv, p, sp);
   } else {
-    ce = gather ? dispatch_simt<__nv_bfloat16, true>(g->head_dim, G, grid, st, p)
-                : dispatch_simt<__nv_bfloat16, false>(g->head_dim, G, grid, st, p);
+    ce = run_attn_simt(g->dtype == HYLRA_F32, gather, g->head_dim, G, grid, st, p);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_check(ce, gather ? "reuse_decode launch" : "full_decode launch");
@@ -436,22 +337,9 @@ int select_threads(int rows) {
     forced = (t == 128 || t == 256 || t == 512 || t == 1024) ? t : 0;
   });
   if (forced) return forced;
-  if (rows <= kNumSMs) return 1024;
-  if (rows <= 2 * kNumSMs) return 512;
+  if (rows <= num_sms()) return 1024;
+  if (rows <= 2 * num_sms()) return 512;
   return 256;
-}
-
-template <int NT>
-cudaError_t launch_select_nt(dim3 grid, size_t smem, cudaStream_t st, const SelectParams& p) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(topk_select_kernel<NT>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sel_smem_bytes(kSelMaxTokens, NT));
-  });
-  if (attr_err != cudaSuccess) return attr_err;
-  return launch_pdl(topk_select_kernel<NT>, grid, dim3(NT), smem, st, p);
 }
 
 struct BlockRows {  // block mode: rows are pooled block scores
@@ -517,19 +405,17 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
                   const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
                   int* flags, cudaStream_t st, const BlockRows& br = BlockRows(),
                   const int32_t* kv_layer_ids = nullptr, const int32_t* out_slots = nullptr,
-                  int force_nt = 0) {
+                  int force_nt = 0, int32_t* idx_mirror = nullptr) {
   SelectParams p{};
   if (int e = build_select_params(&p, g, scores, n_slots, n_valid, budget, sel_group, q, k,
                                   layer_ids, idx, k_stride, info, flags, br, kv_layer_ids,
                                   out_slots))
     return e;
+  p.idx_mirror = idx_mirror;
   dim3 grid(p.n_groups, g->batch, n_slots);
   const int nt = force_nt ? force_nt : select_threads(p.n_groups * g->batch * n_slots);
   cudaError_t ce;
-  if (nt == 1024) ce = launch_select_nt<1024>(grid, sel_smem_bytes(n_valid, 1024), st, p);
-  else if (nt == 512) ce = launch_select_nt<512>(grid, sel_smem_bytes(n_valid, 512), st, p);
-  else if (nt == 128) ce = launch_select_nt<128>(grid, sel_smem_bytes(n_valid, 128), st, p);
-  else ce = launch_select_nt<256>(grid, sel_smem_bytes(n_valid, 256), st, p);
+  ce = run_select(nt, grid, sel_smem_bytes(n_valid, nt), st, p);
   if (ce != cudaSuccess) return cuda_check(ce, "topk_select launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_check(cudaGetLastError(), "topk_select launch");
@@ -543,7 +429,7 @@ int launch_block_select(const hylra_geometry* g, const float* scores, int n_slot
                         const void* k, const int32_t* layer_ids, float* bscores,
                         int32_t* blocks_out, int bk_stride, int32_t* tokens_out,
                         int tok_stride, int32_t* counts_out, int32_t* info, int* flags,
-                        cudaStream_t st) {
+                        cudaStream_t st, int32_t* idx_mirror = nullptr) {
   if (block_size < 1) return fail(HYLRA_ERR_INVALID_INPUT, "block_size must be >= 1");
   if (block_budget < 1)
     return fail(HYLRA_ERR_INVALID_INPUT, "block_budget must be >= 1, got %d", block_budget);
@@ -580,7 +466,8 @@ int launch_block_select(const hylra_geometry* g, const float* scores, int n_slot
   br.row_stride = nb_stride_of(nb);
   br.tok_scores = scores;
   if (int e = launch_select(g, bscores, n_slots, nb, block_budget, sel_group, q, k, layer_ids,
-                            blocks_out, bk_stride, info, flags, st, br))
+                            blocks_out, bk_stride, info, flags, st, br, nullptr, nullptr, 0,
+                            idx_mirror))
     return e;
   if (tokens_out) {
     block_expand_kernel<<<n_slots * g->batch * groups, kPoolThreads, 0, st>>>(
@@ -600,7 +487,10 @@ struct StepLayout {
   size_t off_aug = 0, off_aug_counts = 0;
   size_t off_scores, off_attn, attn_bytes, off_attn_r, attn_bytes_r, total;
   size_t off_sync = 0;  // single-launch step: ticket / done counters + selection ready flags
+  size_t off_ctr_f = 0, off_ctr_r = 0;  // split-K counters of the FULL / REUSE launches
   int n_ready = 0;
+  int* ctr_f(uint8_t* w) const { return reinterpret_cast<int*>(w + off_ctr_f); }
+  int* ctr_r(uint8_t* w) const { return reinterpret_cast<int*>(w + off_ctr_r); }
 };
 
 int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, int budget,
@@ -630,7 +520,17 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
     return fail(HYLRA_ERR_CONFIGURATION, "more than %d layers of one kind", kMaxSlots);
   s->n_groups = g->kv_heads / sel_group;
   const size_t nf = s->full_ids.size();
-  s->off_scores = kHeader;
+  // Layout: every word a kernel expects to find zeroed (the single-launch sync words, the
+  // split-K counters) comes first, at offsets that depend only on the geometry and the
+  // policy; everything sized by n_valid (block / augmentation rows, split-K partials)
+  // follows. A decoder stepping over a growing cache reuses its workspace across many
+  // n_valid values, and a counter that landed on an earlier step's partials would never
+  // fire its merge.
+  s->n_ready = (int)(nf * g->batch * s->n_groups);
+  s->off_sync = kHeader;  // ticket / done, then ready flags and group counters [n_ready] each
+  s->off_ctr_f = align_up(s->off_sync + 256 + 2 * sizeof(int) * (size_t)s->n_ready, 256);
+  s->off_ctr_r = s->off_ctr_f + counter_region_bytes(g);
+  s->off_scores = s->off_ctr_r + counter_region_bytes(g);
   const size_t scores_b = sizeof(float) * nf * g->batch * g->kv_heads * scores_row_stride(g);
   size_t off = align_up(s->off_scores + scores_b, 256);
   if (block_size > 1) {
@@ -659,24 +559,21 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
       off = align_up(off + sizeof(int32_t) * rows, 256);
     }
   }
-  // FULL and REUSE get disjoint attention workspaces: each kernel's split-K counters must
-  // start at zero, and the other launch's partial buffers would otherwise overlap them.
+  // split-K partials of the FULL and REUSE launches (their counters are the fixed regions
+  // above). FULL layers may be launched in two groups (hylra_decode_step_ex with a side
+  // stream), REUSE layers in chunks (layer events): size for the largest any group needs
+  // (fewer pairs can mean more splits). Partials are always written before they are read.
   s->off_attn = off;
-  // FULL layers may be launched in two groups (hylra_decode_step_ex with a side stream)
   s->attn_bytes = 0;
   for (int n = 1; n <= (int)nf; ++n)
-    s->attn_bytes = std::max(s->attn_bytes, attn_layout(g, n, n_valid, false).total);
+    s->attn_bytes = std::max(s->attn_bytes, attn_layout(g, n, n_valid, false, true).total);
   s->off_attn_r = align_up(s->off_attn + s->attn_bytes, 256);
-  // REUSE layers may be launched in chunks (hylra_decode_step_events): size for the
-  // largest workspace any chunk length needs (fewer pairs can mean more splits).
   s->attn_bytes_r = 0;
   for (int n = 1; n <= (int)s->reuse_ids.size(); ++n)
     s->attn_bytes_r = std::max(
-        s->attn_bytes_r, attn_layout(g, n, s->aug_stride ? s->aug_stride : s->k_eff, true).total);
-  s->off_sync = align_up(s->off_attn_r + s->attn_bytes_r, 256);
-  s->n_ready = (int)(nf * g->batch * s->n_groups);
-  // ticket / done, then ready flags and selection-group counters [n_ready] each
-  s->total = align_up(s->off_sync + 256 + 2 * sizeof(int) * (size_t)s->n_ready, 256);
+        s->attn_bytes_r,
+        attn_layout(g, n, s->aug_stride ? s->aug_stride : s->k_eff, true, true).total);
+  s->total = align_up(s->off_attn_r + s->attn_bytes_r, 256);
   return HYLRA_OK;
 }
 
@@ -696,6 +593,16 @@ int device_view(const void* ptr, const void** dev, const char* what) {
   return HYLRA_OK;
 }
 
+// hylra_step_options idx_mirror (device or pinned host memory) as a device address.
+int mirror_view(const hylra_step_options* opt, int32_t** out) {
+  *out = nullptr;
+  if (!opt || !opt->idx_mirror) return HYLRA_OK;
+  const void* dev = nullptr;
+  if (int e = device_view(opt->idx_mirror, &dev, "idx_mirror")) return e;
+  *out = static_cast<int32_t*>(const_cast<void*>(dev));
+  return HYLRA_OK;
+}
+
 // One decode step: FULL layers (+ scores) -> SELECT -> [augment] -> REUSE layers. With
 // `split`, FULL layers read a compact device cache and REUSE layers a compact cache that
 // may live in page-locked host memory (index-guided offload: only selected rows cross the
@@ -710,12 +617,7 @@ int dispatch_step(const hylra_geometry* g, cudaStream_t st, const CUtensorMap& t
                   const SelectParams& sp, const StepSync& ss) {
   const int G = g->q_heads / g->kv_heads;
   cudaError_t ce;
-  if (g->head_dim == 128)
-    ce = G > 8 ? launch_step_mma<128, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
-               : launch_step_mma<128, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
-  else
-    ce = G > 8 ? launch_step_mma<64, true>(ss.n_items, st, tk, tv, pf, pr, sp, ss)
-               : launch_step_mma<64, false>(ss.n_items, st, tk, tv, pf, pr, sp, ss);
+  ce = run_step_mma(g->head_dim, G > 8, ss.n_items, st, tk, tv, pf, pr, sp, ss);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_check(ce, "single-launch step");
 }
@@ -740,6 +642,7 @@ struct StepOpts {
   cudaEvent_t fork = nullptr, select = nullptr, full = nullptr, join = nullptr;
   cudaEvent_t reuse_wait = nullptr;
   void* const* layer_events = nullptr;
+  int32_t* idx_mirror = nullptr;  // device address of the selections' second copy
 };
 
 int record(void* const* evs, int l, cudaStream_t st) {
@@ -750,16 +653,21 @@ int record(void* const* evs, int l, cudaStream_t st) {
 // The step's append option (hylra_step_options append_*): validated here; in_kernel fills
 // *ap for the single-launch kernel (its FULL items write the rows), else hylra_append_kv
 // runs ahead of the step on the same stream.
+int append_impl(const hylra_geometry* g, void* k, void* v, const void* k_rows,
+                const void* v_rows, int pos, int n_layers, const int32_t* layer_ids, int* flags,
+                cudaStream_t st);
+
 int step_append(const hylra_geometry* g, const void* k, const void* v, const void* rows_k,
                 const void* rows_v, int pos, int n_valid, bool in_kernel, StepAppend* ap,
-                cudaStream_t st) {
+                int* flags, cudaStream_t st) {
   if (!rows_k || !rows_v)
     return fail(HYLRA_ERR_CONFIGURATION, "append needs both append_k_rows and append_v_rows");
   if (pos < 0 || pos >= n_valid)
     return fail(HYLRA_ERR_INVALID_INPUT, "append_pos %d not in [0, n_valid=%d)", pos, n_valid);
   if (!in_kernel)
-    return hylra_append_kv(g, const_cast<void*>(k), const_cast<void*>(v), rows_k, rows_v, pos, 0,
-                           nullptr, st);
+    return append_impl(g, const_cast<void*>(k), const_cast<void*>(v), rows_k, rows_v, pos, 0,
+                       nullptr, flags, st);
+  ap->flags = flags;
   if (int e = device_view(rows_k, reinterpret_cast<const void**>(&ap->k_rows), "append_k_rows"))
     return e;
   if (int e = device_view(rows_v, reinterpret_cast<const void**>(&ap->v_rows), "append_v_rows"))
@@ -832,7 +740,8 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     return fail(HYLRA_ERR_CONFIGURATION, "append is not supported with split caches");
   StepAppend app{};
   if (appending)
-    if (int e = step_append(g, k, v, o.app_k, o.app_v, o.app_pos, n_valid, unified, &app, st))
+    if (int e = step_append(g, k, v, o.app_k, o.app_v, o.app_pos, n_valid, unified, &app, flags,
+                            st))
       return e;
   if (unified) {
     std::vector<int32_t> ab_ids(a_ids), ab_slot(a_slot), ab_kv(a_kv);
@@ -845,6 +754,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                     idx, k_stride, nullptr, flags, BlockRows(),
                                     split ? ab_kv.data() : nullptr, ab_slot.data()))
       return e;
+    sp.idx_mirror = o.idx_mirror;
     // sinks / recent: the final CTA of each pair also writes the augmented row
     const int32_t* ridx = idx;
     const int32_t* rcnt = nullptr;
@@ -865,7 +775,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     if (int e = make_attn_params(&pf, &lf, g, false, q, kf, vf, n_valid, n_valid, nf,
                                  ab_ids.data(), nullptr, nullptr, nullptr, 0, sel_group, out,
                                  scores, aws, s.attn_bytes, flags,
-                                 split ? ab_kv.data() : nullptr, nf))
+                                 split ? ab_kv.data() : nullptr, nf, s.ctr_f(w)))
       return e;
     pf.fuse_select = nf;
     const long items_f = (long)lf.splits * g->kv_heads * g->batch * nf;
@@ -877,7 +787,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                    split ? split->vr : v, n_valid, rk, nr,
                                    s.reuse_ids.data(), s.reuse_src.data(), ridx, rcnt, rstride,
                                    sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r,
-                                   flags, split ? rkv.data() : nullptr, nr))
+                                   flags, split ? rkv.data() : nullptr, nr, s.ctr_r(w)))
         return e;
       items_r = (long)lr.splits * g->kv_heads * g->batch * nr;
     }
@@ -918,7 +828,8 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     if (int e = launch_attention(g, false, q, kf, vf, n_valid, n_valid, n, gr.ids->data(),
                                  nullptr, nullptr, nullptr, 0, 1, out,
                                  scores + gr.score_base * score_slot, aws, s.attn_bytes, flags, sx,
-                                 split ? gr.kv->data() : nullptr, nf, fused, n_fused))
+                                 split ? gr.kv->data() : nullptr, nf, fused, n_fused, nullptr, 0,
+                                 0, s.ctr_f(w)))
       return e;
     for (int l : *gr.ids)
       if (int e = record(o.layer_events, l, sx)) return e;
@@ -928,7 +839,8 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
     return launch_select(g, scores + gr.score_base * score_slot, (int)gr.ids->size(), n_valid,
                          budget, sel_group, refine ? q : nullptr, refine ? kf : nullptr,
                          gr.ids->data(), idx, k_stride, nullptr, flags, sx, BlockRows(),
-                         split ? gr.kv->data() : nullptr, gr.slots->data(), force_nt);
+                         split ? gr.kv->data() : nullptr, gr.slots->data(), force_nt,
+                         o.idx_mirror);
   };
   auto reuse = [&](cudaStream_t sx) -> int {
     if (s.reuse_ids.empty()) return HYLRA_OK;
@@ -963,7 +875,8 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                    n_valid, rk, n, s.reuse_ids.data() + c0,
                                    s.reuse_src.data() + c0, ridx, rcnt, rstride, sel_group, out,
                                    nullptr, w + s.off_attn_r, s.attn_bytes_r, flags, sx,
-                                   split ? rkv.data() + c0 : nullptr, nr))
+                                   split ? rkv.data() + c0 : nullptr, nr, nullptr, 0, nullptr,
+                                   0, 0, s.ctr_r(w)))
         return e;
       if (int e = record(o.layer_events, l, sx)) return e;
       c0 = i + 1;
@@ -997,6 +910,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                     ab_ids.data(), idx, k_stride, nullptr, flags, BlockRows(),
                                     split ? ab_kv.data() : nullptr, ab_slot.data()))
       return e;
+    sp.idx_mirror = o.idx_mirror;
     if (int e = full(g_ab, st, &sp, (int)a_ids.size())) return e;
     if (!b_ids.empty()) {
       if (int e = rec(o.fork, st)) return e;
@@ -1038,16 +952,6 @@ bool block_tiles_off() {
 // ======================================================================== extern "C"
 extern "C" {
 
-#ifdef HYLRA_TRACE
-// diagnostics build only: the per-CTA trace buffer of the single-launch kernel (8 x int64
-// per ticket) or NULL
-int hylra_trace_set(void* buf) {
-  return cuda_check(cudaMemcpyToSymbol(hylra::g_trace, &buf, sizeof(buf)), "trace set");
-}
-int hylra_trace_set_select_info(void* buf) {
-  return cuda_check(cudaMemcpyToSymbol(hylra::g_sel_info, &buf, sizeof(buf)), "trace set");
-}
-#endif
 
 int hylra_abi_version(void) { return HYLRA_ABI_VERSION; }
 
@@ -1147,6 +1051,7 @@ int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, 
     o.join = static_cast<cudaEvent_t>(opt->join_event);
     o.reuse_wait = static_cast<cudaEvent_t>(opt->reuse_wait_event);
     o.layer_events = opt->layer_events;
+    if (int e = mirror_view(opt, &o.idx_mirror)) return e;
   }
   return decode_step_impl(g, q, k, v, n_valid, actions, budget, sel_group, refine, sinks, recent,
                           out, idx, k_stride, ws, ws_bytes, stream, nullptr, o);
@@ -1175,6 +1080,70 @@ int hylra_decode_step_offload(const hylra_geometry* g, const void* q, const void
 int hylra_append_kv(const hylra_geometry* g, void* k, void* v, const void* k_rows,
                     const void* v_rows, int pos, int n_layers, const int32_t* layer_ids,
                     void* stream) {
+  return append_impl(g, k, v, k_rows, v_rows, pos, n_layers, layer_ids, nullptr,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int hylra_append_kv_checked(const hylra_geometry* g, void* k, void* v, const void* k_rows,
+                            const void* v_rows, int pos, int n_layers, const int32_t* layer_ids,
+                            void* ws, void* stream) {
+  if (!ws) return fail(HYLRA_ERR_CONFIGURATION, "NULL workspace");
+  return append_impl(g, k, v, k_rows, v_rows, pos, n_layers, layer_ids, static_cast<int*>(ws),
+                     static_cast<cudaStream_t>(stream));
+}
+
+int hylra_check_cache(const hylra_geometry* g, const void* k, const void* v, int n_valid,
+                      int n_layers, const int32_t* layer_ids, void* ws, void* stream) {
+  if (int e = check_geometry(g)) return e;
+  if (!k || !v || !ws) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
+  if (n_valid < 1 || n_valid > g->capacity)
+    return fail(HYLRA_ERR_INVALID_INPUT, "n_valid %d not in [1, capacity=%d]", n_valid,
+                g->capacity);
+  const int L = layer_ids ? n_layers : g->num_layers;
+  if (L < 1 || L > kMaxSlots)
+    return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", L, kMaxSlots);
+  CheckParams p{};
+  const int es = g->dtype == HYLRA_BF16 ? 2 : 4;
+  const int64_t bytes = (int64_t)n_valid * g->head_dim * es;
+  if (bytes % 16 || (g->kv_stride_layer * es) % 16 || (g->kv_stride_batch * es) % 16 ||
+      (g->kv_stride_head * es) % 16 || reinterpret_cast<uintptr_t>(k) % 16 ||
+      reinterpret_cast<uintptr_t>(v) % 16)
+    return fail(HYLRA_ERR_CONFIGURATION, "cache check needs 16-byte aligned rows and strides");
+  p.k = static_cast<const uint8_t*>(k);
+  p.v = static_cast<const uint8_t*>(v);
+  p.flags = static_cast<int*>(ws);
+  p.kv_sl = g->kv_stride_layer * es;
+  p.kv_sb = g->kv_stride_batch * es;
+  p.kv_sh = g->kv_stride_head * es;
+  p.block_chunks = bytes / 16;
+  p.B = g->batch;
+  p.Hkv = g->kv_heads;
+  p.bf16 = g->dtype == HYLRA_BF16;
+  p.n_layers = L;
+  for (int i = 0; i < L; ++i) {
+    const int l = layer_ids ? layer_ids[i] : i;
+    if (l < 0 || l >= g->num_layers)
+      return fail(HYLRA_ERR_CONFIGURATION, "layer id %d out of range", l);
+    p.layers[i] = l;
+  }
+  // a few waves of CTAs over all blocks
+  const int64_t blocks = 2ll * L * g->batch * g->kv_heads;
+  if (blocks > 65535) return fail(HYLRA_ERR_CONFIGURATION, "too many cache blocks to check");
+  const int64_t per_cta = (int64_t)kCheckThreads * kCheckUnroll;
+  const int64_t want = std::max<int64_t>(1, 8ll * num_sms() * 8 / blocks);
+  const int gx = (int)std::min<int64_t>(want, (p.block_chunks + per_cta - 1) / per_cta);
+  check_finite_kernel<<<dim3(gx, (unsigned)blocks), kCheckThreads, 0,
+                        static_cast<cudaStream_t>(stream)>>>(p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_check(cudaGetLastError(), "cache check launch");
+}
+
+}  // extern "C"
+
+namespace {
+int append_impl(const hylra_geometry* g, void* k, void* v, const void* k_rows,
+                const void* v_rows, int pos, int n_layers, const int32_t* layer_ids, int* flags,
+                cudaStream_t st) {
   if (int e = check_geometry(g)) return e;
   if (!k || !v) return fail(HYLRA_ERR_CONFIGURATION, "NULL cache pointer");
   if (pos < 0 || pos >= g->capacity)
@@ -1211,10 +1180,15 @@ int hylra_append_kv(const hylra_geometry* g, void* k, void* v, const void* k_row
   }
   const int64_t total = 2ll * L * g->batch * g->kv_heads * p.chunks;
   const unsigned blocks = (unsigned)((total + kAppendThreads - 1) / kAppendThreads);
-  append_kv_kernel<<<blocks, kAppendThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  p.flags = flags;
+  p.bf16 = g->dtype == HYLRA_BF16;
+  append_kv_kernel<<<blocks, kAppendThreads, 0, st>>>(p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_check(cudaGetLastError(), "append launch");
 }
+}  // namespace
+
+extern "C" {
 
 int hylra_augment_selection(const int32_t* idx, int rows, int k_eff, int k_stride, int n_valid,
                             int sinks, int recent, int32_t* out, int out_stride,
@@ -1290,11 +1264,13 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
   const int nb = (n_valid + block_size - 1) / block_size;
   const bool single = opt && opt->fuse_select == 2 && sel_group == 1 && use_mma_path(g) &&
                       fused_select_fits(g, nb);
+  int32_t* mirror = nullptr;
+  if (int e = mirror_view(opt, &mirror)) return e;
   // the step's new K/V rows: written by the single-launch kernel, else appended ahead
   StepAppend app{};
   if (opt && (opt->append_k_rows || opt->append_v_rows))
     if (int e = step_append(g, k, v, opt->append_k_rows, opt->append_v_rows, opt->append_pos,
-                            n_valid, single, &app, st))
+                            n_valid, single, &app, flags, st))
       return e;
   // single-launch block step (fuse_select = 2): the final CTA of every FULL pair pools its
   // row into blocks, selects them and writes the token coverage the REUSE items gather
@@ -1319,6 +1295,7 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
                                     ab_ids.data(), blocks, bk_stride, nullptr, flags, br, nullptr,
                                     ab_slot.data()))
       return e;
+    sp.idx_mirror = mirror;
     sp.cov_tokens = toks;
     sp.cov_counts = cnts;
     sp.cov_stride = s.tok_stride;
@@ -1326,7 +1303,7 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
     AttnLayout lf{}, lr{};
     if (int e = make_attn_params(&pf, &lf, g, false, q, k, v, n_valid, n_valid, nf, ab_ids.data(),
                                  nullptr, nullptr, nullptr, 0, 1, out, scores, w + s.off_attn,
-                                 s.attn_bytes, flags, nullptr, 0))
+                                 s.attn_bytes, flags, nullptr, 0, s.ctr_f(w)))
       return e;
     pf.fuse_select = nf;
     const long items_f = (long)lf.splits * g->kv_heads * g->batch * nf;
@@ -1335,7 +1312,7 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
       if (int e = make_attn_params(&pr, &lr, g, true, q, k, v, n_valid, s.k_eff, nr,
                                    s.reuse_ids.data(), s.reuse_src.data(), toks, cnts,
                                    s.tok_stride, 1, out, nullptr, w + s.off_attn_r,
-                                   s.attn_bytes_r, flags, nullptr, 0))
+                                   s.attn_bytes_r, flags, nullptr, 0, s.ctr_r(w)))
         return e;
       items_r = (long)lr.splits * g->kv_heads * g->batch * nr;
     }
@@ -1355,13 +1332,13 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
   }
   if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, nf, s.full_ids.data(), nullptr,
                                nullptr, nullptr, 0, 1, out, scores, w + s.off_attn, s.attn_bytes,
-                               flags, st))
+                               flags, st, nullptr, 0, nullptr, 0, nullptr, 0, 0, s.ctr_f(w)))
     return e;
   if (int e = launch_block_select(g, scores, nf, n_valid, block_budget, block_size, sel_group,
                                   refine ? q : nullptr, refine ? k : nullptr, s.full_ids.data(),
                                   reinterpret_cast<float*>(w + s.off_bscores), blocks, bk_stride,
                                   s.reuse_ids.empty() ? nullptr : toks, s.tok_stride, cnts,
-                                  nullptr, flags, st))
+                                  nullptr, flags, st, mirror))
     return e;
   if (!s.reuse_ids.empty()) {
     // whole blocks of 64-row multiples can stream as TMA tiles (the coverage rows are
@@ -1371,7 +1348,7 @@ int hylra_decode_step_blocks_ex(const hylra_geometry* g, const void* q, const vo
                                  s.reuse_ids.data(), s.reuse_src.data(), toks, cnts, s.tok_stride,
                                  sel_group, out, nullptr, w + s.off_attn_r, s.attn_bytes_r, flags,
                                  st, nullptr, 0, nullptr, 0, tiles ? blocks : nullptr, bk_stride,
-                                 block_size))
+                                 block_size, s.ctr_r(w)))
       return e;
   }
   return HYLRA_OK;
@@ -1398,13 +1375,9 @@ int hylra_overlap_counts(const int32_t* idx, int steps, int layers, int rows, in
   chunk = std::max(32, chunk & ~31);
   const size_t smem = (size_t)layers * (chunk / 32) * 4 + n_pairs * sizeof(int);
   if (smem > 220 * 1024) return fail(HYLRA_ERR_CONFIGURATION, "too many layers (%d)", layers);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(overlap_counts_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  });
-  if (attr_err != cudaSuccess) return cuda_check(attr_err, "overlap attribute");
+  if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(overlap_counts_kernel),
+                                      220 * 1024))
+    return cuda_check(e, "overlap attribute");
   dim3 grid(rows, steps);
   overlap_counts_kernel<<<grid, kOvThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       idx, layers, rows, k, k_stride, n_tokens, chunk, counts);
@@ -1423,8 +1396,9 @@ int hylra_read_flags(const void* ws, int32_t* flags_host, void* stream) {
 
 int hylra_clear_flags(void* ws, void* stream) {
   if (!ws) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
-  return cuda_check(cudaMemsetAsync(ws, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)),
-                    "clear flags");
+  return cuda_check(
+      cudaMemsetAsync(ws, 0, 2 * sizeof(int32_t), static_cast<cudaStream_t>(stream)),
+      "clear flags");
 }
 
 }  // extern "C"

@@ -1,0 +1,114 @@
+// launch.cuh — host-side launch plumbing shared by the translation units of libhylra.so:
+// per-device attributes and SM count, programmatic dependent launch, and the entry points
+// of the kernel translation units (k_full.cu, k_reuse.cu, k_simt.cu, k_step.cu, k_select.cu).
+// Each kernel template is instantiated in exactly one of those units so the library builds
+// in parallel; hylra_abi.cu holds the host logic and the extern "C" surface.
+#pragma once
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "attention.cuh"
+#include "select.cuh"
+
+namespace hylra {
+namespace host {
+
+// Per-device facts and function attributes. The library may drive several devices from one
+// process (one host thread per GPU, or one thread switching devices), so nothing
+// device-specific is cached per process: the SM count is read from the current device and
+// the dynamic shared-memory opt-in (cudaFuncSetAttribute applies per device context) is
+// made once per (kernel, device).
+inline int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  return dev;
+}
+
+inline int num_sms() {
+  static std::mutex mu;
+  static std::map<int, int> sms;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 148;  // B200; only reached without a usable device (the launch then fails loudly)
+  }
+  sms[dev] = n;
+  return n;
+}
+
+inline cudaError_t ensure_smem_attr(const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  const auto key = std::make_pair(func, current_device());
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= smem) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done[key] = smem;
+  return e;
+}
+// ------------------------------------------------------------------ launches
+// Programmatic dependent launch for the step's kernels (FULL, SELECT, REUSE): each may be
+// scheduled while its predecessor drains (the kernels wait on griddepcontrol before
+// touching memory). HYLRA_PDL=0 turns it off.
+inline bool pdl_enabled() {
+  static int v = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_PDL");
+    v = (e && *e) ? (atoi(e) != 0) : 1;
+  });
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// ------------------------------------------------------------------ kernel tables
+template <int D, bool GATHER, bool GBIG>
+constexpr int mma_stages() {
+  return D == 128 ? 3 : 5;
+}
+template <int D, bool GATHER, bool GBIG>
+constexpr size_t mma_smem_bytes() {
+  return (size_t)mma_stages<D, GATHER, GBIG>() * MmaSmem<D>::kStageBytes + 1024 + 256 +
+         (GATHER ? kIdxStage * sizeof(int32_t) : 0);
+}
+
+// Kernel-unit entry points (each defined in its own translation unit).
+cudaError_t run_attn_mma(int D, bool gather, bool big, dim3 grid, cudaStream_t st,
+                         const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p,
+                         const SelectParams& sp);
+cudaError_t run_attn_simt(bool f32, bool gather, int D, int G, dim3 grid, cudaStream_t st,
+                          const AttnParams& p);
+cudaError_t run_step_mma(int D, bool big, int n_items, cudaStream_t st, const CUtensorMap& tk,
+                         const CUtensorMap& tv, const AttnParams& pf, const AttnParams& pr,
+                         const SelectParams& sp, const StepSync& ss);
+cudaError_t run_select(int nt, dim3 grid, size_t smem, cudaStream_t st, const SelectParams& p);
+
+}  // namespace host
+}  // namespace hylra

@@ -45,6 +45,8 @@ __host__ __device__ constexpr int sel_chunk() { return NT * 32; }  // tokens per
 struct SelectParams {
   const float* scores;  // [slot][b][kh][row_stride]
   int32_t* idx;         // [slot][b][grp][k_stride]
+  int32_t* idx_mirror;  // optional second copy of idx (same layout), e.g. pinned host memory
+                        // the caller reads after the step: stored alongside idx, no copy
   int32_t* info;        // [row][8] or null
   int* flags;
   const void* q;        // refinement inputs (null: refinement off)
@@ -99,7 +101,7 @@ __host__ __device__ constexpr size_t sel_smem_bytes(int n, int nt, bool big = fa
 #ifdef HYLRA_TRACE
 // diagnostics build only: per-row phase cycles of selections that have no info buffer
 // (the fused ones), [row][8] as SelectParams::info
-__device__ int32_t* g_sel_info;
+static __device__ int32_t* g_sel_info;
 #endif
 
 struct SelSmem {
@@ -127,6 +129,14 @@ __device__ __forceinline__ SelSmem carve(uint8_t* base, int n) {
 }
 
 // ----------------------------------------------------------------------------- helpers
+// A row whose float64 refinement window held more than kCandCap scores: its boundary
+// follows fp32 order (ties to the lower index) instead of the reference's float64 order.
+// Flag bit 4 plus a count of such rows in the word after the flag word (hylra.h).
+__device__ __forceinline__ void refine_skipped(int* flags) {
+  atomicOr(flags, 4);
+  atomicAdd(flags + 1, 1);
+}
+
 struct Red {
   int i[kSelMaxWarps];
   float f[kSelMaxWarps];
@@ -312,7 +322,7 @@ __device__ __forceinline__ double elem_f64(const void* p, int64_t i) {
 // token (lane sub handles dims sub, sub + kLpt, ...), so a warp scores kTpw tokens at once;
 // every lane of the warp must call it (sub-group shuffles).
 constexpr int kLpt = 8, kTpw = 32 / kLpt;
-__device__ double token_score_f64(const SelectParams& p, int layer, int kvl, int b, int grp,
+static __device__ double token_score_f64(const SelectParams& p, int layer, int kvl, int b, int grp,
                                   int tok) {
   const int sub = threadIdx.x & (kLpt - 1);
   const double sqd = sqrt((double)p.D);
@@ -536,7 +546,7 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
     a = block_sum_int<NT>(ca, red);
     z = block_sum_int<NT>(cz, red);
     if (z - a > kCandCap) {
-      if (tid == 0) atomicOr(p.flags, 4);
+      if (tid == 0) refine_skipped(p.flags);
       a = z = k;
     }
   }
@@ -571,6 +581,7 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
   const int n4 = (n + 3) >> 2;
   const int row_id = (p.out_slot[slot] * p.B + b) * p.n_groups + grp;
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
+  int32_t* mir = p.idx_mirror ? p.idx_mirror + (int64_t)row_id * p.k_stride : nullptr;
   int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
 #ifdef HYLRA_TRACE
   if (info == nullptr && g_sel_info != nullptr) info = g_sel_info + row_id * 8;
@@ -595,6 +606,7 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
     for (int i = tid; i < n; i += NT) {
       nanacc = fmaf(rd.at(i), 0.f, nanacc);
       out[i] = i;
+      if (mir) mir[i] = i;
     }
     if (block_sum_int<NT>(nanacc != nanacc ? 1 : 0, red) && tid == 0) atomicOr(p.flags, 2);
     if (info && tid == 0) {
@@ -1082,7 +1094,7 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       nw = red.misc[5];
       if (nw > kCandCap) {
         // the window cannot be held: resolve the exact fp32 ties at T by index order
-        if (refine && tid == 0) atomicOr(p.flags, 4);
+        if (refine && tid == 0) refine_skipped(p.flags);
         if (refine) {
           for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
           sel_sync<NT>();
@@ -1142,7 +1154,10 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
     while (m) {
       const int bit = __ffs(m) - 1;
       m &= m - 1;
-      if (pos < k) out[pos] = tid * 32 + bit;
+      if (pos < k) {
+        out[pos] = tid * 32 + bit;
+        if (mir) mir[pos] = tid * 32 + bit;
+      }
       ++pos;
     }
     run = tot;
@@ -1164,7 +1179,11 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
       while (m) {
         const int bit = __ffs(m) - 1;
         m &= m - 1;
-        if (pos < k) out[pos] = (c0 + j) * kChunk + tid * 32 + bit;
+        if (pos < k) {
+          const int tok = (c0 + j) * kChunk + tid * 32 + bit;
+          out[pos] = tok;
+          if (mir) mir[pos] = tok;
+        }
         ++pos;
       }
       run += (int)((tot[j >> 1] >> (16 * (j & 1))) & 0xffffu);

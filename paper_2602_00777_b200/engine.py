@@ -232,7 +232,8 @@ class HybridDecoder:
             g, self._acts, int(n_valid), self.budget, self.sel_group, self.sinks, self.recent))
 
     def step(self, q: torch.Tensor, n_valid: int | None = None, *, layer_events=None,
-             reuse_wait=None, out: torch.Tensor | None = None, append=None) -> StepResult:
+             reuse_wait=None, out: torch.Tensor | None = None, append=None,
+             idx_out: torch.Tensor | None = None) -> StepResult:
         """Enqueue one decode step. layer_events (optional, L torch.cuda.Event or None):
         event l is recorded once out[l] is final, REUSE layers being launched in chunks
         that end at the evented layers; reuse_wait (optional event): the REUSE launches
@@ -242,7 +243,16 @@ class HybridDecoder:
         append (optional): (k_rows, v_rows, pos) — this step's new K/V rows
         [L, B, Hkv, d] (device or pinned host, cache dtype), written at cache row pos
         (< n_valid) before they are read; the single-launch step writes them inside its one
-        kernel (hylra_step_options append_*)."""
+        kernel (hylra_step_options append_*).
+        idx_out (optional): int32 tensor shaped like the decoder's selections
+        [n_full, B, groups, k_stride], device or pinned host memory, that receives a second
+        copy of every selection as the selecting CTAs write it (hylra_step_options
+        idx_mirror): the per-layer index sets reach the host with no copy after the step."""
+        if idx_out is not None:
+            if idx_out.shape != self.idx.shape or idx_out.dtype != torch.int32 \
+                    or not idx_out.is_contiguous() or not (idx_out.is_cuda or idx_out.is_pinned()):
+                raise ConfigurationError("idx_out must be a contiguous int32 tensor shaped like "
+                                         "the selections, on the device or pinned on the host")
         if out is not None:
             if out.shape != self.out.shape or out.dtype != torch.float32 \
                     or not out.is_contiguous() or not (out.is_cuda or out.is_pinned()):
@@ -252,7 +262,7 @@ class HybridDecoder:
             self.out = out
             try:
                 return self.step(q, n_valid, layer_events=layer_events, reuse_wait=reuse_wait,
-                                 append=append)
+                                 append=append, idx_out=idx_out)
             finally:
                 self.out = own
         g = self._geometry(q)
@@ -265,8 +275,7 @@ class HybridDecoder:
                     f"{len(layer_events)} layer events for {len(self.actions)} layers")
             need = int(lib.hylra_decode_step_workspace_bytes(
                 g, self._acts, n_valid, self.budget, self.sel_group, self.sinks, self.recent))
-            if self.ws.numel() < need:
-                self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
+            self._grow_ws(need)
             opt = _abi.StepOptions()
             if self.single:
                 opt.fuse_select = 2
@@ -278,6 +287,8 @@ class HybridDecoder:
             if reuse_wait is not None:
                 opt.reuse_wait_event = reuse_wait.cuda_event
             self._append_option(opt, append)
+            if idx_out is not None:
+                opt.idx_mirror = idx_out.data_ptr()
             evs = None
             if layer_events is not None:
                 evs = _abi.pointer_array(e.cuda_event if e is not None else None
@@ -296,11 +307,12 @@ class HybridDecoder:
         if self.block_size > 1:
             need = int(lib.hylra_decode_step_blocks_workspace_bytes(
                 g, self._acts, n_valid, self.budget, self.block_size, self.sel_group))
-            if self.ws.numel() < need:
-                self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k.device)
+            self._grow_ws(need)
             opt = _abi.StepOptions()
             opt.fuse_select = 2 if self.single else 0
             self._append_option(opt, append)
+            if idx_out is not None:
+                opt.idx_mirror = idx_out.data_ptr()
             _abi.check(lib.hylra_decode_step_blocks_ex(
                 g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, self._acts,
                 self.budget, self.block_size, self.sel_group, int(self.refine),
@@ -309,6 +321,13 @@ class HybridDecoder:
             bb = min(self.budget, -(-n_valid // self.block_size))
             return StepResult(self.out, self.idx[..., :bb], self.slot_of_layer,
                               self.full_layers)
+
+    def _grow_ws(self, need: int) -> None:
+        """Grow the (zero-filled) workspace to `need` bytes, keeping the flag words."""
+        if self.ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device=self.ws.device)
+            ws[:8].copy_(self.ws[:8])
+            self.ws = ws
 
     def _append_option(self, opt, append) -> None:
         """hylra_step_options append_* from step(append=(k_rows, v_rows, pos))."""
@@ -335,32 +354,53 @@ class HybridDecoder:
                 raise ConfigurationError("new rows must be contiguous [L, B, Hkv, d] device or "
                                          "pinned host tensors of the cache dtype")
         ids = list(range(L)) if layers is None else list(layers)
+        # the new rows are validated as they are written (a NaN / inf sets the cache flag,
+        # raised by check_flags as NumericInputError, attention.py:43-44)
+        _abi.check(_abi.lib().hylra_append_kv_checked(
+            self._cache_geometry(), self.k.data_ptr(), self.v.data_ptr(), k_rows.data_ptr(),
+            v_rows.data_ptr(), int(pos), len(ids), _abi.int32_array(ids), self.ws.data_ptr(),
+            torch.cuda.current_stream(self.k.device).cuda_stream))
+
+    def _cache_geometry(self):
+        L, B, Hkv, cap, d = self.k.shape
         g = _abi.Geometry()
         g.batch, g.q_heads, g.kv_heads, g.head_dim = B, self.q_heads, Hkv, d
         g.capacity, g.num_layers = cap, L
         g.dtype = _abi.HYLRA_BF16 if self.k.dtype == torch.bfloat16 else _abi.HYLRA_F32
         g.kv_stride_layer, g.kv_stride_batch, g.kv_stride_head = self.k.stride()[:3]
-        _abi.check(_abi.lib().hylra_append_kv(
-            g, self.k.data_ptr(), self.v.data_ptr(), k_rows.data_ptr(), v_rows.data_ptr(),
-            int(pos), len(ids), _abi.int32_array(ids),
-            torch.cuda.current_stream(self.k.device).cuda_stream))
+        return g
+
+    def validate_cache(self, n_valid: int | None = None) -> None:
+        """Reject a cache holding NaN / inf in rows [0, n_valid) of any layer, as the
+        reference does when it builds its float64 caches (attention.py:38-46,61-71):
+        NumericInputError. One streaming pass over the cache (hylra_check_cache; ~5 ms for
+        config 2 at B=8), synchronising; appended rows are checked as they are written."""
+        L, B, Hkv, cap, d = self.k.shape
+        n = cap if n_valid is None else int(n_valid)
+        flags = torch.zeros(64, dtype=torch.int32, device=self.k.device)
+        _abi.check(_abi.lib().hylra_check_cache(
+            self._cache_geometry(), self.k.data_ptr(), self.v.data_ptr(), n, L, None,
+            flags.data_ptr(), torch.cuda.current_stream(self.k.device).cuda_stream))
+        _abi.raise_for_flags(flags[:2].tolist())
 
     def flags(self) -> int:
         """Device flag word (synchronises)."""
         return int(self.ws[:4].view(torch.int32).item())
 
-    def check_flags(self) -> None:
-        f = self.flags()
-        if f & _abi.FLAG_INDEX_OUT_OF_RANGE:
-            raise InvalidSelectionError("a selection index is out of range for the cache")
-        if f & _abi.FLAG_NON_FINITE_SCORE:
-            raise NumericInputError("selection scores contain non-finite entries")
-        if f & _abi.FLAG_INTERNAL:
-            from .errors import CudaError
-            raise CudaError("a selection kernel invariant failed (internal error)")
+    def refine_skipped_rows(self) -> int:
+        """Selection rows, since the last clear_flags, whose k-th boundary followed fp32
+        order because the float64 refinement window held too many scores (synchronises)."""
+        return int(self.ws[4:8].view(torch.int32).item())
+
+    def check_flags(self, strict: bool = False) -> None:
+        """Raise the reference exception a kernel flagged (out-of-range index:
+        InvalidSelectionError, non-finite input: NumericInputError). A selection whose
+        float64 refinement was skipped warns (SelectionPrecisionWarning), or raises
+        InvalidSelectionError with strict=True."""
+        _abi.raise_for_flags(self.ws[:8].view(torch.int32).tolist(), strict)
 
     def clear_flags(self) -> None:
-        self.ws[:4].zero_()
+        self.ws[:8].zero_()
 
 
 class OffloadDecoder(HybridDecoder):
@@ -425,8 +465,7 @@ class OffloadDecoder(HybridDecoder):
         st = torch.cuda.current_stream(self.k_full.device).cuda_stream
         need = int(lib.hylra_decode_step_workspace_bytes(
             g, self._acts, n_valid, self.budget, self.sel_group, self.sinks, self.recent))
-        if self.ws.numel() < need:
-            self.ws = torch.zeros(need, dtype=torch.uint8, device=self.k_full.device)
+        self._grow_ws(need)
         kr = self.k_reuse.data_ptr() if self.k_reuse is not None else None
         vr = self.v_reuse.data_ptr() if self.v_reuse is not None else None
         _abi.check(lib.hylra_decode_step_offload(
@@ -553,9 +592,11 @@ class DecodeLoop:
 
     Per step: the query [L, B, Hq, d] and the new token's key/value rows [L, B, Hkv, d]
     come from pinned host buffers (`q_host`, `k_host`, `v_host`), the K/V rows are
-    appended at cache row `pos`, the hybrid step runs over `pos + 1` rows, and the fp32
-    outputs land in the pinned `out_host`. Fill the host buffers, call `run()`; it returns
-    `out_host` after the step completed.
+    appended at cache row `pos`, the hybrid step runs over `pos + 1` rows, the fp32
+    outputs land in the pinned `out_host` and the per-layer top-k index sets in the pinned
+    `sel_host` ([n_full, B, groups, k]; a REUSE layer's set is its source slot's,
+    `slot_of_layer`). Fill the host buffers, call `run()`; it returns `out_host` after the
+    step completed.
 
     zero_copy=True (HybridDecoder): no copy operations at all — hylra_append_kv
     reads the new rows from pinned host memory in place (the FULL layers' rows before the
@@ -578,9 +619,14 @@ class DecodeLoop:
         self.k_host = torch.zeros((L, B, Hkv, d), dtype=dt).pin_memory()
         self.v_host = torch.zeros((L, B, Hkv, d), dtype=dt).pin_memory()
         self.out_host = torch.zeros((L, B, Hq, d), dtype=torch.float32).pin_memory()
+        self.sel_host = torch.zeros(tuple(decoder.idx.shape), dtype=torch.int32).pin_memory()
         self.graph = None
         self.h2d_bytes = (self.q_host.numel() + 2 * self.k_host.numel()) * self.q_host.element_size()
-        self.d2h_bytes = self.out_host.numel() * 4
+        # outputs + the index sets (k_eff of each selection row's k_stride entries)
+        n_sel = decoder.idx[..., 0].numel()
+        k_eff = (min(decoder.budget, pos + 1) if decoder.block_size == 1
+                 else min(decoder.budget, -(-(pos + 1) // decoder.block_size)))
+        self.d2h_bytes = self.out_host.numel() * 4 + n_sel * k_eff * 4
         self.zero_copy = bool(zero_copy) and type(decoder) is HybridDecoder
         if not self.zero_copy:
             self.q_dev = torch.zeros((L, B, Hq, d), dtype=dt, device=k.device)
@@ -602,6 +648,10 @@ class DecodeLoop:
             # the REUSE launch waits on them (hylra_decode_step_ex reuse_wait_event)
             self.ev_rows = torch.cuda.Event()
             self.ev_rows.record()  # torch creates events lazily
+            # the query copy on the side stream: the step waits for it (ev_q), the REUSE
+            # rows' append behind it on the same side stream does not hold the step up
+            self.ev_q = torch.cuda.Event()
+            self.ev_q.record()
 
     def _body(self, q_copy: bool = False):
         dec, pos = self.dec, self.pos
@@ -612,20 +662,21 @@ class DecodeLoop:
                 self.side.wait_stream(main)
                 with torch.cuda.stream(self.side):
                     self.q_dev.copy_(self.q_host, non_blocking=True)
+                    self.ev_q.record(self.side)
                 q = self.q_dev
+            io = dict(out=self.out_host, idx_out=self.sel_host)
             if dec.single or dec.block_size > 1:
                 # the step's append option: the single-launch kernel writes the new rows
                 # itself (one launch); the block-mode multi-launch step appends them first
                 if q_copy:
-                    main.wait_stream(self.side)
-                dec.step(q, pos + 1, out=self.out_host,
-                         append=(self.k_host, self.v_host, pos))
+                    main.wait_event(self.ev_q)
+                dec.step(q, pos + 1, append=(self.k_host, self.v_host, pos), **io)
                 return
             if not self.reuse_layers:
                 dec.append(self.k_host, self.v_host, pos)
                 if q_copy:
-                    main.wait_stream(self.side)
-                dec.step(q, pos + 1, out=self.out_host)
+                    main.wait_event(self.ev_q)
+                dec.step(q, pos + 1, **io)
                 return
             if not q_copy:
                 self.side.wait_stream(main)
@@ -633,7 +684,11 @@ class DecodeLoop:
                 dec.append(self.k_host, self.v_host, pos, self.reuse_layers)
                 self.ev_rows.record(self.side)
             dec.append(self.k_host, self.v_host, pos, self.full_layers)
-            dec.step(q, pos + 1, out=self.out_host, reuse_wait=self.ev_rows)
+            if q_copy:
+                # every kernel of the step reads the queries: the step waits for their copy
+                # (the REUSE rows' append queued behind it keeps overlapping the FULL launch)
+                main.wait_event(self.ev_q)
+            dec.step(q, pos + 1, reuse_wait=self.ev_rows, **io)
             main.wait_stream(self.side)
             return
         self.q_dev.copy_(self.q_host, non_blocking=True)
@@ -642,6 +697,7 @@ class DecodeLoop:
         dec.append(self.kv_dev[0], self.kv_dev[1], pos)
         dec.step(self.q_dev, pos + 1)
         self.out_host.copy_(dec.out, non_blocking=True)
+        self.sel_host.copy_(dec.idx, non_blocking=True)
 
     def _graph(self, q_copy: bool):
         s = torch.cuda.Stream(device=self.dec.k.device)
@@ -732,6 +788,7 @@ def _run(model, actions, budget: int, steps: int, device, refine: bool, sinks: i
     H = cfg.heads
     dec = HybridDecoder(actions, k, v, budget, q_heads=H, sel_group=H, refine=refine,
                         include_sinks=sinks, include_recent=recent)
+    dec.validate_cache()  # attention.py:38-46: non-finite K/V -> NumericInputError
     outs, sels = [], []
     for t in range(steps):
         n_t = cfg.context_len + t
@@ -805,6 +862,7 @@ def hybrid_decode_blocks(model, policy, block_budget: int, block_size: int, step
     H = cfg.heads
     dec = HybridDecoder(actions, k, v, block_budget, q_heads=H, sel_group=H, refine=refine,
                         block_size=block_size)
+    dec.validate_cache()  # attention.py:38-46: non-finite K/V -> NumericInputError
     outs, sels = [], []
     for t in range(steps):
         res = dec.step(q[t], cfg.context_len + t)

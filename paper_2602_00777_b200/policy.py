@@ -20,6 +20,8 @@ __all__ = [
     "Action",
     "LayerPolicy",
     "dp_optimize",
+    "brute_force_policy",
+    "BRUTE_FORCE_MAX_LAYERS",
     "validate_policy",
     "static_jump_policy",
     "policy_from_actions",
@@ -156,6 +158,53 @@ def dp_optimize(matrix: SimilarityMatrix, theta: float) -> LayerPolicy:
             i = opened[j][2]
     actions = tuple(Action.FULL if s == j else Action.REUSE for j, s in enumerate(sources))
     return LayerPolicy(actions, tuple(sources), theta, best[0], best[1], matrix.sha256())
+
+
+# policy.py:36 — the exhaustive planner refuses larger stacks (2^(L-1) sequences)
+BRUTE_FORCE_MAX_LAYERS = 14
+
+
+def brute_force_policy(matrix: SimilarityMatrix, theta: float) -> LayerPolicy:
+    """Exhaustive planner (policy.py:226-270), the reference's cross-check of dp_optimize
+    (acceptance criterion 01, tests/test_acceptance.py:34-56).
+
+    Every feasible action sequence is visited by a depth-first walk that extends a prefix
+    one layer at a time (a REUSE step is taken only when it clears the inclusive
+    threshold, so infeasible prefixes are cut at their first violation instead of being
+    enumerated to the end). Credit is accumulated in ascending layer order along the walk,
+    as the reference sums it, and sequences compare by (FULL count, -credit, sources read
+    from the last layer down): the same objective and tie order as dp_optimize.
+    """
+    theta = _theta(theta)
+    L = matrix.num_layers
+    if L > BRUTE_FORCE_MAX_LAYERS:
+        raise InvalidInputError(
+            f"brute force is limited to {BRUTE_FORCE_MAX_LAYERS} layers, got {L}")
+    M = matrix.values
+    best = [None]  # (key, sources, fulls, credit)
+    sources = [0] * L
+
+    def walk(j: int, fulls: int, credit: float) -> None:
+        if j == L:
+            key = (fulls, -credit, tuple(reversed(sources)))
+            if best[0] is None or key < best[0][0]:
+                best[0] = (key, list(sources), fulls, credit)
+            return
+        # FULL at j
+        sources[j] = j
+        walk(j + 1, fulls + 1, credit + 1.0)
+        # REUSE at j: inherit layer j-1's source if the overlap clears theta
+        src = sources[j - 1]
+        m = float(M[j, src])
+        if m >= theta:
+            sources[j] = src
+            walk(j + 1, fulls, credit + m)
+
+    sources[0] = 0
+    walk(1, 1, 1.0)
+    _, srcs, fulls, credit = best[0]
+    actions = tuple(Action.FULL if s == j else Action.REUSE for j, s in enumerate(srcs))
+    return LayerPolicy(actions, tuple(srcs), theta, fulls, credit, matrix.sha256())
 
 
 def _strictly_better(a: tuple, b: tuple) -> bool:

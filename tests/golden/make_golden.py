@@ -20,6 +20,8 @@ Fixtures
                        and the summed logits.
   topk_cases.json      topk_of_logits on random, tied and saturated logit vectors.
   dp_cases.json        dp_optimize on random similarity matrices x theta grid.
+  brute_force_cases.json  brute_force_policy (policy.py:226-270) on random and quantised
+                       (exact-tie) matrices up to 12 layers x theta grid.
   artifacts/           versioned JSON artifacts WRITTEN BY THE REFERENCE (formats.py) for an
                        H=2 model (L6 d32 N96 seed21 rho0.85): decode-trace (+ sidecars,
                        block_size 4), similarity-matrix, layer-policy, decode-run (token and
@@ -225,6 +227,32 @@ def dp_cases():
     print("dp matrices:", len(out))
 
 
+def brute_force_cases():
+    rng = np.random.default_rng(7031)
+    out = []
+    for trial in range(60):
+        L = int(rng.integers(2, 13))
+        vals = np.zeros((L, L))
+        for j in range(L):
+            vals[j, j] = 1.0
+            for i in range(j):
+                vals[j, i] = float(rng.random())
+        if trial % 2 == 0:  # exact ties
+            vals = np.round(vals * 4) / 4
+            np.fill_diagonal(vals, 1.0)
+            vals[np.triu_indices(L, 1)] = 0.0
+        m = lr.SimilarityMatrix(values=vals, budget=8)
+        res = []
+        for theta in (0.0, 0.25, 0.5, 0.75, 1.0):
+            p = lr.brute_force_policy(m, theta)
+            res.append({"theta": theta, "actions": [a.value for a in p.actions],
+                        "sources": list(p.sources), "full_count": p.full_count,
+                        "cum_similarity": p.cum_similarity, "policy_sha": p.sha256()})
+        out.append({"values": vals.tolist(), "matrix_sha": m.sha256(), "results": res})
+    (HERE / "brute_force_cases.json").write_text(json.dumps(out))
+    print("brute-force matrices:", len(out))
+
+
 def artifacts_fixture():
     from layerreuse import formats as fm
     from layerreuse.synthetic import _S_PROBE, _rng
@@ -272,6 +300,10 @@ def artifacts_fixture():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # named fixtures only, e.g. `make_golden.py brute_force_cases`
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     engine_fixture()
     overlap_fixture()
     mha_fixture()
@@ -279,4 +311,5 @@ if __name__ == "__main__":
     cfg1_fixture()
     topk_cases()
     dp_cases()
+    brute_force_cases()
     artifacts_fixture()

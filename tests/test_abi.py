@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert sorted(_abi.EXPORTED_SYMBOLS) == declared
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.hylra_abi_version() == 5
+    assert lib.hylra_abi_version() == _abi.ABI_VERSION
     assert lib.hylra_status_string(3) == b"InvalidSelectionError"
 
 

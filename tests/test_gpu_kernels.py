@@ -318,6 +318,8 @@ def test_decode_loop_host_io_graph(zero_copy, single, q_copy):
         torch.cuda.synchronize()
         assert torch.equal(dec.idx, ref.selections)
         assert torch.equal(out, ref.outputs.cpu())
+        # the per-layer index sets reach the pinned host buffer in the same launch(es)
+        assert torch.equal(loop.sel_host, ref.selections.cpu())
 
 
 @pytest.mark.parametrize("actions", [

@@ -131,3 +131,34 @@ def test_matrix_hash_matches_reference_fixture(golden_dir):
     assert m.sha256() == str(z["matrix_sha"])
     p = dp_optimize(m, float(z["theta"]))
     assert p.sha256() == str(z["policy_sha"])
+
+
+def test_brute_force_policy_matches_reference_goldens(golden_dir):
+    """brute_force_policy (policy.py:226-270) against the reference's own exhaustive planner
+    on random and exact-tie matrices (tests/golden/brute_force_cases.json), and against
+    dp_optimize (acceptance criterion 01)."""
+    from paper_2602_00777_b200 import brute_force_policy
+
+    cases = json.loads((golden_dir / "brute_force_cases.json").read_text())
+    assert len(cases) == 60
+    for c in cases:
+        m = SimilarityMatrix(values=np.array(c["values"]), budget=8)
+        assert m.sha256() == c["matrix_sha"]
+        for r in c["results"]:
+            p = brute_force_policy(m, r["theta"])
+            assert [a.value for a in p.actions] == r["actions"]
+            assert list(p.sources) == r["sources"]
+            assert p.full_count == r["full_count"]
+            assert p.cum_similarity == r["cum_similarity"]
+            assert p.sha256() == r["policy_sha"]
+            assert dp_optimize(m, r["theta"]).sha256() == r["policy_sha"]
+
+
+def test_brute_force_policy_refuses_large_stacks():
+    from paper_2602_00777_b200 import BRUTE_FORCE_MAX_LAYERS, brute_force_policy
+
+    L = BRUTE_FORCE_MAX_LAYERS + 1
+    with pytest.raises(InvalidInputError):
+        brute_force_policy(SimilarityMatrix(values=np.eye(L), budget=8), 0.5)
+    with pytest.raises(InvalidInputError):
+        brute_force_policy(SimilarityMatrix(values=np.eye(3), budget=8), 1.5)
