@@ -15,13 +15,13 @@ e2e     : same metric through the public API (HybridDecoder.step) with the step'
           the outputs copied back every step
 roofline: the FULL kernel (dominant), algorithmic K/V bytes / CUDA-event launch time vs
           MEASURED_PEAKS.json hbm_gbs
-cpu_baseline: the float64 oracle port of the reference (oracle/cpu_baseline.py) on the
-          host cores, in a torch-free subprocess
+cpu_baseline: the reference's own functions (the unmodified `layerreuse` package installed
+          in baseline/_ref; the float64 oracle port if absent) on the host cores, in a
+          torch-free subprocess (baseline/ref_timing.py)
 N > 1   : launched by torchrun; KV-head sharding (Hkv/N heads per rank, global batch 8*N:
           weak scaling), no collective inside the attention path, one NCCL all-gather of
           the outputs per step.
---impl reference: the reference algorithm's CPU implementation (the oracle port; the
-          reference is pure Python and cannot be installed as a GPU arm) on the host cores.
+--impl reference: the same reference CPU timing on our arm's workload, rank 0 only.
 """
 from __future__ import annotations
 
@@ -58,7 +58,6 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="sequences per GPU")
     ap.add_argument("--no-extra", action="store_true", help="skip the 128K (config 3) line")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--schedule", default="auto",
                     choices=["auto", "fusedsel", "single", "fused3", "dual", "pipelined",
                              "sequential"],
@@ -74,58 +73,57 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- reference arm
-def run_reference(a):
-    """CPU arm: the reference algorithm (float64 oracle port) on this host's cores.
-    Each step = one (sequence, KV-head) group through all layers; tok/s extrapolated."""
-    rank = _env_int("RANK", 0)
-    if rank != 0:
-        return
-    # all host threads for OpenBLAS (torchrun exports OMP_NUM_THREADS=1, which OpenBLAS
-    # would otherwise follow); numpy is first imported below
-    n_threads = os.cpu_count() or 1
-    if "OPENBLAS_NUM_THREADS" not in os.environ:
-        os.environ["OPENBLAS_NUM_THREADS"] = str(n_threads)
-    import numpy as np
+def ref_timing(cfg_name, batch, steps, warmup, workers=0, e2e=False, timeout=1800):
+    """baseline/ref_timing.py in a torch-free subprocess: the reference's own functions
+    (baseline/_ref, else the oracle port) on this host's cores. workers 0 = a process pool
+    over all cores with single-threaded BLAS; 1 = one process with all-core BLAS."""
+    cores = os.cpu_count() or 1
+    n_blas = 1 if workers != 1 else cores
+    env = dict(os.environ)
+    env.update(OPENBLAS_NUM_THREADS=str(n_blas), OMP_NUM_THREADS=str(n_blas),
+               MKL_NUM_THREADS=str(n_blas))
+    cmd = [sys.executable, str(ROOT / "baseline" / "ref_timing.py"), "--config", cfg_name,
+           "--batch", str(batch), "--steps", str(steps), "--warmup", str(warmup),
+           "--workers", str(workers)] + (["--e2e"] if e2e else [])
+    try:
+        r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True,
+                           timeout=timeout)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # noqa: BLE001
+        return {"value": None, "unit": "tok/s", "cores": cores, "kind": "unavailable",
+                "sample": f"failed: {exc}"}
 
-    from oracle.cpu_baseline import full_layer, group_data, reuse_layer
+
+def run_reference(a):
+    """Reference arm: the reference's own CPU implementation of the path (baseline/_ref,
+    the unmodified `layerreuse` package) on the host cores, on our arm's workload (config 2,
+    B = 8 per GPU x N). Rank 0 only under torchrun. Each step = one timed sample (one FULL +
+    one REUSE layer over every (sequence, KV-head) group), extrapolated by layer count to the
+    32-layer step (declared in `extrapolation`)."""
+    if _env_int("RANK", 0) != 0:
+        return
     from paper_2602_00777_b200.synthetic import CONFIGS
 
     cfg = CONFIGS[a.config]
     B = (a.batch or cfg.batch) * a.gpus
-    layers = group_data(cfg, 4)
-    acts = cfg.actions
-
-    def one_step():
-        idx = None
-        for l, act in enumerate(acts):
-            q, k, v = layers[l % len(layers)]
-            if act == "full":
-                idx = full_layer(q, k, v, cfg.budget)
-            else:
-                reuse_layer(q, k, v, idx)
-
-    for _ in range(a.warmup):
-        one_step()
-    times = []
-    for _ in range(a.steps):
-        t0 = time.perf_counter()
-        one_step()
-        times.append(time.perf_counter() - t0)
-    t_group = float(np.mean(times))
-    step = t_group * cfg.kv_heads * B
-    value = B / step
-    cores = _env_int("OPENBLAS_NUM_THREADS", os.cpu_count() or 1)
+    res = ref_timing(cfg.name, B, a.steps, a.warmup, e2e=True)
+    one = ref_timing(cfg.name, B, max(1, min(3, a.steps)), 0, workers=1)
+    value = res.get("value")
     line = {
         "impl": "reference",
         "metric": BASELINE_METRIC, "value": value, "unit": "tok/s", "n_gpus": a.gpus,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": step * 1e3,
+        "steps": res.get("timed_samples", a.steps), "warmup": a.warmup,
+        "ms_per_step": res.get("ms_per_step"),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded N(0,1) + planted critical tokens)",
         "config": _config_dict(cfg, B, a.gpus),
-        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port",
-                         "sample": (f"per step: one (sequence, KV-head) group through all "
-                                    f"{cfg.layers} layers (reference algorithm, float64 numpy "
-                                    f"port), x{cfg.kv_heads * B} groups extrapolated")},
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": res.get("cores"),
+                         "kind": res.get("kind"), "sample": res.get("sample"),
+                         "mode": res.get("mode")},
+        "extrapolation": res.get("extrapolation"),
+        "sample_seconds_per_step": res.get("sample_seconds"),
+        "single_process": {k: one.get(k) for k in ("value", "unit", "cores", "mode", "sample")},
+        "end_to_end_hybrid_decode": res.get("end_to_end_hybrid_decode"),
         "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -381,7 +379,10 @@ def _sanity_check(torch, cfg, q, k, v, dec):
             "heads_per_pair": 1, "flags": "clear"}
 
 
-def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
+def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, strong=False):
+    """One config on this rank. Weak scaling (default): `batch` sequences per GPU, global
+    batch batch x world. strong=True: `batch` is the GLOBAL batch (BASELINE configs 3 and 4:
+    B = 4 sharded by KV head, B = 16 partitioned by batch), split across the ranks."""
     from paper_2602_00777_b200 import _abi
     from paper_2602_00777_b200.attention import geometry, scores_row_stride
     from paper_2602_00777_b200.engine import HybridDecoder, PipelinedDecoder
@@ -389,16 +390,16 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     from paper_2602_00777_b200.synthetic import generate_torch
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    global_batch = batch * world
+    global_batch = batch if strong else batch * world
     # Llama shapes (8 KV heads) shard by KV head; Qwen's 4 KV heads shard by batch (BASELINE
-    # configs 3 and 4). Weak scaling either way: per-GPU work stays that of `batch` at N=1.
+    # configs 3 and 4).
     mode = "kvhead" if cfg.kv_heads >= 8 and cfg.kv_heads % world == 0 else "batch"
     plan = plan_shards(cfg.kv_heads, cfg.q_heads, global_batch, world, mode=mode)[rank]
     if mode == "kvhead":
         local = cfg.with_(batch=global_batch, kv_heads=cfg.kv_heads // world,
                           q_heads=cfg.q_heads // world, seed=cfg.seed + rank)
     else:
-        local = cfg.with_(batch=batch, seed=cfg.seed + rank)
+        local = cfg.with_(batch=global_batch // world, seed=cfg.seed + rank)
     cap = cfg.context  # the e2e step writes the new token at row context-1
     q, k, v = generate_torch(local, dev, capacity=cap)
     L, B, Hq, d = q.shape
@@ -605,7 +606,10 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True):
     ncu = _ncu_traffic().get(f"{cfg.name}_b{B}", {})
     res = {
         "ms_per_step": ms, "value": value, "global_batch": global_batch,
-        "step_gbs": step_bytes / (ms * 1e-3) / 1e9,
+        "scaling": "strong" if strong else "weak",
+        "step_gbs": step_bytes / (ms * 1e-3) / 1e9 * world,   # whole job
+        "per_gpu_hbm_gbs": step_bytes / (ms * 1e-3) / 1e9,    # this rank's K/V bytes / max time
+        "per_gpu_frac_of_peak": step_bytes / (ms * 1e-3) / 1e9 / peak,
         "kernels": {
             "full_ms": t_full, "select_ms": t_sel, "reuse_ms": t_reuse,
             "select_frac_of_full_plus_select": t_sel / (t_full + t_sel),
@@ -665,46 +669,32 @@ def run_ours(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        def cpu_run(n, seconds):
-            env = dict(os.environ)
-            env.update(OPENBLAS_NUM_THREADS=str(n), OMP_NUM_THREADS=str(n),
-                       MKL_NUM_THREADS=str(n))
-            try:
-                r = subprocess.run([sys.executable, "-m", "oracle.cpu_baseline", "--config",
-                                    cfg.name, "--batch", str(batch), "--seconds", str(seconds)],
-                                   cwd=ROOT, env=env, capture_output=True, text=True,
-                                   timeout=600)
-                res = json.loads(r.stdout.strip().splitlines()[-1])
-                res.pop("step_seconds", None)
-                return res
-            except Exception as exc:  # noqa: BLE001
-                return {"value": None, "unit": "tok/s", "cores": n, "kind": "port",
-                        "sample": f"failed: {exc}"}
-
-        # all host threads (the baseline), and one thread (SURVEY §8d's second setting)
-        cpu = cpu_run(os.cpu_count() or 1, a.cpu_seconds)
-        one = cpu_run(1, max(1.0, a.cpu_seconds / 2))
-        cpu["single_thread"] = {"value": one.get("value"), "cores": 1,
-                                "sample": one.get("sample")}
+        # the reference's own functions (baseline/_ref) on all host cores, bounded sample
+        cpu = ref_timing(cfg.name, batch, 3, 1, e2e=True)
+        one = ref_timing(cfg.name, batch, 1, 0, workers=1)
+        cpu["single_process"] = {k: one.get(k) for k in ("value", "cores", "mode")}
 
     extra = {}
     # configs 3 (128K, KV-head shards) and 4 (Qwen, batch shards) at every N; the block,
     # offload and small-batch lines at N = 1 only
     if not a.no_extra:
+        keys = ("value", "ms_per_step", "global_batch", "scaling", "step_gbs",
+                "per_gpu_hbm_gbs", "per_gpu_frac_of_peak", "kernels", "roofline", "schedule",
+                "schedules", "parallelism", "check")
+        # BASELINE configs 3 and 4 at their GLOBAL batch (strong scaling): config 3 B = 4
+        # sharded by KV head, config 4 B = 16 partitioned by batch
         c3 = CONFIGS["cfg3"]
         try:
-            r3 = measure_config(a, c3, c3.batch, rank, world, torch, dist, e2e=False)
-            extra["cfg3_128k_b4"] = {k: r3[k] for k in ("value", "ms_per_step", "step_gbs",
-                                                        "kernels", "roofline", "schedule",
-                                                        "schedules", "parallelism")}
+            r3 = measure_config(a, c3, c3.batch, rank, world, torch, dist, e2e=False,
+                                strong=True)
+            extra["cfg3_128k_b4"] = {k: r3[k] for k in keys}
         except Exception as exc:  # noqa: BLE001
             extra["cfg3_128k_b4"] = {"error": str(exc)}
         c4 = CONFIGS["cfg4"]
         try:
-            r4 = measure_config(a, c4, c4.batch, rank, world, torch, dist, e2e=False)
-            extra["cfg4_qwen_64k_b16"] = {k: r4[k] for k in ("value", "ms_per_step", "step_gbs",
-                                                             "kernels", "roofline", "schedule",
-                                                             "schedules", "parallelism")}
+            r4 = measure_config(a, c4, c4.batch, rank, world, torch, dist, e2e=False,
+                                strong=True)
+            extra["cfg4_qwen_64k_b16"] = {k: r4[k] for k in keys}
         except Exception as exc:  # noqa: BLE001
             extra["cfg4_qwen_64k_b16"] = {"error": str(exc)}
     if not a.no_extra and world == 1:

@@ -452,9 +452,14 @@ def test_single_launch_step_equals_unfused(actions, d, refine, n, B, Hq, Hkv):
         torch.cuda.synchronize()
         assert torch.equal(dec.idx[..., :budget], ref_idx)
         assert torch.equal(dec.out, ref_out)
-    # the synchronisation words are back at zero after every step
-    sync = dec.ws[-(256 + 8 * len(dec.full_layers) * B * Hkv):].view(torch.int32)
-    assert int(sync.abs().sum()) == 0
+    # the synchronisation words and the split-K counters (the fixed region right after the
+    # 256-byte flag header: ticket / done + ready flags + group counters, then the FULL and
+    # REUSE counter regions of 64 slots x B x Hkv ints each) are back at zero after every step
+    n_ready = len(dec.full_layers) * B * Hkv
+    sync_end = 256 + -(-(256 + 8 * n_ready) // 256) * 256
+    ctr = -(-(4 * 64 * B * Hkv) // 256) * 256
+    fixed = dec.ws[256:sync_end + 2 * ctr].view(torch.int32)
+    assert int(fixed.abs().sum()) == 0
 
 
 def test_schedules_bit_identical_at_config2_scale():
