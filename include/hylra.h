@@ -220,6 +220,11 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
  *     layer_events (otherwise the schedules above apply);
  *     reuse_wait_event is waited on before the launch. The
  *     workspace carries the ticket / ready words and the kernel leaves them zeroed.
+ *   fuse_select = 3: the single-launch step with COOPERATIVE selects (token mode, sel_group
+ *     1): every split of a FULL pair classifies its own slice of the score row against the
+ *     k-th value's histogram bin (published by the last split to finish streaming), and the
+ *     last split to classify resolves the row. The select leaves the critical path of small
+ *     batches at the cost of splits waiting on their slowest sibling; same results (ABI 6).
  *   reuse_wait_event: the REUSE launches wait on it (e.g. REUSE layers' queries arriving).
  *   layer_events: L entries (NULL allowed); layer_events[l] is recorded as soon as out[l] is
  *     final — FULL layers right after their FULL launch, REUSE layers after the REUSE
@@ -229,7 +234,7 @@ int hylra_decode_step(const hylra_geometry* g, const void* q, const void* k, con
  * Workspace: as hylra_decode_step.
  */
 typedef struct hylra_step_options {
-  int32_t fuse_select; /* 1 (with side_stream, fork_event, join_event) or 2: see above */
+  int32_t fuse_select; /* 1 (with side_stream, fork_event, join_event), 2 or 3: see above */
   void* side_stream;
   void* fork_event;   /* stream -> side: FULL(A) done   */
   void* select_event; /* side -> stream: SELECT(A) done */

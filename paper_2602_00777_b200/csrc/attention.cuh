@@ -31,6 +31,9 @@ template <bool GATHER>
 constexpr int attn_threads() { return 32 * (kConsumerWarps + (GATHER ? kGatherProducers : 1)); }
 constexpr int kMaxG = 16;
 constexpr int kIdxStage = 2048;  // REUSE: indices staged in shared memory per CTA
+// FULL CTAs use the same 8 KB for their share of the score-row histogram: kHistBins 16-bit
+// counters packed two per word (a split holds < 65536 tokens: hylra_abi.cu checks)
+static_assert(kIdxStage * 4 == kHistBins * 2, "the staging area holds the 16-bit histogram");
 
 struct AttnParams {
   const void* q;
@@ -38,6 +41,8 @@ struct AttnParams {
   const void* v;
   float* out;
   float* scores;        // FULL: [slot][b][kh][cap] or null
+  unsigned* hist;       // FULL: [slot][b][kh][kHistBins] first-level histogram of the score
+                        // row (select.cuh), accumulated by every split, or null
   const int32_t* idx;   // REUSE: [src_slot][b][group][k_stride]
   const int32_t* counts;  // REUSE: optional rows per selection row (block coverage)
   // block-mode REUSE by TMA tiles (blk != null; tensor-core path, blk_size % 64 == 0): the
@@ -243,7 +248,8 @@ __device__ __forceinline__ uint32_t mma_consume_tile(const AttnParams& p, uint32
                                                  const uint32_t (&qa)[D / 16][4],
                                                  float (&o)[D / 8][4], float& m0, float& m1,
                                                  float& l0, float& l1, int row0, int n_rows,
-                                                 float* score_row, int lane) {
+                                                 float* score_row, float* score_buf,
+                                                 int lane) {
   const int g = lane >> 2;
   const int t = lane & 3;
   const float c = p.scale_log2;
@@ -297,16 +303,22 @@ __device__ __forceinline__ uint32_t mma_consume_tile(const AttnParams& p, uint32
     if (g == 0) {
       const int n0 = row0 + 2 * t;
       const int n1 = row0 + 8 + 2 * t;
+      const float s00 = v00 * p.inv_sqrt_d, s01 = v01 * p.inv_sqrt_d;
+      const float s10 = v10 * p.inv_sqrt_d, s11 = v11 * p.inv_sqrt_d;
       if (!tail) {
-        *reinterpret_cast<float2*>(score_row + n0) =
-            make_float2(v00 * p.inv_sqrt_d, v01 * p.inv_sqrt_d);
-        *reinterpret_cast<float2*>(score_row + n1) =
-            make_float2(v10 * p.inv_sqrt_d, v11 * p.inv_sqrt_d);
+        *reinterpret_cast<float2*>(score_row + n0) = make_float2(s00, s01);
+        *reinterpret_cast<float2*>(score_row + n1) = make_float2(s10, s11);
       } else {
-        if (n0 < n_rows) score_row[n0] = v00 * p.inv_sqrt_d;
-        if (n0 + 1 < n_rows) score_row[n0 + 1] = v01 * p.inv_sqrt_d;
-        if (n1 < n_rows) score_row[n1] = v10 * p.inv_sqrt_d;
-        if (n1 + 1 < n_rows) score_row[n1 + 1] = v11 * p.inv_sqrt_d;
+        if (n0 < n_rows) score_row[n0] = s00;
+        if (n0 + 1 < n_rows) score_row[n0 + 1] = s01;
+        if (n1 < n_rows) score_row[n1] = s10;
+        if (n1 + 1 < n_rows) score_row[n1 + 1] = s11;
+      }
+      // the tile's scores for the producer warp's histogram count (released with the stage)
+      if (score_buf != nullptr) {
+        const int r0 = (row0 & (kTileRows - 1)) + 2 * t;
+        *reinterpret_cast<float2*>(score_buf + r0) = make_float2(s00, s01);
+        *reinterpret_cast<float2*>(score_buf + r0 + 8) = make_float2(s10, s11);
       }
     }
   }
@@ -415,17 +427,6 @@ __device__ __forceinline__ void hylra_trace_mark(int k) {
 }
 #endif
 
-// ready flag of a selection row: 0 until the fused select of its FULL pair has written the
-// row's indices (single-launch step); release by one thread after a CTA-scope barrier,
-// acquire by every reader lane
-__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
-}
 
 // Block mode, fused (single-launch step, sel_group 1): the final CTA of a FULL pair pools its
 // token score row into the block row the select reads (block max, as block_pool_kernel;
@@ -561,12 +562,39 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
                                                                p.n_groups + kh / p.sel_group))
                          : p.n_rows;
 
+  // FULL pairs whose row is selected count the row's first-level histogram (select.cuh
+  // hist_bin) in shared memory: the consumer warps leave each tile's 64 scores in a per-stage
+  // buffer, the producer warp (otherwise waiting on the ring) counts them once the stage is
+  // released, and adds its counts to the row's global histogram at the end, so the select
+  // needs no sampling pass nor a pass to bracket the k-th value.
+  uint32_t* hist_smem = nullptr;  // kHistBins 16-bit counters, two per word (the staging area)
+  float* score_buf = nullptr;     // [2 STAGES][64] scores of tile t in buffer t % (2 STAGES)
+  if (!GATHER && p.scores != nullptr && p.hist != nullptr) {
+    hist_smem = reinterpret_cast<uint32_t*>(smem + STAGES * SM::kStageBytes + 256);
+    score_buf = reinterpret_cast<float*>(smem + STAGES * SM::kStageBytes + 256 + kIdxStage * 4);
+  }
+
   if (warp >= kConsumerWarps) {
     // ------------------------------------------------------------- producer warp
     if constexpr (!GATHER) {
-      if (warp == kConsumerWarps && lane == 0) {
-        tma_prefetch_desc(&tmk);
-        tma_prefetch_desc(&tmv);
+      if (warp == kConsumerWarps) {
+        // the scores of tile t (score buffer t % (2 STAGES)) into the shared-memory histogram
+        auto count_tile = [&](int t) {
+          const float* sb = score_buf + (t % (2 * STAGES)) * kTileRows;
+#pragma unroll
+          for (int j = lane; j < kTileRows; j += 32) {
+            if ((t_begin + t) * kTileRows + j < n_rows) {
+              const int bin = hist_bin(sb[j]);
+              atomicAdd(hist_smem + (bin >> 1), 1u << ((bin & 1) << 4));
+            }
+          }
+        };
+        if (hist_smem != nullptr)
+          for (int j = lane; j < kHistBins / 2; j += 32) hist_smem[j] = 0u;
+        if (lane == 0) {
+          tma_prefetch_desc(&tmk);
+          tma_prefetch_desc(&tmv);
+        }
         const uint64_t pol = l2_policy_evict_first();
         // block-mode REUSE: tile t covers rows blk[t / tpb] * blk_size + (t % tpb) * 64; the
         // block ids are loaded kAhead tiles ahead so no TMA issue waits on a global load
@@ -590,16 +618,31 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
             ahead[kAhead - 1] = (i + kAhead < n_my) ? __ldcg(bl + (t_begin + i + kAhead) / tpb) : 0;
           }
           mbar_wait(empty_bar + s, ((i / STAGES) & 1) ^ 1);
-          uint8_t* kt = smem + s * SM::kStageBytes;
-          uint8_t* vt = kt + SM::kTileBytes;
-          mbar_arrive_expect_tx(full_bar + s, SM::kStageBytes);
+          if (lane == 0) {
+            uint8_t* kt = smem + s * SM::kStageBytes;
+            uint8_t* vt = kt + SM::kTileBytes;
+            mbar_arrive_expect_tx(full_bar + s, SM::kStageBytes);
 #pragma unroll
-          for (int bx = 0; bx < SM::kBoxes; ++bx) {
-            tma_load_5d(kt + bx * kTileRows * 128, &tmk, full_bar + s, bx * 64, row, kh, b, kvl,
-                        pol);
-            tma_load_5d(vt + bx * kTileRows * 128, &tmv, full_bar + s, bx * 64, row, kh, b, kvl,
-                        pol);
+            for (int bx = 0; bx < SM::kBoxes; ++bx) {
+              tma_load_5d(kt + bx * kTileRows * 128, &tmk, full_bar + s, bx * 64, row, kh, b,
+                          kvl, pol);
+              tma_load_5d(vt + bx * kTileRows * 128, &tmv, full_bar + s, bx * 64, row, kh, b,
+                          kvl, pol);
+            }
           }
+          // the stage's previous tile is consumed: count its scores behind the refill (its score
+          // buffer is rewritten only by tile i + STAGES, whose load is issued after this count)
+          if (hist_smem != nullptr && i >= STAGES) count_tile(i - STAGES);
+          __syncwarp();
+        }
+        if (hist_smem != nullptr) {
+          // the last STAGES tiles; the consumer warps then add the counts to the row's
+          // histogram (behind the same fence as their split-K partials)
+          for (int t = max(0, n_my - STAGES); t < n_my; ++t) {
+            mbar_wait(empty_bar + t % STAGES, (t / STAGES) & 1);
+            count_tile(t);
+          }
+          asm volatile("bar.arrive 4, %0;" ::"n"(32 * (kConsumerWarps + 1)) : "memory");
         }
       }
     } else {
@@ -748,11 +791,54 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
     const uint32_t vt = kt + SM::kTileBytes;
     const int row0 = (t_begin + i) * kTileRows + rbase;  // first row of this warp's slice
 
-    const uint32_t dep = mma_consume_tile<D, GATHER, GBIG>(p, kt, vt, qa, o, m0, m1, l0, l1,
-                                                           row0, n_rows, score_row, lane);
+    const uint32_t dep = mma_consume_tile<D, GATHER, GBIG>(
+        p, kt, vt, qa, o, m0, m1, l0, l1, row0, n_rows, score_row,
+        score_buf != nullptr ? score_buf + (i % (2 * STAGES)) * kTileRows : nullptr, lane);
     release_stage(empty_bar + s, release_word + warp, dep, lane);
   }
   pdl_launch_dependents();
+  if (hist_smem != nullptr) {
+    // the producer warp has counted every tile: this split's counts join the row's
+    // histogram (L2 reductions, nonzero bins only), made visible by the fence of the
+    // cooperative arrival or of the split-K merge below (or the kernel's end)
+    asm volatile("bar.sync 4, %0;" ::"n"(32 * (kConsumerWarps + 1)) : "memory");
+    unsigned* hist_row = p.hist + ((int64_t)(slot * p.B + b) * p.Hkv + kh) * kHistBins;
+    for (int j = threadIdx.x; j < kHistBins / 2; j += 128) {
+      const uint32_t w = hist_smem[j];
+      if (w & 0xffffu) atomicAdd(hist_row + 2 * j, w & 0xffffu);
+      if (w >> 16) atomicAdd(hist_row + 2 * j + 1, w >> 16);
+    }
+  }
+
+  // ---- cooperative select (single-launch step, select.cuh coop_*): arrive as soon as this
+  //      split's scores and histogram reductions are out; the last split to arrive publishes
+  //      the row's candidate range; the split's slice of scores is prefetched into the drained
+  //      pipeline buffers (past the merge's region) while the merge below runs
+  __shared__ Red sel_red;
+  __shared__ int s_coop;
+  const bool coop = !GATHER && sp.coop != nullptr && slot < p.fuse_select;
+  const int srow = (slot * p.B + b) * p.Hkv + kh;  // score / histogram / coop row
+  CoopRow* rec = coop ? sp.coop + srow : nullptr;
+  constexpr int kSliceOff = ((2 * kConsumerWarps * 16 + kConsumerWarps * 16 * D) * 4 + 1023) & ~1023;
+  constexpr int kSliceCap = STAGES * SM::kStageBytes - kSliceOff;
+  const int s0 = t_begin * kTileRows, s1 = min(n_rows, t_end * kTileRows);
+  const bool slice_smem = coop && (s1 - s0) * 4 <= kSliceCap;
+  if (coop) {
+    __threadfence();  // this split's scores and histogram reductions, before its arrival
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 0) s_coop = atomicAdd(&rec->arrive1, 1) == p.splits - 1;
+    if (slice_smem) {
+      const int n16 = ((s1 - s0) + 3) >> 2;  // 16-byte chunks (rows are padded to 8 scores)
+      for (int i = threadIdx.x; i < n16; i += 128)
+        cp_async_16(smem + kSliceOff + 16 * i, score_row + s0 + 4 * i, true);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (s_coop) {
+      __threadfence();
+      coop_publish<kConsumerWarps * 32>(sp, srow, rec, n_rows, sel_red);
+    }
+  }
 
   // ---- merge the 4 warps through shared memory (pipeline buffers are drained)
   asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -783,11 +869,38 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
   const bool final_cta = merge_and_store<D>(p, slot, b, kh, split, sm_m, sm_l, sm_o,
                                             threadIdx.x, 128, 1);
   if constexpr (!GATHER) {
+    if (coop) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the slice is in, the merge is done
+      const bool last = coop_classify<kConsumerWarps * 32>(
+          sp, srow, rec, score_row,
+          slice_smem ? reinterpret_cast<const float*>(smem + kSliceOff) : nullptr, s0, s1,
+          n_rows, p.splits, sel_red);
+      if (last) {
+#ifdef HYLRA_TRACE
+        if (threadIdx.x == 0) hylra_trace_mark(1);
+#endif
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        coop_final<kConsumerWarps * 32>(sp, kh, b, slot, srow, rec, smem, (size_t)STAGES * SM::kStageBytes,
+                                        sel_red);
+        if (sp.cov_tokens != nullptr) fused_augment(sp, kh, b, slot);
+#ifdef HYLRA_TRACE
+        if (threadIdx.x == 0) hylra_trace_mark(3);
+#endif
+        if (ready_set != nullptr) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // the row's indices are written
+          if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_gpu(ready_set + (sp.out_slot[slot] * p.B + b) * p.n_groups + kh, 1);
+          }
+        }
+      }
+      return;
+    }
     // fused selection: the pair's score row is complete (every split wrote its part before
     // the counter), so its top-k is taken right here while other CTAs keep streaming;
     // the drained pipeline buffers hold the select's shared memory
     if (final_cta && slot < p.fuse_select) {
-      __shared__ Red sel_red;
       __shared__ int s_group_last;
       asm volatile("bar.sync 1, 128;" ::: "memory");  // merge reads of smem are done
       __threadfence();
@@ -810,7 +923,8 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
         if (threadIdx.x == 0) hylra_trace_mark(1);
 #endif
         if (sp.block_size > 1) fused_block_pool(sp, p.Hkv, kh, b, slot);
-        select_row<kConsumerWarps * 32, true>(sp, grp, b, slot, smem, sel_red, false);
+        select_row<kConsumerWarps * 32, true>(sp, grp, b, slot, smem, sel_red, false,
+                                              (size_t)STAGES * SM::kStageBytes);
         if (sp.block_size > 1) fused_block_expand(sp, kh, b, slot);
         else if (sp.cov_tokens != nullptr) fused_augment(sp, grp, b, slot);
 #ifdef HYLRA_TRACE

@@ -286,7 +286,7 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
                      const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0,
                      const SelectParams* fused = nullptr, int fuse_nslots = 0,
                      const int32_t* blk = nullptr, int blk_stride = 0, int blk_size = 0,
-                     int* counters = nullptr) {
+                     int* counters = nullptr, unsigned* hist = nullptr) {
   AttnParams p{};
   AttnLayout lay{};
   if (int e = make_attn_params(&p, &lay, g, gather, q, k, v, n_valid, n_rows, n_layers, layer_ids,
@@ -310,6 +310,9 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
   static const SelectParams no_select{};
   const SelectParams& sp = fused ? *fused : no_select;
   p.fuse_select = (fused && !gather && use_mma_path(g)) ? fuse_nslots : 0;
+  // (a split's 16-bit histogram counters hold < 65536 tokens)
+  p.hist = (!gather && scores != nullptr && p.tiles_per_split * kTileRows < 65536) ? hist
+                                                                                : nullptr;
   if (use_mma_path(g)) {
     CUtensorMap tk{}, tv{};
     if (!gather) {
@@ -405,17 +408,21 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
                   const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
                   int* flags, cudaStream_t st, const BlockRows& br = BlockRows(),
                   const int32_t* kv_layer_ids = nullptr, const int32_t* out_slots = nullptr,
-                  int force_nt = 0, int32_t* idx_mirror = nullptr) {
+                  int force_nt = 0, int32_t* idx_mirror = nullptr, unsigned* hist = nullptr) {
   SelectParams p{};
   if (int e = build_select_params(&p, g, scores, n_slots, n_valid, budget, sel_group, q, k,
                                   layer_ids, idx, k_stride, info, flags, br, kv_layer_ids,
                                   out_slots))
     return e;
   p.idx_mirror = idx_mirror;
+  p.hist = hist;
   dim3 grid(p.n_groups, g->batch, n_slots);
   const int nt = force_nt ? force_nt : select_threads(p.n_groups * g->batch * n_slots);
   cudaError_t ce;
-  ce = run_select(nt, grid, sel_smem_bytes(n_valid, nt), st, p);
+  size_t smem = sel_smem_bytes(n_valid, nt);
+  if (hist) smem = std::max(smem, sel_hist_smem_bytes(n_valid, nt));
+  p.smem_bytes = (uint32_t)smem;
+  ce = run_select(nt, grid, smem, st, p);
   if (ce != cudaSuccess) return cuda_check(ce, "topk_select launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_check(cudaGetLastError(), "topk_select launch");
@@ -488,10 +495,33 @@ struct StepLayout {
   size_t off_scores, off_attn, attn_bytes, off_attn_r, attn_bytes_r, total;
   size_t off_sync = 0;  // single-launch step: ticket / done counters + selection ready flags
   size_t off_ctr_f = 0, off_ctr_r = 0;  // split-K counters of the FULL / REUSE launches
+  size_t off_hist = 0;                  // score-row histograms (0: none)
+  // cooperative select of the single-launch step (select.cuh coop_*; with the histograms):
+  // per score row a 64-byte record (zero at rest), a candidate list and a bitmap
+  size_t off_coop = 0, off_coop_cv = 0, off_coop_ci = 0, off_coop_bits = 0;
+  int coop_words = 0;
   int n_ready = 0;
   int* ctr_f(uint8_t* w) const { return reinterpret_cast<int*>(w + off_ctr_f); }
   int* ctr_r(uint8_t* w) const { return reinterpret_cast<int*>(w + off_ctr_r); }
+  unsigned* hist(uint8_t* w) const {
+    return off_hist ? reinterpret_cast<unsigned*>(w + off_hist) : nullptr;
+  }
 };
+
+// Score-row histograms (select.cuh kHistBins): the cooperative selects of the single-launch
+// step (fuse_select = 3) need them; the other schedules' selects use them only with
+// HYLRA_HIST=1. Measured on B200 (scripts/schedules.py, profiles/r02_hist_ab.txt): counting
+// them costs the FULL kernel ~2-5% (cfg2 B=8 single 1.472 vs 1.450 ms, B=1 FULL launch 181 vs
+// 173 us) and saves less than that in the selects, so the sampled selects stay the default.
+bool hist_enabled() {
+  static int v = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_HIST");
+    v = (e && *e) ? (atoi(e) != 0) : 0;
+  });
+  return v == 1;
+}
 
 int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, int budget,
                 int sel_group, StepLayout* s, int block_size = 1, int sinks = 0,
@@ -530,9 +560,26 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   s->off_sync = kHeader;  // ticket / done, then ready flags and group counters [n_ready] each
   s->off_ctr_f = align_up(s->off_sync + 256 + 2 * sizeof(int) * (size_t)s->n_ready, 256);
   s->off_ctr_r = s->off_ctr_f + counter_region_bytes(g);
-  s->off_scores = s->off_ctr_r + counter_region_bytes(g);
+  // the FULL kernel's per-score-row histograms (select.cuh kHistBins), read and re-zeroed by
+  // the selects: token mode, per-KV-head rows, tensor-core FULL path
+  size_t off = s->off_ctr_r + counter_region_bytes(g);
+  if (block_size == 1 && sel_group == 1 && use_mma_path(g)) {
+    const size_t rows = nf * g->batch * g->kv_heads;
+    s->off_hist = off;
+    off = align_up(off + sizeof(unsigned) * kHistBins * rows, 256);
+    s->off_coop = off;
+    off = align_up(off + sizeof(CoopRow) * rows, 256);
+    s->off_coop_cv = off;
+    off = align_up(off + sizeof(float) * kHistCandCap * rows, 256);
+    s->off_coop_ci = off;
+    off = align_up(off + sizeof(int) * kHistCandCap * rows, 256);
+    s->coop_words = (g->capacity + 31) / 32;
+    s->off_coop_bits = off;
+    off = align_up(off + sizeof(uint32_t) * s->coop_words * rows, 256);
+  }
+  s->off_scores = off;
   const size_t scores_b = sizeof(float) * nf * g->batch * g->kv_heads * scores_row_stride(g);
-  size_t off = align_up(s->off_scores + scores_b, 256);
+  off = align_up(s->off_scores + scores_b, 256);
   if (block_size > 1) {
     // budget counts blocks; REUSE layers read the coverage (<= bb * block_size tokens)
     const int nb = (n_valid + block_size - 1) / block_size;
@@ -634,7 +681,8 @@ bool fused_select_fits(const hylra_geometry* g, int n_valid) {
 // Options of hylra_decode_step_ex (all optional; see include/hylra.h).
 struct StepOpts {
   bool fuse = false;  // selects of the FULL layers feeding REUSE fused into the FULL kernel
-  bool unified = false;  // single-launch step (fuse_select == 2)
+  bool unified = false;  // single-launch step (fuse_select == 2 or 3)
+  bool coop = false;     // ... with the cooperative selects (fuse_select == 3)
   const void* app_k = nullptr;  // the step's new K/V rows [L][B][Hkv][d] (append_* options)
   const void* app_v = nullptr;
   int app_pos = -1;
@@ -710,6 +758,10 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
   const void* kf = split ? split->kf : k;
   const void* vf = split ? split->vf : v;
   const size_t score_slot = (size_t)g->batch * g->kv_heads * scores_row_stride(g);
+  // per score row; slot stride below. Off (null) unless the cooperative single-launch step or
+  // HYLRA_HIST=1 asks for them
+  unsigned* hist = (o.coop || hist_enabled()) ? s.hist(w) : nullptr;
+  const size_t hist_slot = (size_t)g->batch * g->kv_heads * kHistBins;
 
   // FULL layer groups: A = the FULL layers some REUSE layer inherits from (the selection the
   // REUSE launch waits for), B = the others. With a side stream the selects leave the
@@ -778,6 +830,16 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                  split ? ab_kv.data() : nullptr, nf, s.ctr_f(w)))
       return e;
     pf.fuse_select = nf;
+    if (lf.tps * kTileRows >= 65536) hist = nullptr;  // 16-bit per-split histogram counters
+    pf.hist = hist;
+    sp.hist = hist;
+    if (hist && o.coop) {
+      sp.coop = reinterpret_cast<CoopRow*>(w + s.off_coop);
+      sp.coop_cv = reinterpret_cast<float*>(w + s.off_coop_cv);
+      sp.coop_ci = reinterpret_cast<int*>(w + s.off_coop_ci);
+      sp.coop_bits = reinterpret_cast<uint32_t*>(w + s.off_coop_bits);
+      sp.coop_words = s.coop_words;
+    }
     const long items_f = (long)lf.splits * g->kv_heads * g->batch * nf;
     long items_r = 0;
     std::vector<int32_t> rkv(nr);
@@ -829,7 +891,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                  nullptr, nullptr, nullptr, 0, 1, out,
                                  scores + gr.score_base * score_slot, aws, s.attn_bytes, flags, sx,
                                  split ? gr.kv->data() : nullptr, nf, fused, n_fused, nullptr, 0,
-                                 0, s.ctr_f(w)))
+                                 0, s.ctr_f(w), hist ? hist + gr.score_base * hist_slot : nullptr))
       return e;
     for (int l : *gr.ids)
       if (int e = record(o.layer_events, l, sx)) return e;
@@ -840,7 +902,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                          budget, sel_group, refine ? q : nullptr, refine ? kf : nullptr,
                          gr.ids->data(), idx, k_stride, nullptr, flags, sx, BlockRows(),
                          split ? gr.kv->data() : nullptr, gr.slots->data(), force_nt,
-                         o.idx_mirror);
+                         o.idx_mirror, hist ? hist + gr.score_base * hist_slot : nullptr);
   };
   auto reuse = [&](cudaStream_t sx) -> int {
     if (s.reuse_ids.empty()) return HYLRA_OK;
@@ -911,6 +973,7 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                                     split ? ab_kv.data() : nullptr, ab_slot.data()))
       return e;
     sp.idx_mirror = o.idx_mirror;
+    sp.hist = hist;
     if (int e = full(g_ab, st, &sp, (int)a_ids.size())) return e;
     if (!b_ids.empty()) {
       if (int e = rec(o.fork, st)) return e;
@@ -1040,7 +1103,8 @@ int hylra_decode_step_ex(const hylra_geometry* g, const void* q, const void* k, 
   StepOpts o;
   if (opt) {
     o.fuse = opt->fuse_select != 0;
-    o.unified = opt->fuse_select == 2;
+    o.unified = opt->fuse_select == 2 || opt->fuse_select == 3;
+    o.coop = opt->fuse_select == 3;
     o.app_k = opt->append_k_rows;
     o.app_v = opt->append_v_rows;
     o.app_pos = opt->append_pos;

@@ -1,5 +1,7 @@
 // k_select.cu — instantiations of the standalone top-k SELECT kernel (select.cuh
 // topk_select_kernel<NT>, one CTA per row).
+#include <algorithm>
+
 #include "launch.cuh"
 
 namespace hylra {
@@ -8,8 +10,10 @@ namespace host {
 template <int NT>
 static cudaError_t launch_select_nt(dim3 grid, size_t smem, cudaStream_t st,
                                     const SelectParams& p) {
+  const size_t most = std::max(sel_smem_bytes(kSelMaxTokens, NT),
+                               sel_hist_smem_bytes(kSelMaxTokens, NT));
   if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(topk_select_kernel<NT>),
-                                      sel_smem_bytes(kSelMaxTokens, NT)))
+                                      most))
     return e;
   return launch_pdl(topk_select_kernel<NT>, grid, dim3(NT), smem, st, p);
 }

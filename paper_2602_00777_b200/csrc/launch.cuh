@@ -95,8 +95,10 @@ constexpr int mma_stages() {
 }
 template <int D, bool GATHER, bool GBIG>
 constexpr size_t mma_smem_bytes() {
+  // + the REUSE index staging area, which FULL CTAs use for the score-row histogram, and
+  // the FULL CTAs' per-stage score buffers (attention.cuh attn_mma_item)
   return (size_t)mma_stages<D, GATHER, GBIG>() * MmaSmem<D>::kStageBytes + 1024 + 256 +
-         (GATHER ? kIdxStage * sizeof(int32_t) : 0);
+         kIdxStage * sizeof(int32_t) + 2 * mma_stages<D, GATHER, GBIG>() * kTileRows * 4;
 }
 
 // Kernel-unit entry points (each defined in its own translation unit).

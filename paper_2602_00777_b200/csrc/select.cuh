@@ -39,14 +39,46 @@ constexpr int kBins = 2048;
 constexpr int kCandCap = 1024;            // scores collected around the k-th bin
 constexpr int kSmallN = 2048;             // rows sorted outright (small-row path)
 constexpr int kSelMaxTokens = 262144;     // longest row (bitmap = 32 KB)
+
+// First-level histogram of a score row, built by the FULL kernel as it emits the scores
+// (every split adds its tokens with L2 reductions): bin = the top 12 bits of the
+// order-preserving key, so a bin spans 1/8 of a binary octave. The select reads it (and
+// zeroes it for the next step) to find the bin holding the k-th value without touching the
+// row, then makes ONE pass over the row. kHistCandCap bounds the tokens of that bin (plus
+// the refinement margin) the pass may collect; past it the row takes the sampled path.
+constexpr int kHistShift = 20;
+constexpr int kHistBins = 1 << (32 - kHistShift);  // 4096
+constexpr int kHistCandCap = 4096;
+__device__ __forceinline__ int hist_bin(float v) { return (int)(float_key(v) >> kHistShift); }
 template <int NT>
 __host__ __device__ constexpr int sel_chunk() { return NT * 32; }  // tokens per bitmap chunk (one word per thread)
+
+// Per-row state of the cooperative select (below): zero at rest, re-zeroed by the row's final
+// CTA.
+struct CoopRow {
+  int arrive1, arrive2, flag, b1;
+  float c_lo, c_hi;
+  int n_cand, c_above;
+  unsigned vmax_key, vmin_nkey;  // atomicMax of float_key(max) and of ~float_key(min)
+  int bad, pad[5];
+};
+static_assert(sizeof(CoopRow) == 64, "CoopRow is 64 bytes");
 
 struct SelectParams {
   const float* scores;  // [slot][b][kh][row_stride]
   int32_t* idx;         // [slot][b][grp][k_stride]
   int32_t* idx_mirror;  // optional second copy of idx (same layout), e.g. pinned host memory
                         // the caller reads after the step: stored alongside idx, no copy
+  unsigned* hist;       // optional [slot][b][kh][kHistBins] row histograms written by the FULL
+                        // kernel (token rows, sel_group 1): read and re-zeroed by the select
+  uint32_t smem_bytes;  // dynamic shared memory of the standalone select kernel
+  // cooperative select (single-launch step, token rows, sel_group 1; null: off): per score
+  // row its record, candidate list [kHistCandCap] and bitmap [coop_words]
+  CoopRow* coop;
+  float* coop_cv;
+  int* coop_ci;
+  uint32_t* coop_bits;
+  int coop_words;
   int32_t* info;        // [row][8] or null
   int* flags;
   const void* q;        // refinement inputs (null: refinement off)
@@ -96,6 +128,11 @@ __host__ __device__ constexpr size_t sel_fixed_bytes(int nt, bool big = false) {
 }
 __host__ __device__ constexpr size_t sel_smem_bytes(int n, int nt, bool big = false) {
   return sel_bitmap_bytes(n, nt) + sel_fixed_bytes(nt, big);
+}
+// The histogram path: bitmap, candidates (value + index), then a scratch area for the exact
+// T's digit histogram and the float64 window arrays.
+__host__ __device__ constexpr size_t sel_hist_smem_bytes(int n, int nt) {
+  return sel_bitmap_bytes(n, nt) + (size_t)kHistCandCap * 8 + (size_t)kHistBins * 4;
 }
 
 #ifdef HYLRA_TRACE
@@ -272,6 +309,25 @@ __device__ __forceinline__ void block_scan4(const uint32_t (&v)[4], uint32_t (&e
     tot[q] = __shfl_sync(0xffffffffu, t, 31);
     ex[q] = (warp > 0 ? pre : 0u) + x[q] - v[q];
   }
+}
+
+// The finished selection row, copied to its mirror (hylra_step_options idx_mirror; often
+// pinned host memory) with coalesced 16-byte stores once the row is complete: the
+// compaction's own stores are scattered 4-byte writes, which across the link would cost
+// far more than the row's 8 KB. The barrier makes every thread's idx stores visible.
+template <int NT>
+__device__ __forceinline__ void copy_to_mirror(const int32_t* out, int32_t* mir, int k) {
+  if (mir == nullptr) return;
+  sel_sync<NT>();
+  const int tid = threadIdx.x;
+  int done = 0;
+  if (((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(mir)) & 15) == 0) {
+    const int k4 = k >> 2;
+    for (int i = tid; i < k4; i += NT)
+      reinterpret_cast<int4*>(mir)[i] = __ldcg(reinterpret_cast<const int4*>(out) + i);
+    done = k4 << 2;
+  }
+  for (int i = done + tid; i < k; i += NT) mir[i] = __ldcg(out + i);
 }
 
 // Warp-aggregated append: each thread adds `cnt` items; returns its first slot.
@@ -563,6 +619,466 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
   *nw_out = z - a;
 }
 
+// ----------------------------------------------------------------------------- hist path
+// The rank-`rank` (1-based, descending) value among nc floats in shared memory: MSB-first
+// 4 x 8-bit radix select on the order-preserving keys; warp 0 scans each digit histogram.
+template <int NT>
+__device__ float smem_kth_largest(const float* v, int nc, int rank, Red& r) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t prefix = 0, mask = 0;
+  int krem = rank;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int j = tid; j < 256; j += NT) r.hist256[j] = 0;
+    sel_sync<NT>();
+    for (int j = tid; j < nc; j += NT) {
+      const uint32_t key = float_key(v[j]);
+      if ((key & mask) == prefix) atomicAdd(r.hist256 + ((key >> shift) & 255u), 1u);
+    }
+    sel_sync<NT>();
+    if (tid < 32) {
+      // lane l owns digits 255 - 8l .. 248 - 8l (descending)
+      int h[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        h[j] = (int)r.hist256[255 - 8 * lane - j];
+        sum += h[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int acc = incl - sum;  // digits above this lane's
+      if (acc < krem && krem <= incl) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (acc < krem && krem <= acc + h[j]) {
+            r.misc[8] = 255 - 8 * lane - j;
+            r.misc[9] = acc;
+          }
+          acc += h[j];
+        }
+      }
+    }
+    sel_sync<NT>();
+    krem -= r.misc[9];
+    prefix |= (uint32_t)r.misc[8] << shift;
+    mask |= 255u << shift;
+    sel_sync<NT>();
+  }
+  return key_float(prefix);
+}
+
+// The rank-r (1-based, descending) value among the nc candidates, most of which share the
+// top kHistShift-complement bits b1: candidates above bin b1 rank first; inside b1 two digit
+// rounds (bits 19..8 through a 4096-bin histogram in `scratch`, then bits 7..0) find the
+// exact key. Falls back to the 4-round radix select when T lies outside b1.
+template <int NT>
+__device__ float cand_kth_largest(const float* v, int nc, int r, int b1, unsigned* scratch,
+                                  Red& red) {
+  const int tid = threadIdx.x;
+  int hi = 0, in = 0;
+  for (int j = tid; j < nc; j += NT) {
+    const int bj = hist_bin(v[j]);
+    hi += bj > b1;
+    in += bj == b1;
+  }
+  for (int j = tid; j < kHistBins; j += NT) scratch[j] = 0u;
+  hi = block_sum_int<NT>(hi, red);
+  in = block_sum_int<NT>(in, red);
+  if (r <= hi || r > hi + in) return smem_kth_largest<NT>(v, nc, r, red);
+  int rr = r - hi;
+  // digit 1: bits 19..8
+  for (int j = tid; j < nc; j += NT) {
+    const uint32_t key = float_key(v[j]);
+    if ((int)(key >> kHistShift) == b1) atomicAdd(scratch + ((key >> 8) & 0xFFFu), 1u);
+  }
+  sel_sync<NT>();
+  constexpr int PER = kHistBins / NT;
+  int h[PER], sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    h[j] = (int)scratch[tid * PER + j];
+    sum += h[j];
+  }
+  int tot;
+  const int ex = block_scan<NT>(sum, &tot, red);
+  int acc = tot - ex - sum;  // members in higher threads' digits
+  if (acc < rr && rr <= acc + sum) {
+#pragma unroll
+    for (int j = PER - 1; j >= 0; --j) {
+      if (acc < rr && rr <= acc + h[j]) {
+        red.misc[8] = tid * PER + j;
+        red.misc[9] = acc;
+      }
+      acc += h[j];
+    }
+  }
+  for (int j = tid; j < 256; j += NT) red.hist256[j] = 0u;
+  sel_sync<NT>();
+  const uint32_t d1 = (uint32_t)red.misc[8];
+  rr -= red.misc[9];
+  const uint32_t pre = ((uint32_t)b1 << kHistShift) | (d1 << 8);
+  // digit 2: bits 7..0
+  for (int j = tid; j < nc; j += NT) {
+    const uint32_t key = float_key(v[j]);
+    if ((key >> 8) == (pre >> 8)) atomicAdd(red.hist256 + (key & 255u), 1u);
+  }
+  sel_sync<NT>();
+  if (tid < 32) {
+    int hh[8], ss = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hh[j] = (int)red.hist256[255 - 8 * tid - j];
+      ss += hh[j];
+    }
+    int incl = ss;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (tid >= o) incl += y;
+    }
+    int a = incl - ss;
+    if (a < rr && rr <= incl) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (a < rr && rr <= a + hh[j]) red.misc[10] = 255 - 8 * tid - j;
+        a += hh[j];
+      }
+    }
+  }
+  sel_sync<NT>();
+  return key_float(pre | (uint32_t)red.misc[10]);
+}
+
+// Step 1 of the histogram path: from this thread's PER = kHistBins / NT bins of a row
+// histogram (ascending from bin tid * PER), the bin b1 holding rank k from the top and the
+// candidate value range [c_lo, c_hi] = b1 widened by the refinement half-width bound
+// tau_rel * max|s| (max|s| bounded by the occupied range of bins). False when the
+// histogram does not describe the row (count != n) or holds +-inf / NaN bins.
+template <int NT>
+__device__ bool hist_b1(const uint32_t (&hb)[kHistBins / NT], int n, int k, bool refine,
+                        float tau_rel, Red& red, int* b1_out, float* c_lo, float* c_hi) {
+  constexpr int PER = kHistBins / NT;
+  const int tid = threadIdx.x;
+  int sum = 0, nz_hi = -1, nz_lo = kHistBins;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    sum += (int)hb[j];
+    if (hb[j]) {
+      nz_hi = tid * PER + j;
+      nz_lo = min(nz_lo, tid * PER + j);
+    }
+  }
+  int tot;
+  const int ex = block_scan<NT>(sum, &tot, red);
+  const int above_blk = tot - ex - sum;  // tokens in higher threads' bins
+  if (tid == 0) red.misc[0] = -1;
+  sel_sync<NT>();
+  if (above_blk < k && k <= above_blk + sum) {
+    int acc = above_blk;
+#pragma unroll
+    for (int j = PER - 1; j >= 0; --j) {
+      if (acc < k && k <= acc + (int)hb[j]) red.misc[0] = tid * PER + j;
+      acc += (int)hb[j];
+    }
+  }
+  {
+    float fhi = (float)nz_hi, flo = (float)(-nz_lo);
+    int z0 = 0, z1 = 0, z2 = 0;
+    block_reduce_pass_b<NT>(fhi, flo, z0, z1, z2, red);
+    nz_hi = (int)fhi;
+    nz_lo = -(int)flo;
+  }
+  const int b1 = red.misc[0];
+  constexpr int kInfHi = (int)(0xFF800000u >> kHistShift);
+  constexpr int kInfLo = (int)(0x007FFFFFu >> kHistShift);
+  if (tot != n || b1 < 0 || nz_hi >= kInfHi || nz_lo <= kInfLo) return false;
+  const float vmax_b = key_float(((uint32_t)nz_hi << kHistShift) | ((1u << kHistShift) - 1));
+  const float vmin_b = key_float((uint32_t)nz_lo << kHistShift);
+  const float tau_b = refine ? fmaxf(tau_rel * fmaxf(fabsf(vmax_b), fabsf(vmin_b)), 1e-30f) : 0.f;
+  *b1_out = b1;
+  *c_lo = key_float((uint32_t)b1 << kHistShift) - tau_b;
+  *c_hi = key_float(((uint32_t)b1 << kHistShift) | ((1u << kHistShift) - 1)) + tau_b;
+  return true;
+}
+
+// Step 3 of the histogram path, shared with the cooperative select: the exact k-th value T
+// (rank r among the nc candidates), then candidates above the window [T - tau, T + tau]
+// (T exactly without refinement) join `bitmap`, the window goes to wv / wi in `scratch`
+// (>= kHistBins * 4 bytes). *above_add = candidates above the window. False when the window
+// exceeds kCandCap.
+template <int NT>
+__device__ bool cands_window(const float* cand_v, const int* cand_i, int nc, int r, int b1,
+                            float tau, bool refine, uint8_t* scratch, uint32_t* bitmap,
+                            Red& red, double** wv_out, int** wi_out, int* above_add,
+                            int* nw_out) {
+  const int tid = threadIdx.x;
+  const float T = cand_kth_largest<NT>(cand_v, nc, r, b1, reinterpret_cast<unsigned*>(scratch),
+                                       red);
+  const float lo_w = refine ? T - tau : T, hi_w = refine ? T + tau : T;
+  double* wv = reinterpret_cast<double*>(scratch);
+  int* wi = reinterpret_cast<int*>(scratch + (size_t)kCandCap * 8);
+  if (tid == 0) red.misc[5] = 0;
+  sel_sync<NT>();
+  int abv = 0;
+  for (int base = 0; base < nc; base += NT) {  // warp-uniform trip count (warp_append)
+    const int j = base + tid;
+    bool in = false;
+    float v = 0.f;
+    int ii = 0;
+    if (j < nc) {
+      v = cand_v[j];
+      ii = cand_i[j];
+      if (v > hi_w) {
+        atomicOr(bitmap + (ii >> 5), 1u << (ii & 31));
+        ++abv;
+      } else {
+        in = v >= lo_w;
+      }
+    }
+    const int pos = warp_append(in ? 1 : 0, &red.misc[5]);
+    if (in && pos < kCandCap) {
+      wv[pos] = (double)v;
+      wi[pos] = ii;
+    }
+  }
+  *above_add = block_sum_int<NT>(abv, red);  // (its barriers publish misc[5])
+  const int nw = red.misc[5];
+  sel_sync<NT>();
+  if (nw > kCandCap) return false;
+  *wv_out = wv;
+  *wi_out = wi;
+  *nw_out = nw;
+  return true;
+}
+
+// Histogram-driven prefix of a token row's selection (sel_group 1, n > kSmallN), replacing
+// the sampled passes A-D: hb = this thread's kHistBins / NT bins of the row's histogram
+// (ascending from bin tid * (kHistBins / NT)), read and re-zeroed by the caller.
+//  1. the bin b1 holding rank k from the top, the count above it and the occupied range of
+//     bins (which bounds max|s|, hence the refinement half-width tau) — no row access;
+//  2. ONE pass over the row (two chunks of loads in flight): tokens above b1 widened by tau go
+//     straight into the bitmap, tokens of b1 (+- tau) into a candidate list, with max/min and
+//     the non-finite check riding along;
+//  3. the exact k-th value T among the candidates; candidates above the window
+//     [T - tau, T + tau] (T exactly without refinement) join the bitmap, the window goes to
+//     wv / wi for the float64 re-score and rank step of the caller.
+// Same T, tau and window as the sampled path, hence the same selection. Returns false (the
+// caller then runs the sampled path) when the histogram does not describe the row, a bin
+// holds too many candidates, the row holds NaN / inf, or the window exceeds kCandCap.
+template <int NT>
+__device__ __forceinline__ bool hist_select(const SelectParams& p, const RowReader& rd,
+                                            const uint32_t (&hb)[kHistBins / NT], int n, int k,
+                                            bool refine,
+                                            uint8_t* sraw, Red& red, double** wv_out,
+                                            int** wi_out, int* above_out, int* nw_out,
+                                            float* tau_out, int* cin_out, long long* marks) {
+  constexpr int kChunk = sel_chunk<NT>();
+  const int tid = threadIdx.x;
+  // ---- 1. the bin of rank k
+  int b1;
+  float c_lo, c_hi;
+  if (!hist_b1<NT>(hb, n, k, refine, p.tau_rel, red, &b1, &c_lo, &c_hi)) return false;
+  marks[0] = clock64();
+
+  // ---- 2. one pass over the row
+  const size_t bb = sel_bitmap_bytes(n, NT);
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(sraw);
+  float* cand_v = reinterpret_cast<float*>(sraw + bb);
+  int* cand_i = reinterpret_cast<int*>(sraw + bb + 4 * (size_t)kHistCandCap);
+  uint8_t* scratch = sraw + bb + 8 * (size_t)kHistCandCap;
+  const int nwords = (int)(bb / 4);
+  for (int w = tid; w < nwords; w += NT) bitmap[w] = 0u;
+  if (tid == 0) red.misc[3] = 0;
+  sel_sync<NT>();
+  const int nch = (n + kChunk - 1) / kChunk;
+  const int n4 = (n + 3) >> 2;
+  float nanacc = 0.f, vmax = -INFINITY, vmin = INFINITY;
+  int c_above = 0;
+  // the next chunk's loads are in flight while the current one is classified
+  auto load = [&](int c, float4 (&vv)[8]) {
+    const int w4 = (c * kChunk + tid * 32) >> 2;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vv[u] = (w4 + u < n4) ? rd.at4(w4 + u) : make_float4(0, 0, 0, 0);
+  };
+  auto classify = [&](int c, const float4 (&vv)[8]) {
+    const int w4 = (c * kChunk + tid * 32) >> 2;
+    uint32_t word = 0u, cand = 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const float v = lane4(vv[u], cc);
+        if (4 * (w4 + u) + cc < n) {
+          nanacc = fmaf(v, 0.f, nanacc);
+          vmax = fmaxf(vmax, v);
+          vmin = fminf(vmin, v);
+          word |= (v > c_hi) ? (1u << (u * 4 + cc)) : 0u;
+          cand |= (v >= c_lo && v <= c_hi) ? (1u << (u * 4 + cc)) : 0u;
+        }
+      }
+    }
+    bitmap[c * NT + tid] = word;
+    c_above += __popc(word);
+    int pos = warp_append(__popc(cand), &red.misc[3]);
+    while (cand) {
+      const int bit = __ffs(cand) - 1;
+      cand &= cand - 1;
+      if (pos < kHistCandCap) {
+        float e = vv[0].x;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            if (u * 4 + cc == bit) e = lane4(vv[u], cc);
+        cand_v[pos] = e;
+        cand_i[pos] = 4 * w4 + bit;
+      }
+      ++pos;
+    }
+  };
+  {
+    float4 va[8], vb[8];
+    if (nch > 0) load(0, va);
+    for (int c = 0; c < nch; c += 2) {
+      if (c + 1 < nch) load(c + 1, vb);
+      classify(c, va);
+      if (c + 1 < nch) {
+        if (c + 2 < nch) load(c + 2, va);
+        classify(c + 1, vb);
+      }
+    }
+  }
+  int bad, dummy = 0;
+  {
+    float nmin = -vmin;
+    bad = nanacc != nanacc ? 1 : 0;
+    block_reduce_pass_b<NT>(vmax, nmin, bad, c_above, dummy, red);
+    vmin = -nmin;
+  }
+  const int nc = red.misc[3];
+  const int r = k - c_above;
+  *cin_out = nc;
+  marks[1] = clock64();
+  if (bad || nc > kHistCandCap || r < 1 || r > nc) {
+    sel_sync<NT>();
+    return false;
+  }
+  // ---- 3. exact T, the window and the candidates above it
+  const float tau = refine ? fmaxf(p.tau_rel * fmaxf(fabsf(vmax), fabsf(vmin)), 1e-30f) : 0.f;
+  int above_add = 0;
+  if (!cands_window<NT>(cand_v, cand_i, nc, r, b1, tau, refine, scratch, bitmap, red, wv_out,
+                        wi_out, &above_add, nw_out))
+    return false;
+  marks[2] = clock64();
+  *above_out = c_above + above_add;
+  *tau_out = tau;
+  return true;
+}
+
+// Phase-record of one selection row (info[] / diagnostics).
+struct SelStats {
+  int mode, cin;
+  long long t0, t1, t2, t3;
+};
+
+// The common tail of every selection path: the boundary window wv / wi (nw scores, fp32
+// values) is re-scored in float64 (refine) and its top k - above_w by (score desc, index
+// asc) join `bitmap`, whose tokens above the window are already set; then the index-ordered
+// compaction of the bitmap (word w = tokens [32 w, 32 w + 32)) writes the k indices
+// ascending (the reference's canonical TopKSet order), copied to the mirror if any.
+template <int NT>
+__device__ void select_finish(const SelectParams& p, int grp, int b, int slot, uint32_t* bitmap,
+                              double* wv, int* wi, int nw, int above_w, float tau_w, bool refine,
+                              int n, int k, int32_t* out, int32_t* mir, int32_t* info, Red& red,
+                              bool release, uint64_t* keys, const SelStats& st) {
+  constexpr int kChunk = sel_chunk<NT>();
+  const int tid = threadIdx.x;
+  const int nch = (n + kChunk - 1) / kChunk;
+  // ---- window: re-score (refine) and keep the top k - above_w by (score desc, index asc)
+  if (nw > 0) {
+    sel_sync<NT>();
+    if (refine) {
+      if (p.block_size > 1)
+        rescore_f64_blocks<NT>(p, slot, b, grp, wi, wv, nw, tau_w, keys);
+      else rescore_f64<NT>(p, slot, b, grp, wi, wv, nw);
+      sel_sync<NT>();
+    }
+    const int take = k - above_w;
+    for (int j = tid; j < nw; j += NT) {
+      const double vj = wv[j];
+      const int ij = wi[j];
+      int rank = 0;
+      for (int i = 0; i < nw; ++i) {
+        const double vi = wv[i];
+        rank += (vi > vj) || (vi == vj && wi[i] < ij);
+      }
+      if (rank < take) atomicOr(bitmap + (ij >> 5), 1u << (ij & 31));
+    }
+  }
+  sel_sync<NT>();
+
+  const long long t4 = clock64();  // window done: compaction next
+  if (release) pdl_launch_dependents();
+  // ---- E. index-ordered compaction of the bitmap: 8 chunks per block scan (their
+  //         per-thread counts packed 2 x 16 bits per word), 2 barriers per 8 chunks
+  int run = 0;
+  if (nch == 1) {  // one chunk (wide CTAs, short rows): a single-word scan
+    const uint32_t w = bitmap[tid];
+    int tot;
+    int pos = block_scan<NT>(__popc(w), &tot, red);
+    uint32_t m = w;
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      if (pos < k) out[pos] = tid * 32 + bit;
+      ++pos;
+    }
+    run = tot;
+  }
+  for (int c0 = 0; nch > 1 && c0 < nch; c0 += 8) {
+    uint32_t w[8], pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      w[j] = (c0 + j < nch) ? bitmap[(c0 + j) * NT + tid] : 0u;
+      pk[j >> 1] |= (uint32_t)__popc(w[j]) << (16 * (j & 1));
+    }
+    uint32_t ex[4], tot[4];
+    block_scan4<NT>(pk, ex, tot, red);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (c0 + j >= nch) break;
+      int pos = run + (int)((ex[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+      uint32_t m = w[j];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (pos < k) out[pos] = (c0 + j) * kChunk + tid * 32 + bit;
+        ++pos;
+      }
+      run += (int)((tot[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+    }
+  }
+  // invariant: exactly k indices were emitted
+  if (tid == 0 && run != k) atomicOr(p.flags, 8);
+  copy_to_mirror<NT>(out, mir, k);
+  if (info && tid == 0) {
+    info[0] = k;
+    info[1] = nw;
+    info[2] = st.mode;
+    info[3] = st.cin;
+    info[4] = (int32_t)(st.t1 - st.t0);
+    info[5] = (int32_t)(st.t2 - st.t1);
+    info[6] = (int32_t)(st.t3 - st.t2);
+    info[7] = (int32_t)(t4 - st.t3);
+#ifdef HYLRA_TRACE
+    info[1] = (int32_t)(clock64() - t4);  // diagnostics build: compaction cycles in place of nw
+#endif
+  }
+}
+
 // ----------------------------------------------------------------------------- kernel
 // One selection row (slot, b, grp) by the NT threads 0..NT-1 of the calling CTA, with
 // sel_smem_bytes(n_valid, NT) bytes of shared memory at sraw. Called by
@@ -573,7 +1089,7 @@ __device__ void small_row_select(const SelectParams& p, const RowReader& rd, int
 // (twice the registers: the fused select of the FULL kernel, which has them to spare).
 template <int NT, bool PIPE = false>
 __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint8_t* sraw,
-                           Red& red, bool release) {
+                           Red& red, bool release, size_t smem_avail) {
   constexpr int kChunk = sel_chunk<NT>();
   const int tid = threadIdx.x;
   const int n = p.n_valid;
@@ -600,33 +1116,67 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
   }
   rd.hstride = p.row_stride;
 
+  // the row's histogram (token rows, sel_group 1; FULL kernel): read into registers and
+  // re-zeroed for the next step, whatever path the row then takes
+  constexpr int HPER = kHistBins / NT;
+  uint32_t hb[HPER];
+  const bool use_hist = p.hist != nullptr && p.sel_group == 1 && !p.pre_grouped;
+  const bool try_hist = use_hist && k < n && n > kSmallN &&
+                        sel_hist_smem_bytes(n, NT) <= smem_avail;
+  if (use_hist) {
+    uint4* h4 = reinterpret_cast<uint4*>(
+        p.hist + ((int64_t)(slot * p.B + b) * p.Hkv + grp) * kHistBins + tid * HPER);
+#pragma unroll
+    for (int q = 0; q < HPER / 4; ++q) {
+      const uint4 x = __ldcg(h4 + q);
+      hb[4 * q] = x.x;
+      hb[4 * q + 1] = x.y;
+      hb[4 * q + 2] = x.z;
+      hb[4 * q + 3] = x.w;
+      h4[q] = make_uint4(0, 0, 0, 0);
+    }
+  }
+
   if (k >= n) {
     // the budget covers the cache: every index (after the non-finite check)
     float nanacc = 0.f;
     for (int i = tid; i < n; i += NT) {
       nanacc = fmaf(rd.at(i), 0.f, nanacc);
       out[i] = i;
-      if (mir) mir[i] = i;
     }
     if (block_sum_int<NT>(nanacc != nanacc ? 1 : 0, red) && tid == 0) atomicOr(p.flags, 2);
     if (info && tid == 0) {
       for (int j = 0; j < 8; ++j) info[j] = 0;
       info[0] = k;
     }
+    copy_to_mirror<NT>(out, mir, k);
     return;
   }
 
   const int nwords = (int)(sel_bitmap_bytes(n, NT) / 4);
-  for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
-  for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
-  if (tid == 0) red.misc[3] = red.misc[5] = 0;
-
   const bool refine = p.q != nullptr;
   const int nch = (n + kChunk - 1) / kChunk;
   int above_w = 0, nw = 0, mode = 0, cin = 0;
   float tau_w = 0.f;  // refinement half-width
+  double* wv = sm.cv;  // the boundary window (value, index) for the re-score / rank step
+  int* wi = sm.ci;
   long long t1, t2, t3;
-  if (n <= kSmallN) {
+  long long hm[3] = {0, 0, 0};
+  const bool hist_done = try_hist &&
+                         hist_select<NT>(p, rd, hb, n, k, refine, sraw, red, &wv, &wi,
+                                         &above_w, &nw, &tau_w, &cin, hm);
+  if (!hist_done) {
+    for (int w = tid; w < nwords; w += NT) sm.bitmap[w] = 0u;
+    for (int j = tid; j < kBins; j += NT) sm.hist[j] = 0u;
+    if (tid == 0) red.misc[3] = red.misc[5] = 0;
+  }
+  if (hist_done) {
+    // phases: histogram + bin of rank k | row pass | exact T | window (+ the rest below)
+    mode = 6;
+    t1 = hm[0];
+    t2 = hm[1];
+    t3 = clock64();
+  } else if (n <= kSmallN) {
     small_row_select<NT>(p, rd, n, k, refine, sm, red, &above_w, &nw, &tau_w);
     mode = 3;
     t1 = t2 = t3 = clock64();
@@ -1119,87 +1669,220 @@ __device__ void select_row(const SelectParams& p, int grp, int b, int slot, uint
     t3 = clock64();
   }
 
-  // ---- window: re-score (refine) and keep the top k - above_w by (score desc, index asc)
-  if (nw > 0) {
-    sel_sync<NT>();
-    if (refine) {
-      if (p.block_size > 1)
-        rescore_f64_blocks<NT>(p, slot, b, grp, sm.ci, sm.cv, nw, tau_w, sm.keys);
-      else rescore_f64<NT>(p, slot, b, grp, sm.ci, sm.cv, nw);
-      sel_sync<NT>();
-    }
-    const int take = k - above_w;
-    for (int j = tid; j < nw; j += NT) {
-      const double vj = sm.cv[j];
-      const int ij = sm.ci[j];
-      int rank = 0;
-      for (int i = 0; i < nw; ++i) {
-        const double vi = sm.cv[i];
-        rank += (vi > vj) || (vi == vj && sm.ci[i] < ij);
+  SelStats st{mode, cin, t0, t1, t2, t3};
+  select_finish<NT>(p, grp, b, slot, sm.bitmap, wv, wi, nw, above_w, tau_w, refine, n, k, out,
+                    mir, info, red, release, sm.keys, st);
+}
+
+// ----------------------------------------------------------------------------- cooperative
+// Cooperative selection of a FULL pair's row inside the single-launch step (token rows,
+// sel_group 1). Selected by the pair's final CTA alone, a row is read in full (the score row
+// and its histogram) through ONE SM while every other SM streams K/V at the HBM roofline;
+// that SM's share of the saturated memory system (~10 GB/s) made the select ~40 us, the
+// critical path of small-batch steps (scripts/trace_single.py). Here the splits of the pair
+// share the work, each on its own slice of the row, in parallel across SMs:
+//  1. each split, done streaming, arrives on `arrive1`; the last one reads the row histogram
+//     (re-zeroing it), finds the bin of rank k and publishes the candidate range
+//     (coop_publish, release flag);
+//  2. each split classifies its slice, prefetched into shared memory while its split-K merge
+//     runs: bitmap words (tokens above the range) to the row's global bitmap, candidates to
+//     the row's global list, max / min / non-finite / counts by atomics; then it arrives on
+//     `arrive2` (coop_classify);
+//  3. the last one resolves the row — exact T among the candidates, the float64 window, the
+//     compaction — and re-zeroes the record (coop_final).
+// Same T, tau and window as the single-CTA paths, hence the same selection. A row the
+// histogram cannot serve, or with NaN / inf or too many candidates, is selected by step 3's
+// CTA through the sampled path over the global row.
+
+// Step 1: all NT threads of the last split to arrive.
+template <int NT>
+__device__ void coop_publish(const SelectParams& p, int row, CoopRow* rec, int n, Red& red) {
+  constexpr int HPER = kHistBins / NT;
+  const int tid = threadIdx.x;
+  uint32_t hb[HPER];
+  uint4* h4 = reinterpret_cast<uint4*>(p.hist + (int64_t)row * kHistBins + tid * HPER);
+#pragma unroll
+  for (int q = 0; q < HPER / 4; ++q) {
+    const uint4 x = __ldcg(h4 + q);
+    hb[4 * q] = x.x;
+    hb[4 * q + 1] = x.y;
+    hb[4 * q + 2] = x.z;
+    hb[4 * q + 3] = x.w;
+    h4[q] = make_uint4(0, 0, 0, 0);
+  }
+  int b1 = -1;
+  float c_lo = 0.f, c_hi = 0.f;
+  const bool refine = p.q != nullptr;
+  const bool ok = p.k_eff < n && n > kSmallN &&
+                  hist_b1<NT>(hb, n, p.k_eff, refine, p.tau_rel, red, &b1, &c_lo, &c_hi);
+  if (tid == 0) {
+    rec->b1 = ok ? b1 : -1;
+    rec->c_lo = c_lo;
+    rec->c_hi = c_hi;
+    __threadfence();
+    st_release_gpu(&rec->flag, 1);
+  }
+}
+
+// Step 2: all NT threads of every split. slice = the split's scores [s0, s1) in shared
+// memory (or null: read from the global row). Returns true in the last split to arrive.
+template <int NT>
+__device__ bool coop_classify(const SelectParams& p, int row, CoopRow* rec,
+                              const float* score_row, const float* slice, int s0, int s1,
+                              int n, int splits, Red& red) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    // bounded: a flag that never comes (a corrupted workspace) becomes HYLRA_FLAG_INTERNAL
+    for (long long spins = 0; ld_acquire_gpu(&rec->flag) == 0; ++spins) {
+      if (spins > (1ll << 25)) {
+        atomicOr(p.flags, 8);
+        break;
       }
-      if (rank < take) atomicOr(sm.bitmap + (ij >> 5), 1u << (ij & 31));
+      __nanosleep(32);
     }
   }
   sel_sync<NT>();
-
-  if (release) pdl_launch_dependents();
-  // ---- E. index-ordered compaction of the bitmap: 8 chunks per block scan (their
-  //         per-thread counts packed 2 x 16 bits per word), 2 barriers per 8 chunks
-  int run = 0;
-  if (nch == 1) {  // one chunk (wide CTAs, short rows): a single-word scan
-    const uint32_t w = sm.bitmap[tid];
-    int tot;
-    int pos = block_scan<NT>(__popc(w), &tot, red);
-    uint32_t m = w;
-    while (m) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1;
-      if (pos < k) {
-        out[pos] = tid * 32 + bit;
-        if (mir) mir[pos] = tid * 32 + bit;
+  (void)ld_acquire_gpu(&rec->flag);
+  const int b1 = __ldcg(&rec->b1);
+  if (b1 >= 0) {
+    const float c_lo = __ldcg(&rec->c_lo), c_hi = __ldcg(&rec->c_hi);
+    uint32_t* bits = p.coop_bits + (int64_t)row * p.coop_words;
+    float* cv = p.coop_cv + (int64_t)row * kHistCandCap;
+    int* ci = p.coop_ci + (int64_t)row * kHistCandCap;
+    float nanacc = 0.f, vmax = -INFINITY, vmin = INFINITY;
+    int c_above = 0;
+    const int w0 = s0 >> 5, w1 = (s1 + 31) >> 5;
+    for (int base = w0; base < w1; base += NT) {  // warp-uniform trips (warp_append)
+      const int w = base + tid;
+      uint32_t word = 0u, cand = 0u;
+      float4 vv[8];
+      if (w < w1) {
+        const float4* src = slice ? reinterpret_cast<const float4*>(slice + (32 * w - s0))
+                                  : reinterpret_cast<const float4*>(score_row + 32 * w);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) vv[u] = slice ? src[u] : __ldcg(src + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const float v = lane4(vv[u], cc);
+            if (32 * w + 4 * u + cc < s1) {
+              nanacc = fmaf(v, 0.f, nanacc);
+              vmax = fmaxf(vmax, v);
+              vmin = fminf(vmin, v);
+              word |= (v > c_hi) ? (1u << (u * 4 + cc)) : 0u;
+              cand |= (v >= c_lo && v <= c_hi) ? (1u << (u * 4 + cc)) : 0u;
+            }
+          }
+        }
+        bits[w] = word;
+        c_above += __popc(word);
       }
-      ++pos;
-    }
-    run = tot;
-  }
-  for (int c0 = 0; nch > 1 && c0 < nch; c0 += 8) {
-    uint32_t w[8], pk[4] = {0u, 0u, 0u, 0u};
+      int pos = warp_append(__popc(cand), &rec->n_cand);
+      while (cand) {
+        const int bit = __ffs(cand) - 1;
+        cand &= cand - 1;
+        if (pos < kHistCandCap) {
+          float e = vv[0].x;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      w[j] = (c0 + j < nch) ? sm.bitmap[(c0 + j) * NT + tid] : 0u;
-      pk[j >> 1] |= (uint32_t)__popc(w[j]) << (16 * (j & 1));
-    }
-    uint32_t ex[4], tot[4];
-    block_scan4<NT>(pk, ex, tot, red);
+          for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (c0 + j >= nch) break;
-      int pos = run + (int)((ex[j >> 1] >> (16 * (j & 1))) & 0xffffu);
-      uint32_t m = w[j];
-      while (m) {
-        const int bit = __ffs(m) - 1;
-        m &= m - 1;
-        if (pos < k) {
-          const int tok = (c0 + j) * kChunk + tid * 32 + bit;
-          out[pos] = tok;
-          if (mir) mir[pos] = tok;
+            for (int cc = 0; cc < 4; ++cc)
+              if (u * 4 + cc == bit) e = lane4(vv[u], cc);
+          cv[pos] = e;
+          ci[pos] = 32 * w + bit;
         }
         ++pos;
       }
-      run += (int)((tot[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+    }
+    float nmin = -vmin;
+    int bad = nanacc != nanacc ? 1 : 0, dummy = 0;
+    block_reduce_pass_b<NT>(vmax, nmin, bad, c_above, dummy, red);
+    if (tid == 0) {
+      atomicAdd(&rec->c_above, c_above);
+      atomicMax(&rec->vmax_key, float_key(vmax));
+      atomicMax(&rec->vmin_nkey, ~float_key(-nmin));
+      if (bad) atomicOr(&rec->bad, 1);
     }
   }
-  // invariant: exactly k indices were emitted
-  if (tid == 0 && run != k) atomicOr(p.flags, 8);
-  if (info && tid == 0) {
-    info[0] = k;
-    info[1] = nw;
-    info[2] = mode;
-    info[3] = cin;
-    info[4] = (int32_t)(t1 - t0);
-    info[5] = (int32_t)(t2 - t1);
-    info[6] = (int32_t)(t3 - t2);
-    info[7] = (int32_t)(clock64() - t3);
+  __threadfence();
+  sel_sync<NT>();
+  if (tid == 0) red.misc[15] = atomicAdd(&rec->arrive2, 1) == splits - 1;
+  sel_sync<NT>();
+  const bool last = red.misc[15] != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// Step 3: all NT threads of the last split; sraw = `avail` bytes of free shared memory.
+template <int NT>
+__device__ void coop_final(const SelectParams& p, int grp, int b, int slot, int row,
+                           CoopRow* rec, uint8_t* sraw, size_t avail, Red& red) {
+  const int tid = threadIdx.x;
+  const int n = p.n_valid, k = p.k_eff;
+  const long long t0 = clock64();
+  const int b1 = __ldcg(&rec->b1);
+  const int nc = __ldcg(&rec->n_cand);
+  const int c_above = __ldcg(&rec->c_above);
+  const int bad = __ldcg(&rec->bad);
+  const float vmax = key_float(__ldcg(&rec->vmax_key));
+  const float vmin = key_float(~__ldcg(&rec->vmin_nkey));
+  const int r = k - c_above;
+  const size_t bb = sel_bitmap_bytes(n, NT);
+  const bool refine = p.q != nullptr;
+  bool ok = b1 >= 0 && !bad && nc <= kHistCandCap && r >= 1 && r <= nc &&
+            bb + (size_t)kHistCandCap * 8 + (size_t)kHistBins * 4 <= avail;
+  const int row_id = (p.out_slot[slot] * p.B + b) * p.n_groups + grp;
+  int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
+  int32_t* mir = p.idx_mirror ? p.idx_mirror + (int64_t)row_id * p.k_stride : nullptr;
+  int32_t* info = p.info ? p.info + row_id * 8 : nullptr;
+#ifdef HYLRA_TRACE
+  if (info == nullptr && g_sel_info != nullptr) info = g_sel_info + row_id * 8;
+#endif
+  if (ok) {
+    uint32_t* bitmap = reinterpret_cast<uint32_t*>(sraw);
+    float* cand_v = reinterpret_cast<float*>(sraw + bb);
+    int* cand_i = reinterpret_cast<int*>(sraw + bb + 4 * (size_t)kHistCandCap);
+    uint8_t* scratch = sraw + bb + 8 * (size_t)kHistCandCap;
+    const uint32_t* bits = p.coop_bits + (int64_t)row * p.coop_words;
+    const float* cv = p.coop_cv + (int64_t)row * kHistCandCap;
+    const int* ci = p.coop_ci + (int64_t)row * kHistCandCap;
+    const int words = (n + 31) >> 5, nwords = (int)(bb / 4);
+    for (int w = tid; w < nwords; w += NT) bitmap[w] = w < words ? __ldcg(bits + w) : 0u;
+    for (int j = tid; j < nc; j += NT) {
+      cand_v[j] = __ldcg(cv + j);
+      cand_i[j] = __ldcg(ci + j);
+    }
+    sel_sync<NT>();
+    const long long t1 = clock64();
+    const float tau = refine ? fmaxf(p.tau_rel * fmaxf(fabsf(vmax), fabsf(vmin)), 1e-30f) : 0.f;
+    double* wv = nullptr;
+    int* wi = nullptr;
+    int above_add = 0, nw = 0;
+    ok = cands_window<NT>(cand_v, cand_i, nc, r, b1, tau, refine, scratch, bitmap, red, &wv, &wi,
+                          &above_add, &nw);
+    if (ok) {
+      SelStats st{7, nc, t0, t1, t1, clock64()};
+      select_finish<NT>(p, grp, b, slot, bitmap, wv, wi, nw, c_above + above_add, tau, refine, n,
+                        k, out, mir, info, red, false, nullptr, st);
+    }
+  }
+  if (!ok) {  // the sampled path over the global row (the histogram is already re-zeroed)
+    SelectParams q = p;
+    q.hist = nullptr;
+    q.coop = nullptr;
+    sel_sync<NT>();
+    select_row<NT, true>(q, grp, b, slot, sraw, red, false, avail);
+  }
+  if (tid == 0) {  // every other split is past its last access to the record
+    rec->arrive1 = 0;
+    rec->arrive2 = 0;
+    rec->flag = 0;
+    rec->n_cand = 0;
+    rec->c_above = 0;
+    rec->vmax_key = 0u;
+    rec->vmin_nkey = 0u;
+    rec->bad = 0;
   }
 }
 
@@ -1208,7 +1891,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_select_kernel(const Select
   extern __shared__ __align__(16) uint8_t sraw[];
   __shared__ Red red;
   pdl_wait();
-  select_row<NT>(p, blockIdx.x, blockIdx.y, blockIdx.z, sraw, red, true);
+  select_row<NT>(p, blockIdx.x, blockIdx.y, blockIdx.z, sraw, red, true, p.smem_bytes);
 }
 
 }  // namespace hylra

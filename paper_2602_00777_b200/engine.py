@@ -148,6 +148,7 @@ class HybridDecoder:
                                                      or sel_group > 1))
                            and k_cache.dtype == torch.bfloat16 and d in (64, 128))
         self.single = bool(single_launch) and self._single_ok
+        self.coop = False  # single-launch step with cooperative selects ("singlecoop")
         if self.single:
             self.dual = self.fused = False
         self._feeds_all = len(feeds) == len(self.full_layers)
@@ -175,29 +176,37 @@ class HybridDecoder:
 
     @property
     def schedule(self) -> str:
-        return ("single" if self.single else "fusedsel" if self.fused else
-                "dual" if self.dual else "fused3")
+        return (("singlecoop" if self.coop else "single") if self.single else
+                "fusedsel" if self.fused else "dual" if self.dual else "fused3")
 
     def set_schedule(self, name: str) -> None:
-        """Switch between the step schedules ("single", "fusedsel", "fused3"; block mode:
-        "single", "fused3"); every one gives bit-identical outputs and selections, only the
-        launch structure differs."""
-        if name not in ("single", "fusedsel", "fused3"):
+        """Switch between the step schedules ("single", "singlecoop", "fusedsel", "fused3";
+        block mode: "single", "fused3"); every one gives bit-identical outputs and
+        selections, only the launch structure differs. "singlecoop": the single-launch step
+        whose FULL splits select cooperatively (hylra_step_options fuse_select = 3; token
+        mode, sel_group 1)."""
+        if name not in ("single", "singlecoop", "fusedsel", "fused3"):
             raise ConfigurationError(f"unknown schedule {name!r}")
+        if name == "singlecoop" and not (self._single_ok and self._fused_ok):
+            raise ConfigurationError("schedule 'singlecoop' needs token mode, sel_group 1 and "
+                                     "the tensor-core path")
         if (name == "fusedsel" and not self._fused_ok) or (name == "single" and not self._single_ok):
             raise ConfigurationError(f"schedule {name!r} needs the tensor-core path (bf16, "
                                      "head_dim 64/128) and sel_group 1"
                                      + (", token mode and no sinks / recent"
                                         if name == "fusedsel" else ""))
-        self.single, self.fused, self.dual = name == "single", name == "fusedsel", False
+        self.single = name in ("single", "singlecoop")
+        self.coop = name == "singlecoop"
+        self.fused, self.dual = name == "fusedsel", False
         self._count_kernels()
 
     def autotune(self, q: torch.Tensor, n_valid: int | None = None, reps: int = 10) -> dict:
         """Time the schedules this decoder can run on these inputs (CUDA-graph replays, CUDA
         events on the current stream) and keep the fastest. Returns {schedule: ms}. The
         measured steps overwrite `out` / the selections (the next step rewrites them)."""
-        names = ([n for n, ok in (("single", self._single_ok), ("fusedsel", self._fused_ok))
-                  if ok] + ["fused3"])
+        names = ([n for n, ok in (("single", self._single_ok),
+                                  ("singlecoop", self._single_ok and self._fused_ok),
+                                  ("fusedsel", self._fused_ok)) if ok] + ["fused3"])
         times = {}
         cur = torch.cuda.current_stream(self.k.device)
         for name in names:
@@ -278,7 +287,7 @@ class HybridDecoder:
             self._grow_ws(need)
             opt = _abi.StepOptions()
             if self.single:
-                opt.fuse_select = 2
+                opt.fuse_select = 3 if self.coop else 2
             if self.dual or self.fused:
                 opt.fuse_select = int(self.fused)
                 opt.side_stream = self._side.cuda_stream

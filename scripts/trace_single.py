@@ -39,11 +39,13 @@ lib.hylra_trace_set_select_info(None)
 inf = info.view(-1, 8).cpu().numpy()
 inf = inf[inf[:, 0] != 0]
 if len(inf):
-    names = ["A sample", "B pass(+H)", "C+D", "E window+compact"]
+    names = (["hist", "row pass", "T+window", "rescore+rank"] if (inf[:, 2] == 6).all()
+             else ["A sample", "B pass(+H)", "C+D", "E window+compact"])
     print("  fused select phases (median cycles):",
           {nm: int(np.median(inf[:, 4 + j])) for j, nm in enumerate(names)},
           "modes", dict(zip(*[x.tolist() for x in np.unique(inf[:, 2], return_counts=True)])),
-          "band median", int(np.median(inf[:, 3])))
+          "band median", int(np.median(inf[:, 3])), "compaction (diag build)",
+          int(np.median(inf[:, 1])))
 tr = buf.view(-1, 8).cpu().numpy()
 n = int((tr[:, 0] != 0).sum())
 tr = tr[:n]
