@@ -385,7 +385,7 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, 
     B = 4 sharded by KV head, B = 16 partitioned by batch), split across the ranks."""
     from paper_2602_00777_b200 import _abi
     from paper_2602_00777_b200.attention import geometry, scores_row_stride
-    from paper_2602_00777_b200.engine import HybridDecoder, PipelinedDecoder
+    from paper_2602_00777_b200.engine import HybridDecoder, LayerwiseDecoder, PipelinedDecoder
     from paper_2602_00777_b200.sharding import gather_outputs, plan_shards
     from paper_2602_00777_b200.synthetic import generate_torch
 
@@ -416,6 +416,8 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, 
                                  dual_stream=kind == "dual",
                                  fuse_select=kind in ("fusedsel", "single"),
                                  single_launch=kind == "single")
+        if kind == "sequential":
+            return LayerwiseDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1)
         return PipelinedDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1,
                                 schedule=kind)
 

@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define HYLRA_ABI_VERSION 6
+#define HYLRA_ABI_VERSION 7
 
 enum hylra_status {
   HYLRA_OK = 0,
@@ -110,6 +110,16 @@ const char* hylra_status_string(int status);
 const char* hylra_last_error(void);
 /* Host-side count of kernels this library has launched (not graph replays). */
 uint64_t hylra_launch_count(void);
+/* Process-wide tuning overrides (ABI 7; value -1 restores the default rule):
+ *   "rowsel"         1/0: token rows that fit a CTA cluster's shared memory are selected by
+ *                    the shared-memory-resident select (default 1; env HYLRA_ROWSEL);
+ *   "select_threads" 128/256/512/1024: CTA width of the streaming select kernel (default:
+ *                    by row count; env HYLRA_SELECT_THREADS).
+ *   "rowsel_cluster" 1/2/4/8: CTAs per row of the shared-memory-resident select (default:
+ *                    the fewest that hold the row, doubled while the launch stays within
+ *                    one wave of SMs).
+ * Results never depend on them (every select path returns the same index sets). */
+int hylra_set_tuning(const char* name, int value);
 
 /* Bytes of zero-filled workspace the attention ops need for `n_layers` layer
  * slots processed in one call over `rows` rows (n_valid for FULL, k for REUSE). */
@@ -155,6 +165,29 @@ int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, co
                        const int32_t* src_slots, const int32_t* idx, const int32_t* counts,
                        int k_stride, int k_eff, int sel_group, float* out, void* ws,
                        size_t ws_bytes, void* stream);
+
+/*
+ * One layer of a LAYER-SEQUENTIAL decode step (ABI 7): the per-layer body of the reference's
+ * hybrid_decode loop (engine.py:174-194), for callers whose next layer's query depends on
+ * this layer's output (a real model's decode). Launches on `stream`, in order:
+ *   full = 1: FULL attention of `layer` over rows [0, n_valid) -> out; with `scores`
+ *             (fp32 [B][Hkv][round_up(capacity, 8)]) the layer's selection scores; with idx
+ *             as well, its top-min(budget, n_valid) selection (float64 refinement if refine)
+ *             into selection slot `slot` of idx ([slot][B][Hkv/sel_group][k_stride]) by a
+ *             second launch;
+ *   full = 0: REUSE attention of `layer` over the selection in slot `slot` of idx.
+ * prefetch = 1 lets the kernel's producer warps start loading K/V (REUSE: and the indices)
+ * before the previous kernel on the stream has finished (programmatic dependent launch;
+ * only the reads of q wait for it). The caller asserts that the previous kernel wrote none
+ * of those: e.g. not the first REUSE layer after the selection it reads. ws: zero-filled,
+ * hylra_attention_workspace_bytes(g, 1, max(n_valid, k)) bytes, flag word first; kernels of
+ * consecutive layers may overlap, so consecutive calls must alternate between two
+ * workspaces.
+ */
+int hylra_decode_layer(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                       int n_valid, int layer, int full, int slot, int budget, int sel_group,
+                       int refine, int prefetch, float* out, float* scores, int32_t* idx,
+                       int k_stride, void* ws, size_t ws_bytes, void* stream);
 
 /*
  * Block-level selection (paper §3.5; engine.py:212-286): per (slot, b, group) row the

@@ -27,7 +27,7 @@ __all__ = [
     "relative_l2_error", "similarity_from_counts", "LayerReuseError", "ConfigurationError",
     "NumericInputError", "InvalidSelectionError", "InvalidInputError", "CudaError",
     "TopKSet", "BlockSet", "full_attention", "topk_select", "block_select", "sparse_attention",
-    "HybridDecoder", "PipelinedDecoder", "DecodeLoop", "decode_step", "hybrid_decode",
+    "HybridDecoder", "PipelinedDecoder", "LayerwiseDecoder", "DecodeLoop", "decode_step", "hybrid_decode",
     "hybrid_decode_blocks", "run_full_trace", "build_similarity_matrix", "kl_extended",
     "LayerSensitivity", "SensitivityReport", "sensitivity_profile", "CostModelReport",
     "cost_model", "FidelityReport", "fidelity_report", "FidelityTable", "DecodeRunResult",
@@ -42,7 +42,7 @@ def __getattr__(name):
         from . import attention
         return getattr(attention, name)
     if name in ("HybridDecoder", "decode_step", "hybrid_decode", "hybrid_decode_blocks",
-                "run_full_trace", "PipelinedDecoder", "DecodeLoop",
+                "run_full_trace", "PipelinedDecoder", "LayerwiseDecoder", "DecodeLoop",
                 "build_similarity_matrix", "StepResult"):
         from . import engine
         return getattr(engine, name)

@@ -15,7 +15,7 @@ from .errors import STATUS_TO_ERROR, CudaError, LayerReuseError
 LIB_PATH = Path(os.environ.get("HYLRA_LIB") or Path(__file__).resolve().parent / "libhylra.so")
 
 # include/hylra.h HYLRA_ABI_VERSION this binding is written against (checked at load)
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 HYLRA_BF16 = 0
 HYLRA_F32 = 1
@@ -72,11 +72,13 @@ EXPORTED_SYMBOLS = (
     "hylra_status_string",
     "hylra_last_error",
     "hylra_launch_count",
+    "hylra_set_tuning",
     "hylra_attention_workspace_bytes",
     "hylra_select_workspace_bytes",
     "hylra_full_decode",
     "hylra_topk_select",
     "hylra_reuse_decode",
+    "hylra_decode_layer",
     "hylra_decode_step_workspace_bytes",
     "hylra_decode_step",
     "hylra_decode_step_offload",
@@ -159,6 +161,8 @@ def lib() -> ctypes.CDLL:
         l.hylra_status_string.argtypes = [i32]
         l.hylra_last_error.restype = ctypes.c_char_p
         l.hylra_launch_count.restype = ctypes.c_uint64
+        l.hylra_set_tuning.restype = i32
+        l.hylra_set_tuning.argtypes = [ctypes.c_char_p, i32]
         l.hylra_attention_workspace_bytes.restype = sz
         l.hylra_attention_workspace_bytes.argtypes = [gp, i32, i32]
         l.hylra_select_workspace_bytes.restype = sz
@@ -171,6 +175,9 @@ def lib() -> ctypes.CDLL:
         l.hylra_reuse_decode.restype = i32
         l.hylra_reuse_decode.argtypes = [gp, vp, vp, vp, i32, i32, vp, vp, vp, vp, i32, i32,
                                          i32, vp, vp, sz, vp]
+        l.hylra_decode_layer.restype = i32
+        l.hylra_decode_layer.argtypes = [gp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
+                                         vp, vp, vp, i32, vp, sz, vp]
         l.hylra_block_select.restype = i32
         l.hylra_block_select.argtypes = [gp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i32,
                                          vp, i32, vp, vp, vp, sz, vp]
@@ -224,6 +231,24 @@ def check(status: int) -> None:
 
 def launch_count() -> int:
     return int(lib().hylra_launch_count())
+
+
+class tuning:
+    """Context manager over hylra_set_tuning: `with _abi.tuning(rowsel=0): ...` runs the
+    block with the process-wide knobs set and restores the default rules afterwards."""
+
+    def __init__(self, **knobs):
+        self.knobs = knobs
+
+    def __enter__(self):
+        for name, value in self.knobs.items():
+            check(lib().hylra_set_tuning(name.encode(), int(value)))
+        return self
+
+    def __exit__(self, *exc):
+        for name in self.knobs:
+            lib().hylra_set_tuning(name.encode(), -1)
+        return False
 
 
 def int32_array(values) -> ctypes.Array:

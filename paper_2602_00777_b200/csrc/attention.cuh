@@ -73,6 +73,11 @@ struct AttnParams {
   // FULL: launch-local slots [0, fuse_select) select their rows inside the kernel (the last
   // CTA of a pair, once the pair's score row is complete); SelectParams come alongside
   int fuse_select;
+  // layer-sequential launches (hylra_decode_layer prefetch): the producer warps load K/V (and,
+  // REUSE, the indices) before griddepcontrol.wait — the caller guarantees the previous launch
+  // on the stream wrote none of them — so the pipeline fills while that launch drains; the
+  // consumer warps still wait before reading q
+  int early;
 };
 
 // Stage n selection indices from global into shared memory, validated (out-of-range ->
@@ -135,11 +140,17 @@ __device__ __forceinline__ void stage_indices(const int32_t* __restrict__ src, i
 // Cross-warp merge + split-K combine (shared by both kernel families).
 // sm_m/sm_l: [4][16], sm_o: [4][16][D] partial states of the 4 consumer warps, with
 // m in raw dot units (scaled by scale_log2 inside exp2).
+// scratch (optional, scratch_floats floats of shared memory the caller no longer uses): the
+// final CTA stages every split's (m, l) there and merges the output partials with 8 float4
+// L2 loads in flight per thread — a one-layer launch at B = 1 has ~40 splits per pair, whose
+// merge as dependent per-split loads took ~20 us. Same arithmetic, same order, either way.
 template <int D>
 __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, int b, int kh,
                                                 int split, const float* sm_m,
                                                 const float* sm_l, const float* sm_o,
-                                                int tid, int nthreads, int bar_id) {
+                                                int tid, int nthreads, int bar_id,
+                                                float* scratch = nullptr,
+                                                int scratch_floats = 0) {
   const int G = p.G;
   const int layer = p.layers[slot];
   const int pair = (slot * p.B + b) * p.Hkv + kh;
@@ -199,20 +210,82 @@ __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, i
   __threadfence();
   const float* po = p.ws_o + (int64_t)pair * p.splits * G * D;
   const float* pml = p.ws_ml + (int64_t)pair * p.splits * G * 2;
-  for (int e = tid; e < G * D; e += nthreads) {
-    const int g = e / D, d = e % D;
-    float M = -INFINITY;
-    for (int s = 0; s < p.splits; ++s) M = fmaxf(M, __ldcg(pml + (s * G + g) * 2));
-    float acc = 0.f, L = 0.f;
-    for (int s = 0; s < p.splits; ++s) {
-      const float ms = __ldcg(pml + (s * G + g) * 2);
-      const float sc = (ms == -INFINITY) ? 0.f : exp2f((ms - M) * c);
-      acc += __ldcg(po + (int64_t)(s * G + g) * D + d) * sc;
-      L += __ldcg(pml + (s * G + g) * 2 + 1) * sc;
+  const int SG = p.splits * G;
+  if (scratch != nullptr && 3 * SG + 2 * kMaxG <= scratch_floats) {
+    float* s_ml = scratch;          // [split][g][m, l]
+    float* s_sc = scratch + 2 * SG;  // [split][g] rescale factor
+    float* s_M = s_sc + SG;          // [g]
+    float* s_L = s_M + kMaxG;        // [g]
+    const float2* pml2 = reinterpret_cast<const float2*>(pml);
+    for (int i = tid; i < SG; i += nthreads) {
+      const float2 x = __ldcg(pml2 + i);
+      s_ml[2 * i] = x.x;
+      s_ml[2 * i + 1] = x.y;
     }
-    const float val = acc / L;
-    if (!isfinite(val)) atomicOr(p.flags, 2);  // NaN/inf in q, K or V
-    out_base[g * D + d] = val;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+    for (int g = tid; g < G; g += nthreads) {
+      float M = -INFINITY;
+      for (int s = 0; s < p.splits; ++s) M = fmaxf(M, s_ml[2 * (s * G + g)]);
+      s_M[g] = M;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+    for (int i = tid; i < SG; i += nthreads) {
+      const float ms = s_ml[2 * i];
+      s_sc[i] = (ms == -INFINITY) ? 0.f : exp2f((ms - s_M[i % G]) * c);
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+    for (int g = tid; g < G; g += nthreads) {
+      float L = 0.f;
+      for (int s = 0; s < p.splits; ++s) L = fmaf(s_ml[2 * (s * G + g) + 1], s_sc[s * G + g], L);
+      s_L[g] = L;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+    constexpr int D4 = D / 4;
+    const float4* po4 = reinterpret_cast<const float4*>(po);
+    for (int e4 = tid; e4 < G * D4; e4 += nthreads) {
+      const int g = e4 / D4, d = (e4 % D4) * 4;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      int s = 0;
+      auto add = [&](const float4& x, float sc) {
+        a0 = fmaf(x.x, sc, a0);
+        a1 = fmaf(x.y, sc, a1);
+        a2 = fmaf(x.z, sc, a2);
+        a3 = fmaf(x.w, sc, a3);
+      };
+      for (; s + 8 <= p.splits; s += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = __ldcg(po4 + (int64_t)(s + u) * G * D4 + e4);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) add(x[u], s_sc[(s + u) * G + g]);
+      }
+      for (; s < p.splits; ++s) add(__ldcg(po4 + (int64_t)s * G * D4 + e4), s_sc[s * G + g]);
+      const float L = s_L[g];
+      const float v0 = a0 / L, v1 = a1 / L, v2 = a2 / L, v3 = a3 / L;
+      if (!(isfinite(v0) && isfinite(v1) && isfinite(v2) && isfinite(v3)))
+        atomicOr(p.flags, 2);  // NaN/inf in q, K or V
+      float* o = out_base + g * D + d;
+      o[0] = v0;
+      o[1] = v1;
+      o[2] = v2;
+      o[3] = v3;
+    }
+  } else {
+    for (int e = tid; e < G * D; e += nthreads) {
+      const int g = e / D, d = e % D;
+      float M = -INFINITY;
+      for (int s = 0; s < p.splits; ++s) M = fmaxf(M, __ldcg(pml + (s * G + g) * 2));
+      float acc = 0.f, L = 0.f;
+      for (int s = 0; s < p.splits; ++s) {
+        const float ms = __ldcg(pml + (s * G + g) * 2);
+        const float sc = (ms == -INFINITY) ? 0.f : exp2f((ms - M) * c);
+        acc = fmaf(__ldcg(po + (int64_t)(s * G + g) * D + d), sc, acc);
+        L = fmaf(__ldcg(pml + (s * G + g) * 2 + 1), sc, L);
+      }
+      const float val = acc / L;
+      if (!isfinite(val)) atomicOr(p.flags, 2);  // NaN/inf in q, K or V
+      out_base[g * D + d] = val;
+    }
   }
   if (tid == 0) p.counters[pair] = 0;  // leave the workspace zeroed for the next call
   return true;
@@ -537,7 +610,9 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
     }
     mbar_fence_init();
   }
-  pdl_wait();  // before any global read: the previous launch may still be writing
+  // before any global read: the previous launch may still be writing (early: only the reads
+  // of q wait, in the consumer warps below)
+  if (!p.early) pdl_wait();
   if (ready_wait != nullptr && threadIdx.x == 0) {
     // single-launch step: this item's selection row (and its coverage count) is written by
     // a FULL item of the same grid. Bounded: a flag that never comes (it cannot, short of a
@@ -750,6 +825,7 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
   }
 
   // --------------------------------------------------------------- consumer warps
+  if (p.early) pdl_wait();  // q may be the previous launch's output
   const int g = lane >> 2;  // row of the m16n8 fragments (query head within the group)
   const int t = lane & 3;
   const int G = p.G;
@@ -866,8 +942,12 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
           make_float2(o[j][2], o[j][3]);
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
-  const bool final_cta = merge_and_store<D>(p, slot, b, kh, split, sm_m, sm_l, sm_o,
-                                            threadIdx.x, 128, 1);
+  // the merge's scratch: the REUSE index staging area / FULL histogram + score buffers, idle
+  // once the main loop is done
+  const bool final_cta = merge_and_store<D>(
+      p, slot, b, kh, split, sm_m, sm_l, sm_o, threadIdx.x, 128, 1,
+      reinterpret_cast<float*>(smem + STAGES * SM::kStageBytes + 256),
+      kIdxStage + 2 * STAGES * kTileRows);
   if constexpr (!GATHER) {
     if (coop) {
       asm volatile("cp.async.wait_group 0;" ::: "memory");

@@ -92,6 +92,18 @@ int splits_by_waves(int pairs, int tiles, int waves, int min_tiles) {
   return std::min(s, std::max(1, tiles / min_tiles));
 }
 
+// REUSE launches under one wave of 32-tile units: the smallest split (tiles per CTA);
+// HYLRA_REUSE_SMALL_TILES overrides (A/B runs).
+int small_reuse_tiles() {
+  static int v = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_REUSE_SMALL_TILES");
+    v = (e && *e) ? std::max(1, atoi(e)) : 8;
+  });
+  return v;
+}
+
 int choose_splits(int pairs, int tiles, bool gather) {
   static int env[2][2];
   static std::once_flag once;
@@ -127,7 +139,10 @@ int choose_splits(int pairs, int tiles, bool gather) {
       // indices together, the per-CTA start cost no longer favoured shorter units)
       s = s0;
     } else if (units <= kSlots) {
-      s = std::max(s0, std::min(kSlots / pairs, tiles / 8));
+      // under one wave (few pairs: one layer, small batch): split down to kSmallReuseTiles-
+      // tile CTAs, up to one wave (the final merge stages the split scales in shared memory,
+      // so many splits cost little)
+      s = std::max(s0, std::min(kSlots / pairs, tiles / small_reuse_tiles()));
     } else {
       const long full_waves = units / kSlots, rest = units % kSlots;
       s = (full_waves >= 2 || 2 * rest >= kSlots) ? s0
@@ -286,13 +301,14 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
                      const int32_t* kv_layer_ids = nullptr, int kv_layer_count = 0,
                      const SelectParams* fused = nullptr, int fuse_nslots = 0,
                      const int32_t* blk = nullptr, int blk_stride = 0, int blk_size = 0,
-                     int* counters = nullptr, unsigned* hist = nullptr) {
+                     int* counters = nullptr, unsigned* hist = nullptr, int early = 0) {
   AttnParams p{};
   AttnLayout lay{};
   if (int e = make_attn_params(&p, &lay, g, gather, q, k, v, n_valid, n_rows, n_layers, layer_ids,
                                src_slots, idx, counts, k_stride, sel_group, out, scores, ws,
                                ws_bytes, flags, kv_layer_ids, kv_layer_count, counters))
     return e;
+  p.early = early;
   // block-mode REUSE by TMA tiles of the selected blocks: REUSE split rules, the streaming
   // (TMA) kernel
   if (blk != nullptr) {
@@ -339,6 +355,8 @@ int select_threads(int rows) {
     // 128 = the fused select's width (diagnostics: scripts/select_diag.py)
     forced = (t == 128 || t == 256 || t == 512 || t == 1024) ? t : 0;
   });
+  const int o = tuning().select_threads.load(std::memory_order_relaxed);
+  if (o == 128 || o == 256 || o == 512 || o == 1024) return o;
   if (forced) return forced;
   if (rows <= num_sms()) return 1024;
   if (rows <= 2 * num_sms()) return 512;
@@ -416,9 +434,39 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
     return e;
   p.idx_mirror = idx_mirror;
   p.hist = hist;
+  cudaError_t ce;
+  // token rows that fit a CTA cluster's shared memory take the shared-memory-resident
+  // select (rowsel.cuh; same index sets) when the launch fits one wave of SMs (one CTA per
+  // SM: with more rows the streaming select's 4 CTAs per SM win), unless a CTA width is
+  // forced or the FULL kernel's row histograms must be consumed (HYLRA_ROWSEL=0: off;
+  // hylra_set_tuning("rowsel", 1): whatever the row count)
+  const int n_eff = br.block_size > 1 ? p.n_valid : n_valid;
+  const int rows = p.n_groups * g->batch * n_slots;
+  int csz = rowsel_cluster(n_eff);
+  const int forced_rs = tuning().rowsel.load(std::memory_order_relaxed);
+  if (csz > 0) {
+    // few rows: spread each over more CTAs (the select is instruction-bound per SM), as
+    // long as the whole launch stays within one wave of SMs
+    const int forced = tuning().rowsel_cluster.load(std::memory_order_relaxed);
+    if (forced == 1 || forced == 2 || forced == 4 || forced == 8) csz = std::max(csz, forced);
+    else
+      while (csz < kRowselMaxCluster && rows * csz * 2 <= num_sms() &&
+             n_eff / (2 * csz) >= kRowselMinSlice)
+        csz *= 2;
+  }
+  const bool one_wave = csz > 0 && rows * csz <= num_sms();
+  if (rowsel_enabled() && (one_wave || forced_rs == 1) && !force_nt && !hist &&
+      br.block_size <= 1 && csz > 0 &&
+      p.k_eff < n_eff && n_eff > kSmallN && (reinterpret_cast<uintptr_t>(scores) & 15) == 0) {
+    const int S = rowsel_slice(n_eff, csz);
+    dim3 grid(p.n_groups * csz, g->batch, n_slots);
+    ce = run_rowsel(csz, S, grid, rowsel_smem_bytes(S), st, p);
+    if (ce != cudaSuccess) return cuda_check(ce, "rowsel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_check(cudaGetLastError(), "rowsel launch");
+  }
   dim3 grid(p.n_groups, g->batch, n_slots);
   const int nt = force_nt ? force_nt : select_threads(p.n_groups * g->batch * n_slots);
-  cudaError_t ce;
   size_t smem = sel_smem_bytes(n_valid, nt);
   if (hist) smem = std::max(smem, sel_hist_smem_bytes(n_valid, nt));
   p.smem_bytes = (uint32_t)smem;
@@ -1034,6 +1082,17 @@ const char* hylra_last_error(void) { return g_err; }
 
 uint64_t hylra_launch_count(void) { return g_launches.load(); }
 
+int hylra_set_tuning(const char* name, int value) {
+  if (!name) return fail(HYLRA_ERR_CONFIGURATION, "NULL tuning name");
+  std::atomic<int>* knob = nullptr;
+  if (!strcmp(name, "rowsel")) knob = &tuning().rowsel;
+  else if (!strcmp(name, "select_threads")) knob = &tuning().select_threads;
+  else if (!strcmp(name, "rowsel_cluster")) knob = &tuning().rowsel_cluster;
+  if (!knob) return fail(HYLRA_ERR_CONFIGURATION, "unknown tuning knob '%s'", name);
+  knob->store(value < 0 ? -1 : value, std::memory_order_relaxed);
+  return HYLRA_OK;
+}
+
 size_t hylra_attention_workspace_bytes(const hylra_geometry* g, int n_layers, int rows) {
   if (check_geometry(g) || n_layers < 1) return 0;
   // either op (FULL or REUSE) may use the workspace
@@ -1061,6 +1120,47 @@ int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots,
   if (!ws || ws_bytes < kHeader) return fail(HYLRA_ERR_CONFIGURATION, "select workspace too small");
   return launch_select(g, scores, n_slots, n_valid, budget, sel_group, q, k, layer_ids, idx,
                        k_stride, info, static_cast<int*>(ws), static_cast<cudaStream_t>(stream));
+}
+
+int hylra_decode_layer(const hylra_geometry* g, const void* q, const void* k, const void* v,
+                       int n_valid, int layer, int full, int slot, int budget, int sel_group,
+                       int refine, int prefetch, float* out, float* scores, int32_t* idx,
+                       int k_stride, void* ws, size_t ws_bytes, void* stream) {
+  if (!g) return fail(HYLRA_ERR_CONFIGURATION, "NULL geometry");
+  if (int e = check_geometry(g)) return e;
+  if (budget < 1) return fail(HYLRA_ERR_INVALID_INPUT, "budget must be >= 1, got %d", budget);
+  if (sel_group < 1 || g->kv_heads % sel_group != 0)
+    return fail(HYLRA_ERR_CONFIGURATION, "sel_group %d does not divide kv_heads %d", sel_group,
+                g->kv_heads);
+  if (slot < 0 || slot >= kMaxSlots)
+    return fail(HYLRA_ERR_CONFIGURATION, "slot %d not in [0, %d)", slot, kMaxSlots);
+  if (!ws || ws_bytes < kHeader)
+    return fail(HYLRA_ERR_CONFIGURATION, "layer workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* flags = static_cast<int*>(ws);
+  const int32_t ids[1] = {layer};
+  const int32_t src[1] = {slot};
+  const int k_eff = std::min(budget, n_valid);
+  // the early loads need the TMA / cp.async producer warps of the tensor-core kernels
+  const int early = (prefetch && use_mma_path(g)) ? 1 : 0;
+  if (full) {
+    if (idx && !scores)
+      return fail(HYLRA_ERR_CONFIGURATION, "a FULL layer's selection needs its score rows");
+    if (int e = launch_attention(g, false, q, k, v, n_valid, n_valid, 1, ids, nullptr, nullptr,
+                                 nullptr, 0, 1, out, scores, ws, ws_bytes, flags, st, nullptr, 0,
+                                 nullptr, 0, nullptr, 0, 0, nullptr, nullptr, early))
+      return e;
+    if (!idx) return HYLRA_OK;
+    return launch_select(g, scores, 1, n_valid, budget, sel_group, refine ? q : nullptr,
+                         refine ? k : nullptr, ids, idx, k_stride, nullptr, flags, st,
+                         BlockRows(), nullptr, src);
+  }
+  if (!idx) return fail(HYLRA_ERR_CONFIGURATION, "a REUSE layer needs the selections");
+  if (k_stride < k_eff)
+    return fail(HYLRA_ERR_CONFIGURATION, "k_stride %d < selection size %d", k_stride, k_eff);
+  return launch_attention(g, true, q, k, v, n_valid, k_eff, 1, ids, src, idx, nullptr, k_stride,
+                          sel_group, out, nullptr, ws, ws_bytes, flags, st, nullptr, 0, nullptr,
+                          0, nullptr, 0, 0, nullptr, nullptr, early);
 }
 
 int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, const void* v,

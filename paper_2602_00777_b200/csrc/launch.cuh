@@ -5,6 +5,7 @@
 // in parallel; hylra_abi.cu holds the host logic and the extern "C" surface.
 #pragma once
 
+#include <atomic>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -12,6 +13,7 @@
 
 #include "attention.cuh"
 #include "select.cuh"
+#include "rowsel.cuh"
 
 namespace hylra {
 namespace host {
@@ -111,6 +113,34 @@ cudaError_t run_step_mma(int D, bool big, int n_items, cudaStream_t st, const CU
                          const CUtensorMap& tv, const AttnParams& pf, const AttnParams& pr,
                          const SelectParams& sp, const StepSync& ss);
 cudaError_t run_select(int nt, dim3 grid, size_t smem, cudaStream_t st, const SelectParams& p);
+cudaError_t run_rowsel(int cluster, int slice, dim3 grid, size_t smem, cudaStream_t st,
+                       const SelectParams& p);
+
+// Process-wide tuning overrides set through hylra_set_tuning (-1: the environment /
+// automatic rule applies).
+struct Tuning {
+  std::atomic<int> rowsel{-1};
+  std::atomic<int> select_threads{-1};
+  std::atomic<int> rowsel_cluster{-1};
+};
+inline Tuning& tuning() {
+  static Tuning t;
+  return t;
+}
+
+// The shared-memory-resident select (rowsel.cuh) for the rows it covers; HYLRA_ROWSEL=0
+// (or hylra_set_tuning("rowsel", 0)) keeps every row on select_row (A/B runs).
+inline bool rowsel_enabled() {
+  const int o = tuning().rowsel.load(std::memory_order_relaxed);
+  if (o >= 0) return o != 0;
+  static int v = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_ROWSEL");
+    v = (e && *e) ? (atoi(e) != 0) : 1;
+  });
+  return v == 1;
+}
 
 }  // namespace host
 }  // namespace hylra

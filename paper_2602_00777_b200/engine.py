@@ -496,9 +496,8 @@ class PipelinedDecoder(HybridDecoder):
     the HBM-bound FULL stream; only the last FULL layer's selection is exposed. Captured
     into a CUDA graph the whole step is one replay.
 
-    schedule="sequential" instead runs the layers strictly in order on one stream (FULL +
-    SELECT or REUSE per layer), the order a real model's decode imposes when layer l+1's
-    query depends on layer l's output.
+    The layer-sequential order a real model's decode imposes (layer l+1's query depends on
+    layer l's output) is LayerwiseDecoder.
     """
 
     def __init__(self, policy, k_cache, v_cache, budget, *, q_heads, sel_group=1,
@@ -506,8 +505,9 @@ class PipelinedDecoder(HybridDecoder):
         super().__init__(policy, k_cache, v_cache, budget, q_heads=q_heads,
                          sel_group=sel_group, refine=refine, dual_stream=False,
                          fuse_select=False)
-        if schedule not in ("pipelined", "sequential"):
-            raise ConfigurationError(f"unknown schedule {schedule!r}")
+        if schedule != "pipelined":
+            raise ConfigurationError(f"unknown schedule {schedule!r} (the layer-sequential "
+                                     "schedule is LayerwiseDecoder)")
         self.pipe_schedule = schedule
         L, B, Hkv, cap, d = k_cache.shape
         from .attention import scores_row_stride
@@ -583,6 +583,152 @@ class PipelinedDecoder(HybridDecoder):
         if side is not main:
             main.wait_stream(side)
         return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
+
+
+class LayerwiseDecoder(HybridDecoder):
+    """Layer-sequential decode: the reference's per-layer loop (engine.py:174-194) one layer
+    at a time, for callers whose layer l+1 query depends on layer l's output (a model's
+    decode). `layer(l, q)` enqueues layer l on the current stream (hylra_decode_layer):
+
+    * FULL layer feeding REUSE layers: FULL attention + score emission, then its selection
+      (the shared-memory-resident select for few rows), both on the stream — the next REUSE
+      layer needs the indices;
+    * FULL layer no REUSE layer reads: FULL attention on the stream, its selection on a
+      high-priority side stream (joined by `finish()`): only the step's output waits for it;
+    * REUSE layer: the gather over its source FULL layer's selection.
+
+    Every launch uses programmatic dependent launch with early loads: the producer warps
+    of layer l+1 start streaming K/V (REUSE: the indices and gathered rows) while layer l
+    drains, and only the reads of q wait for it — except the first REUSE layer after a
+    selection and the step's first layer (whose inputs the previous launch may have
+    written). Consecutive layers alternate between two workspaces. Selections are
+    bit-identical to HybridDecoder.step's; outputs agree within bf16 rounding (a one-layer
+    launch partitions its rows into more split-K splits than the batched step's)."""
+
+    def __init__(self, policy, k_cache, v_cache, budget, *, q_heads, sel_group=1,
+                 refine=True, prefetch=True):
+        super().__init__(policy, k_cache, v_cache, budget, q_heads=q_heads,
+                         sel_group=sel_group, refine=refine, dual_stream=False,
+                         fuse_select=False, single_launch=False)
+        L, B, Hkv, cap, d = k_cache.shape
+        from .attention import scores_row_stride
+        self.prefetch = bool(prefetch)
+        self.scores = torch.empty((len(self.full_layers), B, Hkv, scores_row_stride(cap)),
+                                  dtype=torch.float32, device=k_cache.device)
+        # does some REUSE layer inherit FULL slot s?
+        self.feeds = [any(self.actions[l] is Action.REUSE and self.slot_of_layer[l] == s
+                          for l in range(L)) for s in range(len(self.full_layers))]
+        self.side = torch.cuda.Stream(device=k_cache.device, priority=-8)
+        n_side = sum(1 for f in self.feeds if not f)
+        self._ev = [(torch.cuda.Event(), torch.cuda.Event()) for _ in range(max(n_side, 1))]
+        self._wsl = [torch.zeros(256, dtype=torch.uint8, device=k_cache.device)
+                     for _ in range(2)]
+        self._side_ws = torch.zeros(256, dtype=torch.uint8, device=k_cache.device)
+        self._turn = 0       # workspace of the next launch
+        self._prev = None    # what the previous launch on the stream wrote: "sel" / other
+        self._pending = []   # side-stream selections to join
+        self.kernels_per_step = L + len(self.full_layers)
+
+    @property
+    def schedule(self) -> str:
+        return "sequential"
+
+    def _ws_for(self, need: int) -> torch.Tensor:
+        t = self._wsl[self._turn]
+        if t.numel() < need:
+            t2 = torch.zeros(need, dtype=torch.uint8, device=t.device)
+            t2[:8].copy_(t[:8])
+            self._wsl[self._turn] = t = t2
+        self._turn ^= 1
+        return t
+
+    def layer(self, l: int, q: torch.Tensor, n_valid: int | None = None) -> torch.Tensor:
+        """Enqueue layer l (q: the [L, B, Hq, d] query stack; layer l's rows are read) on
+        the current stream; returns out[l] (final once the stream reaches it)."""
+        lib = _abi.lib()
+        g = self._geometry(q)
+        n_valid = g.capacity if n_valid is None else int(n_valid)
+        k_eff = min(self.budget, n_valid)
+        main = torch.cuda.current_stream(self.k.device)
+        st = main.cuda_stream
+        s = self.slot_of_layer[l]
+        first = l == 0
+        if self.actions[l] is Action.FULL:
+            ws = self._ws_for(int(lib.hylra_attention_workspace_bytes(g, 1, n_valid)))
+            sc = self.scores[s]
+            sel_here = self.feeds[s]
+            _abi.check(lib.hylra_decode_layer(
+                g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, l, 1, s,
+                self.budget, self.sel_group, int(self.refine),
+                int(self.prefetch and not first), self.out.data_ptr(), sc.data_ptr(),
+                self.idx.data_ptr() if sel_here else None, self.k_stride, ws.data_ptr(),
+                ws.numel(), st))
+            if sel_here:
+                self._prev = "sel"
+            else:
+                # the selection only feeds the step's output: off the critical path
+                e_fork, e_join = self._ev[len(self._pending)]
+                e_fork.record(main)
+                self.side.wait_event(e_fork)
+                _abi.check(lib.hylra_topk_select(
+                    g, sc.data_ptr(), 1, n_valid, self.budget, self.sel_group,
+                    q.data_ptr() if self.refine else None,
+                    self.k.data_ptr() if self.refine else None, _abi.int32_array([l]),
+                    self.idx[s].data_ptr(), self.k_stride, None, self._side_ws.data_ptr(),
+                    self._side_ws.numel(), self.side.cuda_stream))
+                e_join.record(self.side)
+                self._pending.append(e_join)
+                self._prev = "full"
+        else:
+            ws = self._ws_for(int(lib.hylra_attention_workspace_bytes(g, 1, k_eff)))
+            early = self.prefetch and not first and self._prev != "sel"
+            _abi.check(lib.hylra_decode_layer(
+                g, q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), n_valid, l, 0, s,
+                self.budget, self.sel_group, int(self.refine), int(early),
+                self.out.data_ptr(), None, self.idx.data_ptr(), self.k_stride, ws.data_ptr(),
+                ws.numel(), st))
+            self._prev = "reuse"
+        return self.out[l]
+
+    def finish(self) -> None:
+        """Join the side-stream selections into the current stream (end of a step)."""
+        main = torch.cuda.current_stream(self.k.device)
+        for e in self._pending:
+            main.wait_event(e)
+        self._pending = []
+        self._prev = None
+
+    def step(self, q: torch.Tensor, n_valid: int | None = None) -> StepResult:
+        g = self._geometry(q)
+        n_valid = g.capacity if n_valid is None else int(n_valid)
+        self._prev = None
+        for l in range(len(self.actions)):
+            self.layer(l, q, n_valid)
+        self.finish()
+        k_eff = min(self.budget, n_valid)
+        return StepResult(self.out, self.idx[..., :k_eff], self.slot_of_layer, self.full_layers)
+
+    def _flag_words(self):
+        """[flag word OR-ed over the workspaces, refine-skipped rows summed] (synchronises)."""
+        w = torch.stack([t[:8].view(torch.int32)[:2] for t in (*self._wsl, self._side_ws)])
+        words = w.cpu().tolist()
+        flag = 0
+        for f, _ in words:
+            flag |= f
+        return [flag, sum(n for _, n in words)]
+
+    def flags(self) -> int:
+        return self._flag_words()[0]
+
+    def refine_skipped_rows(self) -> int:
+        return self._flag_words()[1]
+
+    def check_flags(self, strict: bool = False) -> None:
+        _abi.raise_for_flags(self._flag_words(), strict)
+
+    def clear_flags(self) -> None:
+        for t in (*self._wsl, self._side_ws):
+            t[:8].zero_()
 
 
 def _runs(layers):

@@ -45,6 +45,25 @@ def test_bench_config_single_launch_matches_oracle(name, batch):
     _free()
 
 
+@pytest.mark.parametrize("batch", [1, 8])
+def test_layer_sequential_decode_matches_oracle(batch):
+    """The layer-sequential schedule (LayerwiseDecoder: one FULL / SELECT / REUSE launch per
+    layer with early loads) at the headline config, against the float64 oracle."""
+    from paper_2602_00777_b200.engine import LayerwiseDecoder
+    cfg = CONFIGS["cfg2"].with_(batch=batch)
+    q, k, v = generate_torch(cfg, "cuda")
+    dec = LayerwiseDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
+    res = dec.step(q, cfg.context)
+    torch.cuda.synchronize()
+    dec.check_flags(strict=True)
+    summary = check_step(q, k, v, cfg.context, cfg.actions, cfg.budget, res.outputs,
+                         res.selections, res.slot_of_layer)
+    print("sequential", batch, summary)
+    assert summary["pairs"] == cfg.layers * batch * cfg.kv_heads
+    del dec, res, q, k, v
+    _free()
+
+
 def test_decode_loop_e2e_step_matches_oracle():
     cfg = CONFIGS["cfg2"]
     q, k, v = generate_torch(cfg, "cuda")

@@ -118,9 +118,13 @@ def test_topk_select_exact(n, budget, kind):
     (2, 262144, 16384, "normal"),    # longest supported row (bitmap 32 KB)
     (300, 262144, 4096, "planted"),
 ])
-def test_topk_select_exact_all_cta_widths(rows, n, budget, kind):
-    """The SELECT CTA width follows the row count (1024 / 512 / 256 threads): every width
-    returns the reference's exact sets, including at the maximum row length."""
+@pytest.mark.parametrize("impl", ["rowsel", "stream"])
+def test_topk_select_exact_all_cta_widths(rows, n, budget, kind, impl):
+    """The streaming SELECT's CTA width follows the row count (1024 / 512 / 256 threads) and
+    the shared-memory-resident select (rowsel.cuh) covers rows up to 8 x 40960 tokens on CTA
+    clusters: every width and cluster size returns the reference's exact sets, including at
+    the maximum row length."""
+    from paper_2602_00777_b200 import _abi
     rng = np.random.default_rng(rows * 7 + n)
     if kind == "normal":
         x = rng.standard_normal((rows, n)).astype(np.float32)
@@ -135,7 +139,8 @@ def test_topk_select_exact_all_cta_widths(rows, n, budget, kind):
     rs = (n + 7) & ~7
     buf = np.zeros((1, rows, 1, rs), dtype=np.float32)
     buf[0, :, 0, :n] = x
-    got = topk_select(torch.from_numpy(buf).to(DEV), budget, n).cpu().numpy()
+    with _abi.tuning(rowsel=1 if impl == "rowsel" else 0):
+        got = topk_select(torch.from_numpy(buf).to(DEV), budget, n).cpu().numpy()
     for r in range(rows):
         want = orc.topk_of_logits(x[r].astype(np.float64), budget)
         np.testing.assert_array_equal(got[0, r, 0], want)
@@ -253,15 +258,19 @@ def test_policy_must_start_full():
         HybridDecoder(("reuse", "full"), k, v, 8, q_heads=4)
 
 
-@pytest.mark.parametrize("schedule", ["pipelined", "sequential"])
+@pytest.mark.parametrize("schedule", ["pipelined", "sequential", "sequential-noprefetch"])
 def test_pipelined_schedules_match_fused(schedule):
-    from paper_2602_00777_b200.engine import PipelinedDecoder
+    from paper_2602_00777_b200.engine import LayerwiseDecoder, PipelinedDecoder
     L, B, Hq, Hkv, d, cap, budget = 8, 2, 16, 4, 128, 4096, 256
     q, k, v, qn, kn, vn = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=21, planted=64)
     actions = ("full", "reuse", "full", "full", "reuse", "reuse", "full", "reuse")
     ref = HybridDecoder(actions, k, v, budget, q_heads=Hq).step(q, cap)
     ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
-    dec = PipelinedDecoder(actions, k, v, budget, q_heads=Hq, schedule=schedule)
+    if schedule.startswith("sequential"):
+        dec = LayerwiseDecoder(actions, k, v, budget, q_heads=Hq,
+                               prefetch=schedule == "sequential")
+    else:
+        dec = PipelinedDecoder(actions, k, v, budget, q_heads=Hq, schedule=schedule)
     res = dec.step(q, cap)
     torch.cuda.synchronize()
     assert torch.equal(res.selections, ref_idx)
@@ -731,3 +740,38 @@ def test_single_launch_with_selection_groups(sel_group, Hkv, Hq, B):
         dec.check_flags()
         assert torch.equal(res.selections, S)
         assert torch.equal(res.outputs, R)
+
+
+def test_layerwise_prefetch_matches_waiting_launches_across_steps():
+    """LayerwiseDecoder's early loads (K/V and indices before griddepcontrol.wait) never read
+    stale data: with queries alternating between steps (so every step's selections differ
+    from the previous step's), the prefetching decoder equals the waiting one bit for bit,
+    eagerly and as CUDA-graph replays."""
+    from paper_2602_00777_b200.engine import LayerwiseDecoder
+    L, B, Hq, Hkv, d, cap, budget = 8, 2, 16, 4, 128, 8192, 512
+    q1, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=5, planted=64)
+    q2 = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=6, planted=64)[0]
+    actions = ("full", "reuse", "reuse", "full", "full", "reuse", "reuse", "reuse")
+    pre = LayerwiseDecoder(actions, k, v, budget, q_heads=Hq, prefetch=True)
+    wait = LayerwiseDecoder(actions, k, v, budget, q_heads=Hq, prefetch=False)
+    for qq in (q1, q2, q1, q2):
+        a, b = pre.step(qq, cap), wait.step(qq, cap)
+        torch.cuda.synchronize()
+        assert torch.equal(a.outputs, b.outputs) and torch.equal(a.selections, b.selections)
+    pre.check_flags(strict=True)
+    qs = q1.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        pre.step(qs, cap)
+    torch.cuda.current_stream().wait_stream(s)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        pre.step(qs, cap)
+    for qq in (q2, q1, q2):
+        qs.copy_(qq)
+        gr.replay()
+        ref = wait.step(qq, cap)
+        torch.cuda.synchronize()
+        assert torch.equal(pre.out, ref.outputs)
+        assert torch.equal(pre.idx[..., :budget], ref.selections)
