@@ -480,6 +480,9 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, 
         del g2, d2
 
     check = _sanity_check(torch, cfg, q, k, v, dec)
+    # selection rows whose float64 boundary refinement was skipped (window over kCandCap):
+    # their k-th boundary followed fp32 order (HYLRA_FLAG_REFINE_SKIPPED; 0 expected)
+    refine_skipped = dec.refine_skipped_rows()
 
     clocks = ClockSampler(_env_int("LOCAL_RANK", 0))
     clocks.start()
@@ -638,7 +641,7 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, 
                       "traffic": ncu.get("full_traffic_bytes_per_launch")}),
         "schedule": kind_used, "parallelism": f"{mode}-shard{world}",
         "gpu_launches": dec.kernels_per_step * a.steps,
-        "schedules": schedules, "check": check,
+        "schedules": schedules, "check": check, "refine_skipped_rows": refine_skipped,
         "e2e": e2e_line, "clocks": clk,
     }
     del graph, dec, q, k, v, scores
@@ -659,6 +662,9 @@ def run_ours(a):
     torch.cuda.set_device(local % n_dev)
     shared_gpu = world > n_dev  # functional check only: ranks share GPUs, gloo collectives
     if world > 1:
+        # communicator setup (ring / NVLS / P2P transport) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if shared_gpu:
             dist.init_process_group("gloo")
         else:
@@ -682,7 +688,7 @@ def run_ours(a):
     if not a.no_extra:
         keys = ("value", "ms_per_step", "global_batch", "scaling", "step_gbs",
                 "per_gpu_hbm_gbs", "per_gpu_frac_of_peak", "kernels", "roofline", "schedule",
-                "schedules", "parallelism", "check")
+                "schedules", "parallelism", "check", "refine_skipped_rows")
         # BASELINE configs 3 and 4 at their GLOBAL batch (strong scaling): config 3 B = 4
         # sharded by KV head, config 4 B = 16 partitioned by batch
         c3 = CONFIGS["cfg3"]
@@ -735,6 +741,7 @@ def run_ours(a):
             "cpu_baseline": cpu, "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
             "clocks": main["clocks"], "schedule": main["schedule"],
             "schedules": main["schedules"], "check": main["check"],
+            "refine_skipped_rows": main["refine_skipped_rows"],
             **({"functional_only": f"{world} ranks on {n_dev} GPU(s), gloo collectives: "
                                    "not a scaling measurement"} if shared_gpu else {}),
             "extra": extra,

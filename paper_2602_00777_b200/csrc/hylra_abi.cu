@@ -92,14 +92,15 @@ int splits_by_waves(int pairs, int tiles, int waves, int min_tiles) {
   return std::min(s, std::max(1, tiles / min_tiles));
 }
 
-// REUSE launches under one wave of 32-tile units: the smallest split (tiles per CTA);
+// REUSE launches under one wave of 32-tile units: the smallest split (tiles per CTA; 4:
+// one-layer REUSE at cfg2 B=1 in the layer-sequential step, 4 vs 8 tiles: 576 vs 619 us/step);
 // HYLRA_REUSE_SMALL_TILES overrides (A/B runs).
 int small_reuse_tiles() {
   static int v = 0;
   static std::once_flag once;
   std::call_once(once, [] {
     const char* e = std::getenv("HYLRA_REUSE_SMALL_TILES");
-    v = (e && *e) ? std::max(1, atoi(e)) : 8;
+    v = (e && *e) ? std::max(1, atoi(e)) : 4;
   });
   return v;
 }

@@ -47,8 +47,10 @@ constexpr int kRowselMinSlice = 4096;   // no finer split when spreading few row
 // Tokens per CTA for an n-token row on a C-CTA cluster (a whole number of bitmap words).
 __host__ __device__ constexpr int rowsel_slice(int n, int c) { return ((n + c - 1) / c + 31) & ~31; }
 // Dynamic shared memory: row slice, window values / indices, two histograms, bitmap.
+constexpr int kRsQMax = 2048;  // staged query floats: sel_group x G x D (refinement)
 __host__ __device__ constexpr size_t rowsel_smem_bytes(int slice) {
-  return (size_t)slice * 4 + (size_t)kCandCap * 12 + 2 * kBins * 4 + (size_t)slice / 8 + 128;
+  return (size_t)slice * 4 + (size_t)kCandCap * 12 + 2 * kBins * 4 + (size_t)slice / 8 +
+         (size_t)kRsQMax * 4 + 128;
 }
 // Smallest cluster (power of two, <= kRowselMaxCluster) whose slices fit; 0 = none.
 __host__ __device__ constexpr int rowsel_cluster(int n) {
@@ -78,6 +80,68 @@ __device__ __forceinline__ T* rs_peer(T* p, int r) {
   else return p;
 }
 
+// float64 selection score of window token `tok` (token_score_f64's arithmetic, operation for
+// operation, so the two selects rank a window identically) with the group's query heads
+// staged in shared memory as floats (qs[(hh G + g) D + i], exact bf16 / fp32 values) and the
+// token's K values fetched once into registers: one memory round trip per token instead of
+// one per query head. kLpt lanes per token; every lane of the warp must call it.
+__device__ __forceinline__ double rs_token_score(const SelectParams& p, const float* qs, int kvl,
+                                                 int b, int grp, int tok) {
+  const int sub = threadIdx.x & (kLpt - 1);
+  const double sqd = sqrt((double)p.D);
+  constexpr int kMaxPer = 128 / kLpt;  // K values per lane (head_dim <= 128)
+  double agg = 0.0;
+  for (int hh = 0; hh < p.sel_group; ++hh) {
+    const int kh = grp * p.sel_group + hh;
+    const int64_t koff = kvl * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
+    // all of the token's loads issued back to back (branch-free: the dtype test is hoisted
+    // and indices past head_dim are clamped, their values unused): one memory latency
+    float kv[kMaxPer];
+    if (p.dtype == 0) {
+      const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.k) + koff;
+#pragma unroll
+      for (int j = 0; j < kMaxPer; ++j) kv[j] = __bfloat162float(kp[min(sub + j * kLpt, p.D - 1)]);
+    } else {
+      const float* kp = reinterpret_cast<const float*>(p.k) + koff;
+#pragma unroll
+      for (int j = 0; j < kMaxPer; ++j) kv[j] = kp[min(sub + j * kLpt, p.D - 1)];
+    }
+    for (int g = 0; g < p.G; ++g) {
+      const float* qr = qs + (hh * p.G + g) * p.D;
+      double part0 = 0.0, part1 = 0.0;
+#pragma unroll
+      for (int j = 0; j + 1 < kMaxPer; j += 2) {
+        const int i = sub + j * kLpt;
+        if (i < p.D) {
+          part0 += (double)qr[i] * (double)kv[j];
+          part1 += (double)qr[i + kLpt] * (double)kv[j + 1];
+        }
+      }
+      double part = part0 + part1;
+#pragma unroll
+      for (int o = kLpt / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      agg += part / sqd;
+    }
+  }
+  return agg;
+}
+
+template <int NT>
+__device__ void rs_rescore(const SelectParams& p, const float* qs, int slot, int b, int grp,
+                           const int* toks, double* vals, int n) {
+  if (qs == nullptr) {
+    rescore_f64<NT>(p, slot, b, grp, toks, vals, n);
+    return;
+  }
+  const int warp = threadIdx.x >> 5, sub = threadIdx.x & (kLpt - 1);
+  const int slot_in_warp = (threadIdx.x & 31) / kLpt;
+  for (int c0 = warp * kTpw; c0 < n; c0 += (NT / 32) * kTpw) {  // warp-uniform trip count
+    const int c = c0 + slot_in_warp;
+    const double agg = rs_token_score(p, qs, p.kv_layers[slot], b, grp, toks[min(c, n - 1)]);
+    if (sub == 0 && c < n) vals[c] = agg;
+  }
+}
+
 template <int C>
 __global__ void __launch_bounds__(kRowselThreads, 1) rowsel_kernel(const SelectParams p, int S) {
   constexpr int NT = kRowselThreads, NW = NT / 32;
@@ -98,7 +162,8 @@ __global__ void __launch_bounds__(kRowselThreads, 1) rowsel_kernel(const SelectP
   double* wv = reinterpret_cast<double*>(rs_smem + (size_t)S * 4);  // CTA 0: candidates / window
   int* wi = reinterpret_cast<int*>(wv + kCandCap);
   unsigned* hist = reinterpret_cast<unsigned*>(wi + kCandCap);  // [2][kBins]
-  uint32_t* bitmap = hist + 2 * kBins;                          // [words]
+  uint32_t* bitmap = hist + 2 * kBins;                          // [S / 32]
+  float* qs = reinterpret_cast<float*>(bitmap + S / 32);        // [kRsQMax] staged queries
   const int row_id = (p.out_slot[slot] * p.B + b) * p.n_groups + grp;
   int32_t* out = p.idx + (int64_t)row_id * p.k_stride;
   int32_t* mir = p.idx_mirror ? p.idx_mirror + (int64_t)row_id * p.k_stride : nullptr;
@@ -129,15 +194,26 @@ __global__ void __launch_bounds__(kRowselThreads, 1) rowsel_kernel(const SelectP
       : p.scores + ((int64_t)(slot * p.B + b) * p.Hkv + grp * p.sel_group) * p.row_stride;
   const int sg = p.pre_grouped ? 1 : p.sel_group;
   const uint32_t bytes = (uint32_t)((m * 4 + 15) & ~15);
-  if (bytes > 0) {
-    if (tid == 0) {
-      mbar_arrive_expect_tx(&bar, bytes);
-      for (uint32_t off = 0; off < bytes; off += 32768u)
-        bulk_load(rs_smem + off, reinterpret_cast<const uint8_t*>(rbase + lo) + off,
-                  min(32768u, bytes - off), &bar);
-    }
-    mbar_wait(&bar, 0);
+  if (bytes > 0 && tid == 0) {
+    mbar_arrive_expect_tx(&bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_load(rs_smem + off, reinterpret_cast<const uint8_t*>(rbase + lo) + off,
+                min(32768u, bytes - off), &bar);
   }
+  // CTA 0 stages the group's query heads for the float64 re-score while the slice lands
+  const int nq = p.sel_group * p.G * p.D;
+  const bool stage_q = refine && cr == 0 && nq <= kRsQMax && p.D <= 128 && p.D % 16 == 0;
+  if (stage_q) {
+    for (int e = tid; e < nq; e += NT) {
+      const int head = e / p.D, i = e % p.D;  // head = hh G + g
+      const int hh = head / p.G, g = head % p.G;
+      const int kh = grp * p.sel_group + hh;
+      const int64_t qo = p.layers[slot] * p.q_sl + b * p.q_sb + (int64_t)(kh * p.G + g) * p.D + i;
+      qs[e] = p.dtype == 0 ? (float)elem_f64<__nv_bfloat16>(p.q, qo) : (float)elem_f64<float>(p.q, qo);
+    }
+  }
+  const float* qsp = stage_q ? qs : nullptr;
+  if (bytes > 0) mbar_wait(&bar, 0);
   const long long t1 = clock64();  // the slice is in
   RS_MARK(0);
   for (int h = 1; h < sg; ++h) {  // the group's other kv-head rows, head order
@@ -332,9 +408,10 @@ __global__ void __launch_bounds__(kRowselThreads, 1) rowsel_kernel(const SelectP
         if (nw > 0) {
           sel_sync<NT>();
           if (refine) {
-            rescore_f64<NT>(p, slot, b, grp, wi, wv, nw);
+            rs_rescore<NT>(p, qsp, slot, b, grp, wi, wv, nw);
             sel_sync<NT>();
           }
+          RS_MARK(6);
           const int take = k - above_w;
           for (int j = tid; j < nw; j += NT) {
             const double vj = wv[j];
@@ -470,7 +547,7 @@ __global__ void __launch_bounds__(kRowselThreads, 1) rowsel_kernel(const SelectP
         }
         if (nw > 0) {
           if (refine) {
-            rescore_f64<NT>(p, slot, b, grp, wi, wv, nw);
+            rs_rescore<NT>(p, qsp, slot, b, grp, wi, wv, nw);
             sel_sync<NT>();
           }
           const int take = k - above_w;
@@ -529,7 +606,7 @@ __global__ void __launch_bounds__(kRowselThreads, 1) rowsel_kernel(const SelectP
     rs_sync<C>();
   }
   const long long t3 = clock64();
-  RS_MARK(6);
+  RS_MARK(7);
   pdl_launch_dependents();
 
   // ---- 5. index-ordered compaction: thread t owns the contiguous words [t wpt, (t+1) wpt);
@@ -576,7 +653,6 @@ __global__ void __launch_bounds__(kRowselThreads, 1) rowsel_kernel(const SelectP
     info[6] = (int32_t)(t3 - t2);
     info[7] = (int32_t)(clock64() - t3);
 #ifdef HYLRA_ROWSEL_PROF
-    RS_MARK(7);
     for (int j = 7; j > 0; --j) info[j] = (int32_t)(pm[j] - pm[j - 1]);
     info[0] = (int32_t)(pm[0] - t0);
 #endif

@@ -1,4 +1,5 @@
-"""Time the REUSE launch of a BASELINE config (all REUSE layers in one launch)."""
+"""Time the REUSE launch of a BASELINE config (all REUSE layers in one launch):
+    python scripts/reuse_sweep.py [cfg2] [batch]"""
 import sys
 from pathlib import Path
 
@@ -11,6 +12,8 @@ from paper_2602_00777_b200.engine import HybridDecoder  # noqa: E402
 from paper_2602_00777_b200.synthetic import CONFIGS, generate_torch  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
+if len(sys.argv) > 2:
+    cfg = cfg.with_(batch=int(sys.argv[2]))
 q, k, v = generate_torch(cfg, "cuda")
 dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
 dec.step(q, cfg.context)
@@ -42,4 +45,4 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 20
 by = len(rl) * cfg.batch * cfg.kv_heads * 2 * ke * cfg.head_dim * 2
-print(f"{cfg.name} reuse {ms * 1e3:.1f} us  {by / ms / 1e6:.0f} GB/s")
+print(f"{cfg.name} B={cfg.batch} reuse {ms * 1e3:.1f} us  {by / ms / 1e6:.0f} GB/s", flush=True)

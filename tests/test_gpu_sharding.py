@@ -8,7 +8,8 @@ the same HybridDecoder over strided views of the full cache (no copies), then th
 are all-gathered once. The gathered outputs and every shard-local index set must equal
 the unsharded GPU step bit for bit. The shapes keep the split-K partition the same at
 both pair counts (bit-equality needs identical partitions; 4 splits of 32 tiles per FULL
-pair, 1 per REUSE pair), which bench.py's shard sizes do not need.
+pair, 1 per REUSE pair: 4-tile selections stay unsplit at either pair count), which
+bench.py's shard sizes do not need.
 """
 import os
 import socket
@@ -25,7 +26,7 @@ import torch.multiprocessing as mp  # noqa: E402
 
 ACTIONS = ("full", "full", "reuse", "full", "reuse", "reuse", "full", "reuse")
 SHAPES = {"kvhead": dict(B=8, Hq=32, Hkv=8), "batch": dict(B=8, Hq=28, Hkv=4)}
-N, BUDGET, D = 8192, 512, 128
+N, BUDGET, D = 8192, 256, 128
 
 
 def _free_port():
