@@ -1,9 +1,12 @@
 # Round profile bundle (one GPU): full bench line, reference arm, ncu launch list of the
-# bench command, ncu --set full captures of the headline step (single launch) and of the
-# fusedsel schedule's FULL / SELECT / REUSE kernels at cfg2 B=8, and the step at B=1.
-# Reports are summarised ON the box (gpurun brings back <= 64 MiB); only the headline
-# capture travels back as an .ncu-rep.
+# bench command, ncu --set full captures of the headline step (single launch), of the
+# fusedsel schedule's FULL / SELECT / REUSE kernels at cfg2 B=8, of the B=1 fused3 step
+# (FULL, shared-memory-resident select, REUSE) and of the layer-sequential schedule's first
+# layers at B=1 (one-layer FULL, its select, one-layer REUSE). Reports are summarised ON the
+# box (gpurun brings back <= 64 MiB); only the headline capture travels back as .ncu-rep.
+#   bash scripts/gpu_profile.sh [--captures-only] [round tag, default r02]
 set -x
+TAG=${2:-r02}
 mkdir -p gpurun_out
 if [ "$1" != "--captures-only" ]; then
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
@@ -17,11 +20,12 @@ cap() {  # name, kernel regex, count, prof_step args...
   timeout 900 ncu -f --set full --import-source on --clock-control none -k regex:"$kre" -c $cnt \
     -o /tmp/$name python scripts/prof_step.py "$@" > gpurun_out/ncu_$name.log 2>&1
   echo "ncu $name rc=$?"
-  python scripts/ncu_summary.py /tmp/$name.ncu-rep --json gpurun_out/ncu_$name.json > gpurun_out/ncu_$name.txt 2>&1
-  python scripts/ncu_lines.py /tmp/$name.ncu-rep "$kre" 40 > gpurun_out/ncu_${name}_lines.txt 2>&1
+  python scripts/ncu_summary.py /tmp/$name.ncu-rep --json gpurun_out/${TAG}_ncu_$name.json > gpurun_out/${TAG}_ncu_$name.txt 2>&1
+  python scripts/ncu_lines.py /tmp/$name.ncu-rep "$kre" 40 > gpurun_out/${TAG}_ncu_${name}_lines.txt 2>&1
 }
 cap single_cfg2_b8 "step_mma_kernel" 1 --config cfg2 --batch 8 --steps 1 --schedule single
 cp /tmp/single_cfg2_b8.ncu-rep gpurun_out/
 cap fusedsel_cfg2_b8 "attn_mma_kernel|topk_select" 3 --config cfg2 --batch 8 --steps 1 --schedule fusedsel
-cap cfg2_b1 "attn_mma_kernel|topk_select|step_mma_kernel" 3 --config cfg2 --batch 1 --steps 1
+cap fused3_cfg2_b1 "attn_mma_kernel|rowsel|topk_select" 3 --config cfg2 --batch 1 --steps 1 --schedule fused3
+cap seq_cfg2_b1 "attn_mma_kernel|rowsel" 4 --config cfg2 --batch 1 --steps 1 --schedule sequential
 ls -la gpurun_out

@@ -5,7 +5,8 @@
 Kernels per step by --schedule: single = step_mma_kernel (every FULL item with its select
 fused, then every REUSE item); fusedsel = attn_mma_kernel (FULL, selects of the layers that
 feed REUSE fused) -> topk_select_kernel (other FULL layers, side stream) -> attn_mma_kernel
-(REUSE gather); fused3 = FULL -> SELECT -> REUSE; auto = HybridDecoder's choice.
+(REUSE gather); fused3 = FULL -> SELECT -> REUSE; sequential = LayerwiseDecoder (per layer:
+FULL + its select, or REUSE); auto = HybridDecoder's choice.
 """
 import argparse
 import sys
@@ -24,7 +25,8 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--block-size", type=int, default=1)
-ap.add_argument("--schedule", default="auto", choices=["auto", "single", "fusedsel", "fused3"])
+ap.add_argument("--schedule", default="auto",
+                choices=["auto", "single", "fusedsel", "fused3", "sequential"])
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 if a.batch:
@@ -32,10 +34,14 @@ if a.batch:
 q, k, v = generate_torch(cfg, "cuda")
 torch.cuda.synchronize()
 bs = a.block_size
-kw = {"auto": {}, "single": {"single_launch": True},
-      "fusedsel": {"single_launch": False}, "fused3": {"fuse_select": False}}[a.schedule]
-dec = HybridDecoder(cfg.actions, k, v, cfg.budget // bs if bs > 1 else cfg.budget,
-                    q_heads=cfg.q_heads, block_size=bs, **kw)
+if a.schedule == "sequential":
+    from paper_2602_00777_b200.engine import LayerwiseDecoder
+    dec = LayerwiseDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
+else:
+    kw = {"auto": {}, "single": {"single_launch": True},
+          "fusedsel": {"single_launch": False}, "fused3": {"fuse_select": False}}[a.schedule]
+    dec = HybridDecoder(cfg.actions, k, v, cfg.budget // bs if bs > 1 else cfg.budget,
+                        q_heads=cfg.q_heads, block_size=bs, **kw)
 for _ in range(a.steps):
     dec.step(q, cfg.context)
 torch.cuda.synchronize()
