@@ -178,8 +178,10 @@ int hylra_reuse_decode(const hylra_geometry* g, const void* q, const void* k, co
  *   full = 0: REUSE attention of `layer` over the selection in slot `slot` of idx.
  * prefetch = 1 lets the kernel's producer warps start loading K/V (REUSE: and the indices)
  * before the previous kernel on the stream has finished (programmatic dependent launch;
- * only the reads of q wait for it). The caller asserts that the previous kernel wrote none
- * of those: e.g. not the first REUSE layer after the selection it reads. ws: zero-filled,
+ * only the reads of q wait for it). This only matters when that previous kernel releases
+ * its dependents early, as this library's kernels do; an ordinary kernel completes first.
+ * The caller asserts that an early-releasing previous kernel wrote none of those: e.g. this
+ * is not the first REUSE layer after the selection it reads. ws: zero-filled,
  * hylra_attention_workspace_bytes(g, 1, max(n_valid, k)) bytes, flag word first; kernels of
  * consecutive layers may overlap, so consecutive calls must alternate between two
  * workspaces.

@@ -5,7 +5,13 @@ per-kernel times and HBM roofline fractions (FULL, SELECT, REUSE) + the whole st
 
 Layer count: the full 32-layer cfg2 policy when the KV cache fits in ~150 GB, else the
 longest prefix of that policy that fits (at least [FULL, REUSE]); per-kernel fractions do
-not depend on the layer count, and each line records the layers used.
+not depend on the layer count, and each line records the layers used. Lines run on a
+prefix also carry the 32-layer step EXTRAPOLATED by layer count (`extrapolated_32_layers`,
+with the factor and the reason), never as a measured value.
+
+Times: per-kernel = mean of back-to-back launches between two CUDA events (device time per
+launch, no host gaps); step = the autotuned schedule's CUDA-graph replay time (the eager
+step, with its host overhead, is `step_ms_eager`).
 """
 import argparse
 import json
@@ -27,17 +33,28 @@ PEAK = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json
 BUDGET_BYTES = 150e9
 
 
-def time_ms(fn, reps=10):
+def time_ms(fn, reps=20):
+    """Mean device time per launch of `reps` back-to-back launches."""
     for _ in range(2):
         fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def time_eager_ms(fn, reps=10):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(reps)]
-    for a, b in ev:
-        a.record()
+    for x, y in ev:
+        x.record()
         fn()
-        b.record()
+        y.record()
     torch.cuda.synchronize()
-    return statistics.median(a.elapsed_time(b) for a, b in ev)
+    return statistics.median(x.elapsed_time(y) for x, y in ev)
 
 
 def point(N, ratio, B):
@@ -81,18 +98,27 @@ def point(N, ratio, B):
         g, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), N, len(rl), rid, rsrc, dec.idx.data_ptr(), None,
         dec.k_stride, min(k, N), 1, dec.out.data_ptr(), wsr.data_ptr(), wsr.numel(), st))) \
         if rl else 0.0
-    t_step = time_ms(lambda: dec.step(q, N))
+    t_eager = time_eager_ms(lambda: dec.step(q, N))
+    t_step = tuned[dec.schedule]  # graph replay of the autotuned schedule
     fb = len(fl) * B * cfg.kv_heads * 2 * N * cfg.head_dim * 2
     rb = len(rl) * B * cfg.kv_heads * 2 * min(k, N) * cfg.head_dim * 2
     res = {"context": N, "top_k": k, "ratio": ratio, "batch": B, "layers": L,
            "schedule": dec.schedule, "autotune_ms": tuned,
            "full_layers": len(fl), "reuse_layers": len(rl),
            "full_ms": t_full, "select_ms": t_sel, "reuse_ms": t_reuse, "step_ms": t_step,
+           "step_ms_eager": t_eager,
            "full_frac": fb / (t_full * 1e-3) / 1e9 / PEAK,
            "reuse_frac": (rb / (t_reuse * 1e-3) / 1e9 / PEAK) if rl else None,
            "select_frac_of_full_plus_select": t_sel / (t_full + t_sel),
            "step_gbs": (fb + rb) / (t_step * 1e-3) / 1e9,
            "tok_per_s_for_these_layers": B / (t_step * 1e-3)}
+    if L < base.layers:
+        f = base.layers / L
+        res["extrapolated_32_layers"] = {
+            "step_ms": t_step * f, "tok_per_s": B / (t_step * f * 1e-3), "factor": f,
+            "by": "layer count (step time x 32 / layers run)",
+            "why": f"32 layers of KV = {per_layer * base.layers / 1e9:.0f} GB > "
+                   f"{BUDGET_BYTES / 1e9:.0f} GB on one GPU"}
     del q, kk, vv, dec, sc, wsf, wsr
     torch.cuda.empty_cache()
     return res
