@@ -46,8 +46,8 @@ def raw(rep):
             # bytes to B, times to ns (ncu picks the unit per value: a 1.46 ms launch is
             # reported as "1.46 msecond", not in ns)
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
-                     "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9
-                     }.get(u.get(m, "byte"), 1)
+                     "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
+                     "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}.get(u.get(m, "byte"), 1)
             return v * scale
         res.append({"id": d.get("ID"), "kernel": d.get("Kernel Name"),
                     "dram_read_bytes": get("dram__bytes_read.sum"),
