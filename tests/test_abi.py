@@ -154,3 +154,44 @@ def test_block_step_append_options_validate_on_the_host():
     with pytest.raises(InvalidInputError, match="append_pos"):
         _abi.check(lib.hylra_decode_step_blocks_ex(g, 1, 1, 1, 2048, acts, 16, 64, 1, 1, 1, 1,
                                                    16, 1, need, None, ctypes.byref(opt)))
+
+
+def test_tuning_knobs_validate_and_restore():
+    """hylra_set_tuning: known knobs accept values and -1 restores the default rule; an unknown
+    knob is a ConfigurationError (no GPU needed)."""
+    lib = _abi.lib()
+    with _abi.tuning(rowsel=0, select_threads=512, rowsel_cluster=4):
+        pass
+    assert lib.hylra_set_tuning(b"rowsel", -1) == 0
+    with pytest.raises(ConfigurationError, match="unknown tuning knob"):
+        _abi.check(lib.hylra_set_tuning(b"no_such_knob", 1))
+    with pytest.raises(ConfigurationError):
+        _abi.check(lib.hylra_set_tuning(None, 1))
+
+
+def test_decode_layer_validates_before_launching():
+    """hylra_decode_layer rejects bad arguments host-side, with the reference's exception
+    classes: budget < 1 -> InvalidInputError, a slot out of range / a REUSE layer without
+    selections / a FULL selection without score rows -> ConfigurationError."""
+    lib = _abi.lib()
+    g = _geom()
+    ws = (ctypes.c_uint8 * 4096)()
+    args = dict(n_valid=2048, layer=0, full=1, slot=0, budget=128, sel_group=1, refine=1,
+                prefetch=0)
+
+    def call(**kw):
+        a = {**args, **kw}
+        return lib.hylra_decode_layer(ctypes.byref(g), 1, 1, 1, a["n_valid"], a["layer"],
+                                      a["full"], a["slot"], a["budget"], a["sel_group"],
+                                      a["refine"], a["prefetch"], 1, kw.get("scores"),
+                                      kw.get("idx"), 128, ws, 4096, None)
+    with pytest.raises(InvalidInputError):
+        _abi.check(call(budget=0))
+    with pytest.raises(ConfigurationError):
+        _abi.check(call(slot=-1))
+    with pytest.raises(ConfigurationError):
+        _abi.check(call(full=0))          # REUSE without selections
+    with pytest.raises(ConfigurationError):
+        _abi.check(call(idx=1))           # a FULL selection needs score rows
+    with pytest.raises(ConfigurationError):
+        _abi.check(call(sel_group=3))     # does not divide kv_heads
