@@ -775,3 +775,29 @@ def test_layerwise_prefetch_matches_waiting_launches_across_steps():
         torch.cuda.synchronize()
         assert torch.equal(pre.out, ref.outputs)
         assert torch.equal(pre.idx[..., :budget], ref.selections)
+
+
+@pytest.mark.parametrize("dtype,d,Hq,Hkv,cap,n_valid,budget,sel_group", [
+    ("bf16", 128, 28, 4, 4096, 4000, 300, 1),   # G = 7 (Qwen), ragged rows
+    ("bf16", 64, 16, 4, 2048, 2048, 128, 4),    # layer-wide sets (the reference's sel_group)
+    ("f32", 64, 8, 2, 1024, 1000, 100, 1),      # CUDA-core path (no early loads)
+    ("bf16", 128, 16, 1, 8192, 8192, 8192, 1),  # budget covers the cache
+])
+def test_layerwise_decoder_matches_oracle(dtype, d, Hq, Hkv, cap, n_valid, budget, sel_group):
+    """LayerwiseDecoder (hylra_decode_layer per layer) against the float64 oracle's step
+    (engine.py:167-197): exact index sets, outputs within the dtype tolerance."""
+    from paper_2602_00777_b200.engine import LayerwiseDecoder
+    L, B = 6, 2
+    q, k, v, qn, kn, vn = make_stack(L, B, Hq, Hkv, d, cap, dtype, seed=d + Hq, planted=48)
+    actions = ("full", "reuse", "full", "full", "reuse", "reuse")
+    dec = LayerwiseDecoder(actions, k, v, budget, q_heads=Hq, sel_group=sel_group)
+    res = dec.step(q, n_valid)
+    torch.cuda.synchronize()
+    dec.check_flags(strict=True)
+    ref_out, ref_sets, _ = orc.hybrid_step(qn, kn, vn, n_valid, actions, budget,
+                                           sel_group=sel_group)
+    sel = res.selections.cpu().numpy()
+    for l in range(L):
+        np.testing.assert_array_equal(sel[res.slot_of_layer[l]], ref_sets[l])
+    tol = 2e-2 if dtype == "bf16" else 1e-3
+    assert max_head_err(res.outputs.double().cpu().numpy(), ref_out) < tol
