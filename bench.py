@@ -379,10 +379,17 @@ def _sanity_check(torch, cfg, q, k, v, dec):
             "heads_per_pair": 1, "flags": "clear"}
 
 
+def _progress(msg):
+    """One line per bench stage on stderr (the JSON result stays the only stdout line)."""
+    print(f"[bench rank {_env_int('RANK', 0)} {time.strftime('%H:%M:%S')}] {msg}",
+          file=sys.stderr, flush=True)
+
+
 def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, strong=False):
     """One config on this rank. Weak scaling (default): `batch` sequences per GPU, global
     batch batch x world. strong=True: `batch` is the GLOBAL batch (BASELINE configs 3 and 4:
     B = 4 sharded by KV head, B = 16 partitioned by batch), split across the ranks."""
+    _progress(f"{cfg.name} batch {batch} ({'global' if strong else 'per GPU'}) on {world} rank(s)")
     from paper_2602_00777_b200 import _abi
     from paper_2602_00777_b200.attention import geometry, scores_row_stride
     from paper_2602_00777_b200.engine import HybridDecoder, LayerwiseDecoder, PipelinedDecoder
@@ -408,8 +415,15 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, 
 
     def make(kind):
         if kind == "auto":
+            _progress(f"{cfg.name}: autotune")
             d = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1)
             d.autotune_ms = d.autotune(q, n_valid)  # fastest of single / fusedsel / fused3
+            if world > 1:
+                # every rank must run the same schedule (the timed loops below hold matching
+                # barriers / all-reduces): the fastest by the max over ranks
+                from paper_2602_00777_b200.sharding import agree_schedule
+                name, d.autotune_ms = agree_schedule(d.autotune_ms, device=dev)
+                d.set_schedule(name)
             return d
         if kind in ("dual", "fused3", "fusedsel", "single"):
             return HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=Hq, sel_group=1,
@@ -471,14 +485,17 @@ def measure_config(a, cfg, batch, rank, world, torch, dist, cpu=True, e2e=True, 
     kind_used = dec.schedule if a.schedule == "auto" else a.schedule
     graph = capture(dec)
     schedules = {}
+    _progress(f"{cfg.name}: headline schedule {kind_used} captured")
     for kind in [x for x in ("fused3", "fusedsel", "single", "dual", "sequential")
                  if x != kind_used]:
+        _progress(f"{cfg.name}: schedule {kind}")
         d2 = make(kind)
         g2 = capture(d2)
         schedules[kind] = {"ms_per_step": time_replays(g2, d2, max(10, a.steps // 2)),
                            "kernels_per_step": d2.kernels_per_step}
         del g2, d2
 
+    _progress(f"{cfg.name}: sanity check and timed region")
     check = _sanity_check(torch, cfg, q, k, v, dec)
     # selection rows whose float64 boundary refinement was skipped (window over kCandCap):
     # their k-th boundary followed fp32 order (HYLRA_FLAG_REFINE_SKIPPED; 0 expected)

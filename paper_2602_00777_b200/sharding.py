@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 from .errors import ConfigurationError
 
-__all__ = ["ShardPlan", "plan_shards", "shard_slices", "gather_outputs"]
+__all__ = ["ShardPlan", "plan_shards", "shard_slices", "gather_outputs", "agree_schedule"]
 
 
 @dataclass(frozen=True)
@@ -90,3 +90,23 @@ def gather_outputs(out_local, plan: ShardPlan, group=None):
     # batch: [P, L, B/P, Hq, d] -> [L, P*B/P, Hq, d]
     return buf.permute(1, 0, 2, 3, 4).reshape(out_local.shape[0], -1, out_local.shape[2],
                                               out_local.shape[3])
+
+
+SCHEDULES = ("single", "singlecoop", "fusedsel", "fused3")
+
+
+def agree_schedule(times: dict, group=None, device="cpu"):
+    """One step schedule for every rank: each rank autotunes its own shard
+    (HybridDecoder.autotune -> {schedule: ms}), but a multi-rank step must run the same
+    schedule everywhere — the timed loops hold matching collectives, and the slowest rank
+    sets the step time. Returns (name, {schedule: max ms over ranks}): the schedule fastest
+    by its max over ranks (a schedule a rank could not time counts as infinitely slow)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(times.get(n, float("inf"))) for n in SCHEDULES],
+                     dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    best = int(torch.argmin(t).item())
+    return SCHEDULES[best], {n: float(x) for n, x in zip(SCHEDULES, t.tolist())
+                             if x != float("inf")}

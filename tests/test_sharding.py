@@ -105,3 +105,36 @@ def test_gloo_two_rank_step_equals_unsharded(mode, blocks):
             b0, b1 = plan.batch
             h0, h1 = plan.kv_heads
             assert np.array_equal(res[r][1][l], ref_sets[l][b0:b1, h0:h1])
+
+
+def _agree_worker(rank, world, port, q):
+    from paper_2602_00777_b200.sharding import agree_schedule
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # each rank's own autotune prefers a different schedule; singlecoop is missing on
+        # rank 1 (a schedule a rank did not time)
+        mine = [{"single": 1.50, "singlecoop": 1.40, "fusedsel": 1.55, "fused3": 1.60},
+                {"single": 1.45, "fusedsel": 1.70, "fused3": 1.52}][rank]
+        q.put((rank, agree_schedule(mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ranks_agree_on_one_schedule():
+    """bench.py under torchrun: every rank must time the same schedule (the timed loops
+    hold matching collectives; differing per-rank autotune picks deadlocked a 2-rank run).
+    The agreed schedule is the fastest by its max over ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    name, times = res[0]
+    assert name == "single" and times == {"single": 1.50, "fusedsel": 1.70, "fused3": 1.60}
