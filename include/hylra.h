@@ -118,6 +118,9 @@ uint64_t hylra_launch_count(void);
  *   "rowsel_cluster" 1/2/4/8: CTAs per row of the shared-memory-resident select (default:
  *                    the fewest that hold the row, doubled while the launch stays within
  *                    one wave of SMs).
+ *   "gather_tma"     1/0: standalone REUSE launches gather rows with TMA tile::gather4
+ *                    (UTMALDG.2D.GATHER4) instead of cp.async, for contiguous caches
+ *                    (default 0: measured 2.3x slower, profiles/r02_gather_tma_ab.txt).
  * Results never depend on them (every select path returns the same index sets). */
 int hylra_set_tuning(const char* name, int value);
 

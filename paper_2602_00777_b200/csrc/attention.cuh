@@ -78,6 +78,12 @@ struct AttnParams {
   // on the stream wrote none of them — so the pipeline fills while that launch drains; the
   // consumer warps still wait before reading q
   int early;
+  // REUSE gather by TMA (tile::gather4 through 2-D row views of K and V passed in the tmk /
+  // tmv slots; contiguous caches, uniform rows, indices staged): rows of (kv layer, b, kh)
+  // start at row ((kvl B + b) Hkv + kh) cap of the view; 0: the cp.async gather
+  int gather_tma;
+  int gather_rows;  // rows of the 2-D views (an index past them is zero-filled)
+  int cap_rows;     // cache rows per (kv layer, b, kh) block (capacity)
 };
 
 // Stage n selection indices from global into shared memory, validated (out-of-range ->
@@ -605,7 +611,7 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
   const int n_my = t_end - t_begin;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar + s, GATHER ? 32 * kGatherProducers : 1);
+      mbar_init(full_bar + s, (GATHER && !p.gather_tma) ? 32 * kGatherProducers : 1);
       mbar_init(empty_bar + s, kConsumerWarps);
     }
     mbar_fence_init();
@@ -747,6 +753,39 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
           asm volatile("bar.sync 3, %0;" ::"n"(32 * kGatherProducers) : "memory");
         else
           __syncwarp();
+      }
+      if (p.gather_tma && staged) {
+        // TMA gather: one lane issues 4-row gathers per stage (K and V, each 128-byte
+        // column box); the staged indices become rows of the 2-D views
+        if (warp == kConsumerWarps && lane == 0) {
+          const uint64_t pol = l2_policy_evict_first();
+          const int base_row = ((kvl * p.B + b) * p.Hkv + kh) * p.cap_rows;
+          for (int i = 0; i < n_my; ++i) {
+            const int s = i % STAGES;
+            mbar_wait(empty_bar + s, ((i / STAGES) & 1) ^ 1);
+            uint8_t* kt = smem + s * SM::kStageBytes;
+            uint8_t* vt = kt + SM::kTileBytes;
+            mbar_arrive_expect_tx(full_bar + s, SM::kStageBytes);
+            const int pos0 = (t_begin + i) * kTileRows;
+#pragma unroll 4
+            for (int r = 0; r < kTileRows; r += 4) {
+              int rw[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int pos = pos0 + r + u;
+                rw[u] = pos < n_rows ? base_row + sidx[pos - pos_begin] : p.gather_rows;
+              }
+#pragma unroll
+              for (int bx = 0; bx < SM::kBoxes; ++bx) {
+                tma_gather4(kt + bx * kTileRows * 128 + r * 128, &tmk, full_bar + s, bx * 64,
+                            rw[0], rw[1], rw[2], rw[3], pol);
+                tma_gather4(vt + bx * kTileRows * 128 + r * 128, &tmv, full_bar + s, bx * 64,
+                            rw[0], rw[1], rw[2], rw[3], pol);
+              }
+            }
+          }
+        }
+        return;
       }
       auto row_at = [&](int pos) -> int {  // pos < n_rows
         if (staged) return sidx[pos - pos_begin];

@@ -75,6 +75,19 @@ __device__ __forceinline__ void tma_load_5d(void* smem_dst, const void* tmap, ui
       "r"(smem_u32(bar)), "l"(cache_policy)
       : "memory");
 }
+// TMA row gather (sm_100): rows r0..r3 of a 2-D tensor map whose box is {cols, 1}, columns
+// [c0, c0 + cols), into 4 consecutive box rows at smem_dst (UTMALDG.2D.GATHER4). Rows past
+// the tensor's extent are zero-filled and still count toward complete_tx.
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const void* tmap, uint64_t* bar,
+                                            int c0, int r0, int r1, int r2, int r3,
+                                            uint64_t cache_policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "r"(smem_u32(bar)), "l"(cache_policy)
+      : "memory");
+}
 // 1-D bulk copy global -> shared (16-byte aligned addresses, size a multiple of 16),
 // completing on `bar` (complete_tx bytes).
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,

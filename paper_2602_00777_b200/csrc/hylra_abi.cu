@@ -241,6 +241,23 @@ int encode_kv_map(CUtensorMap* map, const hylra_geometry* g, const void* base, i
 }
 
 // Validated AttnParams of one FULL or REUSE launch (or of one half of a single-launch step).
+// 2-D row view [rows][D] of a contiguous [L][B][Hkv][cap][D] bf16 cache for the REUSE
+// TMA gather (box: 64 columns x 1 row, 128-byte swizzle: the 4-row gathers land in the
+// same swizzled tile layout as the FULL kernel's boxes).
+int encode_row_view(CUtensorMap* map, const hylra_geometry* g, const void* base, int rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return fail(HYLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)g->head_dim, (cuuint64_t)rows};
+  cuuint64_t st[1] = {(cuuint64_t)g->head_dim * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, st, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HYLRA_ERR_CUDA, "cuTensorMapEncodeTiled (rows) failed (%d)", (int)r);
+  return HYLRA_OK;
+}
+
 int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* g, bool gather,
                      const void* q, const void* k, const void* v, int n_valid, int n_rows,
                      int n_layers, const int32_t* layer_ids, const int32_t* src_slots,
@@ -335,6 +352,21 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
     if (!gather) {
       if (int e = encode_kv_map(&tk, g, k, n_kv)) return e;
       if (int e = encode_kv_map(&tv, g, v, n_kv)) return e;
+    } else if (gather_tma_enabled() && counts == nullptr &&
+               lay.tps * kTileRows <= kIdxStage) {
+      // the TMA row gather needs the cache contiguous across (layer, b, kv-head) blocks
+      const int64_t blk = (int64_t)g->capacity * g->head_dim;
+      const int64_t rows = (int64_t)n_kv * g->batch * g->kv_heads * g->capacity;
+      const bool contiguous = (g->kv_heads == 1 || g->kv_stride_head == blk) &&
+                              (g->batch == 1 || g->kv_stride_batch == blk * g->kv_heads) &&
+                              (n_kv == 1 || g->kv_stride_layer == blk * g->kv_heads * g->batch);
+      if (contiguous && rows < (1ll << 31) - 1) {
+        if (int e = encode_row_view(&tk, g, k, (int)rows)) return e;
+        if (int e = encode_row_view(&tv, g, v, (int)rows)) return e;
+        p.gather_tma = 1;
+        p.gather_rows = (int)rows;
+        p.cap_rows = g->capacity;
+      }
     }
     ce = run_attn_mma(g->head_dim, gather, G > 8, grid, st, tk, tv, p, sp);
   } else {
@@ -1089,6 +1121,7 @@ int hylra_set_tuning(const char* name, int value) {
   if (!strcmp(name, "rowsel")) knob = &tuning().rowsel;
   else if (!strcmp(name, "select_threads")) knob = &tuning().select_threads;
   else if (!strcmp(name, "rowsel_cluster")) knob = &tuning().rowsel_cluster;
+  else if (!strcmp(name, "gather_tma")) knob = &tuning().gather_tma;
   if (!knob) return fail(HYLRA_ERR_CONFIGURATION, "unknown tuning knob '%s'", name);
   knob->store(value < 0 ? -1 : value, std::memory_order_relaxed);
   return HYLRA_OK;

@@ -122,6 +122,7 @@ struct Tuning {
   std::atomic<int> rowsel{-1};
   std::atomic<int> select_threads{-1};
   std::atomic<int> rowsel_cluster{-1};
+  std::atomic<int> gather_tma{-1};
 };
 inline Tuning& tuning() {
   static Tuning t;
@@ -130,6 +131,20 @@ inline Tuning& tuning() {
 
 // The shared-memory-resident select (rowsel.cuh) for the rows it covers; HYLRA_ROWSEL=0
 // (or hylra_set_tuning("rowsel", 0)) keeps every row on select_row (A/B runs).
+// REUSE launches gather rows by TMA (tile::gather4) instead of cp.async where the cache is
+// contiguous; HYLRA_GATHER_TMA / hylra_set_tuning("gather_tma", v) (default: off).
+inline bool gather_tma_enabled() {
+  const int o = tuning().gather_tma.load(std::memory_order_relaxed);
+  if (o >= 0) return o != 0;
+  static int v = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_GATHER_TMA");
+    v = (e && *e) ? (atoi(e) != 0) : 0;
+  });
+  return v == 1;
+}
+
 inline bool rowsel_enabled() {
   const int o = tuning().rowsel.load(std::memory_order_relaxed);
   if (o >= 0) return o != 0;

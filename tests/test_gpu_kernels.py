@@ -801,3 +801,24 @@ def test_layerwise_decoder_matches_oracle(dtype, d, Hq, Hkv, cap, n_valid, budge
         np.testing.assert_array_equal(sel[res.slot_of_layer[l]], ref_sets[l])
     tol = 2e-2 if dtype == "bf16" else 1e-3
     assert max_head_err(res.outputs.double().cpu().numpy(), ref_out) < tol
+
+
+@pytest.mark.parametrize("d,Hq,Hkv,cap,k", [(128, 32, 8, 4096, 1000), (64, 14, 2, 2048, 333),
+                                            (128, 28, 4, 8192, 2048), (128, 16, 16, 512, 64)])
+def test_reuse_tma_gather_equals_cp_async_gather(d, Hq, Hkv, cap, k):
+    """The REUSE gather by TMA row gathers (tile::gather4 over 2-D row views of the cache)
+    returns exactly the cp.async gather's outputs: same rows, same swizzled tile layout,
+    ragged last tiles zero-filled."""
+    from paper_2602_00777_b200 import _abi
+    q, k_, v, *_ = make_stack(3, 2, Hq, Hkv, d, cap, "bf16", seed=k)
+    rng = np.random.default_rng(d + k)
+    idx = np.stack([np.stack([np.stack([np.sort(rng.choice(cap, k, replace=False))
+                                        for _ in range(Hkv)]) for _ in range(2)])
+                    for _ in range(3)]).astype(np.int32)
+    it = torch.from_numpy(idx).to(DEV)
+    with _abi.tuning(gather_tma=0):
+        ref = sparse_attention(q, k_, v, it, cap)
+    with _abi.tuning(gather_tma=1):
+        got = sparse_attention(q, k_, v, it, cap)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
