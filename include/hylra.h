@@ -120,7 +120,7 @@ uint64_t hylra_launch_count(void);
  *                    one wave of SMs).
  *   "gather_tma"     1/0: standalone REUSE launches gather rows with TMA tile::gather4
  *                    (UTMALDG.2D.GATHER4) instead of cp.async, for contiguous caches
- *                    (default 0: measured 2.3x slower, profiles/r02_gather_tma_ab.txt).
+ *                    (default 0: measured 1.5x slower, profiles/r02_gather_tma_ab.txt).
  * Results never depend on them (every select path returns the same index sets). */
 int hylra_set_tuning(const char* name, int value);
 

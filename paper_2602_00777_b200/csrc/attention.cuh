@@ -757,7 +757,13 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
       if (p.gather_tma && staged) {
         // TMA gather: one lane issues 4-row gathers per stage (K and V, each 128-byte
         // column box); the staged indices become rows of the 2-D views
-        if (warp == kConsumerWarps && lane == 0) {
+        // the producer warps' lane 0s share each stage's rows (the first one also arms
+        // the stage's transaction count: a gather completing before it is armed only
+        // drives the count negative within the phase, which cannot complete before the
+        // arrival)
+        const int part = warp - kConsumerWarps;
+        constexpr int kRowsPer = kTileRows / kGatherProducers;
+        if (lane == 0) {
           const uint64_t pol = l2_policy_evict_first();
           const int base_row = ((kvl * p.B + b) * p.Hkv + kh) * p.cap_rows;
           for (int i = 0; i < n_my; ++i) {
@@ -765,10 +771,10 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
             mbar_wait(empty_bar + s, ((i / STAGES) & 1) ^ 1);
             uint8_t* kt = smem + s * SM::kStageBytes;
             uint8_t* vt = kt + SM::kTileBytes;
-            mbar_arrive_expect_tx(full_bar + s, SM::kStageBytes);
+            if (part == 0) mbar_arrive_expect_tx(full_bar + s, SM::kStageBytes);
             const int pos0 = (t_begin + i) * kTileRows;
 #pragma unroll 4
-            for (int r = 0; r < kTileRows; r += 4) {
+            for (int r = part * kRowsPer; r < (part + 1) * kRowsPer; r += 4) {
               int rw[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
