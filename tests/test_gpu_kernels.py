@@ -822,3 +822,34 @@ def test_reuse_tma_gather_equals_cp_async_gather(d, Hq, Hkv, cap, k):
         got = sparse_attention(q, k_, v, it, cap)
     torch.cuda.synchronize()
     assert torch.equal(got, ref)
+
+
+def test_layerwise_decoder_with_model_dependence():
+    """A model's decode: layer l+1's query is computed from layer l's output by the model's
+    own (torch) kernel on the same stream, between LayerwiseDecoder.layer calls. The GPU step
+    must use the queries as they are when each layer runs: the float64 oracle, given the
+    final query stack, reproduces every index set and output. (Were a layer to read its query
+    before the model kernel wrote it, it would see the initial values, far from the final
+    ones.)"""
+    from paper_2602_00777_b200.engine import LayerwiseDecoder
+    L, B, Hq, Hkv, d, cap, budget = 6, 2, 16, 4, 128, 4096, 256
+    q0, k, v, _, kn, vn = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=31, planted=64)
+    actions = ("full", "reuse", "reuse", "full", "reuse", "full")
+    dec = LayerwiseDecoder(actions, k, v, budget, q_heads=Hq)
+    for _ in range(2):  # the second step runs on warm, non-zero workspaces / buffers
+        q = q0.clone()
+        for l in range(L):
+            if l > 0:
+                # the "model": the next query mixes the previous layer's output in
+                q[l] = (0.25 * q0[l].float() + 8.0 * dec.out[l - 1]).to(torch.bfloat16)
+            dec.layer(l, q, cap)
+        dec.finish()
+        torch.cuda.synchronize()
+    dec.check_flags(strict=True)
+    assert (q[1:].float() - q0[1:].float()).abs().mean() > 0.3  # the chain really moved q
+    ref_out, ref_sets, _ = orc.hybrid_step(q.double().cpu().numpy(), kn, vn, cap, actions,
+                                           budget)
+    sel = dec.idx[..., :budget].cpu().numpy()
+    for l in range(L):
+        np.testing.assert_array_equal(sel[dec.slot_of_layer[l]], ref_sets[l])
+    assert max_head_err(dec.out.double().cpu().numpy(), ref_out) < 2e-2
