@@ -138,10 +138,17 @@ class HybridDecoder:
         # (cfg2 B>=4, cfg3 B=4, cfg4 B>=8; not B=1, cfg2 B=2, cfg4 B=4)
         # Block mode: always (its fused block selects are short; cfg2 B=1 229 vs 232 us,
         # B=8 1.44 vs 1.52 ms, scripts/block_single_ab.py).
+        auto_rule = single_launch == "auto"
         if single_launch == "auto":
+            # round 2 (profiles/r02_bench_cfg2_b8.json, scripts/schedules.py): the single
+            # launch from 192 FULL pairs, and from 128 at rows under 64K tokens (cfg2 B=2:
+            # 397 vs 408 / 417 us); below that, long rows keep the fused selects (cfg3 B=1:
+            # fusedsel 731 vs fused3 761 us) and short rows the 3-launch step, whose SELECT is
+            # the shared-memory-resident select (cfg2 B=1: fused3 226 vs fusedsel 236 us)
             pairs = len(self.full_layers) * B * Hkv
             single_launch = (bool(fuse_select) and not dual_stream and len(feeds) > 0
-                             and (pairs >= 192 or block_size > 1))
+                             and (pairs >= 192 or block_size > 1
+                                  or (pairs >= 128 and cap < 65536)))
         # token or block mode (hylra_decode_step_blocks_ex: the FULL pairs' final CTAs pool,
         # select blocks and write the coverage)
         self._single_ok = (not (block_size > 1 and (include_sinks or include_recent
@@ -151,6 +158,8 @@ class HybridDecoder:
         self.coop = False  # single-launch step with cooperative selects ("singlecoop")
         if self.single:
             self.dual = self.fused = False
+        elif auto_rule and self.fused and cap < 65536:
+            self.fused = False
         self._feeds_all = len(feeds) == len(self.full_layers)
         self._has_reuse = has_reuse
         # schedules this decoder can switch between (autotune): the fused-select and
