@@ -763,6 +763,29 @@ def run_ours(a):
                                    "not a scaling measurement"} if shared_gpu else {}),
             "extra": extra,
         }
+        # last key (it survives a truncated stdout tail): the BASELINE configurations at a
+        # glance — tok/s, ms per step, schedule, and the layer-sequential step beside each
+        def brief(r):
+            if not r or "value" not in r:
+                return {"error": (r or {}).get("error", "not run")}
+            sch = r.get("schedules") or {}
+            seq = (sch.get("sequential") or {}).get("ms_per_step")
+            out = {"tok_s": round(r["value"], 1), "ms": round(r["ms_per_step"], 4),
+                   "schedule": r.get("schedule")}
+            if seq:
+                out["sequential_ms"] = round(seq, 4)
+            if r.get("per_gpu_frac_of_peak"):
+                out["per_gpu_frac_of_peak"] = round(r["per_gpu_frac_of_peak"], 3)
+            if r.get("e2e"):
+                out["e2e_tok_s"] = round(r["e2e"]["value"], 1)
+            return out
+        line["summary"] = {
+            "cfg2_b8" if world == 1 else f"cfg2_b{8 * world}_global": brief(main),
+            **{k: brief(extra.get(k)) for k in ("cfg2_b1", "cfg2_b4", "cfg3_128k_b4",
+                                                "cfg4_qwen_64k_b16") if k in extra},
+            "roofline_frac": round(main["roofline"]["frac"], 3),
+            "cpu_reference_tok_s": (cpu or {}).get("value"),
+        }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
