@@ -11,7 +11,10 @@ port (oracle/hylra_oracle.py) stands in and the line says kind "port". Runs as a
 torch-free process.
 
 Number 1 — "kernel-equivalent" step time: exactly the per-layer body of
-the reference's hybrid_decode (engine.py:174-194) minus cache construction:
+the reference's hybrid_decode (engine.py:174-194) minus cache construction. By default each
+timed step runs the WHOLE step — every (sequence, KV-head) group through all layers in
+policy order, on a process pool — so nothing is extrapolated (--sampled: the older one
+FULL + one REUSE layer sample scaled by layer count). Per layer:
   FULL  layer, per (sequence, KV-head) group: G x full_attention (attention.py:210-226),
         the head-order logit sum and TopKSet(topk_of_logits(...)) (attention.py:264-275);
   REUSE layer, per group: sel.as_array() + G x _subset_attention (attention.py:229-241).
@@ -139,6 +142,50 @@ def _group_task(i):
     return t1 - t0, t2 - t1
 
 
+def _group_stack_task(i):
+    """One group's WHOLE layer stack in policy order (engine.py:174-194): every FULL layer
+    (its set replacing the inherited one) and every REUSE layer over the most recent FULL
+    layer's set. The layers run on the group's one FULL / one REUSE cache (identical cost per
+    layer: same N, d, k), so the step executes all of its work; times each kind."""
+    st = _STATE
+    cfg = st["cfg"]
+    qf, cf, qr, cr = st["caches"][i % len(st["caches"])]
+    tf = tr = 0.0
+    sel = None
+    for a in cfg.actions:
+        t0 = time.perf_counter()
+        if a == "full":
+            sel = _full_op(st["ra"], cfg, qf, cf)
+            tf += time.perf_counter() - t0
+        else:
+            _reuse_op(st["ra"], cfg, qr, cr, sel)
+            tr += time.perf_counter() - t0
+    return tf, tr
+
+
+def full_steps(cfg, batch, steps, warmup, workers):
+    """Whole steps on the pool: every (sequence, KV-head) group runs its full layer stack
+    (_group_stack_task). Returns (per-step wall times of the timed steps, median FULL / REUSE
+    busy shares)."""
+    import multiprocessing as mp
+
+    import numpy as np
+    groups = batch * cfg.kv_heads
+    per_worker = max(1, min(4, math.ceil(groups / workers)))
+    walls, shares = [], []
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers, initializer=_worker_init, initargs=(cfg.name, per_worker, 1000)) as pool:
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            res = pool.map(_group_stack_task, range(groups), chunksize=1)
+            wall = time.perf_counter() - t0
+            if it >= warmup:
+                walls.append(wall)
+                bf, br = sum(r[0] for r in res), sum(r[1] for r in res)
+                shares.append(bf / (bf + br))
+    return walls, float(np.median(shares))
+
+
 def kernel_equivalent(cfg, batch, steps, warmup, workers):
     """Median over `steps` samples of (t_full_layer, t_reuse_layer) over all B x Hkv groups."""
     import numpy as np
@@ -230,6 +277,9 @@ def main(argv=None):
                     help="0 = all host cores (a process pool; run with OPENBLAS_NUM_THREADS=1); "
                          "1 = this process only (run with threaded BLAS)")
     ap.add_argument("--e2e", action="store_true", help="also time hybrid_decode (number 2)")
+    ap.add_argument("--sampled", action="store_true",
+                    help="pool mode: time one FULL + one REUSE layer per sample and scale by "
+                         "layer count (the default times whole steps)")
     a = ap.parse_args(argv)
     cfg = _config(a.config)
     B = a.batch or cfg.batch
@@ -239,9 +289,41 @@ def main(argv=None):
     n_full = len(cfg.full_layers)
     n_reuse = cfg.layers - n_full
     groups = B * cfg.kv_heads
+    blas = int(os.environ.get("OPENBLAS_NUM_THREADS", "0") or 0) or cores
+    if workers > 1 and not a.sampled:
+        # whole steps: all groups x all layers per timed step, nothing extrapolated
+        walls, share = full_steps(cfg, B, a.steps, a.warmup, workers)
+        import statistics
+        step = statistics.median(walls)
+        out = {
+            "value": B / step, "unit": "tok/s", "kind": kind, "cores": workers,
+            "mode": f"{workers}-process pool, single-threaded BLAS",
+            "ms_per_step": step * 1e3,
+            "sample": (f"{len(walls)} whole steps (+{a.warmup} warm-up), median: all {groups} "
+                       f"(sequence, KV-head) groups x all {cfg.layers} layers in policy order "
+                       f"({n_full} FULL: G={cfg.group} x full_attention + top-{cfg.budget}; "
+                       f"{n_reuse} REUSE: G x _subset_attention over the inherited set) at "
+                       f"N={cfg.context}, d={cfg.head_dim}, float64, caches built outside the "
+                       f"timer (each group's layers share one FULL and one REUSE cache: same "
+                       f"cost per layer), groups on a {workers}-process pool; FULL share of the "
+                       f"busy time {share:.2f}"),
+            "extrapolation": None,
+            "step_seconds": walls, "timed_samples": len(walls),
+        }
+        if a.e2e:
+            t = end_to_end(cfg)
+            if t is not None:
+                out["end_to_end_hybrid_decode"] = {
+                    "value": B / (t * groups), "unit": "tok/s", "cores": blas,
+                    "group_seconds": t,
+                    "sample": (f"reference hybrid_decode (float64 cache copies + internal "
+                               f"all-FULL baseline) for one (sequence, KV-head) group, "
+                               f"{cfg.layers} layers, T=1, {t:.2f} s; x{groups} groups "
+                               f"(declared extrapolation)")}
+        print(json.dumps(out), flush=True)
+        return
     tf, tr, n = kernel_equivalent(cfg, B, a.steps, a.warmup, workers)
     step = n_full * tf + n_reuse * tr
-    blas = int(os.environ.get("OPENBLAS_NUM_THREADS", "0") or 0) or cores
     where = (f"groups on a {workers}-process pool" if workers > 1 else "groups in one process")
     out = {
         "value": B / step, "unit": "tok/s", "kind": kind,

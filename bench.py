@@ -97,9 +97,9 @@ def ref_timing(cfg_name, batch, steps, warmup, workers=0, e2e=False, timeout=180
 def run_reference(a):
     """Reference arm: the reference's own CPU implementation of the path (baseline/_ref,
     the unmodified `layerreuse` package) on the host cores, on our arm's workload (config 2,
-    B = 8 per GPU x N). Rank 0 only under torchrun. Each step = one timed sample (one FULL +
-    one REUSE layer over every (sequence, KV-head) group), extrapolated by layer count to the
-    32-layer step (declared in `extrapolation`)."""
+    B = 8 per GPU x N). Rank 0 only under torchrun. Each timed step runs the whole step:
+    every (sequence, KV-head) group through all 32 layers on a process pool (nothing
+    extrapolated)."""
     if _env_int("RANK", 0) != 0:
         return
     from paper_2602_00777_b200.synthetic import CONFIGS
@@ -121,7 +121,7 @@ def run_reference(a):
                          "kind": res.get("kind"), "sample": res.get("sample"),
                          "mode": res.get("mode")},
         "extrapolation": res.get("extrapolation"),
-        "sample_seconds_per_step": res.get("sample_seconds"),
+        "step_seconds": res.get("step_seconds"),
         "single_process": {k: one.get(k) for k in ("value", "unit", "cores", "mode", "sample")},
         "end_to_end_hybrid_decode": res.get("end_to_end_hybrid_decode"),
         "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0,
