@@ -126,11 +126,70 @@ __device__ __forceinline__ double rs_token_score(const SelectParams& p, const fl
   return agg;
 }
 
+// One token per warp, its query heads in parallel: lanes g' * kLpt + sub (g' < 32 / kLpt)
+// evaluate head 4c + g' of each chunk c of 4 heads with token_score_f64's per-head arithmetic
+// (the same sub lanes, the same xor tree inside the 8-lane group), and every lane then adds
+// the heads' part / sqrt(d) in head order — the reference order, bit for bit the per-token
+// evaluation of rs_token_score, with the heads' dependent chains overlapped.
+__device__ __forceinline__ double rs_token_score_wide(const SelectParams& p, const float* qs,
+                                                      int kvl, int b, int grp, int tok) {
+  constexpr int kHpw = 32 / kLpt;  // heads per warp pass
+  const int lane = threadIdx.x & 31, sub = lane & (kLpt - 1), gl = lane / kLpt;
+  const double sqd = sqrt((double)p.D);
+  constexpr int kMaxPer = 128 / kLpt;
+  double agg = 0.0;
+  for (int hh = 0; hh < p.sel_group; ++hh) {
+    const int kh = grp * p.sel_group + hh;
+    const int64_t koff = kvl * p.kv_sl + b * p.kv_sb + kh * p.kv_sh + (int64_t)tok * p.D;
+    float kv[kMaxPer];
+    if (p.dtype == 0) {
+      const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.k) + koff;
+#pragma unroll
+      for (int j = 0; j < kMaxPer; ++j) kv[j] = __bfloat162float(kp[min(sub + j * kLpt, p.D - 1)]);
+    } else {
+      const float* kp = reinterpret_cast<const float*>(p.k) + koff;
+#pragma unroll
+      for (int j = 0; j < kMaxPer; ++j) kv[j] = kp[min(sub + j * kLpt, p.D - 1)];
+    }
+    for (int g0 = 0; g0 < p.G; g0 += kHpw) {
+      const int g = min(g0 + gl, p.G - 1);
+      const float* qr = qs + (hh * p.G + g) * p.D;
+      double part0 = 0.0, part1 = 0.0;
+#pragma unroll
+      for (int j = 0; j + 1 < kMaxPer; j += 2) {
+        const int i = sub + j * kLpt;
+        if (i < p.D) {
+          part0 += (double)qr[i] * (double)kv[j];
+          part1 += (double)qr[i + kLpt] * (double)kv[j + 1];
+        }
+      }
+      double part = part0 + part1;
+#pragma unroll
+      for (int o = kLpt / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const double term = part / sqd;
+#pragma unroll
+      for (int u = 0; u < kHpw; ++u) {
+        const double t = __shfl_sync(0xffffffffu, term, u * kLpt);
+        if (g0 + u < p.G) agg += t;
+      }
+    }
+  }
+  return agg;
+}
+
 template <int NT>
 __device__ void rs_rescore(const SelectParams& p, const float* qs, int slot, int b, int grp,
                            const int* toks, double* vals, int n) {
   if (qs == nullptr) {
     rescore_f64<NT>(p, slot, b, grp, toks, vals, n);
+    return;
+  }
+  if (n <= NT / 32) {  // few tokens: one per warp, heads in parallel
+    const int warp = threadIdx.x >> 5;
+    if (warp < n) {
+      const double agg = rs_token_score_wide(p, qs, p.kv_layers[slot], b, grp, toks[warp]);
+      if ((threadIdx.x & 31) == 0) vals[warp] = agg;
+    }
     return;
   }
   const int warp = threadIdx.x >> 5, sub = threadIdx.x & (kLpt - 1);
