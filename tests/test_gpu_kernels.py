@@ -853,3 +853,32 @@ def test_layerwise_decoder_with_model_dependence():
     for l in range(L):
         np.testing.assert_array_equal(sel[dec.slot_of_layer[l]], ref_sets[l])
     assert max_head_err(dec.out.double().cpu().numpy(), ref_out) < 2e-2
+
+
+def test_layerwise_decoder_growing_rows_and_flags():
+    """LayerwiseDecoder across steps with a growing cache (n_valid 3000 -> 4096: workspaces
+    grow, splits change) equals HybridDecoder's selections at every step, refinement off;
+    a non-finite score raises NumericInputError from check_flags, whichever of its
+    workspaces holds the flag, and clear_flags resets them."""
+    from paper_2602_00777_b200.engine import LayerwiseDecoder
+    from paper_2602_00777_b200.errors import NumericInputError
+    L, B, Hq, Hkv, d, cap, budget = 5, 2, 16, 4, 128, 4096, 300
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=77, planted=40)
+    actions = ("full", "reuse", "full", "reuse", "full")
+    lw = LayerwiseDecoder(actions, k, v, budget, q_heads=Hq, refine=False)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, refine=False)
+    for n in (3000, 3500, 4096, 3001):
+        a, r = lw.step(q, n), ref.step(q, n)
+        torch.cuda.synchronize()
+        assert torch.equal(a.selections, r.selections), n
+    lw.check_flags(strict=True)
+    q_bad = q.clone()
+    q_bad[2, 1, 5, 7] = float("nan")
+    lw.step(q_bad, cap)
+    torch.cuda.synchronize()
+    with pytest.raises(NumericInputError):
+        lw.check_flags()
+    lw.clear_flags()
+    lw.step(q, cap)
+    torch.cuda.synchronize()
+    lw.check_flags(strict=True)
