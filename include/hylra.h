@@ -156,6 +156,15 @@ int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots,
                       const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
                       void* ws, size_t ws_bytes, void* stream);
 
+/* hylra_topk_select with options (ABI 7). HYLRA_SELECT_COMPACT: the select runs beside
+ * other work (a side stream under a streaming launch), so the shared-memory-resident select
+ * keeps each row on the fewest CTAs instead of spreading few rows over more SMs. */
+#define HYLRA_SELECT_COMPACT 1
+int hylra_topk_select_ex(const hylra_geometry* g, const float* scores, int n_slots,
+                         int n_valid, int budget, int sel_group, const void* q, const void* k,
+                         const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
+                         void* ws, size_t ws_bytes, void* stream, int options);
+
 /*
  * REUSE attention for layers layer_ids[0..n_layers) (host array): layer i gathers the
  * k_eff rows idx[src_slots[i]][b][kh / sel_group][0..k_eff) of its own K/V and runs

@@ -16,6 +16,7 @@ LIB_PATH = Path(os.environ.get("HYLRA_LIB") or Path(__file__).resolve().parent /
 
 # include/hylra.h HYLRA_ABI_VERSION this binding is written against (checked at load)
 ABI_VERSION = 7
+SELECT_COMPACT = 1  # hylra_topk_select_ex options (include/hylra.h)
 
 HYLRA_BF16 = 0
 HYLRA_F32 = 1
@@ -77,6 +78,7 @@ EXPORTED_SYMBOLS = (
     "hylra_select_workspace_bytes",
     "hylra_full_decode",
     "hylra_topk_select",
+    "hylra_topk_select_ex",
     "hylra_reuse_decode",
     "hylra_decode_layer",
     "hylra_decode_step_workspace_bytes",
@@ -172,6 +174,9 @@ def lib() -> ctypes.CDLL:
         l.hylra_topk_select.restype = i32
         l.hylra_topk_select.argtypes = [gp, vp, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp,
                                         sz, vp]
+        l.hylra_topk_select_ex.restype = i32
+        l.hylra_topk_select_ex.argtypes = [gp, vp, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp,
+                                           vp, sz, vp, i32]
         l.hylra_reuse_decode.restype = i32
         l.hylra_reuse_decode.argtypes = [gp, vp, vp, vp, i32, i32, vp, vp, vp, vp, i32, i32,
                                          i32, vp, vp, sz, vp]

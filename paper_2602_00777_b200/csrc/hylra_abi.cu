@@ -459,7 +459,8 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
                   const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
                   int* flags, cudaStream_t st, const BlockRows& br = BlockRows(),
                   const int32_t* kv_layer_ids = nullptr, const int32_t* out_slots = nullptr,
-                  int force_nt = 0, int32_t* idx_mirror = nullptr, unsigned* hist = nullptr) {
+                  int force_nt = 0, int32_t* idx_mirror = nullptr, unsigned* hist = nullptr,
+                  bool compact = false) {
   SelectParams p{};
   if (int e = build_select_params(&p, g, scores, n_slots, n_valid, budget, sel_group, q, k,
                                   layer_ids, idx, k_stride, info, flags, br, kv_layer_ids,
@@ -482,7 +483,9 @@ int launch_select(const hylra_geometry* g, const float* scores, int n_slots, int
     // long as the whole launch stays within one wave of SMs
     const int forced = tuning().rowsel_cluster.load(std::memory_order_relaxed);
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) csz = std::max(csz, forced);
-    else
+    else if (!compact)
+      // (compact: a select on a side stream beside streaming launches keeps to the fewest
+      // SMs, leaving the rest to them; cfg2 B=1 dual step 217 vs 242 us)
       while (csz < kRowselMaxCluster && rows * csz * 2 <= num_sms() &&
              n_eff / (2 * csz) >= kRowselMinSlice)
         csz *= 2;
@@ -983,7 +986,8 @@ int decode_step_impl(const hylra_geometry* g, const void* q, const void* k, cons
                          budget, sel_group, refine ? q : nullptr, refine ? kf : nullptr,
                          gr.ids->data(), idx, k_stride, nullptr, flags, sx, BlockRows(),
                          split ? gr.kv->data() : nullptr, gr.slots->data(), force_nt,
-                         o.idx_mirror, hist ? hist + gr.score_base * hist_slot : nullptr);
+                         o.idx_mirror, hist ? hist + gr.score_base * hist_slot : nullptr,
+                         sx != st);
   };
   auto reuse = [&](cudaStream_t sx) -> int {
     if (s.reuse_ids.empty()) return HYLRA_OK;
@@ -1151,9 +1155,19 @@ int hylra_topk_select(const hylra_geometry* g, const float* scores, int n_slots,
                       int budget, int sel_group, const void* q, const void* k,
                       const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
                       void* ws, size_t ws_bytes, void* stream) {
+  return hylra_topk_select_ex(g, scores, n_slots, n_valid, budget, sel_group, q, k, layer_ids,
+                              idx, k_stride, info, ws, ws_bytes, stream, 0);
+}
+
+int hylra_topk_select_ex(const hylra_geometry* g, const float* scores, int n_slots,
+                         int n_valid, int budget, int sel_group, const void* q, const void* k,
+                         const int32_t* layer_ids, int32_t* idx, int k_stride, int32_t* info,
+                         void* ws, size_t ws_bytes, void* stream, int options) {
   if (!ws || ws_bytes < kHeader) return fail(HYLRA_ERR_CONFIGURATION, "select workspace too small");
   return launch_select(g, scores, n_slots, n_valid, budget, sel_group, q, k, layer_ids, idx,
-                       k_stride, info, static_cast<int*>(ws), static_cast<cudaStream_t>(stream));
+                       k_stride, info, static_cast<int*>(ws), static_cast<cudaStream_t>(stream),
+                       BlockRows(), nullptr, nullptr, 0, nullptr, nullptr,
+                       (options & HYLRA_SELECT_COMPACT) != 0);
 }
 
 int hylra_decode_layer(const hylra_geometry* g, const void* q, const void* k, const void* v,

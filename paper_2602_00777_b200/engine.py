@@ -119,8 +119,9 @@ class HybridDecoder:
         # selects run on a high-priority side stream under the next streaming launch
         # (hylra_decode_step_ex)
         feeds = [l for l in self.full_layers if l + 1 < L and self.actions[l + 1] is Action.REUSE]
-        self.dual = (bool(dual_stream) and block_size == 1 and not (include_sinks or include_recent)
-                     and 0 < len(feeds) < len(self.full_layers))
+        self._dual_ok = (block_size == 1 and not (include_sinks or include_recent)
+                         and 0 < len(feeds) < len(self.full_layers))
+        self.dual = bool(dual_stream) and self._dual_ok
         # fused selects (token mode): the FULL kernel selects the rows of the FULL layers that
         # feed REUSE layers itself; the other FULL layers' SELECT runs on the side stream
         # under the REUSE launch (hylra_decode_step_ex fuse_select; tensor-core path only)
@@ -140,11 +141,10 @@ class HybridDecoder:
         # B=8 1.44 vs 1.52 ms, scripts/block_single_ab.py).
         auto_rule = single_launch == "auto"
         if single_launch == "auto":
-            # round 2 (profiles/r02_bench_cfg2_b8.json, scripts/schedules.py): the single
+            # round 2 (scripts/dual_ab.py, profiles/r02_schedules_dual.txt): the single
             # launch from 192 FULL pairs, and from 128 at rows under 64K tokens (cfg2 B=2:
-            # 397 vs 408 / 417 us); below that, long rows keep the fused selects (cfg3 B=1:
-            # fusedsel 731 vs fused3 761 us) and short rows the 3-launch step, whose SELECT is
-            # the shared-memory-resident select (cfg2 B=1: fused3 226 vs fusedsel 236 us)
+            # 396 vs 397 / 411 / 414 us); below that, long rows keep the fused selects (cfg3
+            # B=1: fusedsel 730 vs 763 us) and short rows the two-stream step (below)
             pairs = len(self.full_layers) * B * Hkv
             single_launch = (bool(fuse_select) and not dual_stream and len(feeds) > 0
                              and (pairs >= 192 or block_size > 1
@@ -159,7 +159,11 @@ class HybridDecoder:
         if self.single:
             self.dual = self.fused = False
         elif auto_rule and self.fused and cap < 65536:
+            # short rows, few pairs: the two-stream step, whose selects run compact on a side
+            # stream under the next streaming launch (cfg2 B=1: dual 218 vs fused3 224 vs
+            # fusedsel 222 us, scripts/dual_ab.py), else the 3-launch step
             self.fused = False
+            self.dual = self._dual_ok
         self._feeds_all = len(feeds) == len(self.full_layers)
         self._has_reuse = has_reuse
         # schedules this decoder can switch between (autotune): the fused-select and
@@ -168,7 +172,7 @@ class HybridDecoder:
                           and len(feeds) > 0 and sel_group == 1
                           and k_cache.dtype == torch.bfloat16 and d in (64, 128))
         self._count_kernels()
-        if self.dual or self._fused_ok:
+        if self.dual or self._fused_ok or self._dual_ok:
             # high priority: select CTAs are dispatched ahead of the queued FULL / REUSE CTAs
             self._side = torch.cuda.Stream(device=k_cache.device, priority=-8)
             self._events = [torch.cuda.Event() for _ in range(4)]
@@ -189,13 +193,18 @@ class HybridDecoder:
                 "fusedsel" if self.fused else "dual" if self.dual else "fused3")
 
     def set_schedule(self, name: str) -> None:
-        """Switch between the step schedules ("single", "singlecoop", "fusedsel", "fused3";
-        block mode: "single", "fused3"); every one gives bit-identical outputs and
+        """Switch between the step schedules ("single", "singlecoop", "fusedsel", "dual",
+        "fused3"; block mode: "single", "fused3"); every one gives bit-identical outputs and
         selections, only the launch structure differs. "singlecoop": the single-launch step
         whose FULL splits select cooperatively (hylra_step_options fuse_select = 3; token
-        mode, sel_group 1)."""
-        if name not in ("single", "singlecoop", "fusedsel", "fused3"):
+        mode, sel_group 1). "dual": FULL(A) -> FULL(B) -> REUSE with the selects on a
+        high-priority side stream under the next streaming launch (token mode, some but not
+        all FULL layers feeding REUSE layers)."""
+        if name not in ("single", "singlecoop", "fusedsel", "dual", "fused3"):
             raise ConfigurationError(f"unknown schedule {name!r}")
+        if name == "dual" and not self._dual_ok:
+            raise ConfigurationError("schedule 'dual' needs token mode without sinks / recent "
+                                     "and some, but not all, FULL layers feeding REUSE layers")
         if name == "singlecoop" and not (self._single_ok and self._fused_ok):
             raise ConfigurationError("schedule 'singlecoop' needs token mode, sel_group 1 and "
                                      "the tensor-core path")
@@ -206,7 +215,7 @@ class HybridDecoder:
                                         if name == "fusedsel" else ""))
         self.single = name in ("single", "singlecoop")
         self.coop = name == "singlecoop"
-        self.fused, self.dual = name == "fusedsel", False
+        self.fused, self.dual = name == "fusedsel", name == "dual" 
         self._count_kernels()
 
     def autotune(self, q: torch.Tensor, n_valid: int | None = None, reps: int = 10) -> dict:
@@ -215,7 +224,8 @@ class HybridDecoder:
         measured steps overwrite `out` / the selections (the next step rewrites them)."""
         names = ([n for n, ok in (("single", self._single_ok),
                                   ("singlecoop", self._single_ok and self._fused_ok),
-                                  ("fusedsel", self._fused_ok)) if ok] + ["fused3"])
+                                  ("fusedsel", self._fused_ok),
+                                  ("dual", self._dual_ok)) if ok] + ["fused3"])
         times = {}
         cur = torch.cuda.current_stream(self.k.device)
         for name in names:
@@ -679,12 +689,13 @@ class LayerwiseDecoder(HybridDecoder):
                 e_fork, e_join = self._ev[len(self._pending)]
                 e_fork.record(main)
                 self.side.wait_event(e_fork)
-                _abi.check(lib.hylra_topk_select(
+                # compact: the select shares the GPU with the next FULL layer's streaming
+                _abi.check(lib.hylra_topk_select_ex(
                     g, sc.data_ptr(), 1, n_valid, self.budget, self.sel_group,
                     q.data_ptr() if self.refine else None,
                     self.k.data_ptr() if self.refine else None, _abi.int32_array([l]),
                     self.idx[s].data_ptr(), self.k_stride, None, self._side_ws.data_ptr(),
-                    self._side_ws.numel(), self.side.cuda_stream))
+                    self._side_ws.numel(), self.side.cuda_stream, _abi.SELECT_COMPACT))
                 e_join.record(self.side)
                 self._pending.append(e_join)
                 self._prev = "full"

@@ -92,7 +92,7 @@ def gather_outputs(out_local, plan: ShardPlan, group=None):
                                               out_local.shape[3])
 
 
-SCHEDULES = ("single", "singlecoop", "fusedsel", "fused3")
+SCHEDULES = ("single", "singlecoop", "fusedsel", "dual", "fused3")
 
 
 def agree_schedule(times: dict, group=None, device="cpu"):
