@@ -508,7 +508,7 @@ def test_autotune_keeps_results_bit_identical():
     R, I = ref.outputs.clone(), ref.selections.clone()
     dec = HybridDecoder(actions, k, v, budget, q_heads=Hq)
     times = dec.autotune(q, cap, reps=3)
-    assert set(times) == {"single", "singlecoop", "fusedsel", "fused3"}
+    assert set(times) == {"single", "singlecoop", "fusedsel", "dual", "fused3"}
     assert all(t > 0 for t in times.values())
     assert dec.schedule == min(times, key=times.get)
     res = dec.step(q, cap)
