@@ -499,8 +499,9 @@ def test_schedules_bit_identical_at_config2_scale():
 
 
 def test_autotune_keeps_results_bit_identical():
-    """HybridDecoder.autotune times single / fusedsel / fused3 as graph replays and keeps
-    the fastest; whichever it keeps, the step's outputs and selections are unchanged."""
+    """HybridDecoder.autotune times single / singlecoop / fusedsel / dual / fused3 as graph
+    replays and keeps the fastest; whichever it keeps, the step's outputs and selections are
+    unchanged."""
     L, B, Hq, Hkv, d, cap, budget = 6, 2, 16, 4, 128, 4096, 256
     actions = ("full", "reuse", "full", "full", "reuse", "reuse")
     q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=47, planted=32)
