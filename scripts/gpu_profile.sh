@@ -28,4 +28,5 @@ cp /tmp/single_cfg2_b8.ncu-rep gpurun_out/
 cap fusedsel_cfg2_b8 "attn_mma_kernel|topk_select" 3 --config cfg2 --batch 8 --steps 1 --schedule fusedsel
 cap fused3_cfg2_b1 "attn_mma_kernel|rowsel|topk_select" 3 --config cfg2 --batch 1 --steps 1 --schedule fused3
 cap seq_cfg2_b1 "attn_mma_kernel|rowsel" 4 --config cfg2 --batch 1 --steps 1 --schedule sequential
+cap dual_cfg2_b1 "attn_mma_kernel|rowsel" 5 --config cfg2 --batch 1 --steps 1 --schedule dual
 ls -la gpurun_out

@@ -26,7 +26,7 @@ ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--block-size", type=int, default=1)
 ap.add_argument("--schedule", default="auto",
-                choices=["auto", "single", "fusedsel", "fused3", "sequential"])
+                choices=["auto", "single", "fusedsel", "fused3", "dual", "sequential"])
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 if a.batch:
@@ -39,7 +39,8 @@ if a.schedule == "sequential":
     dec = LayerwiseDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
 else:
     kw = {"auto": {}, "single": {"single_launch": True},
-          "fusedsel": {"single_launch": False}, "fused3": {"fuse_select": False}}[a.schedule]
+          "fusedsel": {"single_launch": False}, "fused3": {"fuse_select": False},
+          "dual": {"fuse_select": False, "dual_stream": True}}[a.schedule]
     dec = HybridDecoder(cfg.actions, k, v, cfg.budget // bs if bs > 1 else cfg.budget,
                         q_heads=cfg.q_heads, block_size=bs, **kw)
 for _ in range(a.steps):
