@@ -262,6 +262,36 @@ def _block_mode_line(a, cfg, torch):
             "e2e": e2e}
 
 
+def _sinks_recent_line(a, cfg, torch, sinks=4, recent=64):
+    """Sink / recent augmentation (row f3; engine.py:122-126): cfg2 at B=8 with every REUSE
+    layer reading sorted(selection | [0, sinks) | [n - recent, n)), autotuned, graph
+    replays. Algorithmic bytes count the augmented rows each REUSE (b, kv-head) reads."""
+    from paper_2602_00777_b200.engine import HybridDecoder
+    from paper_2602_00777_b200.synthetic import generate_torch
+
+    q, k, v = generate_torch(cfg, "cuda")
+    dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads,
+                        include_sinks=sinks, include_recent=recent)
+    tuned = dec.autotune(q, cfg.context)
+    dec.step(q, cfg.context)
+    torch.cuda.synchronize()
+    dec.check_flags()
+    ms = tuned[dec.schedule]
+    # augmented rows per REUSE (b, kv-head): the set plus the sink / recent tokens it lacks
+    sel = dec.idx[..., :cfg.budget]
+    extra = ((sel >= sinks) & (sel < cfg.context - recent)).sum(-1).float().mean().item()
+    rows = extra + sinks + recent
+    L, B = q.shape[0], q.shape[1]
+    nf = len(cfg.full_layers)
+    by = (nf * cfg.context + (L - nf) * rows) * B * k.shape[2] * 2 * cfg.head_dim * 2
+    sched = dec.schedule
+    del dec, q, k, v
+    torch.cuda.empty_cache()
+    return {"value": B / (ms * 1e-3), "ms_per_step": ms, "sinks": sinks, "recent": recent,
+            "reuse_rows_mean": rows, "step_gbs": by / (ms * 1e-3) / 1e9, "schedule": sched,
+            "autotune_ms": tuned}
+
+
 def _offload_line(a, cfg, torch, batch=1):
     """Index-guided offload (row f2): cfg2 at B=1 with the 24 REUSE layers' K/V in pinned
     host memory (3.2 GB); the REUSE kernel reads only the selected rows across the link.
@@ -728,6 +758,10 @@ def run_ours(a):
             extra["cfg2_blocks_b8"] = _block_mode_line(a, cfg, torch)
         except Exception as exc:  # noqa: BLE001
             extra["cfg2_blocks_b8"] = {"error": str(exc)}
+        try:
+            extra["cfg2_sinks_recent_b8"] = _sinks_recent_line(a, cfg, torch)
+        except Exception as exc:  # noqa: BLE001
+            extra["cfg2_sinks_recent_b8"] = {"error": str(exc)}
         try:
             extra["cfg2_offload_b1"] = _offload_line(a, cfg, torch)
         except Exception as exc:  # noqa: BLE001
