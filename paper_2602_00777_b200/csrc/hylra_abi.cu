@@ -1581,18 +1581,27 @@ int hylra_overlap_counts(const int32_t* idx, int steps, int layers, int rows, in
   if (!idx || !counts) return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
   if (steps < 1 || layers < 1 || rows < 1 || k < 1 || k_stride < k || n_tokens < 1)
     return fail(HYLRA_ERR_INVALID_INPUT, "invalid overlap dimensions");
-  const int n_pairs = layers * (layers + 1) / 2;
-  const size_t budget = 200 * 1024 - n_pairs * sizeof(int);
+  // chunks: as large as 200 KB of bitmaps allows, then split until the grid covers about
+  // two CTAs per SM
+  const size_t budget = 200 * 1024;
   int chunk = (int)std::min<size_t>(budget / (layers * 4) * 32, (size_t)((n_tokens + 31) & ~31));
   chunk = std::max(32, chunk & ~31);
-  const size_t smem = (size_t)layers * (chunk / 32) * 4 + n_pairs * sizeof(int);
+  while (chunk > 1024 && (int64_t)rows * steps * ((n_tokens + chunk - 1) / chunk) < 2 * num_sms())
+    chunk = std::max(1024, ((chunk / 2) + 31) & ~31);
+  const size_t smem = (size_t)layers * (chunk / 32) * 4;
   if (smem > 220 * 1024) return fail(HYLRA_ERR_CONFIGURATION, "too many layers (%d)", layers);
   if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(overlap_counts_kernel),
                                       220 * 1024))
     return cuda_check(e, "overlap attribute");
-  dim3 grid(rows, steps);
-  overlap_counts_kernel<<<grid, kOvThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      idx, layers, rows, k, k_stride, n_tokens, chunk, counts);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // the chunks add their counts: start from zero
+  if (int e = cuda_check(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)steps * rows *
+                                                        layers * layers, st),
+                         "overlap counts zero"))
+    return e;
+  dim3 grid(rows, steps, (n_tokens + chunk - 1) / chunk);
+  overlap_counts_kernel<<<grid, kOvThreads, smem, st>>>(idx, layers, rows, k, k_stride, n_tokens,
+                                                        chunk, counts);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_check(cudaGetLastError(), "overlap launch");
 }
