@@ -1,38 +1,57 @@
-"""Canonical selection sets (host-only; no torch).
+"""Host-side selection sets (no torch): what the GPU path hands back to a caller of the
+reference's API.
 
-Reference: pkg/src/layerreuse/attention.py — `TopKSet` (:108-140) and `BlockSet` (:143-182),
-with the same canonical-form checks and error types.
+Contract (pkg/src/layerreuse/attention.py): `TopKSet` (:108-140) is a token selection of at
+most `budget` distinct ascending indices; `BlockSet` (:143-182) a selection of distinct
+ascending block ids of width `block_size`. Construction canonicalises to tuples of Python
+ints and raises the reference's exception types (InvalidInputError for a bad budget or
+width, InvalidSelectionError for a bad index list).
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
+
+import numpy as np
 
 from .errors import InvalidInputError, InvalidSelectionError
 
 __all__ = ["TopKSet", "BlockSet"]
 
 
+def _ascending_ids(values, noun: str, empty: str) -> tuple:
+    """`values` as a tuple of ints, non-empty, non-negative and strictly increasing; `noun`
+    names the entries in the error text, `empty` is the message for no entries."""
+    ids = tuple(map(int, values))
+    if len(ids) == 0:
+        raise InvalidSelectionError(empty)
+    arr = np.asarray(ids, dtype=np.int64)
+    if int(arr.min()) < 0:
+        raise InvalidSelectionError(f"{noun} indices must be non-negative")
+    if arr.size > 1 and not bool(np.all(arr[1:] > arr[:-1])):
+        raise InvalidSelectionError(f"{noun} indices must be strictly ascending")
+    return ids
+
+
+def _positive(value: int, name: str) -> None:
+    if value < 1:
+        raise InvalidInputError(f"{name} must be >= 1, got {value}")
+
+
 @dataclass(frozen=True)
 class TopKSet:
-    """Canonical selection: distinct ascending indices plus the requested budget."""
+    """A token selection: distinct ascending indices, at most `budget` of them."""
 
     indices: tuple
     budget: int
 
     def __post_init__(self) -> None:
-        ind = tuple(int(i) for i in self.indices)
-        if self.budget < 1:
-            raise InvalidInputError(f"budget must be >= 1, got {self.budget}")
-        if not ind:
-            raise InvalidSelectionError("selection must contain at least one index")
-        if any(i < 0 for i in ind):
-            raise InvalidSelectionError("token indices must be non-negative")
-        if any(b <= a for a, b in zip(ind, ind[1:])):
-            raise InvalidSelectionError("token indices must be strictly ascending")
-        if len(ind) > self.budget:
+        _positive(self.budget, "budget")
+        ids = _ascending_ids(self.indices, "token",
+                             "selection must contain at least one index")
+        if len(ids) > self.budget:
             raise InvalidSelectionError(
-                f"selection holds {len(ind)} indices but budget is {self.budget}")
-        object.__setattr__(self, "indices", ind)
+                f"selection holds {len(ids)} indices but budget is {self.budget}")
+        object.__setattr__(self, "indices", ids)
 
     @property
     def size(self) -> int:
@@ -41,37 +60,31 @@ class TopKSet:
 
 @dataclass(frozen=True)
 class BlockSet:
-    """Canonical block selection (attention.py:143-182): distinct ascending block indices
-    plus the block width; token_coverage(n) truncates the final block at n."""
+    """A block selection: distinct ascending block ids of `block_size` tokens each; the
+    token coverage of a cache of n tokens truncates the final block at n."""
 
     block_indices: tuple
     block_size: int
 
     def __post_init__(self) -> None:
-        blocks = tuple(int(b) for b in self.block_indices)
-        if self.block_size < 1:
-            raise InvalidInputError(f"block_size must be >= 1, got {self.block_size}")
-        if not blocks:
-            raise InvalidSelectionError("block selection must contain at least one block")
-        if any(b < 0 for b in blocks):
-            raise InvalidSelectionError("block indices must be non-negative")
-        if any(b2 <= b1 for b1, b2 in zip(blocks, blocks[1:])):
-            raise InvalidSelectionError("block indices must be strictly ascending")
-        object.__setattr__(self, "block_indices", blocks)
+        _positive(self.block_size, "block_size")
+        object.__setattr__(self, "block_indices",
+                           _ascending_ids(self.block_indices, "block",
+                                          "block selection must contain at least one block"))
 
     @property
     def size(self) -> int:
         return len(self.block_indices)
 
     def token_coverage(self, n: int):
-        import numpy as np
         if n < 1:
             raise InvalidInputError(f"cache length must be >= 1, got {n}")
-        spans = []
-        for b in self.block_indices:
-            start = b * self.block_size
-            if start >= n:
-                raise InvalidSelectionError(
-                    f"block {b} starts at token {start}, beyond cache length {n}")
-            spans.append(np.arange(start, min(start + self.block_size, n), dtype=np.int64))
-        return np.concatenate(spans)
+        starts = np.asarray(self.block_indices, dtype=np.int64) * self.block_size
+        beyond = np.nonzero(starts >= n)[0]
+        if beyond.size:
+            j = int(beyond[0])
+            raise InvalidSelectionError(
+                f"block {self.block_indices[j]} starts at token {int(starts[j])}, "
+                f"beyond cache length {n}")
+        ends = np.minimum(starts + self.block_size, n)
+        return np.concatenate([np.arange(s, e, dtype=np.int64) for s, e in zip(starts, ends)])
