@@ -121,6 +121,11 @@ uint64_t hylra_launch_count(void);
  *   "gather_tma"     1/0: standalone REUSE launches gather rows with TMA tile::gather4
  *                    (UTMALDG.2D.GATHER4) instead of cp.async, for contiguous caches
  *                    (default 0: measured 1.5x slower, profiles/r02_gather_tma_ab.txt).
+ *   "bulk_merge"     1/0: the split-K final merge pulls a pair's partials into shared
+ *                    memory with cp.async.bulk (default 1; env HYLRA_BULK_MERGE).
+ *   "cluster_merge"  1/0: a REUSE launch split 2-16 ways within one CTA per SM runs each pair's
+ *                    splits as one CTA cluster and merges them through distributed shared
+ *                    memory (default 1; env HYLRA_CLUSTER_MERGE).
  * Results never depend on them (every select path returns the same index sets). */
 int hylra_set_tuning(const char* name, int value);
 

@@ -14,6 +14,8 @@
 // log-sum-exp rule by the last CTA of the pair to finish (no second launch).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "select.cuh"
 
@@ -84,6 +86,10 @@ struct AttnParams {
   int gather_tma;
   int gather_rows;  // rows of the 2-D views (an index past them is zero-filled)
   int cap_rows;     // cache rows per (kv layer, b, kh) block (capacity)
+  int bulk_merge;   // split-K final merge: partials staged by cp.async.bulk (merge_and_store)
+  // REUSE launched as clusters of its `splits` CTAs (grid.x == splits <= 16): the splits of a
+  // pair merge through distributed shared memory (cluster_merge_store), no global round trips
+  int cluster_merge;
 };
 
 // Stage n selection indices from global into shared memory, validated (out-of-range ->
@@ -150,13 +156,19 @@ __device__ __forceinline__ void stage_indices(const int32_t* __restrict__ src, i
 // final CTA stages every split's (m, l) there and merges the output partials with 8 float4
 // L2 loads in flight per thread — a one-layer launch at B = 1 has ~40 splits per pair, whose
 // merge as dependent per-split loads took ~20 us. Same arithmetic, same order, either way.
+// bulk (optional, bulk_cap bytes of drained pipeline buffers, 16-byte aligned): when the
+// pair's partials fit, the final CTA pulls all of them (and the (m, l) pairs) into shared
+// memory with cp.async.bulk — ONE round trip instead of one per 8 splits: the 37-split merge
+// of a one-layer FULL launch at B = 1 was the launch's ~7 us tail (scripts/trace_layer.py).
 template <int D>
 __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, int b, int kh,
                                                 int split, const float* sm_m,
                                                 const float* sm_l, const float* sm_o,
                                                 int tid, int nthreads, int bar_id,
                                                 float* scratch = nullptr,
-                                                int scratch_floats = 0) {
+                                                int scratch_floats = 0,
+                                                uint8_t* bulk = nullptr,
+                                                uint32_t bulk_cap = 0) {
   const int G = p.G;
   const int layer = p.layers[slot];
   const int pair = (slot * p.B + b) * p.Hkv + kh;
@@ -222,13 +234,39 @@ __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, i
     float* s_sc = scratch + 2 * SG;  // [split][g] rescale factor
     float* s_M = s_sc + SG;          // [g]
     float* s_L = s_M + kMaxG;        // [g]
-    const float2* pml2 = reinterpret_cast<const float2*>(pml);
-    for (int i = tid; i < SG; i += nthreads) {
-      const float2 x = __ldcg(pml2 + i);
-      s_ml[2 * i] = x.x;
-      s_ml[2 * i + 1] = x.y;
+    const uint32_t po_bytes = (uint32_t)SG * D * 4;
+    const uint32_t ml_bytes = (uint32_t)SG * 8;
+    const bool use_bulk = bulk != nullptr && po_bytes <= bulk_cap &&
+                          (reinterpret_cast<uintptr_t>(po) & 15) == 0;
+    const bool ml_bulk = use_bulk && ((reinterpret_cast<uintptr_t>(pml) | ml_bytes) & 15) == 0 &&
+                         (smem_u32(s_ml) & 15) == 0;
+    __shared__ __align__(8) uint64_t s_bulk_bar;
+    if (use_bulk) {
+      // every thread's generic accesses of the buffers (ring reads, sm_o) before the async
+      // proxy's writes; the partials (other CTAs' stores, acquired above) before its reads
+      fence_proxy_async_smem();
+      asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+      if (tid == 0) {
+        mbar_init(&s_bulk_bar, 1);
+        mbar_fence_init();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_arrive_expect_tx(&s_bulk_bar, po_bytes + (ml_bulk ? ml_bytes : 0u));
+        for (uint32_t off = 0; off < po_bytes; off += 32768u)
+          bulk_load(bulk + off, reinterpret_cast<const uint8_t*>(po) + off,
+                    min(32768u, po_bytes - off), &s_bulk_bar);
+        if (ml_bulk) bulk_load(s_ml, pml, ml_bytes, &s_bulk_bar);
+      }
+    }
+    if (!ml_bulk) {
+      const float2* pml2 = reinterpret_cast<const float2*>(pml);
+      for (int i = tid; i < SG; i += nthreads) {
+        const float2 x = __ldcg(pml2 + i);
+        s_ml[2 * i] = x.x;
+        s_ml[2 * i + 1] = x.y;
+      }
     }
     asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+    if (use_bulk) mbar_wait(&s_bulk_bar, 0);
     for (int g = tid; g < G; g += nthreads) {
       float M = -INFINITY;
       for (int s = 0; s < p.splits; ++s) M = fmaxf(M, s_ml[2 * (s * G + g)]);
@@ -258,6 +296,10 @@ __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, i
         a2 = fmaf(x.z, sc, a2);
         a3 = fmaf(x.w, sc, a3);
       };
+      if (use_bulk) {
+        const float4* bo4 = reinterpret_cast<const float4*>(bulk);
+        for (; s < p.splits; ++s) add(bo4[s * G * D4 + e4], s_sc[s * G + g]);
+      }
       for (; s + 8 <= p.splits; s += 8) {
         float4 x[8];
 #pragma unroll
@@ -276,6 +318,7 @@ __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, i
       o[2] = v2;
       o[3] = v3;
     }
+    if (use_bulk && tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&s_bulk_bar)) : "memory");
   } else {
     for (int e = tid; e < G * D; e += nthreads) {
       const int g = e / D, d = e % D;
@@ -295,6 +338,109 @@ __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, i
   }
   if (tid == 0) p.counters[pair] = 0;  // leave the workspace zeroed for the next call
   return true;
+}
+
+// Cluster barrier over every thread of the CTA cluster (release / acquire: shared-memory
+// writes before it are visible to the peers' DSMEM reads after it).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+
+// Split-K merge of a REUSE launch whose splits of one pair form a thread-block cluster
+// (p.cluster_merge = C = splits; rank = split). Each CTA combines its 4 warps into its split
+// partial IN ITS OWN SHARED MEMORY (`part`: [G][D] o, then [G][2] (m, l)); after a cluster
+// barrier every rank merges a 1/C slice of the pair's G x D outputs, reading all C partials
+// through DSMEM, and stores it. Arithmetic and order are merge_and_store's (the CTA
+// partial, then the staged merge's max / scale / fmaf chain over splits in ascending
+// order), so the outputs are bit-identical to the global-memory merge — without the
+// partial stores, fence, counter atomic and L2 re-reads (~3-5 us of a one-layer REUSE
+// launch at B = 1, scripts/trace_layer.py). The consumer threads call it; the producer
+// warps meet both cluster barriers in attn_mma_kernel.
+template <int D>
+__device__ __forceinline__ void cluster_merge_store(const AttnParams& p, int slot, int b, int kh,
+                                                    int split, const float* sm_m,
+                                                    const float* sm_l, const float* sm_o,
+                                                    float* part, float* scratch) {
+  const int G = p.G, C = p.cluster_merge, tid = threadIdx.x;
+  constexpr int NT = kConsumerWarps * 32;
+  const int layer = p.layers[slot];
+  float* out_base = p.out + layer * p.o_sl + b * p.o_sb + (int64_t)(kh * G) * D;
+  const float c = p.scale_log2;
+  float* pml = part + G * D;
+  for (int e = tid; e < G * D; e += NT) {
+    const int g = e / D, d = e % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, sm_m[w * 16 + g]);
+    float acc = 0.f, L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      const float mw = sm_m[w * 16 + g];
+      const float sc = (mw == -INFINITY) ? 0.f : exp2f((mw - M) * c);
+      acc += sm_o[(w * 16 + g) * D + d] * sc;
+      L += sm_l[w * 16 + g] * sc;
+    }
+    part[e] = acc;
+    if (d == 0) {
+      pml[g * 2 + 0] = M;
+      pml[g * 2 + 1] = L;
+    }
+  }
+  cluster_sync_all();  // (1) every split's partial is in its CTA's shared memory
+  auto cl = cooperative_groups::this_cluster();
+  const int SG = C * G;
+  float* s_ml = scratch;           // [split][g][m, l]
+  float* s_sc = scratch + 2 * SG;  // [split][g]
+  float* s_M = s_sc + SG;          // [g]
+  float* s_L = s_M + kMaxG;        // [g]
+  for (int i = tid; i < SG; i += NT) {
+    const float* r = cl.map_shared_rank(pml, i / G);
+    s_ml[2 * i] = r[2 * (i % G)];
+    s_ml[2 * i + 1] = r[2 * (i % G) + 1];
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  for (int g = tid; g < G; g += NT) {
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < C; ++s2) M = fmaxf(M, s_ml[2 * (s2 * G + g)]);
+    s_M[g] = M;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  for (int i = tid; i < SG; i += NT) {
+    const float ms = s_ml[2 * i];
+    s_sc[i] = (ms == -INFINITY) ? 0.f : exp2f((ms - s_M[i % G]) * c);
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  for (int g = tid; g < G; g += NT) {
+    float L = 0.f;
+    for (int s2 = 0; s2 < C; ++s2) L = fmaf(s_ml[2 * (s2 * G + g) + 1], s_sc[s2 * G + g], L);
+    s_L[g] = L;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  constexpr int D4 = D / 4;
+  const int n4 = G * D4, per = (n4 + C - 1) / C;
+  const int e_end = min(n4, (split + 1) * per);
+  for (int e4 = split * per + tid; e4 < e_end; e4 += NT) {
+    const int g = e4 / D4, d = (e4 % D4) * 4;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    for (int s2 = 0; s2 < C; ++s2) {
+      const float4 x = reinterpret_cast<const float4*>(cl.map_shared_rank(part, s2))[e4];
+      const float sc = s_sc[s2 * G + g];
+      a0 = fmaf(x.x, sc, a0);
+      a1 = fmaf(x.y, sc, a1);
+      a2 = fmaf(x.z, sc, a2);
+      a3 = fmaf(x.w, sc, a3);
+    }
+    const float L = s_L[g];
+    const float v0 = a0 / L, v1 = a1 / L, v2 = a2 / L, v3 = a3 / L;
+    if (!(isfinite(v0) && isfinite(v1) && isfinite(v2) && isfinite(v3)))
+      atomicOr(p.flags, 2);  // NaN/inf in q, K or V
+    float* o = out_base + g * D + d;
+    o[0] = v0;
+    o[1] = v1;
+    o[2] = v2;
+    o[3] = v3;
+  }
+  cluster_sync_all();  // (2) no CTA leaves while a peer may still read its partial
 }
 
 // ---------------------------------------------------------------------------------
@@ -916,7 +1062,13 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
         p, kt, vt, qa, o, m0, m1, l0, l1, row0, n_rows, score_row,
         score_buf != nullptr ? score_buf + (i % (2 * STAGES)) * kTileRows : nullptr, lane);
     release_stage(empty_bar + s, release_word + warp, dep, lane);
+#ifdef HYLRA_TRACE
+    if (i == 0 && threadIdx.x == 0) hylra_trace_mark(6);
+#endif
   }
+#ifdef HYLRA_TRACE
+  if (threadIdx.x == 0) hylra_trace_mark(7);
+#endif
   pdl_launch_dependents();
   if (hist_smem != nullptr) {
     // the producer warp has counted every tile: this split's counts join the row's
@@ -988,11 +1140,20 @@ __device__ __forceinline__ void attn_mma_item(const CUtensorMap& tmk, const CUte
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
   // the merge's scratch: the REUSE index staging area / FULL histogram + score buffers, idle
-  // once the main loop is done
+  // once the main loop is done; its bulk staging area: the drained pipeline buffers (not
+  // while the cooperative select's slice prefetch is landing in them)
+  if (GATHER && p.cluster_merge > 1) {
+    constexpr int kPartOff = ((2 * kConsumerWarps * 16 + kConsumerWarps * 16 * D) * 4 + 127) & ~127;
+    cluster_merge_store<D>(p, slot, b, kh, split, sm_m, sm_l, sm_o,
+                           reinterpret_cast<float*>(smem + kPartOff),
+                           reinterpret_cast<float*>(smem + STAGES * SM::kStageBytes + 256));
+    return;
+  }
   const bool final_cta = merge_and_store<D>(
       p, slot, b, kh, split, sm_m, sm_l, sm_o, threadIdx.x, 128, 1,
       reinterpret_cast<float*>(smem + STAGES * SM::kStageBytes + 256),
-      kIdxStage + 2 * STAGES * kTileRows);
+      kIdxStage + 2 * STAGES * kTileRows, p.bulk_merge ? smem : nullptr,
+      slice_smem ? 0u : (uint32_t)(STAGES * SM::kStageBytes));
   if constexpr (!GATHER) {
     if (coop) {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1074,8 +1235,25 @@ __global__ void __launch_bounds__(attn_threads<GATHER>(), 2)
                     const __grid_constant__ SelectParams sp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
+#ifdef HYLRA_TRACE
+  // one trace row per CTA: [0 start, 4 done, 5 smid, 6 first stage consumed, 7 main loop end]
+  if (threadIdx.x == 0) {
+    g_trace_row = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    hylra_trace_mark(0);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (g_trace != nullptr) hylra_trace_rec()[5] = smid;
+  }
+#endif
   attn_mma_item<D, GATHER, GBIG, STAGES>(tmk, tmv, p, sp, smem, blockIdx.x, blockIdx.y,
                                          blockIdx.z / p.B, blockIdx.z % p.B, nullptr, nullptr);
+  if (GATHER && p.cluster_merge > 1 && (threadIdx.x >> 5) >= kConsumerWarps) {
+    cluster_sync_all();  // the consumer warps' cluster_merge_store barriers (1) and (2)
+    cluster_sync_all();
+  }
+#ifdef HYLRA_TRACE
+  if (threadIdx.x == 0) hylra_trace_mark(4);
+#endif
 }
 
 // ---------------------------------------------------------------------------------

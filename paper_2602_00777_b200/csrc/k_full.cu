@@ -27,3 +27,11 @@ cudaError_t run_full_mma(int D, bool big, dim3 grid, cudaStream_t st, const CUte
 
 }  // namespace host
 }  // namespace hylra
+
+#ifdef HYLRA_TRACE
+// diagnostics build only: per-CTA trace rows of the standalone FULL / REUSE launches (this
+// translation unit's copy of the trace symbol; scripts/trace_layer.py)
+extern "C" int hylra_trace_set_full(void* buf) {
+  return cudaMemcpyToSymbol(hylra::g_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : 5;
+}
+#endif

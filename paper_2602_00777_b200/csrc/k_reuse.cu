@@ -17,7 +17,10 @@ static cudaError_t launch_reuse(dim3 grid, cudaStream_t st, const CUtensorMap& t
   auto kern = attn_mma_kernel<D, true, GBIG, S>;
   constexpr size_t smem = mma_smem_bytes<D, true, GBIG>();
   if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem)) return e;
-  return launch_pdl(kern, grid, dim3(attn_threads<true>()), smem, st, tk, tv, p, sp);
+  if (p.cluster_merge > 8)
+    if (cudaError_t e = ensure_nonportable_cluster(reinterpret_cast<const void*>(kern))) return e;
+  return launch_pdl_cluster(kern, grid, dim3(attn_threads<true>()), smem, st, p.cluster_merge,
+                            tk, tv, p, sp);
 }
 
 cudaError_t run_attn_mma(int D, bool gather, bool big, dim3 grid, cudaStream_t st,
@@ -33,3 +36,9 @@ cudaError_t run_attn_mma(int D, bool gather, bool big, dim3 grid, cudaStream_t s
 
 }  // namespace host
 }  // namespace hylra
+
+#ifdef HYLRA_TRACE
+extern "C" int hylra_trace_set_reuse(void* buf) {
+  return cudaMemcpyToSymbol(hylra::g_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -60,6 +60,18 @@ inline cudaError_t ensure_smem_attr(const void* func, size_t smem) {
   if (e == cudaSuccess) done[key] = smem;
   return e;
 }
+// Clusters of more than 8 CTAs (the portable limit) need the kernel's opt-in, per device.
+inline cudaError_t ensure_nonportable_cluster(const void* func) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, bool> done;
+  const auto key = std::make_pair(func, current_device());
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) done[key] = true;
+  return e;
+}
 // ------------------------------------------------------------------ launches
 // Programmatic dependent launch for the step's kernels (FULL, SELECT, REUSE): each may be
 // scheduled while its predecessor drains (the kernels wait on griddepcontrol before
@@ -89,6 +101,38 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+
+// The same, launched as clusters of cluster_x CTAs along x (1: no cluster attribute).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                               cudaStream_t st, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// REUSE split-K merge through a CTA cluster's shared memory (default on; env
+// HYLRA_CLUSTER_MERGE, tuning knob "cluster_merge")
+inline bool cluster_merge_enabled();
 
 // ------------------------------------------------------------------ kernel tables
 template <int D, bool GATHER, bool GBIG>
@@ -123,6 +167,8 @@ struct Tuning {
   std::atomic<int> select_threads{-1};
   std::atomic<int> rowsel_cluster{-1};
   std::atomic<int> gather_tma{-1};
+  std::atomic<int> bulk_merge{-1};
+  std::atomic<int> cluster_merge{-1};
 };
 inline Tuning& tuning() {
   static Tuning t;
@@ -133,6 +179,29 @@ inline Tuning& tuning() {
 // (or hylra_set_tuning("rowsel", 0)) keeps every row on select_row (A/B runs).
 // REUSE launches gather rows by TMA (tile::gather4) instead of cp.async where the cache is
 // contiguous; HYLRA_GATHER_TMA / hylra_set_tuning("gather_tma", v) (default: off).
+// split-K final merge stages the partials by cp.async.bulk (default on; env HYLRA_BULK_MERGE)
+inline bool bulk_merge_enabled() {
+  const int o = tuning().bulk_merge.load(std::memory_order_relaxed);
+  if (o >= 0) return o != 0;
+  static int v = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_BULK_MERGE");
+    v = (e && *e) ? (atoi(e) != 0) : 1;
+  });
+  return v != 0;
+}
+inline bool cluster_merge_enabled() {
+  const int o = tuning().cluster_merge.load(std::memory_order_relaxed);
+  if (o >= 0) return o != 0;
+  static int v = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("HYLRA_CLUSTER_MERGE");
+    v = (e && *e) ? (atoi(e) != 0) : 1;
+  });
+  return v != 0;
+}
 inline bool gather_tma_enabled() {
   const int o = tuning().gather_tma.load(std::memory_order_relaxed);
   if (o >= 0) return o != 0;

@@ -884,3 +884,54 @@ def test_layerwise_decoder_growing_rows_and_flags():
     lw.step(q, cap)
     torch.cuda.synchronize()
     lw.check_flags(strict=True)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,cap,budget", [(1, 32, 8, 32768, 2048), (2, 28, 4, 16384, 1024),
+                                                 (1, 16, 2, 8192, 333)])
+def test_bulk_merge_equals_l2_merge(B, Hq, Hkv, cap, budget):
+    """The split-K final merge staging a pair's partials by cp.async.bulk (bulk_merge=1, the
+    default) returns exactly the L2-load merge's outputs, for one-layer FULL launches (~37
+    splits per pair at B=1, partials up to 74 KB; G=7 too large for the staging area at some
+    split counts, so the fallback is covered) and REUSE launches, layer-sequential."""
+    from paper_2602_00777_b200 import _abi
+    from paper_2602_00777_b200.engine import LayerwiseDecoder
+    L = 4
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, 128, cap, "bf16", seed=cap + budget, planted=64)
+    actions = ("full", "reuse", "full", "reuse")
+    outs = {}
+    for m in ((0, 0), (1, 0), (0, 1), (1, 1)):
+        with _abi.tuning(bulk_merge=m[0], cluster_merge=m[1]):
+            dec = LayerwiseDecoder(actions, k, v, budget, q_heads=Hq)
+            res = dec.step(q, cap)
+            torch.cuda.synchronize()
+            dec.check_flags(strict=True)
+            outs[m] = (res.outputs.clone(), res.selections.clone())
+    for m in outs:
+        assert torch.equal(outs[m][0], outs[(0, 0)][0]), m
+        assert torch.equal(outs[m][1], outs[(0, 0)][1]), m
+
+
+@pytest.mark.parametrize("d,Hq,Hkv,cap,k,L,B", [(128, 32, 8, 32768, 2048, 1, 1),
+                                                (128, 32, 8, 8192, 1000, 2, 2),
+                                                (64, 14, 2, 4096, 333, 1, 1),
+                                                (128, 28, 4, 16384, 2048, 1, 3),
+                                                (128, 64, 4, 4096, 700, 1, 1),
+                                                (128, 32, 8, 16384, 4096, 1, 1)])
+def test_reuse_cluster_merge_equals_global_merge(d, Hq, Hkv, cap, k, L, B):
+    """A REUSE launch split 2-8 ways under one wave merges its splits through the CTA
+    cluster's distributed shared memory (cluster_merge=1, the default): bit-identical to
+    the global split-K merge, for d 64 / 128, G 4 / 7 / 16, ragged selections, clusters of
+    2 to 16 (non-portable) CTAs."""
+    from paper_2602_00777_b200 import _abi
+    q, k_, v, *_ = make_stack(L, B, Hq, Hkv, d, cap, "bf16", seed=k + B)
+    rng = np.random.default_rng(d + k + B)
+    idx = np.stack([np.stack([np.stack([np.sort(rng.choice(cap, k, replace=False))
+                                        for _ in range(Hkv)]) for _ in range(B)])
+                    for _ in range(L)]).astype(np.int32)
+    it = torch.from_numpy(idx).to(DEV)
+    with _abi.tuning(cluster_merge=0):
+        ref = sparse_attention(q, k_, v, it, cap)
+    with _abi.tuning(cluster_merge=1):
+        got = sparse_attention(q, k_, v, it, cap)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
