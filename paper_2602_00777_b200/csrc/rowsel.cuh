@@ -42,7 +42,10 @@ namespace hylra {
 constexpr int kRowselThreads = 1024;
 constexpr int kRowselMaxSlice = 40960;  // tokens of a row per CTA
 constexpr int kRowselMaxCluster = 8;
-constexpr int kRowselMinSlice = 4096;   // no finer split when spreading few rows over SMs
+// no finer split when spreading few rows over SMs: a 32K row on 8 CTAs (4096 tokens each)
+// spends ~14K cycles summing the cluster histograms through DSMEM against ~10K on 4 CTAs
+// (scripts/rowsel_prof.py); layer-sequential cfg2 B=1 497 vs 514 us
+constexpr int kRowselMinSlice = 8192;
 
 // Tokens per CTA for an n-token row on a C-CTA cluster (a whole number of bitmap words).
 __host__ __device__ constexpr int rowsel_slice(int n, int c) { return ((n + c - 1) / c + 31) & ~31; }

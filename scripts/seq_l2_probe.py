@@ -34,6 +34,15 @@ def graph_us(fn, reps=20):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
+import os  # noqa: E402
+
+from paper_2602_00777_b200 import _abi  # noqa: E402
+
+# optional tuning knobs for the whole run: SEQ_TUNING="rowsel_cluster=4,bulk_merge=0"
+_tun = dict((kv.split("=")[0], int(kv.split("=")[1]))
+            for kv in os.environ.get("SEQ_TUNING", "").split(",") if kv)
+if _tun:
+    _abi.tuning(**_tun).__enter__()
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 cfg = CONFIGS["cfg2"].with_(batch=B)
 q, k, v = generate_torch(cfg, "cuda")
