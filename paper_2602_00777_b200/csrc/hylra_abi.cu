@@ -295,7 +295,10 @@ int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* 
   p.n_groups = g->kv_heads / p.sel_group;
   p.inv_sqrt_d = (float)(1.0 / std::sqrt((double)g->head_dim));
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)g->head_dim));
-  p.prefetch = kReusePrefetchTiles;
+  {
+    const int o = tuning().reuse_prefetch.load(std::memory_order_relaxed);
+    p.prefetch = o >= 0 ? o : kReusePrefetchTiles;
+  }
   p.bulk_merge = bulk_merge_enabled() ? 1 : 0;
   const int n_kv = kv_layer_ids ? kv_layer_count : g->num_layers;
   for (int i = 0; i < n_layers; ++i) {
@@ -1136,6 +1139,7 @@ int hylra_set_tuning(const char* name, int value) {
   else if (!strcmp(name, "gather_tma")) knob = &tuning().gather_tma;
   else if (!strcmp(name, "bulk_merge")) knob = &tuning().bulk_merge;
   else if (!strcmp(name, "cluster_merge")) knob = &tuning().cluster_merge;
+  else if (!strcmp(name, "reuse_prefetch")) knob = &tuning().reuse_prefetch;
   if (!knob) return fail(HYLRA_ERR_CONFIGURATION, "unknown tuning knob '%s'", name);
   knob->store(value < 0 ? -1 : value, std::memory_order_relaxed);
   return HYLRA_OK;

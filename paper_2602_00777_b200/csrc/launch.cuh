@@ -169,6 +169,7 @@ struct Tuning {
   std::atomic<int> gather_tma{-1};
   std::atomic<int> bulk_merge{-1};
   std::atomic<int> cluster_merge{-1};
+  std::atomic<int> reuse_prefetch{-1};
 };
 inline Tuning& tuning() {
   static Tuning t;
