@@ -126,7 +126,11 @@ uint64_t hylra_launch_count(void);
  *   "cluster_merge"  1/0: a REUSE launch split 2-16 ways within one CTA per SM runs each pair's
  *                    splits as one CTA cluster and merges them through distributed shared
  *                    memory (default 1; env HYLRA_CLUSTER_MERGE).
- * Results never depend on them (every select path returns the same index sets). */
+ *   "reuse_prefetch" REUSE L2 prefetch distance in tiles (default 0, the best measured).
+ *   "fused_fine_splits" 1: FULL launches with fused selects over <= 64 pairs take finer
+ *                    split-K partitions (faster at small batch; outputs then differ from
+ *                    the other schedules' at bf16 level). Default 0.
+ * Index sets never depend on them; outputs neither, except under "fused_fine_splits". */
 int hylra_set_tuning(const char* name, int value);
 
 /* Bytes of zero-filled workspace the attention ops need for `n_layers` layer

@@ -5,6 +5,7 @@
 // split-K grid for the device's SM count, encodes the TMA tensor maps and enqueues on the caller's
 // stream. No allocation, no synchronisation, no retained state besides cached
 // function attributes.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cmath>
@@ -105,7 +106,17 @@ int small_reuse_tiles() {
   return v;
 }
 
-int choose_splits(int pairs, int tiles, bool gather) {
+// Tuning knob "fused_fine_splits" (default off): FULL launches with fused selects (the
+// fusedsel schedule) over few pairs take finer splits, so the pairs' final CTAs, which run
+// the selects, finish staggered under the streaming of the other splits instead of together
+// at the end. Measured: cfg2 B=1 fusedsel 220.7 -> 213.9 us, B=2 393 us (single 406), cfg4
+// B=4 627 us (single 647). Off by default because the outputs then differ from the other
+// schedules' at bf16 level (a different split partition rounds P = exp(s - m) to bf16
+// against a different running max), and every batched schedule returns bit-identical
+// outputs by design (tests/test_gpu_kernels.py, test_gpu_select.py).
+constexpr int kFineMaxPairs = 64;
+
+int choose_splits(int pairs, int tiles, bool gather, bool fine = false) {
   static int env[2][2];
   static std::once_flag once;
   std::call_once(once, [] {
@@ -123,6 +134,8 @@ int choose_splits(int pairs, int tiles, bool gather) {
   int s;
   if (e[0] || e[1]) {
     s = splits_by_waves(pairs, tiles, e[0] ? e[0] : 8, e[1] ? e[1] : 4);
+  } else if (!gather && fine && pairs <= kFineMaxPairs) {
+    s = splits_by_waves(pairs, tiles, 8, 8);
   } else if (!gather) {
     s = splits_by_waves(pairs, tiles, 4, 32);
     // up to one full wave when the rows allow (never just over one: N=8K B=1 at 5 splits
@@ -177,12 +190,12 @@ size_t counter_region_bytes(const hylra_geometry* g) {
 // ext_ctr: the counters live elsewhere (the decode step's fixed counter regions) and the
 // layout holds only the partials
 AttnLayout attn_layout(const hylra_geometry* g, int n_layers, int rows, bool gather,
-                       bool ext_ctr = false) {
+                       bool ext_ctr = false, bool fine = false) {
   AttnLayout a{};
   const int G = g->q_heads / g->kv_heads;
   a.pairs = n_layers * g->batch * g->kv_heads;
   a.tiles = std::max(1, (rows + kTileRows - 1) / kTileRows);
-  a.splits = choose_splits(a.pairs, a.tiles, gather);
+  a.splits = choose_splits(a.pairs, a.tiles, gather, fine);
   a.tps = (a.tiles + a.splits - 1) / a.splits;
   const size_t parts = a.splits;  // partial slots per pair
   a.off_counters = ext_ctr ? 0 : kHeader;
@@ -263,7 +276,8 @@ int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* 
                      int n_layers, const int32_t* layer_ids, const int32_t* src_slots,
                      const int32_t* idx, const int32_t* counts, int k_stride, int sel_group,
                      float* out, float* scores, void* ws, size_t ws_bytes, int* flags,
-                     const int32_t* kv_layer_ids, int kv_layer_count, int* counters = nullptr) {
+                     const int32_t* kv_layer_ids, int kv_layer_count, int* counters = nullptr,
+                     bool fine = false) {
   if (int e = check_geometry(g)) return e;
   if (n_layers < 1 || n_layers > kMaxSlots)
     return fail(HYLRA_ERR_CONFIGURATION, "n_layers %d not in [1, %d]", n_layers, kMaxSlots);
@@ -273,7 +287,7 @@ int make_attn_params(AttnParams* pp, AttnLayout* lay_out, const hylra_geometry* 
   if (n_rows < 1) return fail(HYLRA_ERR_INVALID_INPUT, "no rows to attend over");
   if (!q || !k || !v || !out || !ws || !layer_ids)
     return fail(HYLRA_ERR_CONFIGURATION, "NULL pointer argument");
-  const AttnLayout lay = attn_layout(g, n_layers, n_rows, gather, counters != nullptr);
+  const AttnLayout lay = attn_layout(g, n_layers, n_rows, gather, counters != nullptr, fine);
   if (ws_bytes < lay.total)
     return fail(HYLRA_ERR_CONFIGURATION, "workspace %zu B < required %zu B", ws_bytes, lay.total);
   const int G = g->q_heads / g->kv_heads;
@@ -326,9 +340,12 @@ int launch_attention(const hylra_geometry* g, bool gather, const void* q, const 
                      int* counters = nullptr, unsigned* hist = nullptr, int early = 0) {
   AttnParams p{};
   AttnLayout lay{};
+  const bool fine = fused != nullptr && fuse_nslots > 0 && !gather && blk == nullptr &&
+                    use_mma_path(g) &&
+                    tuning().fused_fine_splits.load(std::memory_order_relaxed) > 0;
   if (int e = make_attn_params(&p, &lay, g, gather, q, k, v, n_valid, n_rows, n_layers, layer_ids,
                                src_slots, idx, counts, k_stride, sel_group, out, scores, ws,
-                               ws_bytes, flags, kv_layer_ids, kv_layer_count, counters))
+                               ws_bytes, flags, kv_layer_ids, kv_layer_count, counters, fine))
     return e;
   p.early = early;
   // block-mode REUSE by TMA tiles of the selected blocks: REUSE split rules, the streaming
@@ -708,7 +725,8 @@ int step_layout(const hylra_geometry* g, const uint8_t* actions, int n_valid, in
   s->off_attn = off;
   s->attn_bytes = 0;
   for (int n = 1; n <= (int)nf; ++n)
-    s->attn_bytes = std::max(s->attn_bytes, attn_layout(g, n, n_valid, false, true).total);
+    s->attn_bytes = std::max({s->attn_bytes, attn_layout(g, n, n_valid, false, true).total,
+                              attn_layout(g, n, n_valid, false, true, true).total});
   s->off_attn_r = align_up(s->off_attn + s->attn_bytes, 256);
   s->attn_bytes_r = 0;
   for (int n = 1; n <= (int)s->reuse_ids.size(); ++n)
@@ -1140,6 +1158,7 @@ int hylra_set_tuning(const char* name, int value) {
   else if (!strcmp(name, "bulk_merge")) knob = &tuning().bulk_merge;
   else if (!strcmp(name, "cluster_merge")) knob = &tuning().cluster_merge;
   else if (!strcmp(name, "reuse_prefetch")) knob = &tuning().reuse_prefetch;
+  else if (!strcmp(name, "fused_fine_splits")) knob = &tuning().fused_fine_splits;
   if (!knob) return fail(HYLRA_ERR_CONFIGURATION, "unknown tuning knob '%s'", name);
   knob->store(value < 0 ? -1 : value, std::memory_order_relaxed);
   return HYLRA_OK;
@@ -1148,8 +1167,9 @@ int hylra_set_tuning(const char* name, int value) {
 size_t hylra_attention_workspace_bytes(const hylra_geometry* g, int n_layers, int rows) {
   if (check_geometry(g) || n_layers < 1) return 0;
   // either op (FULL or REUSE) may use the workspace
-  return std::max(attn_layout(g, n_layers, std::max(rows, 1), false).total,
-                  attn_layout(g, n_layers, std::max(rows, 1), true).total);
+  return std::max({attn_layout(g, n_layers, std::max(rows, 1), false).total,
+                   attn_layout(g, n_layers, std::max(rows, 1), false, false, true).total,
+                   attn_layout(g, n_layers, std::max(rows, 1), true).total});
 }
 
 size_t hylra_select_workspace_bytes(const hylra_geometry* g, int n_slots, int sel_group) {

@@ -170,6 +170,7 @@ struct Tuning {
   std::atomic<int> bulk_merge{-1};
   std::atomic<int> cluster_merge{-1};
   std::atomic<int> reuse_prefetch{-1};
+  std::atomic<int> fused_fine_splits{-1};
 };
 inline Tuning& tuning() {
   static Tuning t;

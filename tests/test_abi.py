@@ -160,7 +160,8 @@ def test_tuning_knobs_validate_and_restore():
     """hylra_set_tuning: known knobs accept values and -1 restores the default rule; an unknown
     knob is a ConfigurationError (no GPU needed)."""
     lib = _abi.lib()
-    with _abi.tuning(gather_tma=1, bulk_merge=0, cluster_merge=0, reuse_prefetch=2):
+    with _abi.tuning(gather_tma=1, bulk_merge=0, cluster_merge=0, reuse_prefetch=2,
+                     fused_fine_splits=1):
         pass
     with _abi.tuning(rowsel=0, select_threads=512, rowsel_cluster=4):
         pass

@@ -935,3 +935,28 @@ def test_reuse_cluster_merge_equals_global_merge(d, Hq, Hkv, cap, k, L, B):
         got = sparse_attention(q, k_, v, it, cap)
     torch.cuda.synchronize()
     assert torch.equal(got, ref)
+
+
+def test_fused_fine_splits_keep_selections():
+    """Tuning knob fused_fine_splits: the fused-select FULL launch over few pairs takes finer
+    split-K partitions. Selections stay bit-identical; outputs move only at bf16 level (P
+    is rounded to bf16 against another running max) and stay deterministic."""
+    from paper_2602_00777_b200 import _abi
+    actions = ("full", "reuse", "full", "full", "reuse", "reuse")
+    L, B, Hq, Hkv, d, n, budget = len(actions), 1, 32, 8, 128, 32768, 2048
+    q, k, v, *_ = make_stack(L, B, Hq, Hkv, d, n, "bf16", seed=77, planted=64)
+    ref = HybridDecoder(actions, k, v, budget, q_heads=Hq, fuse_select=True,
+                        single_launch=False).step(q, n)
+    ref_out, ref_idx = ref.outputs.clone(), ref.selections.clone()
+    with _abi.tuning(fused_fine_splits=1):
+        dec = HybridDecoder(actions, k, v, budget, q_heads=Hq, fuse_select=True,
+                            single_launch=False)
+        a = dec.step(q, n)
+        a_out = a.outputs.clone()
+        b = dec.step(q, n)
+        torch.cuda.synchronize()
+        dec.check_flags(strict=True)
+    assert torch.equal(a.selections, ref_idx)
+    assert torch.equal(b.outputs, a_out)
+    scale = ref_out.abs().amax(dim=-1, keepdim=True).clamp_min(1e-30)
+    assert float(((a_out - ref_out).abs() / scale).max()) < 2e-2
