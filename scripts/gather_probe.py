@@ -62,10 +62,16 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--context", type=int, default=None)
+    ap.add_argument("--budget", type=int, default=None)
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     if a.batch:
         cfg = cfg.with_(batch=a.batch)
+    if a.context:
+        cfg = cfg.with_(context=a.context)
+    if a.budget:
+        cfg = cfg.with_(budget=a.budget)
     q, k, v = generate_torch(cfg, "cuda")
     dec = HybridDecoder(cfg.actions, k, v, cfg.budget, q_heads=cfg.q_heads)
     dec.step(q, cfg.context)
