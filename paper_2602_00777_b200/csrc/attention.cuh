@@ -318,7 +318,7 @@ __device__ __forceinline__ bool merge_and_store(const AttnParams& p, int slot, i
       o[2] = v2;
       o[3] = v3;
     }
-    if (use_bulk && tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&s_bulk_bar)) : "memory");
+    if (use_bulk && tid == 0) mbar_inval(&s_bulk_bar);
   } else {
     for (int e = tid; e < G * D; e += nthreads) {
       const int g = e / D, d = e % D;
