@@ -916,7 +916,8 @@ def test_bulk_merge_equals_l2_merge(B, Hq, Hkv, cap, budget):
                                                 (64, 14, 2, 4096, 333, 1, 1),
                                                 (128, 28, 4, 16384, 2048, 1, 3),
                                                 (128, 64, 4, 4096, 700, 1, 1),
-                                                (128, 32, 8, 16384, 4096, 1, 1)])
+                                                (128, 32, 8, 16384, 4096, 1, 1),
+                                                (64, 16, 2, 4096, 1000, 1, 1)])
 def test_reuse_cluster_merge_equals_global_merge(d, Hq, Hkv, cap, k, L, B):
     """A REUSE launch split 2-8 ways under one wave merges its splits through the CTA
     cluster's distributed shared memory (cluster_merge=1, the default): bit-identical to
